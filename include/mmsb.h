@@ -1,0 +1,127 @@
+/*
+ * mmsb.h -- C ABI of the B200-native multi-MSB replacement RDHEI hot path
+ * (EMR-RDHEI and LMR-RDHEI, arXiv 2302.07992; /root/reference/PAPER.md cited as P:<line>).
+ *
+ * The four calls follow the three parties of the paper (Fig. fig:General_EMR P:467-565,
+ * Fig. fig:General_LMR P:848-970): the content owner ENCODES with K1, the data hider
+ * EMBEDS with K2, the receiver EXTRACTS with K2 only and/or RECOVERS with K1 only
+ * (separability).  Formats, bit orders and readings: DESIGN.md §3.
+ *
+ * Conventions for every call
+ *  - All data pointers (images, keys, messages, per-image outputs, workspace) are DEVICE
+ *    pointers owned by the caller; the library allocates nothing and never synchronises.
+ *    Every call is asynchronous on `stream` (a cudaStream_t passed as void*).
+ *  - Images are [batch][height][width] uint8, row-major (raster index r = y*W + x).
+ *    The GPU path accepts power-of-two height and width in [16, 32768].
+ *  - Keys are [batch][32] bytes (ChaCha20 / RFC 8439 key, nonce 0, counter 0; reading Q12).
+ *  - Message buffers are [batch][stride_bytes], stride_bytes % 16 == 0; message bit k is
+ *    bit (7 - k%8) of byte k/8 (numpy.packbits(bitorder='big')); a stride of
+ *    ceil(7*H*W/8) bytes covers any capacity.
+ *  - Return value = synchronous validation (E_INVAL: null pointer, unsupported shape,
+ *    workspace too small; E_CUDA: a launch failed).  Data-dependent outcomes are written,
+ *    asynchronously, to the per-image device array img_status[batch] (OK, CAPACITY,
+ *    INTEGRITY, BADCASE, FORMAT).
+ *  - `ws` is caller-allocated device scratch of at least mmsb_workspace_bytes(shape) bytes,
+ *    256-byte aligned; one workspace may serve every call made on the same stream.
+ */
+#ifndef MMSB_H
+#define MMSB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    MMSB_OK = 0,
+    MMSB_E_INVAL = 2,
+    MMSB_E_CAPACITY = 3,     /* 32 + n > C: the frame does not fit (reading Q17)          */
+    MMSB_E_INTEGRITY = 4,    /* decrypted length n > C - 32 (wrong K2 or tampering)               */
+    MMSB_E_BADCASE = 5,      /* LMR: no candidate map fits the MSB plane          */
+    MMSB_E_CUDA = 6,
+    MMSB_E_UNIMPLEMENTED = 7,
+    MMSB_E_FORMAT = 8        /* malformed header / stream                                         */
+} mmsb_status;
+
+typedef enum { MMSB_EMR = 0, MMSB_LMR = 1 } mmsb_method;
+
+typedef struct {
+    int32_t method;      /* mmsb_method                                                        */
+    int32_t batch;       /* images in the batch (>= 1)                                         */
+    int32_t height;      /* M (power of two, 16..32768)                                        */
+    int32_t width;       /* N (power of two, 16..32768)                                        */
+    int32_t tile_log2;   /* LMR map-coder tile side 2^t, t in [3, 9] (0 = default 7)           */
+} mmsb_shape;
+
+/* Bytes of device workspace the four calls need for this shape. 0 if the shape is invalid. */
+size_t mmsb_workspace_bytes(const mmsb_shape *shape);
+
+/*
+ * Content owner, encoding phase (EMR: P:575-747; LMR: P:972-988).
+ *   images     [B][H][W] original images I
+ *   k1         [B][32]   image-encryption keys K1
+ *   encrypted  [B][H][W] output I_e (EMR: LSB plane = header || rotated map, P:743-744;
+ *                        LMR: MSB plane = header || tile tables || coded maps)
+ *   b_out      [B] int32 chosen b (eq. optimial_b; LMR P:979); 0 on BADCASE
+ *   capacity_out [B] int64 C = b*zeros (EMR) or (b-1)*zeros (LMR) bits; 0 on BADCASE
+ *   img_status [B] int32 OK or BADCASE (LMR)
+ */
+mmsb_status mmsb_content_owner_encode(const mmsb_shape *shape, const uint8_t *images, const uint8_t *k1,
+                                      uint8_t *encrypted, int32_t *b_out, int64_t *capacity_out,
+                                      int32_t *img_status, void *ws, size_t ws_bytes, void *stream);
+
+/*
+ * Data hider (EMR: P:749-750; LMR: P:990-991).  Needs no K1.
+ *   encrypted  [B][H][W] I_e
+ *   k2         [B][32]   data-hiding keys K2
+ *   msg_bytes  [B][stride_bytes] plain messages, msg_bits[B] (int64) bits each
+ *   marked     [B][H][W] output I_e' (must NOT alias encrypted)
+ * The frame BE32(n) || message is XORed with the K2 keystream and written b (EMR, bit
+ * positions 1..b) or b-1 (LMR, positions 2..b) bits per redundant pixel in raster order of
+ * the rotated domain; all other bits are copied.  img_status: OK, CAPACITY (then marked ==
+ * encrypted), FORMAT, BADCASE.
+ */
+mmsb_status mmsb_hider_embed(const mmsb_shape *shape, const uint8_t *encrypted, const uint8_t *k2,
+                             const uint8_t *msg_bytes, const int64_t *msg_bits, int64_t stride_bytes,
+                             uint8_t *marked, int32_t *img_status, void *ws, size_t ws_bytes, void *stream);
+
+/*
+ * Receiver with K2 only: data extraction, no de-rotation (EMR: P:839-840; LMR: P:1063-1064).
+ *   msg_out     [B][stride_bytes]: the first ceil(max(C-32,0)/32) 32-bit words receive the message bits
+ *               [0, n) followed by zeros; later bytes are untouched.
+ *   msg_bits_out [B] int64: n, or -1 on INTEGRITY / FORMAT / BADCASE.
+ */
+mmsb_status mmsb_receiver_extract(const mmsb_shape *shape, const uint8_t *marked, const uint8_t *k2,
+                                  uint8_t *msg_out, int64_t stride_bytes, int64_t *msg_bits_out,
+                                  int32_t *img_status, void *ws, size_t ws_bytes, void *stream);
+
+/*
+ * Receiver with K1 only: image recovery (EMR: P:819-837; LMR: P:1060-1061).
+ *   recovered [B][H][W]: EMR -> original except the LSB plane (= decrypted bits, reading Q20);
+ *   LMR -> the original exactly.  Zero-filled on FORMAT / BADCASE.
+ */
+mmsb_status mmsb_receiver_recover(const mmsb_shape *shape, const uint8_t *marked, const uint8_t *k1,
+                                  uint8_t *recovered, int32_t *img_status, void *ws, size_t ws_bytes,
+                                  void *stream);
+
+/* Per-image sum of squared differences (int64) of two image batches (P:746 PSNR numerator). */
+mmsb_status mmsb_stats(const mmsb_shape *shape, const uint8_t *original, const uint8_t *recovered,
+                       int64_t *sse_out, void *stream);
+
+/* HOST function on HOST arrays: DER_i = C_i / (H W); PSNR_i = 10 log10(65025 H W / SSE_i),
+ * +inf when SSE_i == 0. */
+void mmsb_der_psnr_host(int32_t batch, int32_t height, int32_t width, const int64_t *capacity_bits,
+                        const int64_t *sse, double *der_out, double *psnr_out);
+
+const char *mmsb_status_string(mmsb_status status);
+
+/* Number of kernels the library launched since load (for the bench's gpu_launches claim). */
+uint64_t mmsb_kernel_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MMSB_H */

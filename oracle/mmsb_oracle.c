@@ -624,7 +624,8 @@ int orc_hide(int method, const uint8_t *E, int M, int N, const uint8_t k2[32], c
 }
 
 /* extraction with K2 only, no de-rotation (EMR P:839-840; LMR P:1063-1064).
- * Output: bytes [0, ceil(max(C-32,0)/8)) of msg_out hold the message bits [0,n) and zeros after. */
+ * Output: the first ceil(max(C-32,0)/32) 32-bit words (4-byte units) of msg_out hold the
+ * message bits [0,n) followed by zeros; bytes after that region are untouched. */
 int orc_extract(int method, const uint8_t *marked, int M, int N, const uint8_t k2[32], uint8_t *msg_out,
                 int64_t stride_bytes, int64_t *msg_bits_out)
 {
@@ -638,7 +639,7 @@ int orc_extract(int method, const uint8_t *marked, int M, int N, const uint8_t k
     int64_t z = 0;
     for (size_t r = 0; r < MN; r++) z += (l[r] == 0);
     int64_t C = (int64_t)bp * z;
-    int64_t region = C > 32 ? (C - 32 + 7) / 8 : 0;
+    int64_t region = C > 32 ? 4 * ((C - 32 + 31) / 32) : 0;
     if (region > stride_bytes) { free(l); return ORC_E_INVAL; }
     memset(msg_out, 0, (size_t)region);
     /* G: concatenated carried bits of the redundant pixels, D = G XOR KS2 */

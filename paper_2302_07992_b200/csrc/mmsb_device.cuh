@@ -1,0 +1,148 @@
+// mmsb_device.cuh -- device-side building blocks of the B200 hot path (sm_100a).
+//
+// Product code only: nothing here is shared with oracle/ (the CPU oracle re-derives every
+// step from the paper independently).  Citations: P:<line> = /root/reference/PAPER.md.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "mmsb_geo.h"
+
+namespace mmsb {
+
+// --------------------------------------------------------------------------------------
+// ChaCha20 block function (RFC 8439 §2.3).  The paper requires only "a cryptographically
+// secure stream cipher"; reading Q12 fixes ChaCha20 with nonce 0 and counter 0, so
+// byte r of the keystream is byte r%64 of block r/64: the stream is in counter form and any
+// position is reachable without generating the prefix ("jump-ahead" = block counter).
+// --------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t rotl32(uint32_t x, int n) { return __funnelshift_l(x, x, n); }
+
+#define MMSB_QR(a, b, c, d)                                                     \
+    a += b; d ^= a; d = rotl32(d, 16); c += d; b ^= c; b = rotl32(b, 12);       \
+    a += b; d ^= a; d = rotl32(d, 8);  c += d; b ^= c; b = rotl32(b, 7);
+
+__device__ __forceinline__ void chacha20_block(const uint32_t k[8], uint32_t counter, uint32_t o[16]) {
+    uint32_t x0 = 0x61707865u, x1 = 0x3320646eu, x2 = 0x79622d32u, x3 = 0x6b206574u;
+    uint32_t x4 = k[0], x5 = k[1], x6 = k[2], x7 = k[3], x8 = k[4], x9 = k[5], x10 = k[6], x11 = k[7];
+    uint32_t x12 = counter, x13 = 0, x14 = 0, x15 = 0;
+#pragma unroll
+    for (int i = 0; i < 10; i++) {
+        MMSB_QR(x0, x4, x8, x12) MMSB_QR(x1, x5, x9, x13) MMSB_QR(x2, x6, x10, x14) MMSB_QR(x3, x7, x11, x15)
+        MMSB_QR(x0, x5, x10, x15) MMSB_QR(x1, x6, x11, x12) MMSB_QR(x2, x7, x8, x13) MMSB_QR(x3, x4, x9, x14)
+    }
+    o[0] = x0 + 0x61707865u; o[1] = x1 + 0x3320646eu; o[2] = x2 + 0x79622d32u; o[3] = x3 + 0x6b206574u;
+    o[4] = x4 + k[0]; o[5] = x5 + k[1]; o[6] = x6 + k[2]; o[7] = x7 + k[3];
+    o[8] = x8 + k[4]; o[9] = x9 + k[5]; o[10] = x10 + k[6]; o[11] = x11 + k[7];
+    o[12] = x12 + counter; o[13] = x13; o[14] = x14; o[15] = x15;
+}
+
+__device__ __forceinline__ void load_key(const uint8_t *keys, int img, uint32_t k[8]) {
+    const uint4 *p = reinterpret_cast<const uint4 *>(keys + (size_t)img * 32);
+    uint4 a = __ldg(p), b = __ldg(p + 1);
+    k[0] = a.x; k[1] = a.y; k[2] = a.z; k[3] = a.w; k[4] = b.x; k[5] = b.y; k[6] = b.z; k[7] = b.w;
+}
+
+__device__ __forceinline__ uint32_t bswap32(uint32_t v) { return __byte_perm(v, 0, 0x0123); }
+
+// --------------------------------------------------------------------------------------
+// Multi-scale block rotation (eq. roration; de-rotation P:819-835).
+//
+// The forward pass at level e rotates each 2^e block clockwise by 90 deg * angle; a
+// one-turn clockwise rotation of an n-block sends offset (y, x) to (x, n-1-y).  Because
+// levels below e keep a pixel inside its 2^e block, every aligned 2^k sub-block with k <= e
+// moves rigidly: the composition over all levels maps aligned tiles onto aligned tiles
+// (DESIGN.md §5.2).  The kernels exploit this at two granularities: 2^tp tiles (upper
+// levels, one walk per tile) and 4x4 "cells" (levels 3..tp, one walk per cell); levels 1
+// and 2 act inside a cell on bytes held in registers (PRMT).
+// --------------------------------------------------------------------------------------
+
+// destination offset -> source offset under `a` clockwise turns of an (m1+1)-block
+__device__ __forceinline__ void inv_turn(int a, int m1, int &y, int &x) {
+    int oy = y, ox = x;
+    if (a == 1) { y = m1 - ox; x = oy; }
+    else if (a == 2) { y = m1 - oy; x = m1 - ox; }
+    else if (a == 3) { y = ox; x = m1 - oy; }
+}
+// source offset -> destination offset under `a` clockwise turns
+__device__ __forceinline__ void fwd_turn(int a, int m1, int &y, int &x) {
+    int oy = y, ox = x;
+    if (a == 1) { y = ox; x = m1 - oy; }
+    else if (a == 2) { y = m1 - oy; x = m1 - ox; }
+    else if (a == 3) { y = m1 - ox; x = oy; }
+}
+
+// A 4x4 cell of bytes: r[i] = row i, byte j = column j (little-endian).
+struct Cell { uint32_t r0, r1, r2, r3; };
+
+// transpose: out[i][j] = in[j][i]
+__device__ __forceinline__ Cell cell_transpose(Cell c) {
+    uint32_t u0 = __byte_perm(c.r0, c.r1, 0x5140);   // [r0.0 r1.0 r0.1 r1.1]
+    uint32_t u1 = __byte_perm(c.r2, c.r3, 0x5140);   // [r2.0 r3.0 r2.1 r3.1]
+    uint32_t v0 = __byte_perm(c.r0, c.r1, 0x7362);   // [r0.2 r1.2 r0.3 r1.3]
+    uint32_t v1 = __byte_perm(c.r2, c.r3, 0x7362);
+    Cell o;
+    o.r0 = __byte_perm(u0, u1, 0x5410);
+    o.r1 = __byte_perm(u0, u1, 0x7632);
+    o.r2 = __byte_perm(v0, v1, 0x5410);
+    o.r3 = __byte_perm(v0, v1, 0x7632);
+    return o;
+}
+
+// rotate the cell clockwise by 90 deg * r:  r odd = transpose + ...; built from transpose,
+// column reversal (byte reverse) and row reversal.
+//   r=1: out[i][j] = in[3-j][i]  = transpose, then reverse columns
+//   r=2: out[i][j] = in[3-i][3-j] = reverse rows and columns
+//   r=3: out[i][j] = in[j][3-i]  = transpose, then reverse rows
+__device__ __forceinline__ Cell cell_rot_cw(Cell c, int r) {
+    if (r & 1) c = cell_transpose(c);
+    const bool rev_cols = (r == 1) || (r == 2);
+    const bool rev_rows = (r == 2) || (r == 3);
+    if (rev_cols) {
+        c.r0 = __byte_perm(c.r0, 0, 0x0123); c.r1 = __byte_perm(c.r1, 0, 0x0123);
+        c.r2 = __byte_perm(c.r2, 0, 0x0123); c.r3 = __byte_perm(c.r3, 0, 0x0123);
+    }
+    if (rev_rows) {
+        uint32_t t = c.r0; c.r0 = c.r3; c.r3 = t;
+        t = c.r1; c.r1 = c.r2; c.r2 = t;
+    }
+    return c;
+}
+
+// Level-1 (2x2) clockwise rotations of the two 2x2 blocks held in a row pair (top, bot):
+// left block = bytes 0,1, right block = bytes 2,3; angles aL, aR.  PRMT indices: top row
+// bytes 0..3, bottom row bytes 4..7.  A 2x2 block [[a,b],[c,d]] turned clockwise once is
+// [[c,a],[d,b]].
+__device__ __forceinline__ void pair_rot_cw(uint32_t &top, uint32_t &bot, int aL, int aR) {
+    // nibble tables indexed by angle: (byte0 src, byte1 src) for the left block
+    const uint32_t TOPS = 0x51450410u;   // a0: 0,1  a1: 4,0  a2: 5,4  a3: 1,5
+    const uint32_t BOTS = 0x40011554u;   // a0: 4,5  a1: 5,1  a2: 1,0  a3: 0,4
+    uint32_t tl = (TOPS >> (8 * aL)) & 0xFF, tr = ((TOPS >> (8 * aR)) & 0xFF) + 0x22;
+    uint32_t bl = (BOTS >> (8 * aL)) & 0xFF, br = ((BOTS >> (8 * aR)) & 0xFF) + 0x22;
+    uint32_t nt = __byte_perm(top, bot, tl | (tr << 8));
+    uint32_t nb = __byte_perm(top, bot, bl | (br << 8));
+    top = nt;
+    bot = nb;
+}
+
+// angle of block (by, bx) of level e in a tile's angle record (2-bit fields, one u64 per row)
+__device__ __forceinline__ int rec_angle(const uint64_t *rec, const Geo &g, int e, int by, int bx) {
+    return (int)((rec[g.lvl_off[e] + by] >> (2 * bx)) & 3);
+}
+
+// 2-bit-field addition mod 4 (SWAR): per field (a + b) mod 4
+__device__ __forceinline__ uint64_t add2(uint64_t a, uint64_t b) {
+    return a ^ b ^ ((a & b & 0x5555555555555555ull) << 1);
+}
+
+// ------------------------------------------------------------------- memory ordering
+__device__ __forceinline__ void st_release(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+}  // namespace mmsb

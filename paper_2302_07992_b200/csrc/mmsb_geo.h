@@ -1,0 +1,64 @@
+// mmsb_geo.h -- shape-derived geometry shared by the host orchestration and the kernels.
+#pragma once
+#include <cstdint>
+
+namespace mmsb {
+
+constexpr int kChunk = 8192;        // raster pixels per scan chunk (embed / extract)
+constexpr int kScanThreads = 256;   // 2 rounds x 256 threads x 16 px
+constexpr int kRecSlots = 64;       // u64 slots of a tile's in-tile angle record
+
+struct Geo {
+    int method;          // 0 EMR, 1 LMR
+    int B;               // images in this launch group
+    int H, W, hlog, wlog;
+    long long HW;
+    int emax;            // floor(log2 min(H, W))                  (reading Q6)
+    int emin;            // 1 (EMR), min(4, emax) (LMR)            (Q10)
+    int tp;              // tile side 2^tp = min(64, min(H, W))
+    int T;
+    int tilesY, tilesX, ntiles;
+    int lvl_off[8];      // record slot of level e's first row (e = 1..tp)
+    int pyr_off[16];     // upper pyramid: counter offset of level e (tp < e <= emax), per image
+    int npyr;            // counters per image
+    int nchunks;         // scan chunks per image
+    int tile_log2;       // LMR coder tile side 2^t
+};
+
+inline int ilog2(long long v) {
+    int e = 0;
+    while ((2LL << e) <= v) e++;
+    return e;
+}
+
+inline bool make_geo(int method, int B, int H, int W, int tile_log2, Geo *g) {
+    if (B < 1 || H < 16 || W < 16 || H > 32768 || W > 32768) return false;
+    if ((H & (H - 1)) || (W & (W - 1))) return false;
+    if (method != 0 && method != 1) return false;
+    if (tile_log2 == 0) tile_log2 = 7;
+    if (tile_log2 < 3 || tile_log2 > 9) return false;
+    g->method = method;
+    g->B = B;
+    g->H = H; g->W = W;
+    g->hlog = ilog2(H); g->wlog = ilog2(W);
+    g->HW = (long long)H * W;
+    g->emax = g->hlog < g->wlog ? g->hlog : g->wlog;
+    g->emin = method == 0 ? 1 : (g->emax < 4 ? g->emax : 4);
+    g->tp = g->emax < 6 ? g->emax : 6;
+    g->T = 1 << g->tp;
+    g->tilesY = H >> g->tp;
+    g->tilesX = W >> g->tp;
+    g->ntiles = g->tilesY * g->tilesX;
+    int off = 0;
+    for (int e = 0; e < 8; e++) g->lvl_off[e] = 0;
+    for (int e = 1; e <= g->tp; e++) { g->lvl_off[e] = off; off += g->T >> e; }
+    int p = 0;
+    for (int e = 0; e < 16; e++) g->pyr_off[e] = 0;
+    for (int e = g->tp + 1; e <= g->emax; e++) { g->pyr_off[e] = p; p += (H >> e) * (W >> e); }
+    g->npyr = p;
+    g->nchunks = (int)((g->HW + kChunk - 1) / kChunk);
+    g->tile_log2 = tile_log2;
+    return true;
+}
+
+}  // namespace mmsb

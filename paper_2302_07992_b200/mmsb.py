@@ -1,0 +1,181 @@
+"""Thin Python binding of the C ABI in include/mmsb.h (argument marshalling only).
+
+Every step of the method runs in libmmsb.so's sm_100a kernels; torch provides device
+memory and the current stream.  There is no CPU fallback: if the library is missing the
+first call raises.  Names follow the ABI (and the paper's three parties).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import torch
+
+from . import build as _build
+
+EMR, LMR = 0, 1
+OK, E_INVAL, E_CAPACITY, E_INTEGRITY, E_BADCASE, E_CUDA, E_UNIMPLEMENTED, E_FORMAT = 0, 2, 3, 4, 5, 6, 7, 8
+
+_lib = None
+
+
+class _Shape(C.Structure):
+    _fields_ = [("method", C.c_int32), ("batch", C.c_int32), ("height", C.c_int32), ("width", C.c_int32),
+                ("tile_log2", C.c_int32)]
+
+
+class MmsbError(RuntimeError):
+    pass
+
+
+def lib():
+    """Loads the in-tree libmmsb.so (never a CPU substitute)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_build.LIB):
+            raise MmsbError(f"{_build.LIB} is missing: run __graft_entry__.build() (nvcc sm_100a) first")
+        L = C.CDLL(_build.LIB)
+        vp, sp = C.c_void_p, C.POINTER(_Shape)
+        L.mmsb_workspace_bytes.restype = C.c_size_t
+        L.mmsb_workspace_bytes.argtypes = [sp]
+        L.mmsb_content_owner_encode.restype = C.c_int
+        L.mmsb_content_owner_encode.argtypes = [sp, vp, vp, vp, vp, vp, vp, vp, C.c_size_t, vp]
+        L.mmsb_hider_embed.restype = C.c_int
+        L.mmsb_hider_embed.argtypes = [sp, vp, vp, vp, vp, C.c_int64, vp, vp, vp, C.c_size_t, vp]
+        L.mmsb_receiver_extract.restype = C.c_int
+        L.mmsb_receiver_extract.argtypes = [sp, vp, vp, vp, C.c_int64, vp, vp, vp, C.c_size_t, vp]
+        L.mmsb_receiver_recover.restype = C.c_int
+        L.mmsb_receiver_recover.argtypes = [sp, vp, vp, vp, vp, vp, C.c_size_t, vp]
+        L.mmsb_stats.restype = C.c_int
+        L.mmsb_stats.argtypes = [sp, vp, vp, vp, vp]
+        L.mmsb_der_psnr_host.restype = None
+        L.mmsb_der_psnr_host.argtypes = [C.c_int32, C.c_int32, C.c_int32, vp, vp, vp, vp]
+        L.mmsb_status_string.restype = C.c_char_p
+        L.mmsb_status_string.argtypes = [C.c_int]
+        L.mmsb_kernel_launches.restype = C.c_uint64
+        L.mmsb_kernel_launches.argtypes = []
+        _lib = L
+    return _lib
+
+
+def _shape(method: int, B: int, H: int, W: int, tile_log2: int = 7) -> _Shape:
+    return _Shape(method, B, H, W, tile_log2)
+
+
+def _ptr(t: torch.Tensor | None):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise MmsbError("mmsb: device tensors required (the product path has no CPU fallback)")
+    if not t.is_contiguous():
+        raise MmsbError("mmsb: contiguous tensors required")
+    return C.c_void_p(t.data_ptr())
+
+
+def _stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _check(rc: int, what: str):
+    if rc != OK:
+        raise MmsbError(f"{what}: {lib().mmsb_status_string(rc).decode()} ({rc})")
+
+
+def kernel_launches() -> int:
+    return int(lib().mmsb_kernel_launches())
+
+
+class Workspace:
+    """Caller-owned device scratch sized by mmsb_workspace_bytes (one per stream)."""
+
+    def __init__(self, method: int, B: int, H: int, W: int, tile_log2: int = 7, device=None):
+        self.shape = _shape(method, B, H, W, tile_log2)
+        n = lib().mmsb_workspace_bytes(C.byref(self.shape))
+        if n == 0:
+            raise MmsbError(f"unsupported shape method={method} B={B} H={H} W={W} t={tile_log2}")
+        self.buf = torch.empty(n, dtype=torch.uint8, device=device or "cuda")
+        self.nbytes = n
+
+
+def _ws(ws: Workspace | None, method, B, H, W, tile_log2, device):
+    if ws is None or (ws.shape.method, ws.shape.batch, ws.shape.height, ws.shape.width, ws.shape.tile_log2) != (
+            method, B, H, W, tile_log2):
+        ws = Workspace(method, B, H, W, tile_log2, device)
+    return ws
+
+
+def encode(method: int, images: torch.Tensor, k1: torch.Tensor, ws: Workspace | None = None, tile_log2: int = 7,
+           out: torch.Tensor | None = None):
+    """Content owner: returns (encrypted, b, capacity_bits, status) -- mmsb_content_owner_encode."""
+    B, H, W = images.shape
+    ws = _ws(ws, method, B, H, W, tile_log2, images.device)
+    enc = out if out is not None else torch.empty_like(images)
+    b = torch.empty(B, dtype=torch.int32, device=images.device)
+    cap = torch.empty(B, dtype=torch.int64, device=images.device)
+    st = torch.empty(B, dtype=torch.int32, device=images.device)
+    rc = lib().mmsb_content_owner_encode(C.byref(ws.shape), _ptr(images), _ptr(k1), _ptr(enc), _ptr(b), _ptr(cap),
+                                         _ptr(st), _ptr(ws.buf), ws.nbytes, _stream())
+    _check(rc, "mmsb_content_owner_encode")
+    return enc, b, cap, st
+
+
+def embed(method: int, encrypted: torch.Tensor, k2: torch.Tensor, msg: torch.Tensor, msg_bits: torch.Tensor,
+          ws: Workspace | None = None, tile_log2: int = 7, out: torch.Tensor | None = None):
+    """Data hider: returns (marked, status) -- mmsb_hider_embed."""
+    B, H, W = encrypted.shape
+    ws = _ws(ws, method, B, H, W, tile_log2, encrypted.device)
+    marked = out if out is not None else torch.empty_like(encrypted)
+    st = torch.empty(B, dtype=torch.int32, device=encrypted.device)
+    rc = lib().mmsb_hider_embed(C.byref(ws.shape), _ptr(encrypted), _ptr(k2), _ptr(msg), _ptr(msg_bits),
+                                msg.shape[1], _ptr(marked), _ptr(st), _ptr(ws.buf), ws.nbytes, _stream())
+    _check(rc, "mmsb_hider_embed")
+    return marked, st
+
+
+def extract(method: int, marked: torch.Tensor, k2: torch.Tensor, stride: int, ws: Workspace | None = None,
+            tile_log2: int = 7, out: torch.Tensor | None = None):
+    """Receiver with K2: returns (msg_bytes, msg_bits, status) -- mmsb_receiver_extract."""
+    B, H, W = marked.shape
+    ws = _ws(ws, method, B, H, W, tile_log2, marked.device)
+    msg = out if out is not None else torch.zeros(B, stride, dtype=torch.uint8, device=marked.device)
+    nb = torch.empty(B, dtype=torch.int64, device=marked.device)
+    st = torch.empty(B, dtype=torch.int32, device=marked.device)
+    rc = lib().mmsb_receiver_extract(C.byref(ws.shape), _ptr(marked), _ptr(k2), _ptr(msg), stride, _ptr(nb),
+                                     _ptr(st), _ptr(ws.buf), ws.nbytes, _stream())
+    _check(rc, "mmsb_receiver_extract")
+    return msg, nb, st
+
+
+def recover(method: int, marked: torch.Tensor, k1: torch.Tensor, ws: Workspace | None = None, tile_log2: int = 7,
+            out: torch.Tensor | None = None):
+    """Receiver with K1: returns (recovered, status) -- mmsb_receiver_recover."""
+    B, H, W = marked.shape
+    ws = _ws(ws, method, B, H, W, tile_log2, marked.device)
+    rec = out if out is not None else torch.empty_like(marked)
+    st = torch.empty(B, dtype=torch.int32, device=marked.device)
+    rc = lib().mmsb_receiver_recover(C.byref(ws.shape), _ptr(marked), _ptr(k1), _ptr(rec), _ptr(st), _ptr(ws.buf),
+                                     ws.nbytes, _stream())
+    _check(rc, "mmsb_receiver_recover")
+    return rec, st
+
+
+def stats(original: torch.Tensor, recovered: torch.Tensor, out: torch.Tensor | None = None):
+    """Per-image SSE (int64) -- mmsb_stats."""
+    B, H, W = original.shape
+    sh = _shape(EMR, B, H, W)
+    sse = out if out is not None else torch.empty(B, dtype=torch.int64, device=original.device)
+    rc = lib().mmsb_stats(C.byref(sh), _ptr(original), _ptr(recovered), _ptr(sse), _stream())
+    _check(rc, "mmsb_stats")
+    return sse
+
+
+def der_psnr(H: int, W: int, capacity_bits, sse):
+    """Host DER / PSNR from integers (mmsb_der_psnr_host)."""
+    import numpy as np
+
+    cap = np.ascontiguousarray(np.asarray(capacity_bits, dtype=np.int64))
+    s = np.ascontiguousarray(np.asarray(sse, dtype=np.int64))
+    der = np.zeros(len(cap), np.float64)
+    psnr = np.zeros(len(cap), np.float64)
+    lib().mmsb_der_psnr_host(len(cap), H, W, cap.ctypes.data, s.ctypes.data, der.ctypes.data, psnr.ctypes.data)
+    return der, psnr

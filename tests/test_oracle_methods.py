@@ -61,7 +61,8 @@ def test_emr_round_trip_and_lsb_only_loss(shape, kind):
         st3, out, nb = O.extract(O.EMR, Em, k2, S.msg_stride(*shape))
         assert st3 == O.OK and nb == n
         assert np.array_equal(_msg_bits(out, n), _msg_bits(msg, n))
-        assert not _msg_bits(out, 8 * ((C - 32 + 7) // 8))[n:].any()
+        assert not _msg_bits(out, 32 * ((C - 32 + 31) // 32))[n:].any()
+        assert not out[4 * ((C - 32 + 31) // 32):].any()       # region is whole 32-bit words
         st4, R = O.recover(O.EMR, Em, k1)
         assert st4 == O.OK
         assert np.array_equal(R >> 1, img >> 1)              # bits 1..7 exact
