@@ -52,7 +52,7 @@ typedef struct {
     int32_t batch;       /* images in the batch (>= 1)                                         */
     int32_t height;      /* M (power of two, 16..32768)                                        */
     int32_t width;       /* N (power of two, 16..32768)                                        */
-    int32_t tile_log2;   /* LMR map-coder tile side 2^t, t in [3, 9] (0 = default 7)           */
+    int32_t tile_log2;   /* LMR map-coder tile side 2^t, t in [3, 7] (0 = default 7)           */
 } mmsb_shape;
 
 /* Bytes of device workspace the four calls need for this shape. 0 if the shape is invalid. */
@@ -119,6 +119,14 @@ const char *mmsb_status_string(mmsb_status status);
 
 /* Number of kernels the library launched since load (for the bench's gpu_launches claim). */
 uint64_t mmsb_kernel_launches(void);
+
+/* Live per-kernel timing.  mmsb_profile_enable(1) clears the record and brackets every later
+ * kernel launch with CUDA events on its launch stream; mmsb_profile_enable(0) stops.  After the
+ * caller synchronises, mmsb_profile_read(k, ...) returns, for kernel class k in [0, K), its name,
+ * the summed event time in ms, the number of launches and the pixels they processed; the return
+ * value is K (the number of kernel classes), or < 0 for an invalid k / unfinished events. */
+void mmsb_profile_enable(int on);
+int mmsb_profile_read(int kernel, const char **name, double *total_ms, int64_t *launches, int64_t *units);
 
 #ifdef __cplusplus
 }

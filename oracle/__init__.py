@@ -62,10 +62,10 @@ def lib():
                 "orc_tile_decode": (None, [u8p, C.c_int, C.c_int, C.c_int, u8p]),
                 "orc_tile_count": (C.c_int, [C.c_int, C.c_int, C.c_int]),
                 "orc_encode": (C.c_int, [C.c_int, u8p, C.c_int, C.c_int, u8p, C.c_int, u8p, i32p, i64p]),
-                "orc_hide": (C.c_int, [C.c_int, u8p, C.c_int, C.c_int, u8p, u8p, C.c_int64, u8p]),
-                "orc_extract": (C.c_int, [C.c_int, u8p, C.c_int, C.c_int, u8p, u8p, C.c_int64, i64p]),
-                "orc_recover": (C.c_int, [C.c_int, u8p, C.c_int, C.c_int, u8p, u8p]),
-                "orc_capacity": (C.c_int, [C.c_int, u8p, C.c_int, C.c_int, i32p, i64p]),
+                "orc_hide": (C.c_int, [C.c_int, u8p, C.c_int, C.c_int, C.c_int, u8p, u8p, C.c_int64, u8p]),
+                "orc_extract": (C.c_int, [C.c_int, u8p, C.c_int, C.c_int, C.c_int, u8p, u8p, C.c_int64, i64p]),
+                "orc_recover": (C.c_int, [C.c_int, u8p, C.c_int, C.c_int, C.c_int, u8p, u8p]),
+                "orc_capacity": (C.c_int, [C.c_int, u8p, C.c_int, C.c_int, C.c_int, i32p, i64p]),
                 "orc_sse": (C.c_int64, [u8p, u8p, C.c_int64]),
                 "orc_der_psnr": (None, [C.c_int, C.c_int, C.c_int64, C.c_int64,
                                         C.POINTER(C.c_double), C.POINTER(C.c_double)]),
@@ -186,40 +186,40 @@ def encode(method: int, img: np.ndarray, k1: bytes, tile_log2: int = 7):
     return st, E, b.value, cap.value
 
 
-def hide(method: int, E: np.ndarray, k2: bytes, msg: np.ndarray, msg_bits: int):
+def hide(method: int, E: np.ndarray, k2: bytes, msg: np.ndarray, msg_bits: int, tile_log2: int = 7):
     E = _u8(E)
     M, N = E.shape
     out = np.zeros_like(E)
     m = _u8(msg) if len(msg) else np.zeros(1, np.uint8)
     k = _u8(bytearray(k2))
-    st = lib().orc_hide(method, _p(E), M, N, _p(k), _p(m), msg_bits, _p(out))
+    st = lib().orc_hide(method, _p(E), M, N, tile_log2, _p(k), _p(m), msg_bits, _p(out))
     return st, out
 
 
-def extract(method: int, marked: np.ndarray, k2: bytes, stride_bytes: int, fill: int = 0):
+def extract(method: int, marked: np.ndarray, k2: bytes, stride_bytes: int, fill: int = 0, tile_log2: int = 7):
     marked = _u8(marked)
     M, N = marked.shape
     out = np.full(stride_bytes, fill, np.uint8)
     nb = C.c_int64(0)
     k = _u8(bytearray(k2))
-    st = lib().orc_extract(method, _p(marked), M, N, _p(k), _p(out), stride_bytes, C.byref(nb))
+    st = lib().orc_extract(method, _p(marked), M, N, tile_log2, _p(k), _p(out), stride_bytes, C.byref(nb))
     return st, out, nb.value
 
 
-def recover(method: int, marked: np.ndarray, k1: bytes):
+def recover(method: int, marked: np.ndarray, k1: bytes, tile_log2: int = 7):
     marked = _u8(marked)
     M, N = marked.shape
     out = np.zeros_like(marked)
     k = _u8(bytearray(k1))
-    st = lib().orc_recover(method, _p(marked), M, N, _p(k), _p(out))
+    st = lib().orc_recover(method, _p(marked), M, N, tile_log2, _p(k), _p(out))
     return st, out
 
 
-def capacity(method: int, marked: np.ndarray):
+def capacity(method: int, marked: np.ndarray, tile_log2: int = 7):
     marked = _u8(marked)
     M, N = marked.shape
     b, cap = C.c_int32(0), C.c_int64(0)
-    st = lib().orc_capacity(method, _p(marked), M, N, C.byref(b), C.byref(cap))
+    st = lib().orc_capacity(method, _p(marked), M, N, tile_log2, C.byref(b), C.byref(cap))
     return st, b.value, cap.value
 
 

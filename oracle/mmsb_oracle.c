@@ -513,7 +513,7 @@ static int lmr_encode(const uint8_t *I, int M, int N, const uint8_t k1[32], int 
 }
 
 /* parses the MSB-plane header and decodes the rotated map (want_eta: also eta) */
-static int lmr_read_maps(const uint8_t *Em, int M, int N, int *b, uint8_t *l, uint8_t *eta)
+static int lmr_read_maps(const uint8_t *Em, int M, int N, int t_expected, int *b, uint8_t *l, uint8_t *eta)
 {
     int64_t MN = (int64_t)M * N, pos = 0;
 #define RD(nb) ({ uint32_t v_ = 0; for (int i_ = 0; i_ < (nb); i_++) v_ = (v_ << 1) | (Em[pos++] >> 7); v_; })
@@ -521,7 +521,8 @@ static int lmr_read_maps(const uint8_t *Em, int M, int N, int *b, uint8_t *l, ui
     int field = (int)RD(3);
     if (field == 7) return ORC_E_BADCASE;
     int t = (int)RD(4);
-    if (t < 3 || t > 9) return ORC_E_FORMAT;
+    /* t is shared protocol knowledge like the method (reading Q15); the header repeats it */
+    if (t < 3 || t > 9 || t != t_expected) return ORC_E_FORMAT;
     int T = orc_tile_count(M, N, t);
     if (7 + 32 * (int64_t)T > MN) return ORC_E_FORMAT;
     int *sz = (int *)malloc(sizeof(int) * 2 * T);
@@ -567,18 +568,18 @@ int orc_encode(int method, const uint8_t *I, int M, int N, const uint8_t k1[32],
     return ORC_E_INVAL;
 }
 
-static int read_map(int method, const uint8_t *Em, int M, int N, int *b, uint8_t *l, uint8_t *eta)
+static int read_map(int method, const uint8_t *Em, int M, int N, int t, int *b, uint8_t *l, uint8_t *eta)
 {
     if (method == ORC_EMR) return emr_read_map(Em, M, N, b, l);
-    return lmr_read_maps(Em, M, N, b, l, eta);
+    return lmr_read_maps(Em, M, N, t, b, l, eta);
 }
 
-int orc_capacity(int method, const uint8_t *marked, int M, int N, int32_t *b_out, int64_t *capacity_out)
+int orc_capacity(int method, const uint8_t *marked, int M, int N, int tile_log2, int32_t *b_out, int64_t *capacity_out)
 {
     size_t MN = (size_t)M * N;
     uint8_t *l = (uint8_t *)malloc(MN);
     int b = 0;
-    int st = read_map(method, marked, M, N, &b, l, NULL);
+    int st = read_map(method, marked, M, N, tile_log2, &b, l, NULL);
     int64_t z = 0;
     if (st == ORC_OK)
         for (size_t r = 0; r < MN; r++) z += (l[r] == 0);
@@ -591,14 +592,14 @@ int orc_capacity(int method, const uint8_t *marked, int M, int N, int32_t *b_out
 /* data hiding (EMR P:749-750; LMR P:990-991): frame F = BE32(n) || msg (Q17), encrypted with
  * the K2 keystream, written b (EMR) or b-1 (LMR) bits per redundant pixel in raster order of
  * the rotated domain, MSB first (Q18); unused capacity is left untouched (Q19). */
-int orc_hide(int method, const uint8_t *E, int M, int N, const uint8_t k2[32], const uint8_t *msg, int64_t msg_bits,
-             uint8_t *marked)
+int orc_hide(int method, const uint8_t *E, int M, int N, int tile_log2, const uint8_t k2[32], const uint8_t *msg,
+             int64_t msg_bits, uint8_t *marked)
 {
     size_t MN = (size_t)M * N;
     memcpy(marked, E, MN);
     uint8_t *l = (uint8_t *)malloc(MN);
     int b = 0;
-    int st = read_map(method, E, M, N, &b, l, NULL);
+    int st = read_map(method, E, M, N, tile_log2, &b, l, NULL);
     if (st != ORC_OK) { free(l); return st; }
     int bp = carried_bits(method, b);
     int64_t z = 0;
@@ -626,14 +627,14 @@ int orc_hide(int method, const uint8_t *E, int M, int N, const uint8_t k2[32], c
 /* extraction with K2 only, no de-rotation (EMR P:839-840; LMR P:1063-1064).
  * Output: the first ceil(max(C-32,0)/32) 32-bit words (4-byte units) of msg_out hold the
  * message bits [0,n) followed by zeros; bytes after that region are untouched. */
-int orc_extract(int method, const uint8_t *marked, int M, int N, const uint8_t k2[32], uint8_t *msg_out,
-                int64_t stride_bytes, int64_t *msg_bits_out)
+int orc_extract(int method, const uint8_t *marked, int M, int N, int tile_log2, const uint8_t k2[32],
+                uint8_t *msg_out, int64_t stride_bytes, int64_t *msg_bits_out)
 {
     size_t MN = (size_t)M * N;
     uint8_t *l = (uint8_t *)malloc(MN);
     int b = 0;
     *msg_bits_out = -1;
-    int st = read_map(method, marked, M, N, &b, l, NULL);
+    int st = read_map(method, marked, M, N, tile_log2, &b, l, NULL);
     if (st != ORC_OK) { free(l); return st; }
     int bp = carried_bits(method, b);
     int64_t z = 0;
@@ -674,12 +675,12 @@ int orc_extract(int method, const uint8_t *marked, int M, int N, const uint8_t k
 /* image recovery with K1 only (EMR P:819-837; LMR P:1060-1061): decrypt all bits (Q20),
  * restore the MSB plane from eta (LMR), de-rotate image and map(s), then restore the b MSBs
  * (EMR) or bits 2..b (LMR) row by row from omega = the last non-redundant pixel. */
-int orc_recover(int method, const uint8_t *marked, int M, int N, const uint8_t k1[32], uint8_t *out)
+int orc_recover(int method, const uint8_t *marked, int M, int N, int tile_log2, const uint8_t k1[32], uint8_t *out)
 {
     size_t MN = (size_t)M * N;
     uint8_t *l = (uint8_t *)malloc(MN), *eta = (uint8_t *)malloc(MN);
     int b = 0;
-    int st = read_map(method, marked, M, N, &b, l, method == ORC_LMR ? eta : NULL);
+    int st = read_map(method, marked, M, N, tile_log2, &b, l, method == ORC_LMR ? eta : NULL);
     if (st != ORC_OK) {
         memset(out, 0, MN);
         free(l); free(eta);

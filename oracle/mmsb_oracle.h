@@ -68,13 +68,14 @@ int orc_tile_count(int M, int N, int t);
 /* ---- the four calls (P:575, P:816-843 EMR; P:972-1067 LMR) ---- */
 int orc_encode(int method, const uint8_t *I, int M, int N, const uint8_t k1[32], int tile_log2,
                uint8_t *E, int32_t *b_out, int64_t *capacity_out);
-int orc_hide(int method, const uint8_t *E, int M, int N, const uint8_t k2[32],
+/* tile_log2: LMR coder tile side, shared protocol knowledge (must equal the header's t) */
+int orc_hide(int method, const uint8_t *E, int M, int N, int tile_log2, const uint8_t k2[32],
              const uint8_t *msg, int64_t msg_bits, uint8_t *marked);
-int orc_extract(int method, const uint8_t *marked, int M, int N, const uint8_t k2[32],
+int orc_extract(int method, const uint8_t *marked, int M, int N, int tile_log2, const uint8_t k2[32],
                 uint8_t *msg_out, int64_t stride_bytes, int64_t *msg_bits_out);
-int orc_recover(int method, const uint8_t *marked, int M, int N, const uint8_t k1[32], uint8_t *out);
+int orc_recover(int method, const uint8_t *marked, int M, int N, int tile_log2, const uint8_t k1[32], uint8_t *out);
 /* capacity C that the hider/receiver derive from a marked image (header + map) */
-int orc_capacity(int method, const uint8_t *marked, int M, int N, int32_t *b_out, int64_t *capacity_out);
+int orc_capacity(int method, const uint8_t *marked, int M, int N, int tile_log2, int32_t *b_out, int64_t *capacity_out);
 
 /* ---- statistics (P:630 DER, P:746 PSNR; Q23) ---- */
 int64_t orc_sse(const uint8_t *a, const uint8_t *b, int64_t n);

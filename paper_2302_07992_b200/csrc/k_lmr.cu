@@ -1,0 +1,518 @@
+// k_lmr.cu -- LMR-RDHEI specific kernels: the bi-level tile coder that stands in
+// for JBIG-KIT (builder-defined, reading Q16), the candidate walk until the coded maps
+// fit the first-MSB plane, the MSB-plane writer and the decoders used by
+// the hider, the K2 receiver and the K1 receiver.
+//
+// Coder (O15): tiles of side min(2^t, dim) coded independently in tile raster
+// order; 10-pixel causal tile-local context, MSB->LSB (0,-1) (0,-2) (-1,-2) (-1,-1) (-1,0)
+// (-1,+1) (-1,+2) (-2,-1) (-2,0) (-2,+1), out-of-tile pixels 0; per context a 16-bit
+// probability of a 0, p0 = 32768 initially, p0 += (65536-p0)>>4 after a 0, p0 -= p0>>4 after
+// a 1; carry-propagating range coder, 32-bit range, bound = (range>>16)*p0, renormalise below
+// 2^24 one byte at a time through a cache byte + 0xFF run, flush = 5 byte shifts; the
+// decoder reads bytes past the end of the tile's stream as 0.
+//
+// One GPU thread codes one tile (the coder is serial within a tile).  Each thread's model
+// (1024 x u16) lives in shared memory interleaved across the 32 lanes of the warp
+// (entry ctx of lane l at u16 index ctx*32 + l: at most 2-way bank conflicts).
+#include "mmsb_device.cuh"
+#include "mmsb_kernels.h"
+
+namespace mmsb {
+
+constexpr int kCoderThreads = 32;                 // one warp per CTA (smem-bound: 64 KB of models)
+constexpr int kRowWords = 6;                      // padded MSB-first row: 2 lead bits + <= 128 + pad
+
+__host__ __device__ inline int lmr_tile_side(int t, int dim) { return (1 << t) < dim ? (1 << t) : dim; }
+__host__ __device__ inline int lmr_tile_count(int H, int W, int t) {
+    const int th = lmr_tile_side(t, H), tw = lmr_tile_side(t, W);
+    return ((H + th - 1) / th) * ((W + tw - 1) / tw);
+}
+__host__ __device__ inline int lmr_tile_cap(int t, int H, int W) {   // >= 1.1 * raw + 64 bytes
+    const int n = lmr_tile_side(t, H) * lmr_tile_side(t, W);
+    return n / 8 + n / 64 + 64;
+}
+
+// context bits from the two previous rows: rows are MSB-first with pixel x at padded bit x+2
+__device__ __forceinline__ uint32_t row_window(const uint32_t *row, int pos, int nbits) {
+    const uint64_t w = ((uint64_t)row[pos >> 5] << 32) | row[(pos >> 5) + 1];
+    return (uint32_t)((w << (pos & 31)) >> (64 - nbits));
+}
+
+struct RcEnc {
+    uint64_t low;
+    uint32_t range;
+    uint32_t cache;
+    uint32_t cache_size;
+    uint8_t *out;
+    int n, cap;
+    __device__ __forceinline__ void put(uint32_t v) {
+        if (n < cap) out[n] = (uint8_t)v;
+        n++;
+    }
+    __device__ __forceinline__ void shift_low() {
+        if ((uint32_t)low < 0xFF000000u || (low >> 32) != 0) {
+            const uint32_t carry = (uint32_t)(low >> 32);
+            uint32_t temp = cache;
+            do {
+                put((temp + carry) & 0xFFu);
+                temp = 0xFFu;
+            } while (--cache_size != 0);
+            cache = ((uint32_t)low >> 24) & 0xFFu;
+        }
+        cache_size++;
+        low = (uint64_t)((uint32_t)low << 8);
+    }
+};
+
+// ======================================================================================
+// coder_encode_kernel: one thread per (image, plane slot, coder tile).
+//   slot 0 = rotated eta (MSB of I_r, eq. MSB_map) -- wave 0 only;
+//   slot 1 = rotated location map L_b = [c_r < b] of candidate order[wave].
+// Images already decided (state != 0) are skipped.
+// ======================================================================================
+__global__ void __launch_bounds__(kCoderThreads) coder_encode_kernel(Geo g, int wave, const uint8_t *__restrict__ ceta,
+                                                                     const LmrPlan *__restrict__ plan,
+                                                                     uint8_t *__restrict__ streams,
+                                                                     int32_t *__restrict__ sizes) {
+    extern __shared__ uint16_t p0s[];                                  // [1024][32]
+    __shared__ uint32_t rows[kCoderThreads][3][kRowWords];
+    const int lane = threadIdx.x;
+    const int Tc = lmr_tile_count(g.H, g.W, g.tile_log2);
+    const int nslots = wave == 0 ? 2 : 1;
+    const long long gid = (long long)blockIdx.x * kCoderThreads + lane;
+    const long long total = (long long)g.B * nslots * Tc;
+    const bool active0 = gid < total;
+    const int img = active0 ? (int)(gid / ((long long)nslots * Tc)) : 0;
+    const int rem = active0 ? (int)(gid % ((long long)nslots * Tc)) : 0;
+    const int slot = wave == 0 ? rem / Tc : 1;
+    const int tile = rem % Tc;
+    const LmrPlan pl = plan[img];
+    const bool active = active0 && pl.state == 0;
+    if (!__any_sync(0xffffffffu, active)) return;
+
+    const int th = lmr_tile_side(g.tile_log2, g.H), tw = lmr_tile_side(g.tile_log2, g.W);
+    const int TN = (g.W + tw - 1) / tw;
+    const int y0 = (tile / TN) * th, x0 = (tile % TN) * tw;
+    const int h = g.H - y0 < th ? g.H - y0 : th, w = g.W - x0 < tw ? g.W - x0 : tw;
+    const int b = slot == 0 ? 0 : pl.order[wave];
+    const int cap = lmr_tile_cap(g.tile_log2, g.H, g.W);
+
+    for (int c = 0; c < 1024; c++) p0s[c * 32 + lane] = 32768;
+    uint32_t(*R)[kRowWords] = rows[lane];
+    for (int r = 0; r < 3; r++)
+        for (int k = 0; k < kRowWords; k++) R[r][k] = 0;
+
+    RcEnc e{0, 0xFFFFFFFFu, 0, 1, streams + (((size_t)img * 2 + slot) * Tc + tile) * cap, 0, cap};
+    const uint8_t *src = ceta + (size_t)img * g.HW;
+    if (active) {
+        for (int y = 0; y < h; y++) {
+            uint32_t *cur = R[y % 3];
+            const uint32_t *p1 = R[(y + 2) % 3], *p2 = R[(y + 1) % 3];     // rows y-1, y-2 (zero when absent)
+            for (int k = 0; k < kRowWords; k++) cur[k] = 0;
+            uint32_t hist2 = 0;                                            // bits (0,-1), (0,-2)
+            const uint8_t *rowp = src + (size_t)(y0 + y) * g.W + x0;
+            for (int x = 0; x < w; x++) {
+                const uint8_t v = rowp[x];
+                const uint32_t bit = slot == 0 ? (uint32_t)(v >> 7) : (uint32_t)((v & 0xF) < b);
+                const uint32_t ctx = ((hist2 & 1u) << 9) | ((hist2 >> 1) << 8) |
+                                     (row_window(p1, x, 5) << 3) | row_window(p2, x + 1, 3);
+                uint16_t *pp = &p0s[ctx * 32 + lane];
+                const uint32_t p = *pp;
+                const uint32_t bound = (e.range >> 16) * p;
+                if (bit == 0) {
+                    e.range = bound;
+                    *pp = (uint16_t)(p + ((65536u - p) >> 4));
+                } else {
+                    e.low += bound;
+                    e.range -= bound;
+                    *pp = (uint16_t)(p - (p >> 4));
+                }
+                while (e.range < (1u << 24)) {
+                    e.range <<= 8;
+                    e.shift_low();
+                }
+                hist2 = ((hist2 << 1) | bit) & 3u;
+                if (bit) cur[(x + 2) >> 5] |= 0x80000000u >> ((x + 2) & 31);
+            }
+            // keep the two padding words beyond the row zero for the next rows' windows
+        }
+        for (int i = 0; i < 5; i++) e.shift_low();
+        sizes[((size_t)img * 2 + slot) * Tc + tile] = (e.n <= cap && e.n <= 65535) ? e.n : -1;
+    }
+}
+
+// ======================================================================================
+// lmr_plan_kernel: candidate order per image from the label histogram: b in [2,8] ordered by
+// (b-1) * zeros(b) descending, ties -> smaller b (readings Q5, Q22).
+// ======================================================================================
+__global__ void lmr_plan_kernel(Geo g, const uint32_t *__restrict__ hist, LmrPlan *__restrict__ plan) {
+    const int img = blockIdx.x * blockDim.x + threadIdx.x;
+    if (img >= g.B) return;
+    LmrPlan p{};
+    long long val[9];
+    for (int b = 2; b <= 8; b++) val[b] = (long long)(b - 1) * (g.HW - (long long)hist[img * 8 + b]);
+    int ord[7];
+    for (int k = 0; k < 7; k++) ord[k] = k + 2;
+    for (int k = 1; k < 7; k++) {
+        const int b = ord[k];
+        int j = k - 1;
+        while (j >= 0 && val[ord[j]] < val[b]) { ord[j + 1] = ord[j]; j--; }
+        ord[j + 1] = b;
+    }
+    for (int k = 0; k < 7; k++) p.order[k] = (int8_t)ord[k];
+    p.state = 0;
+    p.b = 0;
+    p.K = 0;
+    plan[img] = p;
+}
+
+// ======================================================================================
+// lmr_fit_kernel: one warp per image after wave `wave`: the first candidate for which
+// 7 + 16 (T_eta + T_L) + 8 (bytes_eta + bytes_L) <= M N decides b; otherwise the
+// image stays undecided, and after the last candidate it is a bad case.
+// Also produces the exclusive byte offsets of the streams (eta tiles, then map tiles).
+// ======================================================================================
+__global__ void lmr_fit_kernel(Geo g, int wave, const int32_t *__restrict__ sizes, LmrPlan *__restrict__ plan,
+                               int32_t *__restrict__ offsets) {
+    const int img = blockIdx.x, lane = threadIdx.x;
+    if (plan[img].state != 0) return;
+    const int Tc = lmr_tile_count(g.H, g.W, g.tile_log2);
+    const int32_t *sz = sizes + (size_t)img * 2 * Tc;
+    long long tot = 0;
+    int bad = 0;
+    for (int k = lane; k < 2 * Tc; k += 32) {
+        const int s = sz[k];
+        if (s < 0) bad = 1;
+        tot += s;
+    }
+#pragma unroll
+    for (int s2 = 16; s2 > 0; s2 >>= 1) {
+        tot += __shfl_xor_sync(0xffffffffu, tot, s2);
+        bad |= __shfl_xor_sync(0xffffffffu, bad, s2);
+    }
+    const long long K = 7 + 32ll * Tc + 8 * tot;
+    const bool fits = !bad && K <= g.HW;
+    if (fits) {
+        // exclusive prefix of the 2 Tc stream sizes (eta tiles then map tiles), warp-serial chunks
+        int run = 0;
+        for (int k0 = 0; k0 < 2 * Tc; k0 += 32) {
+            const int k = k0 + lane;
+            const int s = k < 2 * Tc ? sz[k] : 0;
+            int v = s;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, v, d);
+                if (lane >= d) v += t;
+            }
+            if (k < 2 * Tc) offsets[(size_t)img * 2 * Tc + k] = run + v - s;
+            run += __shfl_sync(0xffffffffu, v, 31);
+        }
+    }
+    if (lane == 0) {
+        LmrPlan p = plan[img];
+        if (fits) { p.state = 1; p.b = p.order[wave]; p.K = K; }
+        else if (wave == 6) { p.state = 2; p.b = 0; p.K = 0; }
+        plan[img] = p;
+    }
+}
+
+// ======================================================================================
+// lmr_msb_write_kernel: writes the first-MSB plane of I_e (layout reading Q15):
+//   [b-2: 3 bits][t: 4 bits][16-bit byte lengths of the eta tiles][... of the map tiles]
+//   [eta tile bytes][map tile bytes], MSB first, pixel r <- stream bit r for r < K; the
+//   remaining MSBs keep I_r XOR s.  Bad case: the b-field 7 (bits r = 0..2 set).
+// One thread per 16 pixels; the stream bits of its pixels are gathered from the tile slots.
+// ======================================================================================
+__device__ __forceinline__ uint32_t stream_bit(const Geo &g, int Tc, const LmrPlan &pl, const int32_t *sz,
+                                               const int32_t *off, const uint8_t *slots, int cap, long long r) {
+    if (r < 3) return ((uint32_t)(pl.b - 2) >> (2 - r)) & 1u;
+    if (r < 7) return ((uint32_t)g.tile_log2 >> (6 - r)) & 1u;
+    const long long hdr = 7 + 32ll * Tc;
+    if (r < hdr) {
+        const int k = (int)((r - 7) >> 4), bi = (int)((r - 7) & 15);
+        return ((uint32_t)sz[k] >> (15 - bi)) & 1u;
+    }
+    const long long q = r - hdr;
+    const long long byte = q >> 3;
+    // locate the stream holding `byte` (binary search over the exclusive offsets)
+    int lo = 0, hi = 2 * Tc - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (off[mid] <= byte) lo = mid; else hi = mid - 1;
+    }
+    const int k = lo;
+    const int slot = k < Tc ? 0 : 1, tile = k < Tc ? k : k - Tc;
+    const uint8_t v = slots[((size_t)slot * Tc + tile) * cap + (byte - off[k])];
+    return (v >> (7 - (q & 7))) & 1u;
+}
+
+__global__ void __launch_bounds__(256) lmr_msb_write_kernel(Geo g, const LmrPlan *__restrict__ plan,
+                                                            const int32_t *__restrict__ sizes,
+                                                            const int32_t *__restrict__ offsets,
+                                                            const uint8_t *__restrict__ streams,
+                                                            const uint32_t *__restrict__ hist,
+                                                            uint8_t *__restrict__ enc, int32_t *__restrict__ b_out,
+                                                            int64_t *__restrict__ cap_out,
+                                                            int32_t *__restrict__ status) {
+    const int img = blockIdx.y;
+    const LmrPlan pl = plan[img];
+    const int Tc = lmr_tile_count(g.H, g.W, g.tile_log2);
+    const int cap = lmr_tile_cap(g.tile_log2, g.H, g.W);
+    uint8_t *E = enc + (size_t)img * g.HW;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (pl.state == 1) {
+            b_out[img] = pl.b;
+            cap_out[img] = (long long)(pl.b - 1) * (g.HW - (long long)hist[img * 8 + pl.b]);
+            status[img] = 0;
+        } else {
+            b_out[img] = 0;
+            cap_out[img] = 0;
+            status[img] = 5;
+            E[0] |= 0x80; E[1] |= 0x80; E[2] |= 0x80;           // b-field 7: bad case
+        }
+    }
+    if (pl.state != 1) return;
+    const int32_t *sz = sizes + (size_t)img * 2 * Tc;
+    const int32_t *off = offsets + (size_t)img * 2 * Tc;
+    const uint8_t *slots = streams + (size_t)img * 2 * Tc * cap;
+    for (long long p = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * 16; p < pl.K;
+         p += (long long)gridDim.x * blockDim.x * 16) {
+        uint4 u = *reinterpret_cast<const uint4 *>(E + p);
+        uint32_t wv[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+        for (int i = 0; i < 16; i++) {
+            const long long r = p + i;
+            if (r < pl.K) {
+                const uint32_t bit = stream_bit(g, Tc, pl, sz, off, slots, cap, r);
+                const int sh = 8 * (i & 3) + 7;
+                wv[i >> 2] = (wv[i >> 2] & ~(1u << sh)) | (bit << sh);
+            }
+        }
+        *reinterpret_cast<uint4 *>(E + p) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+    }
+}
+
+// ======================================================================================
+// Decoding side.
+// lmr_pack_kernel: MSB plane of the marked image -> bytes (stream bit r = MSB of pixel r).
+// ======================================================================================
+__global__ void __launch_bounds__(256) lmr_pack_kernel(long long HW, int B, const uint8_t *__restrict__ in,
+                                                       uint8_t *__restrict__ mbuf) {
+    const long long n16 = (long long)B * HW / 16;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += (long long)gridDim.x * blockDim.x) {
+        const uint4 u = __ldg(reinterpret_cast<const uint4 *>(in) + i);
+        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+        uint32_t out = 0;
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            const uint32_t m = (w[k] >> 7) & 0x01010101u;                 // MSB of each byte
+            const uint32_t b4 = ((m * 0x08040201u) >> 24) & 0xFu;           // pixel 0 -> bit 3
+            out |= b4 << (12 - 4 * k);
+        }
+        // out: 16 bits, pixel 0 at bit 15 -> two stream bytes
+        reinterpret_cast<uint16_t *>(mbuf)[i] = (uint16_t)(((out >> 8) & 0xFFu) | ((out & 0xFFu) << 8));
+    }
+}
+
+// lmr_header_kernel: one warp per image parses b, t and the 2 T tile lengths; validates the
+// layout (FORMAT) or the bad-case marker (BADCASE); exclusive offsets of the streams.
+__device__ __forceinline__ uint32_t mbuf_bits(const uint8_t *m, long long pos, int n) {
+    uint32_t v = 0;
+    for (int i = 0; i < n; i++) v = (v << 1) | ((m[(pos + i) >> 3] >> (7 - ((pos + i) & 7))) & 1u);
+    return v;
+}
+
+__global__ void lmr_header_kernel(Geo g, const uint8_t *__restrict__ mbuf, int32_t *__restrict__ lmr_b,
+                                  int32_t *__restrict__ lmr_t, int32_t *__restrict__ offsets,
+                                  int32_t *__restrict__ sizes, int32_t *__restrict__ status,
+                                  int64_t *__restrict__ msg_bits_out) {
+    const int img = blockIdx.x, lane = threadIdx.x;
+    const uint8_t *m = mbuf + (size_t)img * (g.HW / 8);
+    const int field = (int)mbuf_bits(m, 0, 3), t = (int)mbuf_bits(m, 3, 4);
+    int st = 0;
+    if (field == 7) st = 5;
+    else if (t != g.tile_log2) st = 8;           // t is shared protocol knowledge (reading Q15)
+    int Tc = 0;
+    if (!st) {
+        Tc = lmr_tile_count(g.H, g.W, t);
+        if (7 + 32ll * Tc > g.HW) st = 8;
+    }
+    long long run = 0;
+    if (!st) {
+        for (int k0 = 0; k0 < 2 * Tc; k0 += 32) {
+            const int k = k0 + lane;
+            const int s = k < 2 * Tc ? (int)mbuf_bits(m, 7 + 16ll * k, 16) : 0;
+            int v = s;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int tt = __shfl_up_sync(0xffffffffu, v, d);
+                if (lane >= d) v += tt;
+            }
+            if (k < 2 * Tc) {
+                offsets[(size_t)img * 2 * g.ntiles_coder + k] = (int)run + v - s;
+                sizes[(size_t)img * 2 * g.ntiles_coder + k] = s;
+            }
+            run += __shfl_sync(0xffffffffu, v, 31);
+        }
+        if (7 + 32ll * Tc + 8 * run > g.HW) st = 8;
+    }
+    if (lane == 0) {
+        lmr_b[img] = st ? 0 : field + 2;
+        lmr_t[img] = st ? 0 : t;
+        if (st) {
+            status[img] = st;
+            if (msg_bits_out) msg_bits_out[img] = -1;
+        }
+    }
+}
+
+// coder_decode_kernel: one thread per (image, plane, tile); plane 0 = eta (recover only),
+// plane 1 = map.  Decoded bits go to packed planes (bit x&31 of word (y W + x) >> 5).
+__global__ void __launch_bounds__(kCoderThreads) coder_decode_kernel(Geo g, int want_eta, const uint8_t *__restrict__ mbuf,
+                                                                     const int32_t *__restrict__ lmr_b,
+                                                                     const int32_t *__restrict__ lmr_t,
+                                                                     const int32_t *__restrict__ offsets,
+                                                                     const int32_t *__restrict__ sizes,
+                                                                     uint32_t *__restrict__ eta_bits,
+                                                                     uint32_t *__restrict__ map_bits) {
+    extern __shared__ uint16_t p0s[];
+    __shared__ uint32_t rows[kCoderThreads][3][kRowWords];
+    const int lane = threadIdx.x;
+    const int TcM = g.ntiles_coder;
+    const int nplanes = want_eta ? 2 : 1;
+    const long long gid = (long long)blockIdx.x * kCoderThreads + lane;
+    const long long total = (long long)g.B * nplanes * TcM;
+    bool active = gid < total;
+    const int img = active ? (int)(gid / ((long long)nplanes * TcM)) : 0;
+    const int rem = active ? (int)(gid % ((long long)nplanes * TcM)) : 0;
+    const int plane = want_eta ? rem / TcM : 1;
+    const int tile = rem % TcM;
+    const int b = lmr_b[img], t = lmr_t[img];
+    int Tc = 0;
+    if (active && b >= 2) Tc = lmr_tile_count(g.H, g.W, t);
+    active = active && b >= 2 && tile < Tc;
+    if (!__any_sync(0xffffffffu, active)) return;
+
+    const int th = lmr_tile_side(t > 0 ? t : 7, g.H), tw = lmr_tile_side(t > 0 ? t : 7, g.W);
+    const int TN = (g.W + tw - 1) / tw;
+    const int y0 = (tile / TN) * th, x0 = (tile % TN) * tw;
+    const int h = g.H - y0 < th ? g.H - y0 : th, w = g.W - x0 < tw ? g.W - x0 : tw;
+
+    for (int c = 0; c < 1024; c++) p0s[c * 32 + lane] = 32768;
+    uint32_t(*R)[kRowWords] = rows[lane];
+    for (int r = 0; r < 3; r++)
+        for (int k = 0; k < kRowWords; k++) R[r][k] = 0;
+    if (!active) return;
+
+    const int k = (plane == 0 ? 0 : Tc) + tile;
+    const int nbytes = sizes[(size_t)img * 2 * TcM + k];
+    const long long bit0 = 7 + 32ll * Tc + 8ll * offsets[(size_t)img * 2 * TcM + k];
+    const uint8_t *m = mbuf + (size_t)img * (g.HW / 8);
+    int pos = 0;
+    auto next = [&]() -> uint32_t {
+        uint32_t v = 0;
+        if (pos < nbytes) {
+            const long long bb = bit0 + 8ll * pos;
+            const uint32_t hi = m[bb >> 3], lo = m[(bb >> 3) + 1];
+            v = (((hi << 8) | lo) >> (8 - (bb & 7))) & 0xFFu;
+        }
+        pos++;
+        return v;
+    };
+    uint32_t range = 0xFFFFFFFFu, code = 0;
+    for (int i = 0; i < 5; i++) code = (code << 8) | next();
+    uint32_t *plane_out = plane == 0 ? eta_bits : map_bits;
+    for (int y = 0; y < h; y++) {
+        uint32_t *cur = R[y % 3];
+        const uint32_t *p1 = R[(y + 2) % 3], *p2 = R[(y + 1) % 3];
+        for (int kk = 0; kk < kRowWords; kk++) cur[kk] = 0;
+        uint32_t hist2 = 0, acc = 0;
+        const long long rowbit = (long long)img * g.HW + (long long)(y0 + y) * g.W + x0;
+        for (int x = 0; x < w; x++) {
+            const uint32_t ctx = ((hist2 & 1u) << 9) | ((hist2 >> 1) << 8) | (row_window(p1, x, 5) << 3) |
+                                 row_window(p2, x + 1, 3);
+            uint16_t *pp = &p0s[ctx * 32 + lane];
+            const uint32_t p = *pp;
+            const uint32_t bound = (range >> 16) * p;
+            uint32_t bit;
+            if (code < bound) {
+                range = bound;
+                bit = 0;
+                *pp = (uint16_t)(p + ((65536u - p) >> 4));
+            } else {
+                code -= bound;
+                range -= bound;
+                bit = 1;
+                *pp = (uint16_t)(p - (p >> 4));
+            }
+            while (range < (1u << 24)) {
+                range <<= 8;
+                code = (code << 8) | next();
+            }
+            hist2 = ((hist2 << 1) | bit) & 3u;
+            if (bit) cur[(x + 2) >> 5] |= 0x80000000u >> ((x + 2) & 31);
+            acc |= bit << (x & 31);
+            if ((x & 31) == 31 || x == w - 1) {
+                const long long wb = rowbit + (x & ~31);
+                if ((w & 31) == 0) plane_out[wb >> 5] = acc;
+                else atomicOr(plane_out + (wb >> 5), acc << (wb & 31));
+                acc = 0;
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------- launchers
+int lmr_tile_cap_host(int t, int H, int W) { return lmr_tile_cap(t, H, W); }
+
+static size_t coder_smem() { return 1024 * 32 * sizeof(uint16_t); }
+
+void lmr_set_smem_attrs() {
+    static bool done = false;
+    if (done) return;
+    cudaFuncSetAttribute(coder_encode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)coder_smem());
+    cudaFuncSetAttribute(coder_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)coder_smem());
+    done = true;
+}
+
+void launch_lmr_plan(const Geo &g, const uint32_t *hist, LmrPlan *plan, cudaStream_t st) {
+    lmr_plan_kernel<<<(g.B + 127) / 128, 128, 0, st>>>(g, hist, plan);
+}
+
+void launch_coder_encode(const Geo &g, int wave, const uint8_t *ceta, const LmrPlan *plan, uint8_t *streams,
+                         int32_t *sizes, cudaStream_t st) {
+    lmr_set_smem_attrs();
+    const int Tc = lmr_tile_count(g.H, g.W, g.tile_log2);
+    const long long total = (long long)g.B * (wave == 0 ? 2 : 1) * Tc;
+    const unsigned grid = (unsigned)((total + kCoderThreads - 1) / kCoderThreads);
+    coder_encode_kernel<<<grid, kCoderThreads, coder_smem(), st>>>(g, wave, ceta, plan, streams, sizes);
+}
+
+void launch_lmr_fit(const Geo &g, int wave, const int32_t *sizes, LmrPlan *plan, int32_t *offsets, cudaStream_t st) {
+    lmr_fit_kernel<<<g.B, 32, 0, st>>>(g, wave, sizes, plan, offsets);
+}
+
+void launch_lmr_msb_write(const Geo &g, const LmrPlan *plan, const int32_t *sizes, const int32_t *offsets,
+                          const uint8_t *streams, const uint32_t *hist, uint8_t *enc, int32_t *b_out, int64_t *cap_out,
+                          int32_t *status, cudaStream_t st) {
+    const long long n16 = g.HW / 16;
+    int bx = (int)((n16 + 255) / 256);
+    if (bx > 64) bx = 64;
+    dim3 grid(bx, g.B);
+    lmr_msb_write_kernel<<<grid, 256, 0, st>>>(g, plan, sizes, offsets, streams, hist, enc, b_out, cap_out, status);
+}
+
+void launch_lmr_decode(const Geo &g, bool want_eta, const uint8_t *marked, uint8_t *mbuf, int32_t *lmr_b,
+                       int32_t *lmr_t, int32_t *offsets, int32_t *sizes, uint32_t *eta_bits, uint32_t *map_bits,
+                       int32_t *status, int64_t *msg_bits_out, cudaStream_t st) {
+    lmr_set_smem_attrs();
+    const long long n16 = (long long)g.B * g.HW / 16;
+    lmr_pack_kernel<<<(unsigned)((n16 + 255) / 256 < 148 * 16 ? (n16 + 255) / 256 : 148 * 16), 256, 0, st>>>(
+        g.HW, g.B, marked, mbuf);
+    lmr_header_kernel<<<g.B, 32, 0, st>>>(g, mbuf, lmr_b, lmr_t, offsets, sizes, status, msg_bits_out);
+    const long long total = (long long)g.B * (want_eta ? 2 : 1) * g.ntiles_coder;
+    coder_decode_kernel<<<(unsigned)((total + kCoderThreads - 1) / kCoderThreads), kCoderThreads, coder_smem(), st>>>(
+        g, want_eta ? 1 : 0, mbuf, lmr_b, lmr_t, offsets, sizes, eta_bits, map_bits);
+}
+
+}  // namespace mmsb

@@ -13,7 +13,7 @@
 namespace mmsb {
 
 constexpr unsigned long long kFlagAgg = 1ull << 62, kFlagInc = 2ull << 62, kValMask = (1ull << 62) - 1;
-constexpr int kKbufWords = 8192 * 7 / 32 + 64;     // bits of one chunk + block alignment + pad
+constexpr int kKbufWords = kChunk * 7 / 32 + 64;   // bits of one chunk + block alignment + pad
 
 __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t x, uint32_t *wsum, uint32_t &total) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -57,8 +57,96 @@ __device__ __forceinline__ uint32_t zero_mask16(const uint4 &u, long long p, lon
     }
 }
 
+// ---- per-thread bit streams of 16 pixels, specialised on b' (bits per redundant pixel) and
+// on the bit position of the carried field (SHIFT = 8 - b for EMR, 7 - b' for LMR).
+
+// embed: the zero pixels of mm receive consecutive b'-bit groups of the frame bits held in
+// kbuf (big-endian bit order), starting at relative bit `rel`; bits at or past `fend` are
+// not written (a partially filled last pixel keeps its remaining bits, reading Q19).
+template <int BP, int SHIFT>
+__device__ __forceinline__ void embed16(uint32_t w[4], uint32_t mm, const uint32_t *kbuf, long long rel,
+                                        long long fend) {
+    const int cnt = __popc(mm);
+    if (!cnt || rel >= fend) return;
+    constexpr uint32_t FM = ((1u << BP) - 1u) << SHIFT;
+    if (rel + (long long)cnt * BP <= fend) {
+        int wi = (int)(rel >> 5);
+        const int off = (int)(rel & 31);
+        unsigned long long win = (((unsigned long long)kbuf[wi] << 32) | kbuf[wi + 1]) << off;
+        int avail = 64 - off;
+        wi += 2;
+#pragma unroll
+        for (int i = 0; i < 16; i++) {
+            if ((mm >> i) & 1u) {
+                if (avail < BP) {
+                    win |= (unsigned long long)kbuf[wi++] << (32 - avail);
+                    avail += 32;
+                }
+                const uint32_t val = (uint32_t)(win >> (64 - BP));
+                w[i >> 2] = (w[i >> 2] & ~(FM << (8 * (i & 3)))) | (val << (SHIFT + 8 * (i & 3)));
+                win <<= BP;
+                avail -= BP;
+            }
+        }
+    } else {
+        long long k = rel;
+#pragma unroll
+        for (int i = 0; i < 16; i++) {
+            if (((mm >> i) & 1u) && k < fend) {
+                const int nb = (fend - k) < BP ? (int)(fend - k) : BP;
+                const int wv = (int)(k >> 5), off = (int)(k & 31);
+                const unsigned long long win = ((unsigned long long)kbuf[wv] << 32) | kbuf[wv + 1];
+                const uint32_t val = (uint32_t)(win >> (64 - off - BP)) & ((1u << BP) - 1u);
+                const uint32_t msk = (((1u << nb) - 1u) << (BP - nb)) << SHIFT;
+                w[i >> 2] = (w[i >> 2] & ~(msk << (8 * (i & 3)))) | (((val << SHIFT) & msk) << (8 * (i & 3)));
+            }
+            if ((mm >> i) & 1u) k += BP;
+        }
+    }
+}
+
+// extract: the zero pixels' b'-bit fields are appended in raster order and ORed into kbuf at
+// relative bit `rel`; the first and the last (partial) words are shared with the neighbouring
+// threads (shared-memory atomics), the words in between belong to this thread alone.
+template <int BP, int SHIFT>
+__device__ __forceinline__ void extract16(const uint32_t w[4], uint32_t mm, uint32_t *kbuf, long long rel) {
+    if (!mm) return;
+    int wi = (int)(rel >> 5);
+    int nacc = (int)(rel & 31);                 // leading pad (zeros) up to the word boundary
+    unsigned long long acc = 0;
+    bool first = true;
+#pragma unroll
+    for (int i = 0; i < 16; i++) {
+        if ((mm >> i) & 1u) {
+            const uint32_t val = (w[i >> 2] >> (8 * (i & 3) + SHIFT)) & ((1u << BP) - 1u);
+            acc = (acc << BP) | val;
+            nacc += BP;
+            if (nacc >= 32) {
+                const uint32_t word = (uint32_t)(acc >> (nacc - 32));
+                if (first) atomicOr(&kbuf[wi], word);
+                else kbuf[wi] = word;
+                first = false;
+                wi++;
+                nacc -= 32;
+            }
+        }
+    }
+    if (nacc > 0) atomicOr(&kbuf[wi], (uint32_t)(acc & ((1ull << nacc) - 1ull)) << (32 - nacc));
+}
+
+#define MMSB_BP_SWITCH(bp, METHOD, BODY)                                                   \
+    switch (bp) {                                                                          \
+        case 1: { constexpr int BP = 1, SH = (METHOD == 0 ? 8 : 7) - 1; BODY; } break;     \
+        case 2: { constexpr int BP = 2, SH = (METHOD == 0 ? 8 : 7) - 2; BODY; } break;     \
+        case 3: { constexpr int BP = 3, SH = (METHOD == 0 ? 8 : 7) - 3; BODY; } break;     \
+        case 4: { constexpr int BP = 4, SH = (METHOD == 0 ? 8 : 7) - 4; BODY; } break;     \
+        case 5: { constexpr int BP = 5, SH = (METHOD == 0 ? 8 : 7) - 5; BODY; } break;     \
+        case 6: { constexpr int BP = 6, SH = (METHOD == 0 ? 8 : 7) - 6; BODY; } break;     \
+        default: { constexpr int BP = 7, SH = (METHOD == 0 ? 8 : 7) - 7; BODY; } break;    \
+    }
+
 template <int METHOD, bool EMBED>
-__global__ void __launch_bounds__(kScanThreads) scan_kernel(Geo g, const uint8_t *__restrict__ in,
+__global__ void __launch_bounds__(kScanThreads, 8) scan_kernel(Geo g, const uint8_t *__restrict__ in,
                                                             uint8_t *__restrict__ out, const uint8_t *__restrict__ keys,
                                                             const uint8_t *__restrict__ msg,
                                                             const int64_t *__restrict__ msg_bits, long long stride,
@@ -121,26 +209,36 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(Geo g, const uint8_t
     excl[1] = block_exclusive_scan(cnt[1], wsum, tot[1]) + tot[0];
     const unsigned long long agg = (unsigned long long)tot[0] + tot[1];
 
-    // ---- single-pass decoupled look-back over the image's chunks (ticket order = issue order)
-    if (tid == 0) {
+    // ---- single-pass decoupled look-back over the image's chunks (ticket order = issue order).
+    // Warp 0 publishes this chunk's aggregate, then inspects 32 predecessors per probe: every
+    // lane spins on its own predecessor until that one has published, the nearest inclusive
+    // prefix ends the walk, aggregates in front of it are summed (warp reduction).
+    if (tid < 32) {
         unsigned long long *st = ws.states + (size_t)img * g.nchunks;
         unsigned long long prefix = 0;
         if (chunk == 0) {
-            st_release(st, kFlagInc | agg);
+            if (tid == 0) st_release(st, kFlagInc | agg);
         } else {
-            st_release(st + chunk, kFlagAgg | agg);
-            int k = chunk - 1;
+            if (tid == 0) st_release(st + chunk, kFlagAgg | agg);
+            int base = chunk - 1;
             while (true) {
-                const unsigned long long v = ld_acquire(st + k);
-                const unsigned long long f = v & ~kValMask;
-                if (f == 0) continue;                        // predecessor not published yet
-                prefix += v & kValMask;
-                if (f == kFlagInc) break;
-                k--;
+                const int k = base - tid;
+                unsigned long long v = kFlagInc;                 // before chunk 0: inclusive 0
+                if (k >= 0) {
+                    do { v = ld_acquire(st + k); } while ((v & ~kValMask) == 0);
+                }
+                const unsigned inc = __ballot_sync(0xffffffffu, (v & ~kValMask) == kFlagInc);
+                const int last = inc ? __ffs(inc) - 1 : 31;
+                unsigned long long val = tid <= last ? (v & kValMask) : 0ull;
+#pragma unroll
+                for (int s2 = 16; s2 > 0; s2 >>= 1) val += __shfl_xor_sync(0xffffffffu, val, s2);
+                prefix += val;
+                if (inc) break;
+                base -= 32;
             }
-            st_release(st + chunk, kFlagInc | (prefix + agg));
+            if (tid == 0) st_release(st + chunk, kFlagInc | (prefix + agg));
         }
-        sh_ll[0] = (long long)prefix;
+        if (tid == 0) sh_ll[0] = (long long)prefix;
     }
     __syncthreads();
     const long long prefix = sh_ll[0];
@@ -158,17 +256,20 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(Geo g, const uint8_t
         if (lo < hie) {
             const int nblk = (int)(((hie - 1) >> 9) - blk0 + 1);
             const uint8_t *mimg = msg + (size_t)img * stride;
-            for (int t = tid; t < nblk; t += kScanThreads) {
-                uint32_t ks[16];
-                chacha20_block(key, (uint32_t)(blk0 + t), ks);
+            for (int t0 = 0; t0 < nblk; t0 += kScanThreads / 4) {       // 4 lanes per ChaCha block
+                const int t = t0 + (tid >> 2), cl = tid & 3;
+                uint32_t ks[4];
+                chacha20_block_x4(key, (uint32_t)(blk0 + t), ks);
+                if (t < nblk) {
 #pragma unroll
-                for (int j = 0; j < 16; j++) {
-                    const long long wi = (blk0 + t) * 16 + j;        // frame word index (BE)
-                    uint32_t fw;
-                    if (wi == 0) fw = (uint32_t)n;
-                    else if (4 * wi <= stride) fw = bswap32(__ldg(reinterpret_cast<const uint32_t *>(mimg) + (wi - 1)));
-                    else fw = 0;
-                    kbuf[t * 16 + j] = fw ^ bswap32(ks[j]);
+                    for (int j = 0; j < 4; j++) {
+                        const long long wi = (blk0 + t) * 16 + 4 * j + cl;   // frame word index (BE)
+                        uint32_t fw;
+                        if (wi == 0) fw = (uint32_t)n;
+                        else if (4 * wi <= stride) fw = bswap32(__ldg(reinterpret_cast<const uint32_t *>(mimg) + (wi - 1)));
+                        else fw = 0;
+                        kbuf[t * 16 + 4 * j + cl] = fw ^ bswap32(ks[j]);
+                    }
                 }
             }
             if (tid == 0) kbuf[nblk * 16] = 0;
@@ -180,22 +281,8 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(Geo g, const uint8_t
             const long long p = p0 + r * (kScanThreads * 16) + tid * 16;
             if (p >= g.HW) continue;
             uint32_t w[4] = {pix[r].x, pix[r].y, pix[r].z, pix[r].w};
-            long long k = (prefix + excl[r]) * bp;
-            uint32_t mm = m[r];
-            while (mm && k < hie) {
-                const int i = __ffs(mm) - 1;
-                mm &= mm - 1;
-                const int nb = (F - k) < bp ? (int)(F - k) : bp;
-                const long long rel = k - base;
-                const int wv = (int)(rel >> 5), off = (int)(rel & 31);
-                const unsigned long long win = ((unsigned long long)kbuf[wv] << 32) | kbuf[wv + 1];
-                const uint32_t val = (uint32_t)(win >> (64 - off - nb)) & ((1u << nb) - 1u);
-                const int shift = (METHOD == 0 ? 8 : 7) - nb;
-                const uint32_t msk = ((1u << nb) - 1u) << shift;
-                const int wi = i >> 2, sb = 8 * (i & 3);
-                w[wi] = (w[wi] & ~(msk << sb)) | ((val << shift) << sb);
-                k += bp;
-            }
+            const long long rel = (prefix + excl[r]) * bp - base;
+            MMSB_BP_SWITCH(bp, METHOD, (embed16<BP, SH>(w, m[r], kbuf, rel, hie - base)))
             *reinterpret_cast<uint4 *>(out + (size_t)img * g.HW + p) = make_uint4(w[0], w[1], w[2], w[3]);
         }
         // ---- the image's last CTA decides the capacity outcome (32 + n <= C)
@@ -231,31 +318,19 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(Geo g, const uint8_t
 #pragma unroll
             for (int r = 0; r < 2; r++) {
                 const uint32_t w[4] = {pix[r].x, pix[r].y, pix[r].z, pix[r].w};
-                long long k = (prefix + excl[r]) * bp;
-                uint32_t mm = m[r];
-                while (mm) {
-                    const int i = __ffs(mm) - 1;
-                    mm &= mm - 1;
-                    const uint32_t px8 = (w[i >> 2] >> (8 * (i & 3))) & 0xFFu;
-                    const uint32_t val = (px8 >> (8 - b)) & ((1u << bp) - 1u);
-                    const long long rel = k - base;
-                    const int wv = (int)(rel >> 5), off = (int)(rel & 31);
-                    if (off + bp <= 32) {
-                        atomicOr(&kbuf[wv], val << (32 - off - bp));
-                    } else {
-                        atomicOr(&kbuf[wv], val >> (off + bp - 32));
-                        atomicOr(&kbuf[wv + 1], val << (64 - off - bp));
-                    }
-                    k += bp;
-                }
+                const long long rel = (prefix + excl[r]) * bp - base;
+                MMSB_BP_SWITCH(bp, METHOD, (extract16<BP, SH>(w, m[r], kbuf, rel)))
             }
         }
         __syncthreads();
-        for (int t = tid; t < nblk; t += kScanThreads) {
-            uint32_t ks[16];
-            chacha20_block(key, (uint32_t)(blk0 + t), ks);
+        for (int t0 = 0; t0 < nblk; t0 += kScanThreads / 4) {           // 4 lanes per ChaCha block
+            const int t = t0 + (tid >> 2), cl = tid & 3;
+            uint32_t ks[4];
+            chacha20_block_x4(key, (uint32_t)(blk0 + t), ks);
+            if (t < nblk) {
 #pragma unroll
-            for (int j = 0; j < 16; j++) kbuf[t * 16 + j] ^= bswap32(ks[j]);
+                for (int j = 0; j < 4; j++) kbuf[t * 16 + 4 * j + cl] ^= bswap32(ks[j]);
+            }
         }
         __syncthreads();
         uint32_t *mo = reinterpret_cast<uint32_t *>(msg_out + (size_t)img * stride);
@@ -268,7 +343,7 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(Geo g, const uint8_t
                 uint32_t v = kbuf[W - basew];
                 if (s0 == W * 32 && e0 == W * 32 + 32) {
                     if (W == 0) ws.hdr[img] = v;
-                    else mo[W - 1] = bswap32(v);
+                    else if (4 * W <= stride) mo[W - 1] = bswap32(v);
                 } else {
                     const int len = (int)(e0 - s0), st0 = (int)(s0 - W * 32);
                     const uint32_t msk = (len == 32 ? 0xFFFFFFFFu : ((1u << len) - 1u)) << (32 - st0 - len);
@@ -297,22 +372,24 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(Geo g, const uint8_t
                     cv |= (uint32_t)v;
                 } else {
                     if (cw == 0) ws.hdr[img] = cv;
-                    else if (cw > 0) mo[cw - 1] = bswap32(cv);
+                    else if (cw > 0 && 4 * cw <= stride) mo[cw - 1] = bswap32(cv);
                     cw = W;
                     cv = (uint32_t)v;
                 }
             }
             if (cw == 0) ws.hdr[img] = cv;
-            else if (cw > 0) mo[cw - 1] = bswap32(cv);
+            else if (cw > 0 && 4 * cw <= stride) mo[cw - 1] = bswap32(cv);
             __threadfence_block();
             const unsigned long long last = ld_acquire(ws.states + (size_t)img * g.nchunks + g.nchunks - 1);
             const long long C = (long long)(last & kValMask) * bp;
+            const long long rw = C > 32 ? (C - 32 + 31) / 32 : 0;
+            const bool fits = 4 * rw <= stride;
             const long long n = C >= 32 ? (long long)__ldcg(ws.hdr + img) : -1;
-            const bool ok = C >= 32 && n <= C - 32;
-            sh_ll[1] = C;
+            const bool ok = fits && C >= 32 && n <= C - 32;
+            sh_ll[1] = fits ? C : 0;
             sh_ll[2] = ok ? n : -1;
             msg_bits_out[img] = ok ? n : -1;
-            status[img] = ok ? 0 : 4;
+            status[img] = ok ? 0 : (fits ? 4 : 2);           // region beyond the caller's rows: E_INVAL
         }
         __syncthreads();
         const long long C = sh_ll[1], n = sh_ll[2];

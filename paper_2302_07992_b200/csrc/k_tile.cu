@@ -19,11 +19,49 @@ namespace mmsb {
 //   HIST: non-redundant counts per b = 2..8 of the label c = #leading equal bits of p and
 //   its left neighbour (eq. gliding1/2 P:611-625 reduce to the left neighbour).
 // ======================================================================================
+// destination tile -> source tile under the levels above the tile (walk e = emax .. tp+1)
+__device__ __forceinline__ void upper_walk_inverse(const Geo &g, const uint32_t *pyr_img, int dty, int dtx,
+                                                   int &sty, int &stx, int &q) {
+    int y = dty, x = dtx;
+    q = 0;
+    for (int e = g.emax; e > g.tp; e--) {
+        const int k = e - g.tp, m1 = (1 << k) - 1;
+        const int by = y >> k, bx = x >> k;
+        const int a = (int)(__ldcg(pyr_img + g.pyr_off[e] + by * (g.W >> e) + bx) & 3u);
+        int oy = y & m1, ox = x & m1;
+        inv_turn(a, m1, oy, ox);
+        y = (by << k) | oy;
+        x = (bx << k) | ox;
+        q += a;
+    }
+    sty = y; stx = x; q &= 3;
+}
+
+// original tile -> destination tile (walk e = tp+1 .. emax)
+__device__ __forceinline__ void upper_walk_forward(const Geo &g, const uint32_t *pyr_img, int oty, int otx,
+                                                   int &dty, int &dtx, int &q) {
+    int y = oty, x = otx;
+    q = 0;
+    for (int e = g.tp + 1; e <= g.emax; e++) {
+        const int k = e - g.tp, m1 = (1 << k) - 1;
+        const int by = y >> k, bx = x >> k;
+        const int a = (int)(__ldcg(pyr_img + g.pyr_off[e] + by * (g.W >> e) + bx) & 3u);
+        int oy = y & m1, ox = x & m1;
+        fwd_turn(a, m1, oy, ox);
+        y = (by << k) | oy;
+        x = (bx << k) | ox;
+        q += a;
+    }
+    dty = y; dtx = x; q &= 3;
+}
+
 template <int TP, bool HIST>
 __global__ void __launch_bounds__(256) ks_tile_kernel(Geo g, const uint8_t *__restrict__ keys,
                                                       const uint8_t *__restrict__ images,
                                                       uint8_t *__restrict__ s_out, uint64_t *__restrict__ rec_out,
-                                                      uint32_t *__restrict__ pyr, uint32_t *__restrict__ hist) {
+                                                      uint32_t *__restrict__ pyr, uint32_t *__restrict__ hist,
+                                                      uint32_t *__restrict__ done, int32_t *__restrict__ fwd_map,
+                                                      int32_t *__restrict__ inv_map) {
     constexpr int T = 1 << TP, NW = T / 4, TPC = 256 / T;
     __shared__ __align__(16) uint32_t sbuf[TPC][T][NW];
     __shared__ uint64_t rec[TPC][kRecSlots];
@@ -144,42 +182,26 @@ __global__ void __launch_bounds__(256) ks_tile_kernel(Geo g, const uint8_t *__re
         uint4 v = *reinterpret_cast<const uint4 *>(&sbuf[l2][r][seg * 4]);
         *reinterpret_cast<uint4 *>(s_out + (size_t)img * g.HW + (size_t)(tyy * T + r) * g.W + txx * T + seg * 16) = v;
     }
-}
-
-// destination tile -> source tile under the levels above the tile (walk e = emax .. tp+1)
-__device__ __forceinline__ void upper_walk_inverse(const Geo &g, const uint32_t *pyr_img, int dty, int dtx,
-                                                   int &sty, int &stx, int &q) {
-    int y = dty, x = dtx;
-    q = 0;
-    for (int e = g.emax; e > g.tp; e--) {
-        const int k = e - g.tp, m1 = (1 << k) - 1;
-        const int by = y >> k, bx = x >> k;
-        const int a = (int)(pyr_img[g.pyr_off[e] + by * (g.W >> e) + bx] & 3u);
-        int oy = y & m1, ox = x & m1;
-        inv_turn(a, m1, oy, ox);
-        y = (by << k) | oy;
-        x = (bx << k) | ox;
-        q += a;
+    // the image's last CTA turns the completed upper pyramid into tile maps (one walk per tile):
+    //   inv_map[dest tile] = source tile << 2 | q,  fwd_map[original tile] = dest tile << 2 | q
+    __shared__ int last;
+    __syncthreads();
+    if (tid == 0) {
+        __threadfence();
+        last = atomicAdd(done + img, 1u) == gridDim.x - 1;
     }
-    sty = y; stx = x; q &= 3;
-}
-
-// original tile -> destination tile (walk e = tp+1 .. emax)
-__device__ __forceinline__ void upper_walk_forward(const Geo &g, const uint32_t *pyr_img, int oty, int otx,
-                                                   int &dty, int &dtx, int &q) {
-    int y = oty, x = otx;
-    q = 0;
-    for (int e = g.tp + 1; e <= g.emax; e++) {
-        const int k = e - g.tp, m1 = (1 << k) - 1;
-        const int by = y >> k, bx = x >> k;
-        const int a = (int)(pyr_img[g.pyr_off[e] + by * (g.W >> e) + bx] & 3u);
-        int oy = y & m1, ox = x & m1;
-        fwd_turn(a, m1, oy, ox);
-        y = (by << k) | oy;
-        x = (bx << k) | ox;
-        q += a;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    const uint32_t *pyr_img = pyr + (size_t)img * g.npyr;
+    for (int t = tid; t < g.ntiles; t += 256) {
+        const int ty2 = t / g.tilesX, tx2 = t % g.tilesX;
+        int y, x, q;
+        upper_walk_inverse(g, pyr_img, ty2, tx2, y, x, q);
+        inv_map[(size_t)img * g.ntiles + t] = ((y * g.tilesX + x) << 2) | q;
+        upper_walk_forward(g, pyr_img, ty2, tx2, y, x, q);
+        fwd_map[(size_t)img * g.ntiles + t] = ((y * g.tilesX + x) << 2) | q;
     }
-    dty = y; dtx = x; q &= 3;
 }
 
 // EMR optimal b from the non-redundant counts (eq. optimial_b; ties -> smaller b)
@@ -206,6 +228,7 @@ __global__ void __launch_bounds__(256) perm_encode_kernel(Geo g, const uint8_t *
                                                           const uint64_t *__restrict__ recs,
                                                           const uint32_t *__restrict__ pyr,
                                                           const uint32_t *__restrict__ hist,
+                                                          const int32_t *__restrict__ inv_map,
                                                           uint8_t *__restrict__ enc, uint8_t *__restrict__ ceta_out,
                                                           int32_t *__restrict__ b_out, int64_t *__restrict__ cap_out,
                                                           int32_t *__restrict__ status) {
@@ -213,20 +236,20 @@ __global__ void __launch_bounds__(256) perm_encode_kernel(Geo g, const uint8_t *
     __shared__ uint32_t src[T * RS];
     __shared__ uint32_t lab[METHOD == 1 ? T * RS : 1];
     __shared__ uint64_t rec[kRecSlots];
-    __shared__ int sh[4];
+    __shared__ int sh[1];
 
     const int tid = threadIdx.x, img = blockIdx.y;
     const int dty = blockIdx.x / g.tilesX, dtx = blockIdx.x % g.tilesX;
     const uint8_t *I = images + (size_t)img * g.HW;
 
-    if (tid == 0) {
-        int sty, stx, q;
-        upper_walk_inverse(g, pyr + (size_t)img * g.npyr, dty, dtx, sty, stx, q);
-        sh[0] = METHOD == 0 ? emr_select_b(hist + img * 8, g.HW) : 0;
-        sh[1] = sty; sh[2] = stx; sh[3] = q;
-    }
+    const int mp = __ldg(inv_map + (size_t)img * g.ntiles + blockIdx.x);
+    const int stile = mp >> 2, q_up = mp & 3;
+    const int sty = stile / g.tilesX, stx = stile % g.tilesX;
+    if (tid == 0) sh[0] = METHOD == 0 ? emr_select_b(hist + img * 8, g.HW) : 0;
+    if (tid < kRecSlots) rec[tid] = recs[((size_t)img * g.ntiles + stile) * kRecSlots + tid];
     __syncthreads();
-    const int b = sh[0], sty = sh[1], stx = sh[2], q_up = sh[3];
+    const int b = sh[0];
+    (void)pyr;
 
     // source tile + left halo -> labels -> carrier (EMR) or I and ceta (LMR)
     const uint32_t M = METHOD == 0 ? (0xFFu << (8 - b)) & 0xFFu : 0;
@@ -267,8 +290,6 @@ __global__ void __launch_bounds__(256) perm_encode_kernel(Geo g, const uint8_t *
             if constexpr (METHOD == 1) lab[r * RS + seg * 4 + i] = cw[i];
         }
     }
-    const int stile = sty * g.tilesX + stx;
-    if (tid < kRecSlots) rec[tid] = recs[((size_t)img * g.ntiles + stile) * kRecSlots + tid];
     __syncthreads();
 
     // cells: destination cell -> source cell (levels 3..tp), then in-cell levels 1, 2
@@ -357,28 +378,55 @@ __device__ __forceinline__ uint32_t bytes_to_bits4(uint32_t l) { return (l | (l 
 //   X = I_e' XOR s (every bit, Q20); EMR: map bit = raw LSB of I_e' (r < 3 forced to 1);
 //   LMR: MSB := eta_r and the map come from the decoded planes.  Inverse cell transform,
 //   then omega := masked bits of the last non-redundant pixel, replaced into redundant ones.
+//   The next destination tile (I_e', s, angle record) is prefetched with cp.async while the
+//   current one is processed (double buffer).
 // ======================================================================================
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N> __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
 template <int TP, int METHOD>
 __global__ void __launch_bounds__(256) recover_strip_kernel(Geo g, const uint8_t *__restrict__ marked,
                                                             const uint8_t *__restrict__ s_scr,
                                                             const uint64_t *__restrict__ recs,
-                                                            const uint32_t *__restrict__ pyr,
+                                                            const int32_t *__restrict__ fwd_map,
                                                             const uint32_t *__restrict__ eta_bits,
                                                             const uint32_t *__restrict__ map_bits,
                                                             const int32_t *__restrict__ lmr_b,
                                                             uint8_t *__restrict__ out, int32_t *__restrict__ status) {
     constexpr int T = 1 << TP, NW = T / 4, RS = NW + 1, NC = T / 4, NCELL = NC * NC, CPT = T * T / 16;
     constexpr int SEGS = T / 16;                      // 16-pixel segments per row
+    __shared__ __align__(16) uint8_t eraw[2][T * T];
+    __shared__ __align__(16) uint8_t sraw[2][T * T];
+    __shared__ __align__(16) uint64_t rec[2][kRecSlots];
     __shared__ uint32_t xin[T * RS], lin[T * RS], xo[T * RS], lo[T * RS];
-    __shared__ uint64_t rec[kRecSlots];
     __shared__ uint8_t carry[T];
-    __shared__ int sh[4];
+    __shared__ int sh_b;
 
     const int tid = threadIdx.x, img = blockIdx.y, ty = blockIdx.x;
     const uint8_t *Em = marked + (size_t)img * g.HW;
     const uint8_t *S = s_scr + (size_t)img * g.HW;
+    const int32_t *fm = fwd_map + (size_t)img * g.ntiles + (size_t)ty * g.tilesX;
     uint8_t *O = out + (size_t)img * g.HW;
 
+    auto prefetch = [&](int tx, int buf) {
+        const int mp = __ldg(fm + tx), dt = mp >> 2;
+        const int dty = dt / g.tilesX, dtx = dt % g.tilesX;
+        for (int c = tid; c < CPT; c += 256) {
+            const int r = c / (T / 16), seg = c % (T / 16);
+            const size_t off = (size_t)(dty * T + r) * g.W + (size_t)dtx * T + seg * 16;
+            cp_async16(&eraw[buf][r * T + seg * 16], Em + off);
+            cp_async16(&sraw[buf][r * T + seg * 16], S + off);
+        }
+        if (tid < kRecSlots / 2)
+            cp_async16(&rec[buf][2 * tid], recs + ((size_t)img * g.ntiles + (size_t)ty * g.tilesX + tx) * kRecSlots + 2 * tid);
+        cp_async_commit();
+    };
+
+    prefetch(0, 0);
     if (tid == 0) {
         int b;
         if constexpr (METHOD == 0) {
@@ -387,12 +435,14 @@ __global__ void __launch_bounds__(256) recover_strip_kernel(Geo g, const uint8_t
             if (ty == 0) status[img] = b < 0 ? 8 : 0;
         } else {
             b = lmr_b[img];                             // <= 0: status already set by the decoder
+            if (ty == 0 && b > 0) status[img] = 0;
         }
-        sh[0] = b;
+        sh_b = b;
     }
     __syncthreads();
-    const int b = sh[0];
+    const int b = sh_b;
     if (b <= 0) {
+        cp_async_wait<0>();
         for (int c = tid; c < T * g.W / 16; c += 256) {
             const int r = c / (g.W / 16), col = c % (g.W / 16);
             *reinterpret_cast<uint4 *>(O + (size_t)(ty * T + r) * g.W + col * 16) = make_uint4(0, 0, 0, 0);
@@ -402,32 +452,35 @@ __global__ void __launch_bounds__(256) recover_strip_kernel(Geo g, const uint8_t
     const uint32_t mask = METHOD == 0 ? ((0xFFu << (8 - b)) & 0xFFu) : (0x7Fu & ~(0xFFu >> b));
 
     for (int tx = 0; tx < g.tilesX; tx++) {
-        if (tid == 0) {
-            int dty, dtx, q;
-            upper_walk_forward(g, pyr + (size_t)img * g.npyr, ty, tx, dty, dtx, q);
-            sh[1] = dty; sh[2] = dtx; sh[3] = q;
+        const int buf = tx & 1;
+        if (tx + 1 < g.tilesX) {
+            prefetch(tx + 1, buf ^ 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
         }
         __syncthreads();
-        const int dty = sh[1], dtx = sh[2], q_up = sh[3];
+        const int mp = __ldg(fm + tx), dt = mp >> 2, q_up = mp & 3;
+        const int dty = dt / g.tilesX, dtx = dt % g.tilesX;
         // destination tile: X = E' ^ s, map bits
         for (int c = tid; c < CPT; c += 256) {
             const int r = c / (T / 16), seg = c % (T / 16);
-            const size_t off = (size_t)(dty * T + r) * g.W + (size_t)dtx * T + seg * 16;
-            const uint4 e = __ldg(reinterpret_cast<const uint4 *>(Em + off));
-            const uint4 s = __ldg(reinterpret_cast<const uint4 *>(S + off));
-            uint32_t ew[4] = {e.x, e.y, e.z, e.w}, sw[4] = {s.x, s.y, s.z, s.w};
+            const uint4 e = *reinterpret_cast<const uint4 *>(&eraw[buf][r * T + seg * 16]);
+            const uint4 sv = *reinterpret_cast<const uint4 *>(&sraw[buf][r * T + seg * 16]);
+            uint32_t ew[4] = {e.x, e.y, e.z, e.w}, sw[4] = {sv.x, sv.y, sv.z, sv.w};
             uint32_t mb16 = 0, eb16 = 0;
             if constexpr (METHOD == 1) {
-                const size_t bit = (size_t)img * g.HW + off;     // 16-aligned, never straddles a word
+                const size_t bit = (size_t)img * g.HW + (size_t)(dty * T + r) * g.W + (size_t)dtx * T + seg * 16;
                 mb16 = (__ldg(map_bits + (bit >> 5)) >> (bit & 31)) & 0xFFFFu;
                 eb16 = (__ldg(eta_bits + (bit >> 5)) >> (bit & 31)) & 0xFFFFu;
             }
+            const bool first = dt == 0 && r == 0 && seg == 0;
 #pragma unroll
             for (int i = 0; i < 4; i++) {
                 uint32_t x = ew[i] ^ sw[i], l;
                 if constexpr (METHOD == 0) {
                     l = ew[i] & 0x01010101u;
-                    if (i == 0 && off == 0) l |= 0x00010101u;    // r = 0..2 carry the header, map = 1
+                    if (i == 0 && first) l |= 0x00010101u;      // r = 0..2 carry the header, map = 1
                 } else {
                     l = bits4_to_bytes(mb16 >> (4 * i));
                     x = (x & 0x7F7F7F7Fu) | (bits4_to_bytes(eb16 >> (4 * i)) << 7);   // MSB from eta
@@ -436,8 +489,8 @@ __global__ void __launch_bounds__(256) recover_strip_kernel(Geo g, const uint8_t
                 lin[r * RS + seg * 4 + i] = l;
             }
         }
-        if (tid < kRecSlots) rec[tid] = recs[((size_t)img * g.ntiles + ty * g.tilesX + tx) * kRecSlots + tid];
         __syncthreads();
+        const uint64_t *rc = rec[buf];
         // cells: original cell -> destination cell, inverse content transform
         for (int c = tid; c < NCELL; c += 256) {
             const int cy = c / NC, cx = c % NC;
@@ -445,7 +498,7 @@ __global__ void __launch_bounds__(256) recover_strip_kernel(Geo g, const uint8_t
             for (int e = (g.emin > 3 ? g.emin : 3); e <= TP; e++) {
                 const int k = e - 2, m1 = (1 << k) - 1;
                 const int by = py >> k, bx = px >> k;
-                const int a = rec_angle(rec, g, e, by, bx);
+                const int a = rec_angle(rc, g, e, by, bx);
                 int oy = py & m1, ox = px & m1;
                 fwd_turn(a, m1, oy, ox);
                 py = (by << k) | oy;
@@ -454,7 +507,7 @@ __global__ void __launch_bounds__(256) recover_strip_kernel(Geo g, const uint8_t
             }
             fwd_turn(q_up, NC - 1, py, px);
             q += q_up;
-            if (g.emin <= 2) q += rec_angle(rec, g, 2, cy, cx);
+            if (g.emin <= 2) q += rec_angle(rc, g, 2, cy, cx);
             Cell x = {xin[(4 * py) * RS + px], xin[(4 * py + 1) * RS + px], xin[(4 * py + 2) * RS + px],
                       xin[(4 * py + 3) * RS + px]};
             Cell l = {lin[(4 * py) * RS + px], lin[(4 * py + 1) * RS + px], lin[(4 * py + 2) * RS + px],
@@ -463,8 +516,8 @@ __global__ void __launch_bounds__(256) recover_strip_kernel(Geo g, const uint8_t
             x = cell_rot_cw(x, rinv);
             l = cell_rot_cw(l, rinv);
             if (g.emin <= 1) {
-                const uint32_t a01 = (uint32_t)(rec[g.lvl_off[1] + 2 * cy] >> (4 * cx)) & 0xFu;
-                const uint32_t a23 = (uint32_t)(rec[g.lvl_off[1] + 2 * cy + 1] >> (4 * cx)) & 0xFu;
+                const uint32_t a01 = (uint32_t)(rc[g.lvl_off[1] + 2 * cy] >> (4 * cx)) & 0xFu;
+                const uint32_t a23 = (uint32_t)(rc[g.lvl_off[1] + 2 * cy + 1] >> (4 * cx)) & 0xFu;
                 const int aL0 = (4 - (a01 & 3)) & 3, aR0 = (4 - (a01 >> 2)) & 3;
                 const int aL1 = (4 - (a23 & 3)) & 3, aR1 = (4 - (a23 >> 2)) & 3;
                 pair_rot_cw(x.r0, x.r1, aL0, aR0);
@@ -521,61 +574,61 @@ __global__ void __launch_bounds__(256) recover_strip_kernel(Geo g, const uint8_t
 // ---------------------------------------------------------------------------- launchers
 template <int TP>
 static void launch_ks_tp(const Geo &g, int G, const uint8_t *keys, const uint8_t *images, uint8_t *s, uint64_t *rec,
-                         uint32_t *pyr, uint32_t *hist, cudaStream_t st) {
+                         uint32_t *pyr, uint32_t *hist, uint32_t *done, int32_t *fwd, int32_t *inv, cudaStream_t st) {
     constexpr int T = 1 << TP, TPC = 256 / T;
     dim3 grid((g.ntiles + TPC - 1) / TPC, G);
-    if (images) ks_tile_kernel<TP, true><<<grid, 256, 0, st>>>(g, keys, images, s, rec, pyr, hist);
-    else ks_tile_kernel<TP, false><<<grid, 256, 0, st>>>(g, keys, images, s, rec, pyr, hist);
+    if (images) ks_tile_kernel<TP, true><<<grid, 256, 0, st>>>(g, keys, images, s, rec, pyr, hist, done, fwd, inv);
+    else ks_tile_kernel<TP, false><<<grid, 256, 0, st>>>(g, keys, images, s, rec, pyr, hist, done, fwd, inv);
 }
 
 void launch_ks_tile(const Geo &g, int G, const uint8_t *keys, const uint8_t *images, uint8_t *s, uint64_t *rec,
-                    uint32_t *pyr, uint32_t *hist, cudaStream_t st) {
+                    uint32_t *pyr, uint32_t *hist, uint32_t *done, int32_t *fwd, int32_t *inv, cudaStream_t st) {
     switch (g.tp) {
-        case 4: launch_ks_tp<4>(g, G, keys, images, s, rec, pyr, hist, st); break;
-        case 5: launch_ks_tp<5>(g, G, keys, images, s, rec, pyr, hist, st); break;
-        default: launch_ks_tp<6>(g, G, keys, images, s, rec, pyr, hist, st); break;
+        case 4: launch_ks_tp<4>(g, G, keys, images, s, rec, pyr, hist, done, fwd, inv, st); break;
+        case 5: launch_ks_tp<5>(g, G, keys, images, s, rec, pyr, hist, done, fwd, inv, st); break;
+        default: launch_ks_tp<6>(g, G, keys, images, s, rec, pyr, hist, done, fwd, inv, st); break;
     }
 }
 
 template <int TP>
 static void launch_perm_tp(const Geo &g, int G, const uint8_t *images, const uint8_t *s, const uint64_t *rec,
-                           const uint32_t *pyr, const uint32_t *hist, uint8_t *enc, uint8_t *ceta, int32_t *b_out,
-                           int64_t *cap_out, int32_t *status, cudaStream_t st) {
+                           const uint32_t *pyr, const uint32_t *hist, const int32_t *inv, uint8_t *enc, uint8_t *ceta,
+                           int32_t *b_out, int64_t *cap_out, int32_t *status, cudaStream_t st) {
     dim3 grid(g.ntiles, G);
     if (g.method == 0)
-        perm_encode_kernel<TP, 0><<<grid, 256, 0, st>>>(g, images, s, rec, pyr, hist, enc, ceta, b_out, cap_out, status);
+        perm_encode_kernel<TP, 0><<<grid, 256, 0, st>>>(g, images, s, rec, pyr, hist, inv, enc, ceta, b_out, cap_out, status);
     else
-        perm_encode_kernel<TP, 1><<<grid, 256, 0, st>>>(g, images, s, rec, pyr, hist, enc, ceta, b_out, cap_out, status);
+        perm_encode_kernel<TP, 1><<<grid, 256, 0, st>>>(g, images, s, rec, pyr, hist, inv, enc, ceta, b_out, cap_out, status);
 }
 
 void launch_perm_encode(const Geo &g, int G, const uint8_t *images, const uint8_t *s, const uint64_t *rec,
-                        const uint32_t *pyr, const uint32_t *hist, uint8_t *enc, uint8_t *ceta, int32_t *b_out,
-                        int64_t *cap_out, int32_t *status, cudaStream_t st) {
+                        const uint32_t *pyr, const uint32_t *hist, const int32_t *inv, uint8_t *enc, uint8_t *ceta,
+                        int32_t *b_out, int64_t *cap_out, int32_t *status, cudaStream_t st) {
     switch (g.tp) {
-        case 4: launch_perm_tp<4>(g, G, images, s, rec, pyr, hist, enc, ceta, b_out, cap_out, status, st); break;
-        case 5: launch_perm_tp<5>(g, G, images, s, rec, pyr, hist, enc, ceta, b_out, cap_out, status, st); break;
-        default: launch_perm_tp<6>(g, G, images, s, rec, pyr, hist, enc, ceta, b_out, cap_out, status, st); break;
+        case 4: launch_perm_tp<4>(g, G, images, s, rec, pyr, hist, inv, enc, ceta, b_out, cap_out, status, st); break;
+        case 5: launch_perm_tp<5>(g, G, images, s, rec, pyr, hist, inv, enc, ceta, b_out, cap_out, status, st); break;
+        default: launch_perm_tp<6>(g, G, images, s, rec, pyr, hist, inv, enc, ceta, b_out, cap_out, status, st); break;
     }
 }
 
 template <int TP>
 static void launch_rec_tp(const Geo &g, int G, const uint8_t *marked, const uint8_t *s, const uint64_t *rec,
-                          const uint32_t *pyr, const uint32_t *eta, const uint32_t *map, const int32_t *lmr_b,
+                          const int32_t *fwd, const uint32_t *eta, const uint32_t *map, const int32_t *lmr_b,
                           uint8_t *out, int32_t *status, cudaStream_t st) {
     dim3 grid(g.tilesY, G);
     if (g.method == 0)
-        recover_strip_kernel<TP, 0><<<grid, 256, 0, st>>>(g, marked, s, rec, pyr, eta, map, lmr_b, out, status);
+        recover_strip_kernel<TP, 0><<<grid, 256, 0, st>>>(g, marked, s, rec, fwd, eta, map, lmr_b, out, status);
     else
-        recover_strip_kernel<TP, 1><<<grid, 256, 0, st>>>(g, marked, s, rec, pyr, eta, map, lmr_b, out, status);
+        recover_strip_kernel<TP, 1><<<grid, 256, 0, st>>>(g, marked, s, rec, fwd, eta, map, lmr_b, out, status);
 }
 
 void launch_recover_strip(const Geo &g, int G, const uint8_t *marked, const uint8_t *s, const uint64_t *rec,
-                          const uint32_t *pyr, const uint32_t *eta, const uint32_t *map, const int32_t *lmr_b,
+                          const int32_t *fwd, const uint32_t *eta, const uint32_t *map, const int32_t *lmr_b,
                           uint8_t *out, int32_t *status, cudaStream_t st) {
     switch (g.tp) {
-        case 4: launch_rec_tp<4>(g, G, marked, s, rec, pyr, eta, map, lmr_b, out, status, st); break;
-        case 5: launch_rec_tp<5>(g, G, marked, s, rec, pyr, eta, map, lmr_b, out, status, st); break;
-        default: launch_rec_tp<6>(g, G, marked, s, rec, pyr, eta, map, lmr_b, out, status, st); break;
+        case 4: launch_rec_tp<4>(g, G, marked, s, rec, fwd, eta, map, lmr_b, out, status, st); break;
+        case 5: launch_rec_tp<5>(g, G, marked, s, rec, fwd, eta, map, lmr_b, out, status, st); break;
+        default: launch_rec_tp<6>(g, G, marked, s, rec, fwd, eta, map, lmr_b, out, status, st); break;
     }
 }
 

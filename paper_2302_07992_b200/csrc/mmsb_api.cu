@@ -4,6 +4,8 @@
 #include <atomic>
 #include <cmath>
 #include <cstring>
+#include <mutex>
+#include <vector>
 
 #include "mmsb.h"
 #include "mmsb_geo.h"
@@ -12,6 +14,43 @@
 namespace mmsb {
 
 static std::atomic<unsigned long long> g_launches{0};
+
+// ---- live per-kernel timing (CUDA events recorded on the launch stream around each kernel)
+enum KernelId { K_KS_ENC = 0, K_KS_REC, K_PERM_ENC, K_RECOVER, K_EMBED, K_EXTRACT, K_STATS, K_LMR_PLAN,
+                K_CODER_ENC, K_LMR_FIT, K_LMR_MSB, K_LMR_DECODE, K_COUNT };
+static const char *kKernelNames[K_COUNT] = {"ks_tile_kernel<hist>", "ks_tile_kernel", "perm_encode_kernel",
+                                            "recover_strip_kernel", "scan_kernel<embed>", "scan_kernel<extract>",
+                                            "stats_kernel", "lmr_plan_kernel", "coder_encode_kernel",
+                                            "lmr_fit_kernel", "lmr_msb_write_kernel",
+                                            "lmr_pack+header+coder_decode_kernels"};
+struct ProfRec { int id; cudaEvent_t a, b; long long units; };
+static std::mutex g_prof_mu;
+static bool g_prof_on = false;
+static std::vector<ProfRec> g_prof;
+static std::vector<cudaEvent_t> g_event_pool;
+
+static cudaEvent_t prof_event() {
+    if (!g_event_pool.empty()) { cudaEvent_t e = g_event_pool.back(); g_event_pool.pop_back(); return e; }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+
+// runs `launch` (one kernel) and, when profiling, brackets it with events; `units` = pixels it processes
+template <class F> static void run_kernel(int id, cudaStream_t st, long long units, F &&launch, int nkernels = 1) {
+    std::unique_lock<std::mutex> lk(g_prof_mu);
+    g_launches += nkernels;
+    if (!g_prof_on) {
+        lk.unlock();
+        launch();
+        return;
+    }
+    ProfRec r{id, prof_event(), prof_event(), units};
+    cudaEventRecord(r.a, st);
+    launch();
+    cudaEventRecord(r.b, st);
+    g_prof.push_back(r);
+}
 
 // Images per tile-kernel group: the group's keystream scratch (1 B/px), its images and
 // their outputs are meant to stay in the 126 MB L2 between the keystream kernel and the
@@ -22,9 +61,9 @@ static size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
 
 struct Layout {
     int G;
-    size_t s, rec, pyr, hist, tile_zero_end;                 // per-group tile state
+    size_t s, rec, fwd, inv, pyr, hist, tdone, tile_zero_end; // per-group tile state
     size_t ticket, states, done, parts, hdr, scan_zero_end;  // per-call scan state
-    size_t ceta, eta_bits, map_bits, lmr_b, total;
+    size_t ceta, eta_bits, map_bits, lmr_b, lmr_t, plan, streams, sizes, offsets, mbuf, total;
 };
 
 static Layout layout(const Geo &g) {
@@ -36,8 +75,11 @@ static Layout layout(const Geo &g) {
     size_t o = 0;
     L.s = o; o = align256(o + (size_t)G * g.HW);
     L.rec = o; o = align256(o + (size_t)G * g.ntiles * kRecSlots * 8);
+    L.fwd = o; o = align256(o + (size_t)G * g.ntiles * 4);
+    L.inv = o; o = align256(o + (size_t)G * g.ntiles * 4);
     L.pyr = o; o = align256(o + (size_t)G * (g.npyr > 0 ? g.npyr : 1) * 4);
     L.hist = o; o = align256(o + (size_t)G * 8 * 4);
+    L.tdone = o; o = align256(o + (size_t)G * 4);
     L.tile_zero_end = o;
     L.ticket = o; o = align256(o + 16);
     L.states = o; o = align256(o + (size_t)g.B * g.nchunks * 8);
@@ -49,6 +91,14 @@ static Layout layout(const Geo &g) {
     L.eta_bits = o; o = align256(o + (g.method == 1 ? (size_t)g.B * g.HW / 8 : 0));
     L.map_bits = o; o = align256(o + (g.method == 1 ? (size_t)g.B * g.HW / 8 : 0));
     L.lmr_b = o; o = align256(o + (size_t)g.B * 4);
+    L.lmr_t = o; o = align256(o + (size_t)g.B * 4);
+    const bool lmr = g.method == 1;
+    const size_t Tc = (size_t)g.ntiles_coder;
+    L.plan = o; o = align256(o + (lmr ? (size_t)G * sizeof(LmrPlan) : 0));
+    L.streams = o; o = align256(o + (lmr ? (size_t)G * 2 * Tc * lmr_tile_cap_host(g.tile_log2, g.H, g.W) : 0));
+    L.sizes = o; o = align256(o + (lmr ? (size_t)g.B * 2 * Tc * 4 : 0));
+    L.offsets = o; o = align256(o + (lmr ? (size_t)g.B * 2 * Tc * 4 : 0));
+    L.mbuf = o; o = align256(o + (lmr ? (size_t)g.B * g.HW / 8 + 16 : 0));
     L.total = o;
     return L;
 }
@@ -63,6 +113,21 @@ static mmsb_status check_launch() {
 }
 
 template <class T> static T *at(void *ws, size_t off) { return reinterpret_cast<T *>(static_cast<char *>(ws) + off); }
+
+// LMR receiving side: MSB plane -> header -> decoded rotated map (and eta) planes
+static void lmr_decode_all(const Geo &g, const Layout &L, bool want_eta, const uint8_t *marked, void *ws,
+                           int32_t *img_status, int64_t *msg_bits_out, cudaStream_t st) {
+    const int tw = (1 << g.tile_log2) < g.W ? (1 << g.tile_log2) : g.W;
+    if (tw % 32) {   // tiles narrower than a word share words: the decoder ORs into zeroed planes
+        cudaMemsetAsync(at<char>(ws, L.map_bits), 0, (size_t)g.B * g.HW / 8, st);
+        if (want_eta) cudaMemsetAsync(at<char>(ws, L.eta_bits), 0, (size_t)g.B * g.HW / 8, st);
+    }
+    run_kernel(K_LMR_DECODE, st, (long long)g.B * g.HW, [&] {
+        launch_lmr_decode(g, want_eta, marked, at<uint8_t>(ws, L.mbuf), at<int32_t>(ws, L.lmr_b),
+                          at<int32_t>(ws, L.lmr_t), at<int32_t>(ws, L.offsets), at<int32_t>(ws, L.sizes),
+                          at<uint32_t>(ws, L.eta_bits), at<uint32_t>(ws, L.map_bits), img_status, msg_bits_out, st);
+    }, 3);
+}
 
 }  // namespace mmsb
 
@@ -84,17 +149,43 @@ mmsb_status mmsb_content_owner_encode(const mmsb_shape *shape, const uint8_t *im
         return MMSB_E_INVAL;
     const Layout L = layout(g);
     if (ws_bytes < L.total) return MMSB_E_INVAL;
-    if (g.method != 0) return MMSB_E_UNIMPLEMENTED;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     for (int g0 = 0; g0 < g.B; g0 += L.G) {
         const int n = g.B - g0 < L.G ? g.B - g0 : L.G;
         if (cudaMemsetAsync(at<char>(ws, L.pyr), 0, L.tile_zero_end - L.pyr, st) != cudaSuccess) return MMSB_E_CUDA;
-        launch_ks_tile(g, n, k1 + (size_t)g0 * 32, images + (size_t)g0 * g.HW, at<uint8_t>(ws, L.s),
-                       at<uint64_t>(ws, L.rec), at<uint32_t>(ws, L.pyr), at<uint32_t>(ws, L.hist), st);
-        launch_perm_encode(g, n, images + (size_t)g0 * g.HW, at<uint8_t>(ws, L.s), at<uint64_t>(ws, L.rec),
-                           at<uint32_t>(ws, L.pyr), at<uint32_t>(ws, L.hist), encrypted + (size_t)g0 * g.HW,
-                           at<uint8_t>(ws, L.ceta), b_out + g0, capacity_out + g0, img_status + g0, st);
-        g_launches += 2;
+        const long long px = (long long)n * g.HW;
+        run_kernel(K_KS_ENC, st, px, [&] {
+            launch_ks_tile(g, n, k1 + (size_t)g0 * 32, images + (size_t)g0 * g.HW, at<uint8_t>(ws, L.s),
+                           at<uint64_t>(ws, L.rec), at<uint32_t>(ws, L.pyr), at<uint32_t>(ws, L.hist),
+                           at<uint32_t>(ws, L.tdone), at<int32_t>(ws, L.fwd), at<int32_t>(ws, L.inv), st);
+        });
+        run_kernel(K_PERM_ENC, st, px, [&] {
+            launch_perm_encode(g, n, images + (size_t)g0 * g.HW, at<uint8_t>(ws, L.s), at<uint64_t>(ws, L.rec),
+                               at<uint32_t>(ws, L.pyr), at<uint32_t>(ws, L.hist), at<int32_t>(ws, L.inv),
+                               encrypted + (size_t)g0 * g.HW,
+                               at<uint8_t>(ws, L.ceta), b_out + g0, capacity_out + g0, img_status + g0, st);
+        });
+        if (g.method == 1) {
+            // LMR: code eta and the candidate maps until both fit the MSB plane, then write it
+            Geo gg = g;
+            gg.B = n;
+            LmrPlan *plan = at<LmrPlan>(ws, L.plan);
+            run_kernel(K_LMR_PLAN, st, px, [&] { launch_lmr_plan(gg, at<uint32_t>(ws, L.hist), plan, st); });
+            for (int w = 0; w < 7; w++) {
+                run_kernel(K_CODER_ENC, st, px, [&] {
+                    launch_coder_encode(gg, w, at<uint8_t>(ws, L.ceta), plan, at<uint8_t>(ws, L.streams),
+                                        at<int32_t>(ws, L.sizes), st);
+                });
+                run_kernel(K_LMR_FIT, st, px, [&] {
+                    launch_lmr_fit(gg, w, at<int32_t>(ws, L.sizes), plan, at<int32_t>(ws, L.offsets), st);
+                });
+            }
+            run_kernel(K_LMR_MSB, st, px, [&] {
+                launch_lmr_msb_write(gg, plan, at<int32_t>(ws, L.sizes), at<int32_t>(ws, L.offsets),
+                                     at<uint8_t>(ws, L.streams), at<uint32_t>(ws, L.hist),
+                                     encrypted + (size_t)g0 * g.HW, b_out + g0, capacity_out + g0, img_status + g0, st);
+            });
+        }
     }
     return check_launch();
 }
@@ -108,14 +199,15 @@ mmsb_status mmsb_hider_embed(const mmsb_shape *shape, const uint8_t *encrypted, 
     if (stride_bytes <= 0 || stride_bytes % 16 || marked == encrypted) return MMSB_E_INVAL;
     const Layout L = layout(g);
     if (ws_bytes < L.total) return MMSB_E_INVAL;
-    if (g.method != 0) return MMSB_E_UNIMPLEMENTED;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (cudaMemsetAsync(at<char>(ws, L.ticket), 0, L.scan_zero_end - L.ticket, st) != cudaSuccess) return MMSB_E_CUDA;
+    if (g.method == 1) lmr_decode_all(g, L, false, encrypted, ws, img_status, nullptr, st);
     ScanWS sw{at<unsigned int>(ws, L.ticket), at<unsigned long long>(ws, L.states), at<unsigned int>(ws, L.done),
               at<unsigned long long>(ws, L.parts), at<uint32_t>(ws, L.hdr)};
-    launch_scan(g, true, encrypted, marked, k2, msg_bytes, msg_bits, stride_bytes, nullptr, nullptr, img_status, sw,
-                at<uint32_t>(ws, L.map_bits), at<int32_t>(ws, L.lmr_b), st);
-    g_launches += 1;
+    run_kernel(K_EMBED, st, (long long)g.B * g.HW, [&] {
+        launch_scan(g, true, encrypted, marked, k2, msg_bytes, msg_bits, stride_bytes, nullptr, nullptr, img_status,
+                    sw, at<uint32_t>(ws, L.map_bits), at<int32_t>(ws, L.lmr_b), st);
+    });
     return check_launch();
 }
 
@@ -125,18 +217,19 @@ mmsb_status mmsb_receiver_extract(const mmsb_shape *shape, const uint8_t *marked
     Geo g;
     if (!geo_of(shape, &g) || !marked || !k2 || !msg_out || !msg_bits_out || !img_status || !ws)
         return MMSB_E_INVAL;
-    // every capacity (<= 7 bits per pixel) must fit the caller's rows
-    if (stride_bytes <= 0 || stride_bytes % 16 || stride_bytes < (7 * g.HW + 7) / 8) return MMSB_E_INVAL;
+    // a capacity region larger than the caller's rows is reported per image (E_INVAL status)
+    if (stride_bytes <= 0 || stride_bytes % 16) return MMSB_E_INVAL;
     const Layout L = layout(g);
     if (ws_bytes < L.total) return MMSB_E_INVAL;
-    if (g.method != 0) return MMSB_E_UNIMPLEMENTED;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (cudaMemsetAsync(at<char>(ws, L.ticket), 0, L.scan_zero_end - L.ticket, st) != cudaSuccess) return MMSB_E_CUDA;
+    if (g.method == 1) lmr_decode_all(g, L, false, marked, ws, img_status, msg_bits_out, st);
     ScanWS sw{at<unsigned int>(ws, L.ticket), at<unsigned long long>(ws, L.states), at<unsigned int>(ws, L.done),
               at<unsigned long long>(ws, L.parts), at<uint32_t>(ws, L.hdr)};
-    launch_scan(g, false, marked, nullptr, k2, nullptr, nullptr, stride_bytes, msg_out, msg_bits_out, img_status, sw,
-                at<uint32_t>(ws, L.map_bits), at<int32_t>(ws, L.lmr_b), st);
-    g_launches += 1;
+    run_kernel(K_EXTRACT, st, (long long)g.B * g.HW, [&] {
+        launch_scan(g, false, marked, nullptr, k2, nullptr, nullptr, stride_bytes, msg_out, msg_bits_out,
+                    img_status, sw, at<uint32_t>(ws, L.map_bits), at<int32_t>(ws, L.lmr_b), st);
+    });
     return check_launch();
 }
 
@@ -147,18 +240,23 @@ mmsb_status mmsb_receiver_recover(const mmsb_shape *shape, const uint8_t *marked
     if (!geo_of(shape, &g) || !marked || !k1 || !recovered || !img_status || !ws) return MMSB_E_INVAL;
     const Layout L = layout(g);
     if (ws_bytes < L.total) return MMSB_E_INVAL;
-    if (g.method != 0) return MMSB_E_UNIMPLEMENTED;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (g.method == 1) lmr_decode_all(g, L, true, marked, ws, img_status, nullptr, st);
     for (int g0 = 0; g0 < g.B; g0 += L.G) {
         const int n = g.B - g0 < L.G ? g.B - g0 : L.G;
         if (cudaMemsetAsync(at<char>(ws, L.pyr), 0, L.tile_zero_end - L.pyr, st) != cudaSuccess) return MMSB_E_CUDA;
-        launch_ks_tile(g, n, k1 + (size_t)g0 * 32, nullptr, at<uint8_t>(ws, L.s), at<uint64_t>(ws, L.rec),
-                       at<uint32_t>(ws, L.pyr), at<uint32_t>(ws, L.hist), st);
-        launch_recover_strip(g, n, marked + (size_t)g0 * g.HW, at<uint8_t>(ws, L.s), at<uint64_t>(ws, L.rec),
-                             at<uint32_t>(ws, L.pyr), at<uint32_t>(ws, L.eta_bits) + (size_t)g0 * g.HW / 32,
-                             at<uint32_t>(ws, L.map_bits) + (size_t)g0 * g.HW / 32, at<int32_t>(ws, L.lmr_b) + g0,
-                             recovered + (size_t)g0 * g.HW, img_status + g0, st);
-        g_launches += 2;
+        const long long px = (long long)n * g.HW;
+        run_kernel(K_KS_REC, st, px, [&] {
+            launch_ks_tile(g, n, k1 + (size_t)g0 * 32, nullptr, at<uint8_t>(ws, L.s), at<uint64_t>(ws, L.rec),
+                           at<uint32_t>(ws, L.pyr), at<uint32_t>(ws, L.hist), at<uint32_t>(ws, L.tdone),
+                           at<int32_t>(ws, L.fwd), at<int32_t>(ws, L.inv), st);
+        });
+        run_kernel(K_RECOVER, st, px, [&] {
+            launch_recover_strip(g, n, marked + (size_t)g0 * g.HW, at<uint8_t>(ws, L.s), at<uint64_t>(ws, L.rec),
+                                 at<int32_t>(ws, L.fwd), at<uint32_t>(ws, L.eta_bits) + (size_t)g0 * g.HW / 32,
+                                 at<uint32_t>(ws, L.map_bits) + (size_t)g0 * g.HW / 32,
+                                 at<int32_t>(ws, L.lmr_b) + g0, recovered + (size_t)g0 * g.HW, img_status + g0, st);
+        });
     }
     return check_launch();
 }
@@ -169,8 +267,7 @@ mmsb_status mmsb_stats(const mmsb_shape *shape, const uint8_t *original, const u
     if (!geo_of(shape, &g) || !original || !recovered || !sse_out) return MMSB_E_INVAL;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (cudaMemsetAsync(sse_out, 0, (size_t)g.B * 8, st) != cudaSuccess) return MMSB_E_CUDA;
-    launch_stats(g.HW, g.B, original, recovered, sse_out, st);
-    g_launches += 1;
+    run_kernel(K_STATS, st, (long long)g.B * g.HW, [&] { launch_stats(g.HW, g.B, original, recovered, sse_out, st); });
     return check_launch();
 }
 
@@ -198,5 +295,32 @@ const char *mmsb_status_string(mmsb_status s) {
 }
 
 uint64_t mmsb_kernel_launches(void) { return g_launches.load(); }
+
+void mmsb_profile_enable(int on) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    for (auto &r : g_prof) { g_event_pool.push_back(r.a); g_event_pool.push_back(r.b); }
+    g_prof.clear();
+    g_prof_on = on != 0;
+}
+
+int mmsb_profile_read(int kernel, const char **name, double *total_ms, int64_t *launches, int64_t *units) {
+    if (kernel < 0 || kernel >= K_COUNT) return -1;
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    double t = 0;
+    int64_t n = 0, u = 0;
+    for (auto &r : g_prof) {
+        if (r.id != kernel) continue;
+        float ms = 0;
+        if (cudaEventElapsedTime(&ms, r.a, r.b) != cudaSuccess) return -2;
+        t += ms;
+        n++;
+        u += r.units;
+    }
+    if (name) *name = kKernelNames[kernel];
+    if (total_ms) *total_ms = t;
+    if (launches) *launches = n;
+    if (units) *units = u;
+    return K_COUNT;
+}
 
 }  // extern "C"

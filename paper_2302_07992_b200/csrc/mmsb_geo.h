@@ -4,8 +4,8 @@
 
 namespace mmsb {
 
-constexpr int kChunk = 8192;        // raster pixels per scan chunk (embed / extract)
-constexpr int kScanThreads = 256;   // 2 rounds x 256 threads x 16 px
+constexpr int kScanThreads = 128;   // threads per scan CTA
+constexpr int kChunk = 2 * kScanThreads * 16;   // raster pixels per scan chunk: 2 rounds x 16 px per thread
 constexpr int kRecSlots = 64;       // u64 slots of a tile's in-tile angle record
 
 struct Geo {
@@ -23,6 +23,7 @@ struct Geo {
     int npyr;            // counters per image
     int nchunks;         // scan chunks per image
     int tile_log2;       // LMR coder tile side 2^t
+    int ntiles_coder;    // LMR coder tiles per plane
 };
 
 inline int ilog2(long long v) {
@@ -36,7 +37,7 @@ inline bool make_geo(int method, int B, int H, int W, int tile_log2, Geo *g) {
     if ((H & (H - 1)) || (W & (W - 1))) return false;
     if (method != 0 && method != 1) return false;
     if (tile_log2 == 0) tile_log2 = 7;
-    if (tile_log2 < 3 || tile_log2 > 9) return false;
+    if (tile_log2 < 3 || tile_log2 > 7) return false;   // GPU coder rows hold <= 128 pixels
     g->method = method;
     g->B = B;
     g->H = H; g->W = W;
@@ -58,6 +59,10 @@ inline bool make_geo(int method, int B, int H, int W, int tile_log2, Geo *g) {
     g->npyr = p;
     g->nchunks = (int)((g->HW + kChunk - 1) / kChunk);
     g->tile_log2 = tile_log2;
+    {
+        const int th = (1 << tile_log2) < H ? (1 << tile_log2) : H, tw = (1 << tile_log2) < W ? (1 << tile_log2) : W;
+        g->ntiles_coder = ((H + th - 1) / th) * ((W + tw - 1) / tw);
+    }
     return true;
 }
 

@@ -15,23 +15,34 @@ struct ScanWS {
     uint32_t *hdr;                   // [B] frame length word (extract)
 };
 
-struct LmrWS {
-    uint8_t *ceta;                   // [G][H][W] rotated (I & 0x80) | label c
-    uint32_t *eta_bits;              // [B][H*W/32] decoded rotated eta (MSB map)
-    uint32_t *map_bits;              // [B][H*W/32] decoded rotated location map
-    int32_t *b;                      // [B] decoded b (<= 0: bad / malformed)
-    uint8_t *streams;                // coder output scratch
-    int32_t *sizes;                  // per tile byte counts
-    int32_t *cand;                   // per image candidate state
+// LMR encode state of one image: candidate order (P:985 walk), decision and header length K
+struct LmrPlan {
+    int8_t order[7];
+    int8_t state;                    // 0 undecided, 1 fits (b), 2 bad case
+    int32_t b;
+    long long K;                     // MSB-plane bits used: 7 + 32 T + 8 (bytes_eta + bytes_map)
 };
 
+void launch_lmr_plan(const Geo &g, const uint32_t *hist, LmrPlan *plan, cudaStream_t st);
+void launch_coder_encode(const Geo &g, int wave, const uint8_t *ceta, const LmrPlan *plan, uint8_t *streams,
+                         int32_t *sizes, cudaStream_t st);
+void launch_lmr_fit(const Geo &g, int wave, const int32_t *sizes, LmrPlan *plan, int32_t *offsets, cudaStream_t st);
+void launch_lmr_msb_write(const Geo &g, const LmrPlan *plan, const int32_t *sizes, const int32_t *offsets,
+                          const uint8_t *streams, const uint32_t *hist, uint8_t *enc, int32_t *b_out, int64_t *cap_out,
+                          int32_t *status, cudaStream_t st);
+void launch_lmr_decode(const Geo &g, bool want_eta, const uint8_t *marked, uint8_t *mbuf, int32_t *lmr_b,
+                       int32_t *lmr_t, int32_t *offsets, int32_t *sizes, uint32_t *eta_bits, uint32_t *map_bits,
+                       int32_t *status, int64_t *msg_bits_out, cudaStream_t st);
+int lmr_tile_cap_host(int t, int H, int W);
+
 void launch_ks_tile(const Geo &g, int G, const uint8_t *keys, const uint8_t *images, uint8_t *s, uint64_t *rec,
-                    uint32_t *pyr, uint32_t *hist, cudaStream_t st);
+                    uint32_t *pyr, uint32_t *hist, uint32_t *done, int32_t *fwd_map, int32_t *inv_map,
+                    cudaStream_t st);
 void launch_perm_encode(const Geo &g, int G, const uint8_t *images, const uint8_t *s, const uint64_t *rec,
-                        const uint32_t *pyr, const uint32_t *hist, uint8_t *enc, uint8_t *ceta, int32_t *b_out,
-                        int64_t *cap_out, int32_t *status, cudaStream_t st);
+                        const uint32_t *pyr, const uint32_t *hist, const int32_t *inv_map, uint8_t *enc,
+                        uint8_t *ceta, int32_t *b_out, int64_t *cap_out, int32_t *status, cudaStream_t st);
 void launch_recover_strip(const Geo &g, int G, const uint8_t *marked, const uint8_t *s, const uint64_t *rec,
-                          const uint32_t *pyr, const uint32_t *eta, const uint32_t *map, const int32_t *lmr_b,
+                          const int32_t *fwd_map, const uint32_t *eta, const uint32_t *map, const int32_t *lmr_b,
                           uint8_t *out, int32_t *status, cudaStream_t st);
 void launch_scan(const Geo &g, bool embed, const uint8_t *in, uint8_t *out, const uint8_t *keys, const uint8_t *msg,
                  const int64_t *msg_bits, long long stride, uint8_t *msg_out, int64_t *msg_bits_out, int32_t *status,
