@@ -419,8 +419,8 @@ def kernel_model(name, der):
         "ks_tile_kernel": dict(bytes=0.0, ops=CHACHA_OPS_PER_BYTE * 1.0),
         "perm_encode_kernel": dict(bytes=2.0, ops=0.0),
         "recover_strip_kernel": dict(bytes=2.0, ops=0.0),
-        "scan_kernel<embed>": dict(bytes=2.0 + d8, ops=CHACHA_OPS_PER_BYTE * d8),
-        "scan_kernel<extract>": dict(bytes=1.0 + d8, ops=CHACHA_OPS_PER_BYTE * d8),
+        "scan_kernel<embed>+finish": dict(bytes=2.0 + d8, ops=CHACHA_OPS_PER_BYTE * d8),
+        "scan_kernel<extract>+finish": dict(bytes=1.0 + d8, ops=CHACHA_OPS_PER_BYTE * d8),
         "stats_kernel": dict(bytes=2.0, ops=0.0),
     }.get(name, dict(bytes=0.0, ops=0.0))
 

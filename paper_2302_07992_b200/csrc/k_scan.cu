@@ -7,40 +7,27 @@
 // rotated domain, in raster order (Q18), carry b' bits each: EMR b' = b at bit positions
 // 1..b, LMR b' = b-1 at positions 2..b.  Zero pixel j carries frame bits
 // [j b', (j+1) b'); only bits < |F| are written (Q19).
+//
+// One CTA (256 threads) per 16384-pixel raster chunk, in blockIdx order (chunk-major within
+// an image).  The chunk arrives in shared memory by one bulk copy (cp.async.bulk + mbarrier),
+// so the whole chunk is in flight before any thread computes; thread t owns the 16-pixel
+// groups t, t+256, t+512, t+768 of the chunk.  A chunk publishes its zero count (aggregate)
+// and, once the look-back has found its prefix, its inclusive count; the K2 keystream of the
+// chunk's frame bits is one ChaCha20 block per thread.  The per-image epilogue (capacity and
+// integrity checks, boundary words of the extracted string) runs in a second small kernel, so
+// the chunk CTAs retire without a grid-wide completion counter.
 #include "mmsb_device.cuh"
 #include "mmsb_kernels.h"
 
 namespace mmsb {
 
 constexpr unsigned long long kFlagAgg = 1ull << 62, kFlagInc = 2ull << 62, kValMask = (1ull << 62) - 1;
-constexpr int kKbufWords = kChunk * 7 / 32 + 64;   // bits of one chunk + block alignment + pad
+constexpr int kMaxBlk = kChunk * 7 / 512 + 2;          // ChaCha blocks a chunk's bits can touch
+constexpr int kKbufWords = kMaxBlk * 16 + 2;
 
-__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t x, uint32_t *wsum, uint32_t &total) {
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    uint32_t v = x;
-#pragma unroll
-    for (int s = 1; s < 32; s <<= 1) {
-        uint32_t t = __shfl_up_sync(0xffffffffu, v, s);
-        if (lane >= s) v += t;
-    }
-    if (lane == 31) wsum[wid] = v;
-    __syncthreads();
-    uint32_t off = 0, tot = 0;
-#pragma unroll
-    for (int w = 0; w < kScanThreads / 32; w++) {
-        const uint32_t ws = wsum[w];
-        if (w < wid) off += ws;
-        tot += ws;
-    }
-    __syncthreads();
-    total = tot;
-    return off + v - x;
-}
-
-// 16 zero-pixel flags of the pixels [p, p+16) of image img (bit i = pixel p+i is redundant)
+// 16 zero-pixel flags of the pixels [p, p+16) of the chunk (bit i = pixel p+i is redundant)
 template <int METHOD>
-__device__ __forceinline__ uint32_t zero_mask16(const uint4 &u, long long p, long long bitbase,
-                                                const uint32_t *__restrict__ map_bits) {
+__device__ __forceinline__ uint32_t zero_mask16(const uint4 &u, long long p_img, const uint32_t *smap, int p_rel) {
     if constexpr (METHOD == 0) {
         const uint32_t w[4] = {u.x, u.y, u.z, u.w};
         uint32_t m = 0;
@@ -49,89 +36,116 @@ __device__ __forceinline__ uint32_t zero_mask16(const uint4 &u, long long p, lon
             const uint32_t l = ~w[i] & 0x01010101u;              // LSB == 0 -> redundant
             m |= ((l | (l >> 7) | (l >> 14) | (l >> 21)) & 0xFu) << (4 * i);
         }
-        if (p == 0) m &= ~7u;                                    // r = 0..2 hold the header (Q14)
+        if (p_img == 0) m &= ~7u;                                // r = 0..2 hold the header (Q14)
         return m;
     } else {
-        const long long bit = bitbase + p;
-        return ~(__ldg(map_bits + (bit >> 5)) >> (bit & 31)) & 0xFFFFu;
+        return ~(smap[p_rel >> 5] >> (p_rel & 31)) & 0xFFFFu;
     }
 }
 
-// ---- per-thread bit streams of 16 pixels, specialised on b' (bits per redundant pixel) and
-// on the bit position of the carried field (SHIFT = 8 - b for EMR, 7 - b' for LMR).
+// ---- per-thread bit streams of 16 pixels, specialised on b' (BP, bits per redundant pixel)
+// and on the bit position of the carried field (SHIFT = 8 - b for EMR, 7 - b' for LMR).
+// Both directions work on one 32-bit word (4 pixels) at a time with byte permutes: the
+// fields of the set pixels of a word are consecutive in the frame stream, so a word needs
+// one 32-bit window of the stream and one PRMT whose selector depends only on the word's
+// 4-bit zero mask m4 (tables esel / csel in shared memory).
+//   esel[m4] nibble i = number of set bits of m4 below i   (stream field -> pixel byte)
+//   csel[m4] nibble k = index of the k-th set bit, 4 (zero byte) past popc(m4)
 
-// embed: the zero pixels of mm receive consecutive b'-bit groups of the frame bits held in
-// kbuf (big-endian bit order), starting at relative bit `rel`; bits at or past `fend` are
-// not written (a partially filled last pixel keeps its remaining bits, reading Q19).
+// 4 consecutive BP-bit fields, MSB-first at the top of x, -> byte i = field i at bit SHIFT
 template <int BP, int SHIFT>
-__device__ __forceinline__ void embed16(uint32_t w[4], uint32_t mm, const uint32_t *kbuf, long long rel,
-                                        long long fend) {
-    const int cnt = __popc(mm);
-    if (!cnt || rel >= fend) return;
-    constexpr uint32_t FM = ((1u << BP) - 1u) << SHIFT;
-    if (rel + (long long)cnt * BP <= fend) {
-        int wi = (int)(rel >> 5);
-        const int off = (int)(rel & 31);
-        unsigned long long win = (((unsigned long long)kbuf[wi] << 32) | kbuf[wi + 1]) << off;
-        int avail = 64 - off;
-        wi += 2;
+__device__ __forceinline__ uint32_t fields_to_bytes(uint32_t x) {
+    uint32_t e = 0;
 #pragma unroll
-        for (int i = 0; i < 16; i++) {
-            if ((mm >> i) & 1u) {
-                if (avail < BP) {
-                    win |= (unsigned long long)kbuf[wi++] << (32 - avail);
-                    avail += 32;
-                }
-                const uint32_t val = (uint32_t)(win >> (64 - BP));
-                w[i >> 2] = (w[i >> 2] & ~(FM << (8 * (i & 3)))) | (val << (SHIFT + 8 * (i & 3)));
-                win <<= BP;
-                avail -= BP;
-            }
-        }
-    } else {
-        long long k = rel;
+    for (int i = 0; i < 4; i++) {
+        constexpr uint32_t FM = ((1u << BP) - 1u) << SHIFT;
+        const int sh = 32 - (i + 1) * BP - (8 * i + SHIFT);     // right shift placing field i
+        const uint32_t t = sh >= 0 ? (x >> sh) : (x << -sh);
+        e |= t & (FM << (8 * i));
+    }
+    return e;
+}
+// byte k (field value < 2^BP) -> BP-bit fields MSB-first at the top of the result
+template <int BP>
+__device__ __forceinline__ uint32_t bytes_to_fields(uint32_t c) {
+    uint32_t p = 0;
 #pragma unroll
-        for (int i = 0; i < 16; i++) {
-            if (((mm >> i) & 1u) && k < fend) {
-                const int nb = (fend - k) < BP ? (int)(fend - k) : BP;
-                const int wv = (int)(k >> 5), off = (int)(k & 31);
-                const unsigned long long win = ((unsigned long long)kbuf[wv] << 32) | kbuf[wv + 1];
-                const uint32_t val = (uint32_t)(win >> (64 - off - BP)) & ((1u << BP) - 1u);
-                const uint32_t msk = (((1u << nb) - 1u) << (BP - nb)) << SHIFT;
-                w[i >> 2] = (w[i >> 2] & ~(msk << (8 * (i & 3)))) | (((val << SHIFT) & msk) << (8 * (i & 3)));
-            }
-            if ((mm >> i) & 1u) k += BP;
+    for (int k = 0; k < 4; k++) {
+        const int sh = 32 - (k + 1) * BP - 8 * k;                // left shift placing byte k
+        const uint32_t t = sh >= 0 ? (c << sh) : (c >> -sh);
+        p |= t & (((1u << BP) - 1u) << (32 - (k + 1) * BP));
+    }
+    return p;
+}
+__device__ __forceinline__ uint32_t mask4_to_bytes(uint32_t m4) { return ((m4 & 0xFu) * 0x00204081u) & 0x01010101u; }
+
+// embed (fast path: every field of the group lies below the frame end): the set pixels of
+// the 16-pixel group receive consecutive BP-bit fields of the stream in kbuf from bit `rel`
+template <int BP, int SHIFT>
+__device__ __forceinline__ void embed16(uint32_t w[4], uint32_t mm, const uint32_t *kbuf, int rel,
+                                        const uint32_t *esel) {
+    constexpr uint32_t FMB = ((1u << BP) - 1u) << SHIFT;
+    int o = rel;
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+        const uint32_t m4 = (mm >> (4 * j)) & 0xFu;
+        const int wi = o >> 5;
+        const uint32_t x = __funnelshift_l(kbuf[wi + 1], kbuf[wi], o);   // stream bits [o, o+32)
+        const uint32_t e = fields_to_bytes<BP, SHIFT>(x);
+        const uint32_t v = __byte_perm(e, 0, esel[m4]);
+        const uint32_t msk = mask4_to_bytes(m4) * FMB;
+        w[j] = (w[j] & ~msk) | (v & msk);
+        o += BP * __popc(m4);
+    }
+}
+
+// embed, general path (the group reaches the frame end `fend`): bit by bit, bits at or past
+// fend untouched (a partially filled last pixel keeps its remaining bits, reading Q19)
+template <int BP, int SHIFT>
+__device__ __noinline__ void embed16_tail(uint32_t w[4], uint32_t mm, const uint32_t *kbuf, long long rel,
+                                          long long fend) {
+    long long k = rel;
+    for (int i = 0; i < 16; i++) {
+        if (!((mm >> i) & 1u)) continue;
+        for (int t = 0; t < BP; t++, k++) {
+            if (k >= fend) return;
+            const uint32_t bit = (kbuf[k >> 5] >> (31 - (k & 31))) & 1u;
+            const int pos = 8 * (i & 3) + SHIFT + BP - 1 - t;
+            w[i >> 2] = (w[i >> 2] & ~(1u << pos)) | (bit << pos);
         }
     }
 }
 
-// extract: the zero pixels' b'-bit fields are appended in raster order and ORed into kbuf at
-// relative bit `rel`; the first and the last (partial) words are shared with the neighbouring
-// threads (shared-memory atomics), the words in between belong to this thread alone.
+// extract: the set pixels' BP-bit fields appended in raster order, ORed into kbuf from bit
+// `rel`; the first and last (partial) words are shared with the neighbouring threads
+// (shared-memory atomics), the words in between belong to this thread alone.
 template <int BP, int SHIFT>
-__device__ __forceinline__ void extract16(const uint32_t w[4], uint32_t mm, uint32_t *kbuf, long long rel) {
-    if (!mm) return;
-    int wi = (int)(rel >> 5);
-    int nacc = (int)(rel & 31);                 // leading pad (zeros) up to the word boundary
+__device__ __forceinline__ void extract16(const uint32_t w[4], uint32_t mm, uint32_t *kbuf, int rel,
+                                          const uint32_t *csel) {
+    constexpr uint32_t FB = ((1u << BP) - 1u) * 0x01010101u;
+    int wi = rel >> 5;
+    int nacc = rel & 31;                        // valid bits at the top of acc (leading pad = 0)
     unsigned long long acc = 0;
     bool first = true;
 #pragma unroll
-    for (int i = 0; i < 16; i++) {
-        if ((mm >> i) & 1u) {
-            const uint32_t val = (w[i >> 2] >> (8 * (i & 3) + SHIFT)) & ((1u << BP) - 1u);
-            acc = (acc << BP) | val;
-            nacc += BP;
-            if (nacc >= 32) {
-                const uint32_t word = (uint32_t)(acc >> (nacc - 32));
-                if (first) atomicOr(&kbuf[wi], word);
-                else kbuf[wi] = word;
-                first = false;
-                wi++;
-                nacc -= 32;
-            }
+    for (int j = 0; j < 4; j++) {
+        const uint32_t m4 = (mm >> (4 * j)) & 0xFu;
+        const uint32_t t = (w[j] >> SHIFT) & FB;                  // byte i = field of pixel i
+        const uint32_t c = __byte_perm(t, 0, csel[m4]);           // set pixels' fields, in order
+        const uint32_t p = bytes_to_fields<BP>(c);
+        acc |= ((unsigned long long)p << 32) >> nacc;
+        nacc += BP * __popc(m4);
+        if (nacc >= 32) {
+            const uint32_t word = (uint32_t)(acc >> 32);
+            if (first) atomicOr(&kbuf[wi], word);
+            else kbuf[wi] = word;
+            first = false;
+            wi++;
+            acc <<= 32;
+            nacc -= 32;
         }
     }
-    if (nacc > 0) atomicOr(&kbuf[wi], (uint32_t)(acc & ((1ull << nacc) - 1ull)) << (32 - nacc));
+    if (nacc > 0 && (nacc > (rel & 31) || !first)) atomicOr(&kbuf[wi], (uint32_t)(acc >> 32));
 }
 
 #define MMSB_BP_SWITCH(bp, METHOD, BODY)                                                   \
@@ -145,192 +159,215 @@ __device__ __forceinline__ void extract16(const uint32_t w[4], uint32_t mm, uint
         default: { constexpr int BP = 7, SH = (METHOD == 0 ? 8 : 7) - 7; BODY; } break;    \
     }
 
+// b of an image as the hider / K2 receiver sees it: EMR from the 3 header LSBs (Q14; FORMAT
+// if > 5 -> 0), LMR from the decoded MSB-plane header (0 on BADCASE / FORMAT)
+template <int METHOD>
+__device__ __forceinline__ int image_b(const uint8_t *img0, const int32_t *lmr_b, int img) {
+    if constexpr (METHOD == 0) {
+        const int field = ((img0[0] & 1) << 2) | ((img0[1] & 1) << 1) | (img0[2] & 1);
+        return field > 5 ? 0 : field + 2;
+    } else {
+        return lmr_b[img];
+    }
+}
+
 template <int METHOD, bool EMBED>
-__global__ void __launch_bounds__(kScanThreads, 8) scan_kernel(Geo g, const uint8_t *__restrict__ in,
+__global__ void __launch_bounds__(kScanThreads, 4) scan_kernel(Geo g, const uint8_t *__restrict__ in,
                                                             uint8_t *__restrict__ out, const uint8_t *__restrict__ keys,
                                                             const uint8_t *__restrict__ msg,
                                                             const int64_t *__restrict__ msg_bits, long long stride,
-                                                            uint8_t *__restrict__ msg_out,
-                                                            int64_t *__restrict__ msg_bits_out,
-                                                            int32_t *__restrict__ status, ScanWS ws,
+                                                            uint8_t *__restrict__ msg_out, ScanWS ws,
                                                             const uint32_t *__restrict__ map_bits,
                                                             const int32_t *__restrict__ lmr_b) {
-    __shared__ uint32_t wsum[kScanThreads / 32];
-    __shared__ uint32_t kbuf[kKbufWords];
-    __shared__ long long sh_ll[4];
-    __shared__ int sh_i[4];
+    __shared__ __align__(128) uint4 spx[kChunk / 16];
+    __shared__ __align__(16) uint32_t smap[METHOD == 1 ? kChunk / 32 : 4];
+    __shared__ __align__(16) uint32_t kbuf[kKbufWords];
+    __shared__ __align__(8) uint64_t bar;
+    __shared__ uint32_t wtot[kScanThreads / 32][kScanRounds];
+    __shared__ long long sh_prefix;
+    __shared__ uint32_t esel[16], csel[16];
 
-    const int tid = threadIdx.x;
-    if (tid == 0) sh_i[0] = (int)atomicAdd(ws.ticket, 1u);
-    __syncthreads();
-    const int ticket = sh_i[0];
-    const int img = ticket / g.nchunks, chunk = ticket % g.nchunks;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int img = blockIdx.x / g.nchunks, chunk = blockIdx.x % g.nchunks;
+    const int cpx = g.HW < kChunk ? (int)g.HW : kChunk;      // pixels of this chunk
+    const long long p0 = (long long)chunk * cpx;
     const uint8_t *src = in + (size_t)img * g.HW;
 
-    int b, bp;
-    if constexpr (METHOD == 0) {
-        const int field = ((src[0] & 1) << 2) | ((src[1] & 1) << 1) | (src[2] & 1);
-        b = field > 5 ? 0 : field + 2;
-        bp = b;
-    } else {
-        b = lmr_b[img];
-        bp = b - 1;
+    if (tid == 0) {
+        mbar_init(&bar, 1);
+        const unsigned bytes = (unsigned)cpx + (METHOD == 1 ? (unsigned)cpx / 8 : 0u);
+        mbar_expect_tx(&bar, bytes);
+        bulk_g2s(spx, src + p0, (unsigned)cpx, &bar);
+        if constexpr (METHOD == 1)
+            bulk_g2s(smap, map_bits + ((size_t)img * g.HW + p0) / 32, (unsigned)cpx / 8, &bar);
     }
-    const long long p0 = (long long)chunk * kChunk;
-    if (b < 2) {                                            // FORMAT (EMR) / BADCASE, FORMAT (LMR)
+    if (tid < 16) {                                          // PRMT selector tables (see embed16)
+        uint32_t e = 0, c = 0;
+        int k = 0;
+        for (int i = 0; i < 4; i++) {
+            e |= (uint32_t)__popc(tid & ((1 << i) - 1)) << (4 * i);
+            if ((tid >> i) & 1) c |= (uint32_t)i << (4 * k++);
+        }
+        for (; k < 4; k++) c |= 4u << (4 * k);
+        esel[tid] = e;
+        csel[tid] = c;
+    }
+    const int b = image_b<METHOD>(src, lmr_b, img);
+    const int bp = METHOD == 0 ? b : b - 1;
+    uint32_t key[8];
+    load_key(keys, img, key);
+    long long n = 0;
+    if constexpr (EMBED) n = msg_bits[img];
+    __syncthreads();                                         // barrier initialised
+    mbar_wait(&bar, 0);
+
+    if (b < 2) {                                             // FORMAT (EMR) / BADCASE, FORMAT (LMR)
         if constexpr (EMBED) {
-            for (long long p = p0 + tid * 16; p < p0 + kChunk && p < g.HW; p += kScanThreads * 16)
-                *reinterpret_cast<uint4 *>(out + (size_t)img * g.HW + p) =
-                    __ldg(reinterpret_cast<const uint4 *>(src + p));
+            for (int q = tid; q < cpx / 16; q += kScanThreads)
+                *reinterpret_cast<uint4 *>(out + (size_t)img * g.HW + p0 + 16 * q) = spx[q];
         }
-        if (chunk == 0 && tid == 0) {
-            if constexpr (METHOD == 0) status[img] = 8;
-            if constexpr (!EMBED) msg_bits_out[img] = -1;
-        }
-        return;
+        return;                                              // statuses: scan_finish_kernel
     }
 
-    // ---- per-thread zero masks (2 rounds x 16 px) and the block-local exclusive scan
-    uint4 pix[2];
-    uint32_t m[2], cnt[2], excl[2], tot[2];
+    // ---- per-thread zero masks and counts, round r = 16-pixel group tid + 256 r
+    // (the pixels stay in shared memory; they are re-read after the keystream phase)
+    uint32_t m[kScanRounds];
 #pragma unroll
-    for (int r = 0; r < 2; r++) {
-        const long long p = p0 + r * (kScanThreads * 16) + tid * 16;
-        if (p < g.HW) {
-            pix[r] = __ldg(reinterpret_cast<const uint4 *>(src + p));
-            m[r] = zero_mask16<METHOD>(pix[r], p, (long long)img * g.HW, map_bits);
-        } else {
-            pix[r] = make_uint4(0, 0, 0, 0);
-            m[r] = 0;
-        }
-        cnt[r] = __popc(m[r]);
+    for (int r = 0; r < kScanRounds; r++) {
+        const int q = r * kScanThreads + tid;
+        m[r] = 16 * q < cpx ? zero_mask16<METHOD>(spx[q], p0 + 16 * q, smap, 16 * q) : 0u;
     }
-    excl[0] = block_exclusive_scan(cnt[0], wsum, tot[0]);
-    excl[1] = block_exclusive_scan(cnt[1], wsum, tot[1]) + tot[0];
-    const unsigned long long agg = (unsigned long long)tot[0] + tot[1];
+    // warp-inclusive scans of the 4 round counts, two per packed u32 (counts <= 512 per warp)
+    uint32_t c01 = __popc(m[0]) | ((uint32_t)__popc(m[1]) << 16);
+    uint32_t c23 = __popc(m[2]) | ((uint32_t)__popc(m[3]) << 16);
+    uint32_t i01 = c01, i23 = c23;
+#pragma unroll
+    for (int s = 1; s < 32; s <<= 1) {
+        const uint32_t t01 = __shfl_up_sync(0xffffffffu, i01, s), t23 = __shfl_up_sync(0xffffffffu, i23, s);
+        if (lane >= s) { i01 += t01; i23 += t23; }
+    }
+    if (lane == 31) {
+        wtot[wid][0] = i01 & 0xFFFFu; wtot[wid][1] = i01 >> 16;
+        wtot[wid][2] = i23 & 0xFFFFu; wtot[wid][3] = i23 >> 16;
+    }
+    __syncthreads();
+    // exclusive offset of each of this thread's groups inside the chunk, and the chunk total
+    uint32_t excl[kScanRounds];
+    uint32_t agg = 0;
+    {
+        const uint32_t e01 = i01 - c01, e23 = i23 - c23;
+        const uint32_t ein[4] = {e01 & 0xFFFFu, e01 >> 16, e23 & 0xFFFFu, e23 >> 16};
+#pragma unroll
+        for (int r = 0; r < kScanRounds; r++) {
+            uint32_t before = 0;
+#pragma unroll
+            for (int w = 0; w < kScanThreads / 32; w++) before += w < wid ? wtot[w][r] : 0u;
+            excl[r] = agg + before + ein[r];
+#pragma unroll
+            for (int w = 0; w < kScanThreads / 32; w++) agg += wtot[w][r];
+        }
+    }
 
-    // ---- single-pass decoupled look-back over the image's chunks (ticket order = issue order).
-    // Warp 0 publishes this chunk's aggregate, then inspects 32 predecessors per probe: every
-    // lane spins on its own predecessor until that one has published, the nearest inclusive
-    // prefix ends the walk, aggregates in front of it are summed (warp reduction).
-    if (tid < 32) {
+    // ---- single-pass decoupled look-back over the image's chunks (blockIdx order).  Warp 0
+    // publishes the aggregate, then inspects 32 predecessors per probe: each lane spins on its
+    // own predecessor until it has published; the nearest inclusive prefix ends the walk and
+    // the aggregates in front of it are summed.
+    if (wid == 0) {
         unsigned long long *st = ws.states + (size_t)img * g.nchunks;
         unsigned long long prefix = 0;
         if (chunk == 0) {
-            if (tid == 0) st_release(st, kFlagInc | agg);
+            if (lane == 0) st_relaxed(st, kFlagInc | agg);
         } else {
-            if (tid == 0) st_release(st + chunk, kFlagAgg | agg);
+            if (lane == 0) st_relaxed(st + chunk, kFlagAgg | agg);
             int base = chunk - 1;
             while (true) {
-                const int k = base - tid;
+                const int k = base - lane;
                 unsigned long long v = kFlagInc;                 // before chunk 0: inclusive 0
                 if (k >= 0) {
-                    do { v = ld_acquire(st + k); } while ((v & ~kValMask) == 0);
+                    do { v = ld_relaxed(st + k); } while ((v & ~kValMask) == 0);
                 }
                 const unsigned inc = __ballot_sync(0xffffffffu, (v & ~kValMask) == kFlagInc);
                 const int last = inc ? __ffs(inc) - 1 : 31;
-                unsigned long long val = tid <= last ? (v & kValMask) : 0ull;
+                unsigned long long val = lane <= last ? (v & kValMask) : 0ull;
 #pragma unroll
                 for (int s2 = 16; s2 > 0; s2 >>= 1) val += __shfl_xor_sync(0xffffffffu, val, s2);
                 prefix += val;
                 if (inc) break;
                 base -= 32;
             }
-            if (tid == 0) st_release(st + chunk, kFlagInc | (prefix + agg));
+            if (lane == 0) st_relaxed(st + chunk, kFlagInc | (prefix + agg));
         }
-        if (tid == 0) sh_ll[0] = (long long)prefix;
+        if (lane == 0) sh_prefix = (long long)prefix;
     }
     __syncthreads();
-    const long long prefix = sh_ll[0];
+    const long long prefix = sh_prefix;
     const long long lo = prefix * bp, hi = (prefix + (long long)agg) * bp;
 
-    uint32_t key[8];
-    load_key(keys, img, key);
-
     if constexpr (EMBED) {
-        const long long n = msg_bits[img];
         const bool n_ok = n >= 0 && n <= 8 * stride && n <= 0xFFFFFFFFll;
         const long long F = n_ok ? 32 + n : 0;
         const long long hie = hi < F ? hi : F;
         const long long blk0 = lo >> 9;
-        if (lo < hie) {
-            const int nblk = (int)(((hie - 1) >> 9) - blk0 + 1);
-            const uint8_t *mimg = msg + (size_t)img * stride;
-            for (int t0 = 0; t0 < nblk; t0 += kScanThreads / 4) {       // 4 lanes per ChaCha block
-                const int t = t0 + (tid >> 2), cl = tid & 3;
-                uint32_t ks[4];
-                chacha20_block_x4(key, (uint32_t)(blk0 + t), ks);
-                if (t < nblk) {
+        const int nblk = lo < hie ? (int)(((hie - 1) >> 9) - blk0 + 1) : 0;
+        if (tid < nblk) {
+            // frame words [16 (blk0 + tid), +16): word 0 = n, word i >= 1 = message word i - 1
+            const long long fw0 = (blk0 + tid) * 16;
+            uint32_t ks[16];
+            chacha20_block(key, (uint32_t)(blk0 + tid), ks);
+            const uint32_t *mw = reinterpret_cast<const uint32_t *>(msg + (size_t)img * stride);
+            const long long nmw = stride / 4;                    // message words in the row
 #pragma unroll
-                    for (int j = 0; j < 4; j++) {
-                        const long long wi = (blk0 + t) * 16 + 4 * j + cl;   // frame word index (BE)
-                        uint32_t fw;
-                        if (wi == 0) fw = (uint32_t)n;
-                        else if (4 * wi <= stride) fw = bswap32(__ldg(reinterpret_cast<const uint32_t *>(mimg) + (wi - 1)));
-                        else fw = 0;
-                        kbuf[t * 16 + 4 * j + cl] = fw ^ bswap32(ks[j]);
-                    }
-                }
+            for (int j = 0; j < 16; j++) {
+                const long long wi = fw0 + j;
+                uint32_t fw;
+                if (wi == 0) fw = (uint32_t)n;
+                else if (wi - 1 < nmw) fw = bswap32(__ldg(mw + (wi - 1)));
+                else fw = 0;
+                kbuf[tid * 16 + j] = fw ^ bswap32(ks[j]);
             }
-            if (tid == 0) kbuf[nblk * 16] = 0;
         }
         __syncthreads();
         const long long base = blk0 * 512;
-#pragma unroll
-        for (int r = 0; r < 2; r++) {
-            const long long p = p0 + r * (kScanThreads * 16) + tid * 16;
-            if (p >= g.HW) continue;
-            uint32_t w[4] = {pix[r].x, pix[r].y, pix[r].z, pix[r].w};
-            const long long rel = (prefix + excl[r]) * bp - base;
-            MMSB_BP_SWITCH(bp, METHOD, (embed16<BP, SH>(w, m[r], kbuf, rel, hie - base)))
-            *reinterpret_cast<uint4 *>(out + (size_t)img * g.HW + p) = make_uint4(w[0], w[1], w[2], w[3]);
-        }
-        // ---- the image's last CTA decides the capacity outcome (32 + n <= C)
-        __syncthreads();
-        if (tid == 0) {
-            __threadfence();
-            sh_i[1] = atomicAdd(ws.done + img, 1u) == (unsigned)(g.nchunks - 1);
-        }
-        __syncthreads();
-        if (sh_i[1]) {
-            __threadfence();
-            const unsigned long long last = ld_acquire(ws.states + (size_t)img * g.nchunks + g.nchunks - 1);
-            const long long C = (long long)(last & kValMask) * bp;
-            const bool fits = n_ok && 32 + n <= C;
-            if (!fits) {                                         // CAPACITY: marked = encrypted
-                for (long long p = tid * 16; p < g.HW; p += kScanThreads * 16)
-                    *reinterpret_cast<uint4 *>(out + (size_t)img * g.HW + p) =
-                        __ldg(reinterpret_cast<const uint4 *>(src + p));
+        const long long fend = hie - base;
+        uint8_t *dst = out + (size_t)img * g.HW + p0;
+        MMSB_BP_SWITCH(bp, METHOD, ({
+            _Pragma("unroll 1")
+            for (int r = 0; r < kScanRounds; r++) {
+                const int q = r * kScanThreads + tid;
+                if (16 * q >= cpx) continue;
+                const uint4 u = spx[q];
+                uint32_t w[4] = {u.x, u.y, u.z, u.w};
+                const long long rel = (prefix + excl[r]) * BP - base;
+                const int cnt = __popc(m[r]);
+                if (cnt && rel < fend) {
+                    if (rel + (long long)cnt * BP <= fend) embed16<BP, SH>(w, m[r], kbuf, (int)rel, esel);
+                    else embed16_tail<BP, SH>(w, m[r], kbuf, rel, fend);
+                }
+                *reinterpret_cast<uint4 *>(dst + 16 * q) = make_uint4(w[0], w[1], w[2], w[3]);
             }
-            if (tid == 0) status[img] = fits ? 0 : (n_ok ? 3 : 2);
-        }
+        }))
     } else {
         // ---- extract: gather the chunk's bit string G[lo, hi) into smem, XOR KS2, write words
         const long long blk0 = lo >> 9;
         const long long base = blk0 * 512, basew = blk0 * 16;
-        int nblk = 0;
-        if (lo < hi) {
-            nblk = (int)(((hi - 1) >> 9) - blk0 + 1);
-            for (int t = tid; t < nblk * 16 + 1; t += kScanThreads) kbuf[t] = 0;
-        }
+        const int nblk = lo < hi ? (int)(((hi - 1) >> 9) - blk0 + 1) : 0;
+        for (int t = tid; t < nblk * 16 + 1; t += kScanThreads) kbuf[t] = 0;
         __syncthreads();
-        if (lo < hi) {
-#pragma unroll
-            for (int r = 0; r < 2; r++) {
-                const uint32_t w[4] = {pix[r].x, pix[r].y, pix[r].z, pix[r].w};
-                const long long rel = (prefix + excl[r]) * bp - base;
-                MMSB_BP_SWITCH(bp, METHOD, (extract16<BP, SH>(w, m[r], kbuf, rel)))
+        MMSB_BP_SWITCH(bp, METHOD, ({
+            _Pragma("unroll 1")
+            for (int r = 0; r < kScanRounds; r++) {
+                if (!m[r]) continue;
+                const uint4 u = spx[r * kScanThreads + tid];
+                const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+                extract16<BP, SH>(w, m[r], kbuf, (int)((prefix + excl[r]) * BP - base), csel);
             }
-        }
+        }))
+        uint32_t ks[16];
+        if (tid < nblk) chacha20_block(key, (uint32_t)(blk0 + tid), ks);
         __syncthreads();
-        for (int t0 = 0; t0 < nblk; t0 += kScanThreads / 4) {           // 4 lanes per ChaCha block
-            const int t = t0 + (tid >> 2), cl = tid & 3;
-            uint32_t ks[4];
-            chacha20_block_x4(key, (uint32_t)(blk0 + t), ks);
-            if (t < nblk) {
+        if (tid < nblk) {
 #pragma unroll
-                for (int j = 0; j < 4; j++) kbuf[t * 16 + 4 * j + cl] ^= bswap32(ks[j]);
-            }
+            for (int j = 0; j < 16; j++) kbuf[tid * 16 + j] ^= bswap32(ks[j]);
         }
         __syncthreads();
         uint32_t *mo = reinterpret_cast<uint32_t *>(msg_out + (size_t)img * stride);
@@ -340,62 +377,96 @@ __global__ void __launch_bounds__(kScanThreads, 8) scan_kernel(Geo g, const uint
             for (long long W = w0 + tid; W <= w1; W += kScanThreads) {
                 const long long s0 = W * 32 > lo ? W * 32 : lo;
                 const long long e0 = W * 32 + 32 < hi ? W * 32 + 32 : hi;
-                uint32_t v = kbuf[W - basew];
+                const uint32_t v = kbuf[W - basew];
                 if (s0 == W * 32 && e0 == W * 32 + 32) {
                     if (W == 0) ws.hdr[img] = v;
                     else if (4 * W <= stride) mo[W - 1] = bswap32(v);
-                } else {
+                } else {                                     // shared word: merged by scan_finish
                     const int len = (int)(e0 - s0), st0 = (int)(s0 - W * 32);
                     const uint32_t msk = (len == 32 ? 0xFFFFFFFFu : ((1u << len) - 1u)) << (32 - st0 - len);
                     parts[W == w0 ? 0 : 1] = ((unsigned long long)(W + 1) << 32) | (v & msk);
                 }
             }
         }
-        // ---- the image's last CTA: combine boundary words, check the length, zero the tail
-        __syncthreads();
+    }
+}
+
+// ======================================================================================
+// scan_finish_kernel: one CTA per image, after the chunk kernel.
+//   embed:   C = b' * (inclusive zero count of the last chunk); status OK if 32 + n <= C
+//            (P:750), else CAPACITY (E_INVAL for an invalid n) and the marked image is reset
+//            to the encrypted one; EMR FORMAT (b-field > 5) -> status FORMAT.
+//   extract: merges the boundary words of the extracted string (several chunks can share a
+//            word), checks n = BE32 header <= C - 32 (else INTEGRITY, nothing kept), zeroes
+//            the capacity region past n.
+// ======================================================================================
+template <int METHOD, bool EMBED>
+__global__ void __launch_bounds__(256) scan_finish_kernel(Geo g, const uint8_t *__restrict__ in,
+                                                          uint8_t *__restrict__ out,
+                                                          const int64_t *__restrict__ msg_bits, long long stride,
+                                                          uint8_t *__restrict__ msg_out,
+                                                          int64_t *__restrict__ msg_bits_out,
+                                                          int32_t *__restrict__ status, ScanWS ws,
+                                                          const int32_t *__restrict__ lmr_b) {
+    __shared__ long long sh[2];
+    const int img = blockIdx.x, tid = threadIdx.x;
+    const uint8_t *src = in + (size_t)img * g.HW;
+    const int b = image_b<METHOD>(src, lmr_b, img);
+    if (b < 2) {
         if (tid == 0) {
-            __threadfence();
-            sh_i[1] = atomicAdd(ws.done + img, 1u) == (unsigned)(g.nchunks - 1);
+            if constexpr (METHOD == 0) status[img] = 8;      // FORMAT; LMR: set by the decoder
+            if constexpr (!EMBED) msg_bits_out[img] = -1;
+        }
+        return;
+    }
+    const int bp = METHOD == 0 ? b : b - 1;
+    const unsigned long long last = ld_acquire(ws.states + (size_t)img * g.nchunks + g.nchunks - 1);
+    const long long C = (long long)(last & kValMask) * bp;
+    if constexpr (EMBED) {
+        const long long n = msg_bits[img];
+        const bool n_ok = n >= 0 && n <= 8 * stride && n <= 0xFFFFFFFFll;
+        const bool fits = n_ok && 32 + n <= C;
+        if (tid == 0) status[img] = fits ? 0 : (n_ok ? 3 : 2);
+        if (!fits) {                                          // CAPACITY: marked = encrypted
+            for (long long p = tid * 16; p < g.HW; p += 256 * 16)
+                *reinterpret_cast<uint4 *>(out + (size_t)img * g.HW + p) =
+                    __ldg(reinterpret_cast<const uint4 *>(src + p));
+        }
+    } else {
+        uint32_t *mo = reinterpret_cast<uint32_t *>(msg_out + (size_t)img * stride);
+        const unsigned long long *pp = ws.parts + (size_t)img * g.nchunks * 2;
+        const long long rw = C > 32 ? (C - 32 + 31) / 32 : 0;
+        const bool fits = 4 * rw <= stride;
+        // shared words: zero them, then OR every part in (byte order commutes with OR)
+        for (int k = tid; k < 2 * g.nchunks; k += 256) {
+            const unsigned long long v = __ldcg(pp + k);
+            if (!v) continue;
+            const long long W = (long long)(v >> 32) - 1;
+            if (W == 0) ws.hdr[img] = 0;
+            else if (4 * W <= stride) mo[W - 1] = 0;
         }
         __syncthreads();
-        if (!sh_i[1]) return;
-        __threadfence();
+        for (int k = tid; k < 2 * g.nchunks; k += 256) {
+            const unsigned long long v = __ldcg(pp + k);
+            if (!v) continue;
+            const long long W = (long long)(v >> 32) - 1;
+            if (W == 0) atomicOr(ws.hdr + img, (uint32_t)v);
+            else if (4 * W <= stride) atomicOr(mo + (W - 1), bswap32((uint32_t)v));
+        }
+        __syncthreads();
         if (tid == 0) {
-            const unsigned long long *pp = ws.parts + (size_t)img * g.nchunks * 2;
-            long long cw = -1;
-            uint32_t cv = 0;
-            for (int k = 0; k < 2 * g.nchunks; k++) {
-                const unsigned long long v = __ldcg(pp + k);
-                if (!v) continue;
-                const long long W = (long long)(v >> 32) - 1;
-                if (W == cw) {
-                    cv |= (uint32_t)v;
-                } else {
-                    if (cw == 0) ws.hdr[img] = cv;
-                    else if (cw > 0 && 4 * cw <= stride) mo[cw - 1] = bswap32(cv);
-                    cw = W;
-                    cv = (uint32_t)v;
-                }
-            }
-            if (cw == 0) ws.hdr[img] = cv;
-            else if (cw > 0 && 4 * cw <= stride) mo[cw - 1] = bswap32(cv);
-            __threadfence_block();
-            const unsigned long long last = ld_acquire(ws.states + (size_t)img * g.nchunks + g.nchunks - 1);
-            const long long C = (long long)(last & kValMask) * bp;
-            const long long rw = C > 32 ? (C - 32 + 31) / 32 : 0;
-            const bool fits = 4 * rw <= stride;
             const long long n = C >= 32 ? (long long)__ldcg(ws.hdr + img) : -1;
             const bool ok = fits && C >= 32 && n <= C - 32;
-            sh_ll[1] = fits ? C : 0;
-            sh_ll[2] = ok ? n : -1;
+            sh[0] = fits ? C : 0;
+            sh[1] = ok ? n : -1;
             msg_bits_out[img] = ok ? n : -1;
-            status[img] = ok ? 0 : (fits ? 4 : 2);           // region beyond the caller's rows: E_INVAL
+            status[img] = ok ? 0 : (fits ? 4 : 2);            // region beyond the caller's rows: E_INVAL
         }
         __syncthreads();
-        const long long C = sh_ll[1], n = sh_ll[2];
-        const long long region_w = C > 32 ? (C - 32 + 31) / 32 : 0;
-        const long long keep = n < 0 ? 0 : n;                  // INTEGRITY -> zero everything
-        for (long long W = keep / 32 + tid; W < region_w; W += kScanThreads) {
+        const long long Cf = sh[0], nn = sh[1];
+        const long long region_w = Cf > 32 ? (Cf - 32 + 31) / 32 : 0;
+        const long long keep = nn < 0 ? 0 : nn;                // INTEGRITY -> zero everything
+        for (long long W = keep / 32 + tid; W < region_w; W += 256) {
             uint32_t v = 0;
             if (W == keep / 32 && (keep & 31)) v = bswap32(__ldcg(mo + W)) & ~(0xFFFFFFFFu >> (keep & 31));
             mo[W] = bswap32(v);
@@ -409,8 +480,10 @@ static void launch_scan_t(const Geo &g, const uint8_t *in, uint8_t *out, const u
                           int32_t *status, const ScanWS &ws, const uint32_t *map_bits, const int32_t *lmr_b,
                           cudaStream_t st) {
     const unsigned grid = (unsigned)((long long)g.B * g.nchunks);
-    scan_kernel<METHOD, EMBED><<<grid, kScanThreads, 0, st>>>(g, in, out, keys, msg, msg_bits, stride, msg_out,
-                                                              msg_bits_out, status, ws, map_bits, lmr_b);
+    scan_kernel<METHOD, EMBED><<<grid, kScanThreads, 0, st>>>(g, in, out, keys, msg, msg_bits, stride, msg_out, ws,
+                                                              map_bits, lmr_b);
+    scan_finish_kernel<METHOD, EMBED><<<g.B, 256, 0, st>>>(g, in, out, msg_bits, stride, msg_out, msg_bits_out,
+                                                           status, ws, lmr_b);
 }
 
 void launch_scan(const Geo &g, bool embed, const uint8_t *in, uint8_t *out, const uint8_t *keys, const uint8_t *msg,

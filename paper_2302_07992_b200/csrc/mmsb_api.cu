@@ -19,7 +19,7 @@ static std::atomic<unsigned long long> g_launches{0};
 enum KernelId { K_KS_ENC = 0, K_KS_REC, K_PERM_ENC, K_RECOVER, K_EMBED, K_EXTRACT, K_STATS, K_LMR_PLAN,
                 K_CODER_ENC, K_LMR_FIT, K_LMR_MSB, K_LMR_DECODE, K_COUNT };
 static const char *kKernelNames[K_COUNT] = {"ks_tile_kernel<hist>", "ks_tile_kernel", "perm_encode_kernel",
-                                            "recover_strip_kernel", "scan_kernel<embed>", "scan_kernel<extract>",
+                                            "recover_strip_kernel", "scan_kernel<embed>+finish", "scan_kernel<extract>+finish",
                                             "stats_kernel", "lmr_plan_kernel", "coder_encode_kernel",
                                             "lmr_fit_kernel", "lmr_msb_write_kernel",
                                             "lmr_pack+header+coder_decode_kernels"};
@@ -62,7 +62,7 @@ static size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
 struct Layout {
     int G;
     size_t s, rec, fwd, inv, pyr, hist, tdone, tile_zero_end; // per-group tile state
-    size_t ticket, states, done, parts, hdr, scan_zero_end;  // per-call scan state
+    size_t states, parts, hdr, scan_zero_end;  // per-call scan state
     size_t ceta, eta_bits, map_bits, lmr_b, lmr_t, plan, streams, sizes, offsets, mbuf, total;
 };
 
@@ -81,9 +81,7 @@ static Layout layout(const Geo &g) {
     L.hist = o; o = align256(o + (size_t)G * 8 * 4);
     L.tdone = o; o = align256(o + (size_t)G * 4);
     L.tile_zero_end = o;
-    L.ticket = o; o = align256(o + 16);
     L.states = o; o = align256(o + (size_t)g.B * g.nchunks * 8);
-    L.done = o; o = align256(o + (size_t)g.B * 4);
     L.parts = o; o = align256(o + (size_t)g.B * g.nchunks * 16);
     L.hdr = o; o = align256(o + (size_t)g.B * 4);
     L.scan_zero_end = o;
@@ -200,14 +198,13 @@ mmsb_status mmsb_hider_embed(const mmsb_shape *shape, const uint8_t *encrypted, 
     const Layout L = layout(g);
     if (ws_bytes < L.total) return MMSB_E_INVAL;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if (cudaMemsetAsync(at<char>(ws, L.ticket), 0, L.scan_zero_end - L.ticket, st) != cudaSuccess) return MMSB_E_CUDA;
+    if (cudaMemsetAsync(at<char>(ws, L.states), 0, L.scan_zero_end - L.states, st) != cudaSuccess) return MMSB_E_CUDA;
     if (g.method == 1) lmr_decode_all(g, L, false, encrypted, ws, img_status, nullptr, st);
-    ScanWS sw{at<unsigned int>(ws, L.ticket), at<unsigned long long>(ws, L.states), at<unsigned int>(ws, L.done),
-              at<unsigned long long>(ws, L.parts), at<uint32_t>(ws, L.hdr)};
+    ScanWS sw{at<unsigned long long>(ws, L.states), at<unsigned long long>(ws, L.parts), at<uint32_t>(ws, L.hdr)};
     run_kernel(K_EMBED, st, (long long)g.B * g.HW, [&] {
         launch_scan(g, true, encrypted, marked, k2, msg_bytes, msg_bits, stride_bytes, nullptr, nullptr, img_status,
                     sw, at<uint32_t>(ws, L.map_bits), at<int32_t>(ws, L.lmr_b), st);
-    });
+    }, 2);
     return check_launch();
 }
 
@@ -222,14 +219,13 @@ mmsb_status mmsb_receiver_extract(const mmsb_shape *shape, const uint8_t *marked
     const Layout L = layout(g);
     if (ws_bytes < L.total) return MMSB_E_INVAL;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if (cudaMemsetAsync(at<char>(ws, L.ticket), 0, L.scan_zero_end - L.ticket, st) != cudaSuccess) return MMSB_E_CUDA;
+    if (cudaMemsetAsync(at<char>(ws, L.states), 0, L.scan_zero_end - L.states, st) != cudaSuccess) return MMSB_E_CUDA;
     if (g.method == 1) lmr_decode_all(g, L, false, marked, ws, img_status, msg_bits_out, st);
-    ScanWS sw{at<unsigned int>(ws, L.ticket), at<unsigned long long>(ws, L.states), at<unsigned int>(ws, L.done),
-              at<unsigned long long>(ws, L.parts), at<uint32_t>(ws, L.hdr)};
+    ScanWS sw{at<unsigned long long>(ws, L.states), at<unsigned long long>(ws, L.parts), at<uint32_t>(ws, L.hdr)};
     run_kernel(K_EXTRACT, st, (long long)g.B * g.HW, [&] {
         launch_scan(g, false, marked, nullptr, k2, nullptr, nullptr, stride_bytes, msg_out, msg_bits_out,
                     img_status, sw, at<uint32_t>(ws, L.map_bits), at<int32_t>(ws, L.lmr_b), st);
-    });
+    }, 2);
     return check_launch();
 }
 

@@ -4,8 +4,9 @@
 
 namespace mmsb {
 
-constexpr int kScanThreads = 128;   // threads per scan CTA
-constexpr int kChunk = 2 * kScanThreads * 16;   // raster pixels per scan chunk: 2 rounds x 16 px per thread
+constexpr int kScanThreads = 256;   // threads per scan CTA
+constexpr int kScanRounds = 4;      // 16-pixel groups per thread
+constexpr int kChunk = kScanRounds * kScanThreads * 16;   // raster pixels per scan chunk (16384)
 constexpr int kRecSlots = 64;       // u64 slots of a tile's in-tile angle record
 
 struct Geo {

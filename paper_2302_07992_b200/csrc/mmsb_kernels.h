@@ -8,9 +8,7 @@
 namespace mmsb {
 
 struct ScanWS {
-    unsigned int *ticket;            // CTA issue order (decoupled look-back needs it)
-    unsigned long long *states;      // [B][nchunks] flag | value
-    unsigned int *done;              // [B] finished chunks (last CTA does the per-image fixup)
+    unsigned long long *states;      // [B][nchunks] flag | value (decoupled look-back)
     unsigned long long *parts;       // [B][nchunks][2] boundary words of the extracted bit string
     uint32_t *hdr;                   // [B] frame length word (extract)
 };
