@@ -1,0 +1,743 @@
+// k_fused.cu -- the content owner's encode and the K1 receiver's recovery, each ONE launch
+// over the whole batch (sm_100a).  Citations: P:<line> = /root/reference/PAPER.md; design
+// and roofline: DESIGN.md §5.
+//
+// Each launch mixes two CTA roles, scheduled by blockIdx in image groups:
+//   K (keystream) CTAs  -- a4: ChaCha20(K1) for TPC tiles (one 64-byte block per tile row,
+//       P:656, Q12), the tile's in-tile angle record (levels 1..tp, eq. roration),
+//       the tile total into the upper angle pyramid, and (encode) the per-image label
+//       histogram (eq. gliding1/2 P:604-625 reduce to the left neighbour).  The
+//       keystream goes to a tile-major scratch that only one consumer reads.
+//   W (worker) CTAs -- one per tile, after the image's K CTAs have signalled:
+//       encode (perm_role): a3 + a5, destination tile <- permuted source tile (+ left halo),
+//       location map into the LSB (EMR) or label plane for the coder (LMR), XOR s.
+//       recover (rec_role): a10, original tile <- de-permuted destination tile, decrypted,
+//       rows copied forward with the carry from the tile to the left found by a per-row
+//       decoupled look-back (the copy-forward of P:837 / P:1061 is a scan along each row).
+// Grid order: K(0) | K(1) W(0) | K(2) W(1) | ... | W(n-1): the keystream of group g+1 runs
+// while group g is permuted; a W CTA only ever waits for K CTAs dispatched before it.
+// The consumed keystream tile and angle record are dropped from L2 (discard.global.L2),
+// so the scratch never costs HBM bandwidth.
+#include "mmsb_device.cuh"
+#include "mmsb_kernels.h"
+
+namespace mmsb {
+
+struct Role {
+    int key, img, idx;
+};
+
+__device__ __forceinline__ Role role_of(const FusedSched &sc, int x) {
+    const int SK = sc.GI * sc.nK, SW = sc.GI * sc.nW;
+    int key, grp, loc;
+    if (x < SK) {
+        key = 1; grp = 0; loc = x;
+    } else {
+        const int x2 = x - SK, pair = x2 / (SK + SW), off = x2 % (SK + SW);
+        if (pair < sc.ngroups - 1 && off < SK) { key = 1; grp = pair + 1; loc = off; }
+        else { key = 0; grp = pair; loc = pair < sc.ngroups - 1 ? off - SK : off; }
+    }
+    Role r;
+    r.key = key;
+    r.img = grp * sc.GI + loc / (key ? sc.nK : sc.nW);
+    r.idx = loc % (key ? sc.nK : sc.nW);
+    return r;
+}
+
+// destination tile -> source tile under the levels above the tile (walk e = emax .. tp+1)
+__device__ __forceinline__ void upper_walk_inverse(const Geo &g, const uint32_t *pyr_img, int dty, int dtx,
+                                                   int &sty, int &stx, int &q) {
+    int y = dty, x = dtx;
+    q = 0;
+    for (int e = g.emax; e > g.tp; e--) {
+        const int k = e - g.tp, m1 = (1 << k) - 1;
+        const int by = y >> k, bx = x >> k;
+        const int a = (int)(__ldcg(pyr_img + g.pyr_off[e] + by * (g.W >> e) + bx) & 3u);
+        int oy = y & m1, ox = x & m1;
+        inv_turn(a, m1, oy, ox);
+        y = (by << k) | oy;
+        x = (bx << k) | ox;
+        q += a;
+    }
+    sty = y; stx = x; q &= 3;
+}
+
+// original tile -> destination tile (walk e = tp+1 .. emax)
+__device__ __forceinline__ void upper_walk_forward(const Geo &g, const uint32_t *pyr_img, int oty, int otx,
+                                                   int &dty, int &dtx, int &q) {
+    int y = oty, x = otx;
+    q = 0;
+    for (int e = g.tp + 1; e <= g.emax; e++) {
+        const int k = e - g.tp, m1 = (1 << k) - 1;
+        const int by = y >> k, bx = x >> k;
+        const int a = (int)(__ldcg(pyr_img + g.pyr_off[e] + by * (g.W >> e) + bx) & 3u);
+        int oy = y & m1, ox = x & m1;
+        fwd_turn(a, m1, oy, ox);
+        y = (by << k) | oy;
+        x = (bx << k) | ox;
+        q += a;
+    }
+    dty = y; dtx = x; q &= 3;
+}
+
+// EMR optimal b from the non-redundant counts (eq. optimial_b; ties -> smaller b)
+__device__ __forceinline__ int emr_select_b(const uint32_t *hist_img, long long HW) {
+    int best = 2;
+    long long bestv = 2 * (HW - (long long)__ldcg(hist_img + 2));
+    for (int b = 3; b <= 7; b++) {
+        const long long v = (long long)b * (HW - (long long)__ldcg(hist_img + b));
+        if (v > bestv) { best = b; bestv = v; }
+    }
+    return best;
+}
+
+__device__ __forceinline__ void wait_keys(const TileWS &ws, int img, int nK) {
+    while (ld_acquire_u32(ws.kdone + img) < (unsigned)nK) __nanosleep(128);
+}
+
+// ======================================================================================
+// K role: one thread per tile row, TPC = 256 / T tiles per CTA.
+// ======================================================================================
+template <int TP, bool HIST>
+__device__ __forceinline__ void key_role(const Geo &g, int img, int kidx, const uint8_t *__restrict__ keys,
+                                         const uint8_t *__restrict__ images, const TileWS &ws, uint8_t *smem) {
+    constexpr int T = 1 << TP, NW = T / 4, TPC = 256 / T;
+    uint64_t(*rec)[kRecSlots] = reinterpret_cast<uint64_t(*)[kRecSlots]>(smem);
+
+    const int tid = threadIdx.x, lt = tid / T, row = tid % T;
+    const int tile = kidx * TPC + lt;
+    const bool valid = tile < g.ntiles;
+    const int ty = valid ? tile / g.tilesX : 0, tx = valid ? tile % g.tilesX : 0;
+    const long long o = (long long)(ty * T + row) * g.W + (long long)tx * T;
+
+    uint32_t key[8];
+    load_key(keys, img, key);
+    uint32_t blk[16];
+    chacha20_block(key, (uint32_t)(o >> 6), blk);
+    uint32_t w[NW];
+    if constexpr (NW == 16) {
+#pragma unroll
+        for (int i = 0; i < 16; i++) w[i] = blk[i];
+    } else {
+        const int boff = (int)((o & 63) >> 2);
+#pragma unroll
+        for (int i = 0; i < NW; i++) w[i] = blk[boff + i];
+    }
+    // keystream row -> tile-major scratch (a warp writes whole tiles rows: contiguous)
+    if (valid) {
+        uint8_t *sd = ws.s + ((size_t)img * g.ntiles + tile) * (T * T) + row * T;
+#pragma unroll
+        for (int i = 0; i < NW; i += 4)
+            *reinterpret_cast<uint4 *>(sd + 4 * i) = make_uint4(w[i], w[i + 1], w[i + 2], w[i + 3]);
+    }
+
+    // level 1: 2x2 block sums mod 4 -- horizontal pair sums per row, then the partner row
+    uint64_t h1 = 0;
+#pragma unroll
+    for (int i = 0; i < NW; i++) {
+        const uint32_t v = w[i] & 0x03030303u;
+        const uint32_t p = (v + (v >> 8)) & 0x00030003u;
+        const uint32_t q = (p & 3u) | ((p >> 14) & 0xCu);
+        h1 |= (uint64_t)q << (4 * i);
+    }
+    const uint64_t partner = __shfl_xor_sync(0xffffffffu, h1, 1);
+    if ((row & 1) == 0) rec[lt][g.lvl_off[1] + row / 2] = add2(h1, partner);
+
+    if constexpr (HIST) {
+        // label histogram of this tile row: for b = 2..8, pixels with c < b (non-redundant),
+        // i.e. x = p ^ left >= 2^(8-b).  Bit-smear x into a thermometer code y, then count
+        // bit (8-b) of y with byte-lane counters (<= 16 * 8 per lane: no overflow).
+        const uint8_t *src = images + (size_t)img * g.HW + o;
+        uint32_t iw[NW];
+#pragma unroll
+        for (int i = 0; i < NW; i += 4) {
+            const uint4 u = valid ? __ldg(reinterpret_cast<const uint4 *>(src) + i / 4) : make_uint4(0, 0, 0, 0);
+            iw[i] = u.x; iw[i + 1] = u.y; iw[i + 2] = u.z; iw[i + 3] = u.w;
+        }
+        uint32_t prev = (valid && tx > 0) ? ((uint32_t)__ldg(src - 1) << 24) : 0u;
+        uint32_t acc[7] = {0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+        for (int i = 0; i < NW; i++) {
+            const uint32_t left = __byte_perm(prev, iw[i], 0x6543);   // [prev.b3, w.b0, w.b1, w.b2]
+            uint32_t x = iw[i] ^ left;
+            if (i == 0 && tx == 0) x |= 0xFFu;                     // column 0 is non-redundant
+            prev = iw[i];
+            uint32_t y = x | ((x >> 1) & 0x7F7F7F7Fu);
+            y |= (y >> 2) & 0x3F3F3F3Fu;
+            y |= (y >> 4) & 0x0F0F0F0Fu;                           // byte = 2^bitlen(x) - 1
+            const uint32_t y4 = (y >> 4) & 0x0F0F0F0Fu;
+            acc[0] += y & 0x01010101u; acc[1] += y & 0x02020202u;
+            acc[2] += y & 0x04040404u; acc[3] += y & 0x08080808u;
+            acc[4] += y4 & 0x01010101u; acc[5] += y4 & 0x02020202u; acc[6] += y4 & 0x04040404u;
+        }
+#pragma unroll
+        for (int k = 0; k < 7; k++) {                              // threshold bit k <-> b = 8 - k
+            uint32_t v = valid ? (((acc[k] >> (k & 3)) * 0x01010101u) >> 24) : 0u;
+#pragma unroll
+            for (int s = 16; s > 0; s >>= 1) v += __shfl_xor_sync(0xffffffffu, v, s);
+            if ((tid & 31) == 0 && v) atomicAdd(&ws.hist[img * 8 + 8 - k], v);
+        }
+    }
+    __syncthreads();
+
+    // levels 2..tp: quad-tree sums mod 4 of the level below
+#pragma unroll
+    for (int e = 2; e <= TP; e++) {
+        const int R = T >> e;
+        for (int t = tid; t < TPC * R; t += 256) {
+            const int l2 = t / R, r = t % R;
+            const uint64_t v = add2(rec[l2][g.lvl_off[e - 1] + 2 * r], rec[l2][g.lvl_off[e - 1] + 2 * r + 1]);
+            const uint64_t pe = v & 0x3333333333333333ull, po = (v >> 2) & 0x3333333333333333ull;
+            uint64_t s = (pe + po) & 0x3333333333333333ull;
+            s = (s | (s >> 2)) & 0x0F0F0F0F0F0F0F0Full;
+            s = (s | (s >> 4)) & 0x00FF00FF00FF00FFull;
+            s = (s | (s >> 8)) & 0x0000FFFF0000FFFFull;
+            s = (s | (s >> 16)) & 0x00000000FFFFFFFFull;
+            rec[l2][g.lvl_off[e] + r] = s;
+        }
+        __syncthreads();
+    }
+
+    // upper pyramid: the tile total (= level-tp angle) into every enclosing block
+    if (valid && row == 0) {
+        const uint32_t tv = (uint32_t)(rec[lt][g.lvl_off[TP]] & 3u);
+        if (tv)
+            for (int e = TP + 1; e <= g.emax; e++) {
+                const int k = e - TP;
+                atomicAdd(&ws.pyr[(size_t)img * g.npyr + g.pyr_off[e] + (ty >> k) * (g.W >> e) + (tx >> k)], tv);
+            }
+    }
+    // records out
+    for (int t = tid; t < TPC * kRecSlots; t += 256) {
+        const int l2 = t / kRecSlots, slot = t % kRecSlots;
+        const int tl = kidx * TPC + l2;
+        if (tl < g.ntiles) ws.rec[((size_t)img * g.ntiles + tl) * kRecSlots + slot] = rec[l2][slot];
+    }
+    // publish: every thread's writes fenced, then one arrival per CTA
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) atomicAdd(ws.kdone + img, 1u);
+}
+
+// ======================================================================================
+// W role, encode: one CTA per destination tile (a3, a5).
+//   EMR: carrier v = (I & 0xFE) | l with l = [c < b] (location map), permuted as a
+//        whole byte; E = v_r XOR (s & 0xFE) (eq. image_encryption P:739 + LSB map P:744);
+//        header b-2 in the LSBs of r = 0..2 (Q14).
+//   LMR: E = I_r XOR s; second plane ceta = (I & 0x80) | c permuted alongside (for the coder).
+// ======================================================================================
+template <int TP, int METHOD>
+struct PermSmem {
+    static constexpr int T = 1 << TP, RS = T / 4 + 1;
+    uint8_t ss[T * T];                       // keystream of the destination tile (bulk copy)
+    uint32_t src[T * RS];                    // source tile carrier words (row stride RS)
+    uint32_t lab[METHOD == 1 ? T * RS : 1];  // LMR: label | eta words
+    uint64_t rec[kRecSlots];
+    uint64_t bar;
+    int sh[4];
+};
+
+template <int TP, int METHOD>
+__device__ __forceinline__ void perm_role(const Geo &g, int img, int dtile, int nK, const uint8_t *__restrict__ images,
+                                          const TileWS &ws, uint8_t *__restrict__ enc, uint8_t *__restrict__ ceta_out,
+                                          int32_t *__restrict__ b_out, int64_t *__restrict__ cap_out,
+                                          int32_t *__restrict__ status, uint8_t *smem) {
+    constexpr int T = 1 << TP, RS = T / 4 + 1, NC = T / 4, NCELL = NC * NC, CPT = T * T / 16;
+    PermSmem<TP, METHOD> &S = *reinterpret_cast<PermSmem<TP, METHOD> *>(smem);
+    const int tid = threadIdx.x;
+    const int dty = dtile / g.tilesX, dtx = dtile % g.tilesX;
+    const uint8_t *I = images + (size_t)img * g.HW;
+    const uint8_t *sg = ws.s + ((size_t)img * g.ntiles + dtile) * (T * T);
+
+    if (tid == 0) {
+        wait_keys(ws, img, nK);
+        mbar_init(&S.bar, 1);
+        mbar_expect_tx(&S.bar, T * T);
+        bulk_g2s(S.ss, sg, T * T, &S.bar);
+        int sty, stx, q;
+        upper_walk_inverse(g, ws.pyr + (size_t)img * g.npyr, dty, dtx, sty, stx, q);
+        S.sh[0] = sty * g.tilesX + stx;
+        S.sh[1] = q;
+        S.sh[2] = METHOD == 0 ? emr_select_b(ws.hist + img * 8, g.HW) : 0;
+    }
+    __syncthreads();
+    const int stile = S.sh[0], q_up = S.sh[1], b = S.sh[2];
+    const int sty = stile / g.tilesX, stx = stile % g.tilesX;
+    const uint64_t *recg = ws.rec + ((size_t)img * g.ntiles + stile) * kRecSlots;
+    if (tid < kRecSlots) S.rec[tid] = __ldcg(recg + tid);
+
+    // source tile + left halo -> labels -> carrier (EMR) or I and ceta (LMR)
+    const uint32_t M = METHOD == 0 ? (0xFFu << (8 - b)) & 0xFFu : 0;
+    const uint32_t MB = M * 0x01010101u;
+    for (int c = tid; c < CPT; c += 256) {
+        const int r = c / (T / 16), seg = c % (T / 16);
+        const long long gx = (long long)stx * T + seg * 16;
+        const uint8_t *p = I + (size_t)(sty * T + r) * g.W + gx;
+        const uint4 u = __ldg(reinterpret_cast<const uint4 *>(p));
+        const uint32_t iw[4] = {u.x, u.y, u.z, u.w};
+        uint32_t prev = gx > 0 ? ((uint32_t)__ldg(p - 1) << 24) : 0u;
+        uint32_t vw[4], cw[4];
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            uint32_t x = iw[i] ^ __byte_perm(prev, iw[i], 0x6543);
+            if (i == 0 && gx == 0) x |= 0xFFu;                     // column 0: always non-redundant
+            prev = iw[i];
+            if constexpr (METHOD == 0) {
+                const uint32_t t = x & MB;
+                const uint32_t nz = (((t & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | t) & 0x80808080u;   // byte != 0
+                vw[i] = (iw[i] & 0xFEFEFEFEu) | (nz >> 7);
+            } else {
+                // c = #leading equal bits (8 if equal), per byte; column 0 -> 0
+                uint32_t cv = 0;
+#pragma unroll
+                for (int j = 0; j < 4; j++) {
+                    const uint32_t xb = (x >> (8 * j)) & 0xFFu;
+                    const uint32_t cj = xb ? (uint32_t)(__clz(xb) - 24) : 8u;
+                    cv |= cj << (8 * j);
+                }
+                cw[i] = cv | (iw[i] & 0x80808080u);
+                vw[i] = iw[i];
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            S.src[r * RS + seg * 4 + i] = vw[i];
+            if constexpr (METHOD == 1) S.lab[r * RS + seg * 4 + i] = cw[i];
+        }
+    }
+    mbar_wait(&S.bar, 0);
+    __syncthreads();
+    // the consumed scratch (this tile's keystream, the source tile's record) leaves L2 unwritten
+    if (tid < (T * T) / 128) discard_l2(sg + 128 * tid);
+    else if (tid >= 64 && tid < 64 + kRecSlots * 8 / 128) discard_l2(recg + 16 * (tid - 64));
+
+    // cells: destination cell -> source cell (levels 3..tp), then in-cell levels 1, 2
+    for (int c = tid; c < NCELL; c += 256) {
+        const int cy = c / NC, cx = c % NC;
+        int py = cy, px = cx;
+        inv_turn(q_up, NC - 1, py, px);
+        int q = q_up;
+        for (int e = TP; e >= 3 && e >= g.emin; e--) {
+            const int k = e - 2, m1 = (1 << k) - 1;
+            const int by = py >> k, bx = px >> k;
+            const int a = rec_angle(S.rec, g, e, by, bx);
+            int oy = py & m1, ox = px & m1;
+            inv_turn(a, m1, oy, ox);
+            py = (by << k) | oy;
+            px = (bx << k) | ox;
+            q += a;
+        }
+        Cell v = {S.src[(4 * py) * RS + px], S.src[(4 * py + 1) * RS + px], S.src[(4 * py + 2) * RS + px],
+                  S.src[(4 * py + 3) * RS + px]};
+        Cell cl;
+        if constexpr (METHOD == 1)
+            cl = {S.lab[(4 * py) * RS + px], S.lab[(4 * py + 1) * RS + px], S.lab[(4 * py + 2) * RS + px],
+                  S.lab[(4 * py + 3) * RS + px]};
+        if (g.emin <= 1) {
+            const uint32_t a01 = (uint32_t)(S.rec[g.lvl_off[1] + 2 * py] >> (4 * px)) & 0xFu;
+            const uint32_t a23 = (uint32_t)(S.rec[g.lvl_off[1] + 2 * py + 1] >> (4 * px)) & 0xFu;
+            pair_rot_cw(v.r0, v.r1, a01 & 3, a01 >> 2);
+            pair_rot_cw(v.r2, v.r3, a23 & 3, a23 >> 2);
+            if constexpr (METHOD == 1) {
+                pair_rot_cw(cl.r0, cl.r1, a01 & 3, a01 >> 2);
+                pair_rot_cw(cl.r2, cl.r3, a23 & 3, a23 >> 2);
+            }
+        }
+        if (g.emin <= 2) q += rec_angle(S.rec, g, 2, py, px);
+        v = cell_rot_cw(v, q & 3);
+        if constexpr (METHOD == 1) cl = cell_rot_cw(cl, q & 3);
+
+        const uint32_t *sw = reinterpret_cast<const uint32_t *>(S.ss) + (4 * cy) * (T / 4) + cx;
+        const uint32_t s0 = sw[0], s1 = sw[T / 4], s2 = sw[2 * (T / 4)], s3 = sw[3 * (T / 4)];
+        const size_t base = (size_t)(dty * T + 4 * cy) * g.W + (size_t)dtx * T + 4 * cx;
+        uint32_t e0, e1, e2, e3;
+        if constexpr (METHOD == 0) {
+            e0 = v.r0 ^ (s0 & 0xFEFEFEFEu); e1 = v.r1 ^ (s1 & 0xFEFEFEFEu);
+            e2 = v.r2 ^ (s2 & 0xFEFEFEFEu); e3 = v.r3 ^ (s3 & 0xFEFEFEFEu);
+            if (dtile == 0 && c == 0) {
+                // header: LSB(E[r]) = bit (2 - r) of b - 2 for r = 0..2; the map there is forced
+                // to 1, so capacity counts zeros after forcing (Q14)
+                const uint32_t m = v.r0 & 0x00010101u;
+                const int forced = (int)(m & 1u) + (int)((m >> 8) & 1u) + (int)((m >> 16) & 1u);
+                const uint32_t hb = (uint32_t)(b - 2);
+                const uint32_t hdr = ((hb >> 2) & 1u) | (((hb >> 1) & 1u) << 8) | ((hb & 1u) << 16);
+                e0 = (e0 & 0xFFFEFEFEu) | hdr;
+                const long long zeros = g.HW - (long long)__ldcg(ws.hist + img * 8 + b);
+                b_out[img] = b;
+                cap_out[img] = (long long)b * (zeros - (3 - forced));
+                status[img] = 0;
+            }
+        } else {
+            e0 = v.r0 ^ s0; e1 = v.r1 ^ s1; e2 = v.r2 ^ s2; e3 = v.r3 ^ s3;
+            uint8_t *co = ceta_out + (size_t)img * g.HW + base;
+            *reinterpret_cast<uint32_t *>(co) = cl.r0;
+            *reinterpret_cast<uint32_t *>(co + g.W) = cl.r1;
+            *reinterpret_cast<uint32_t *>(co + 2 * (size_t)g.W) = cl.r2;
+            *reinterpret_cast<uint32_t *>(co + 3 * (size_t)g.W) = cl.r3;
+        }
+        uint8_t *eo = enc + (size_t)img * g.HW + base;
+        *reinterpret_cast<uint32_t *>(eo) = e0;
+        *reinterpret_cast<uint32_t *>(eo + g.W) = e1;
+        *reinterpret_cast<uint32_t *>(eo + 2 * (size_t)g.W) = e2;
+        *reinterpret_cast<uint32_t *>(eo + 3 * (size_t)g.W) = e3;
+    }
+}
+
+// ======================================================================================
+// W role, recover: one CTA per ORIGINAL tile (a10).
+//   X = I_e' XOR s (every bit, Q20); EMR: map bit = raw LSB of I_e' (r < 3 forced to 1);
+//   LMR: MSB := eta_r and the map come from the decoded planes.  Inverse cell transform,
+//   then per row omega := masked bits of the last non-redundant pixel, replaced into the
+//   redundant ones.  The carry into the tile's rows comes from the tiles to
+//   the left (per-row decoupled look-back: aggregate = last non-redundant value of the row
+//   inside the tile, inclusive = carry out).
+// ======================================================================================
+__device__ __forceinline__ uint32_t bits4_to_bytes(uint32_t m4) { return ((m4 & 0xFu) * 0x00204081u) & 0x01010101u; }
+__device__ __forceinline__ uint32_t bytes_to_bits4(uint32_t l) { return (l | (l >> 7) | (l >> 14) | (l >> 21)) & 0xFu; }
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+template <int TP>
+struct RecSmem {
+    static constexpr int T = 1 << TP, RS = T / 4 + 1;
+    uint8_t ss[T * T];                       // keystream of the destination tile (bulk copy)
+    uint8_t es[T * T];                       // marked destination tile (cp.async)
+    uint32_t xin[T * RS], lin[T * RS];       // destination domain: decrypted words, map bytes
+    uint32_t xo[T * RS], lo[T * RS];         // original domain
+    uint64_t rec[kRecSlots];
+    uint32_t mbits[T][2], ebits[T][2];       // LMR: decoded map / eta bits of the destination rows
+    uint8_t rowval[T], carry[T];
+    uint32_t rowhas[2];
+    uint64_t bar;
+    int sh[4];
+};
+
+template <int TP, int METHOD>
+__device__ __forceinline__ void rec_role(const Geo &g, int img, int otile, int nK, const uint8_t *__restrict__ marked,
+                                         const TileWS &ws, const uint32_t *__restrict__ eta_bits,
+                                         const uint32_t *__restrict__ map_bits, const int32_t *__restrict__ lmr_b,
+                                         uint8_t *__restrict__ out, int32_t *__restrict__ status, uint8_t *smem) {
+    constexpr int T = 1 << TP, RS = T / 4 + 1, NC = T / 4, NCELL = NC * NC, CPT = T * T / 16, SEGS = T / 16;
+    RecSmem<TP> &S = *reinterpret_cast<RecSmem<TP> *>(smem);
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int ty = otile / g.tilesX, tx = otile % g.tilesX;
+    const uint8_t *Em = marked + (size_t)img * g.HW;
+    uint8_t *O = out + (size_t)img * g.HW;
+    const size_t tslot = (size_t)img * g.ntiles + otile;
+
+    if (tid == 0) {
+        int b;
+        if constexpr (METHOD == 0) {
+            const int field = ((Em[0] & 1) << 2) | ((Em[1] & 1) << 1) | (Em[2] & 1);
+            b = field > 5 ? -1 : field + 2;
+            if (otile == 0) status[img] = b < 0 ? 8 : 0;
+        } else {
+            b = __ldcg(lmr_b + img);                    // <= 0: status already set by the decoder
+            if (otile == 0 && b > 0) status[img] = 0;
+        }
+        S.sh[2] = b;
+        if (b > 0) {
+            wait_keys(ws, img, nK);
+            int dty, dtx, q;
+            upper_walk_forward(g, ws.pyr + (size_t)img * g.npyr, ty, tx, dty, dtx, q);
+            S.sh[0] = dty * g.tilesX + dtx;
+            S.sh[1] = q;
+            mbar_init(&S.bar, 1);
+            mbar_expect_tx(&S.bar, T * T);
+            bulk_g2s(S.ss, ws.s + ((size_t)img * g.ntiles + S.sh[0]) * (T * T), T * T, &S.bar);
+        }
+    }
+    __syncthreads();
+    const int b = S.sh[2];
+    if (b <= 0) {                                       // FORMAT / BADCASE: zero-filled output
+        for (int c = tid; c < CPT; c += 256) {
+            const int r = c / SEGS, seg = c % SEGS;
+            *reinterpret_cast<uint4 *>(O + (size_t)(ty * T + r) * g.W + (size_t)tx * T + seg * 16) =
+                make_uint4(0, 0, 0, 0);
+        }
+        return;
+    }
+    const int dt = S.sh[0], q_up = S.sh[1];
+    const int dty = dt / g.tilesX, dtx = dt % g.tilesX;
+    const uint32_t mask = METHOD == 0 ? ((0xFFu << (8 - b)) & 0xFFu) : (0x7Fu & ~(0xFFu >> b));
+    for (int c = tid; c < CPT; c += 256) {
+        const int r = c / SEGS, seg = c % SEGS;
+        cp_async16(&S.es[r * T + seg * 16], Em + (size_t)(dty * T + r) * g.W + (size_t)dtx * T + seg * 16);
+    }
+    const uint64_t *recg = ws.rec + tslot * kRecSlots;
+    if (tid < kRecSlots) S.rec[tid] = __ldcg(recg + tid);
+    if constexpr (METHOD == 1) {
+        if (tid < T) {
+            const size_t bit = (size_t)img * g.HW + (size_t)(dty * T + tid) * g.W + (size_t)dtx * T;
+            const int nw = T >= 32 ? T / 32 : 1;
+            for (int k = 0; k < 2; k++) {
+                S.mbits[tid][k] = k < nw ? (__ldg(map_bits + (bit >> 5) + k) >> (bit & 31)) : 0u;
+                S.ebits[tid][k] = k < nw ? (__ldg(eta_bits + (bit >> 5) + k) >> (bit & 31)) : 0u;
+            }
+        }
+    }
+    cp_async_wait_all();
+    mbar_wait(&S.bar, 0);
+    __syncthreads();
+    if (tid < (T * T) / 128) discard_l2(ws.s + ((size_t)img * g.ntiles + dt) * (T * T) + 128 * tid);
+    else if (tid >= 64 && tid < 64 + kRecSlots * 8 / 128) discard_l2(recg + 16 * (tid - 64));
+
+    // destination tile: X = E' ^ s, map bits
+    for (int c = tid; c < CPT; c += 256) {
+        const int r = c / SEGS, seg = c % SEGS;
+        const uint4 e = *reinterpret_cast<const uint4 *>(&S.es[r * T + seg * 16]);
+        const uint4 sv = *reinterpret_cast<const uint4 *>(&S.ss[r * T + seg * 16]);
+        const uint32_t ew[4] = {e.x, e.y, e.z, e.w}, sw[4] = {sv.x, sv.y, sv.z, sv.w};
+        uint32_t mb16 = 0, eb16 = 0;
+        if constexpr (METHOD == 1) {
+            mb16 = (S.mbits[r][seg >> 1] >> (16 * (seg & 1))) & 0xFFFFu;
+            eb16 = (S.ebits[r][seg >> 1] >> (16 * (seg & 1))) & 0xFFFFu;
+        }
+        const bool first = dt == 0 && r == 0 && seg == 0;
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            uint32_t x = ew[i] ^ sw[i], l;
+            if constexpr (METHOD == 0) {
+                l = ew[i] & 0x01010101u;
+                if (i == 0 && first) l |= 0x00010101u;      // r = 0..2 carry the header, map = 1
+            } else {
+                l = bits4_to_bytes(mb16 >> (4 * i));
+                x = (x & 0x7F7F7F7Fu) | (bits4_to_bytes(eb16 >> (4 * i)) << 7);   // MSB from eta
+            }
+            S.xin[r * RS + seg * 4 + i] = x;
+            S.lin[r * RS + seg * 4 + i] = l;
+        }
+    }
+    __syncthreads();
+    // cells: original cell -> destination cell, inverse content transform
+    for (int c = tid; c < NCELL; c += 256) {
+        const int cy = c / NC, cx = c % NC;
+        int py = cy, px = cx, q = 0;
+        for (int e = (g.emin > 3 ? g.emin : 3); e <= TP; e++) {
+            const int k = e - 2, m1 = (1 << k) - 1;
+            const int by = py >> k, bx = px >> k;
+            const int a = rec_angle(S.rec, g, e, by, bx);
+            int oy = py & m1, ox = px & m1;
+            fwd_turn(a, m1, oy, ox);
+            py = (by << k) | oy;
+            px = (bx << k) | ox;
+            q += a;
+        }
+        fwd_turn(q_up, NC - 1, py, px);
+        q += q_up;
+        if (g.emin <= 2) q += rec_angle(S.rec, g, 2, cy, cx);
+        Cell x = {S.xin[(4 * py) * RS + px], S.xin[(4 * py + 1) * RS + px], S.xin[(4 * py + 2) * RS + px],
+                  S.xin[(4 * py + 3) * RS + px]};
+        Cell l = {S.lin[(4 * py) * RS + px], S.lin[(4 * py + 1) * RS + px], S.lin[(4 * py + 2) * RS + px],
+                  S.lin[(4 * py + 3) * RS + px]};
+        const int rinv = (4 - (q & 3)) & 3;
+        x = cell_rot_cw(x, rinv);
+        l = cell_rot_cw(l, rinv);
+        if (g.emin <= 1) {
+            const uint32_t a01 = (uint32_t)(S.rec[g.lvl_off[1] + 2 * cy] >> (4 * cx)) & 0xFu;
+            const uint32_t a23 = (uint32_t)(S.rec[g.lvl_off[1] + 2 * cy + 1] >> (4 * cx)) & 0xFu;
+            const int aL0 = (4 - (a01 & 3)) & 3, aR0 = (4 - (a01 >> 2)) & 3;
+            const int aL1 = (4 - (a23 & 3)) & 3, aR1 = (4 - (a23 >> 2)) & 3;
+            pair_rot_cw(x.r0, x.r1, aL0, aR0);
+            pair_rot_cw(x.r2, x.r3, aL1, aR1);
+            pair_rot_cw(l.r0, l.r1, aL0, aR0);
+            pair_rot_cw(l.r2, l.r3, aL1, aR1);
+        }
+        S.xo[(4 * cy) * RS + cx] = x.r0; S.xo[(4 * cy + 1) * RS + cx] = x.r1;
+        S.xo[(4 * cy + 2) * RS + cx] = x.r2; S.xo[(4 * cy + 3) * RS + cx] = x.r3;
+        S.lo[(4 * cy) * RS + cx] = l.r0; S.lo[(4 * cy + 1) * RS + cx] = l.r1;
+        S.lo[(4 * cy + 2) * RS + cx] = l.r2; S.lo[(4 * cy + 3) * RS + cx] = l.r3;
+    }
+    __syncthreads();
+
+    // ---- row summaries: SEGS threads per row, 16 pixels each
+    const bool rowthr = tid < T * SEGS;
+    const int r = tid / SEGS, seg = tid % SEGS;
+    uint32_t xw[4] = {0, 0, 0, 0}, lw[4] = {0, 0, 0, 0};
+    int has = 0, val = 0;
+    if (rowthr) {
+#pragma unroll
+        for (int i = 0; i < 4; i++) { xw[i] = S.xo[r * RS + seg * 4 + i]; lw[i] = S.lo[r * RS + seg * 4 + i]; }
+        if (tx == 0 && seg == 0) lw[0] |= 1u;           // column 0: omega starts at its bits
+        uint32_t m16 = 0;
+#pragma unroll
+        for (int i = 0; i < 4; i++) m16 |= bytes_to_bits4(lw[i]) << (4 * i);
+        has = m16 != 0;
+        if (has) {
+            const int li = 31 - __clz(m16);
+            val = (int)((xw[li >> 2] >> (8 * (li & 3))) & mask);
+        }
+    }
+    // exclusive "last non-redundant" across the row's segments (without the tile carry-in)
+    const unsigned gm = SEGS >= 32 ? 0xffffffffu : (((1u << SEGS) - 1u) << (lane & ~(SEGS - 1)));
+    int ehas = 0, evl = 0;
+    for (int s2 = 0; s2 < SEGS; s2++) {
+        const int oh = __shfl_sync(gm, has, (lane & ~(SEGS - 1)) + s2, 32);
+        const int ov = __shfl_sync(gm, val, (lane & ~(SEGS - 1)) + s2, 32);
+        if (s2 < seg && oh) { ehas = 1; evl = ov; }
+    }
+    const int rval = has ? val : evl;                   // last non-redundant value of the row so far
+    if (rowthr && seg == SEGS - 1) S.rowval[r] = (uint8_t)rval;
+    // rows with a non-redundant pixel inside the tile (their carry out is known outright);
+    // column 0 makes every row of the strip's first tile such a row
+    if (tid < 64) {
+        bool any = false;
+        if (tid < T) {
+            uint32_t a = 0;
+            for (int i = 0; i < T / 4; i++) a |= S.lo[tid * RS + i];
+            any = a != 0 || tx == 0;
+        }
+        const unsigned bl = __ballot_sync(0xffffffffu, any);
+        if (lane == 0) S.rowhas[tid >> 5] = bl;
+    }
+    __syncthreads();
+    const bool first_tile = tx == 0;
+    if (tid < T) {
+        ws.ragg[tslot * T + tid] = S.rowval[tid];
+        if (first_tile) ws.rinc[tslot * T + tid] = S.rowval[tid];
+    }
+    if (tid == 0) ws.rhas[tslot] = (uint64_t)S.rowhas[0] | ((uint64_t)S.rowhas[1] << 32);
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) st_relaxed_u32(ws.rflag + tslot, first_tile ? 2u : 1u);
+
+    // ---- look-back for the carry into each row (warp 0; lane owns rows lane, lane + 32)
+    if (!first_tile && tid < 32) {
+        bool u0 = lane < T, u1 = lane + 32 < T;
+        uint32_t c0 = 0, c1 = 0;
+        size_t k = tslot - 1;                           // tile to the left, same strip
+        while (__any_sync(0xffffffffu, u0 || u1)) {
+            unsigned f;
+            do { f = ld_acquire_u32(ws.rflag + k); } while (f == 0);
+            if (f == 2) {
+                if (u0) { c0 = __ldcg(ws.rinc + k * T + lane); u0 = false; }
+                if (u1) { c1 = __ldcg(ws.rinc + k * T + lane + 32); u1 = false; }
+            } else {
+                const uint64_t hm = __ldcg(ws.rhas + k);
+                if (u0 && ((hm >> lane) & 1u)) { c0 = __ldcg(ws.ragg + k * T + lane); u0 = false; }
+                if (u1 && ((hm >> (lane + 32)) & 1u)) { c1 = __ldcg(ws.ragg + k * T + lane + 32); u1 = false; }
+            }
+            k--;
+        }
+        if (lane < T) S.carry[lane] = (uint8_t)c0;
+        if (lane + 32 < T) S.carry[lane + 32] = (uint8_t)c1;
+    }
+    __syncthreads();
+    if (!first_tile && tx + 1 < g.tilesX) {             // carry out for the tiles to the right
+        if (tid < T) {
+            const bool h = (S.rowhas[tid >> 5] >> (tid & 31)) & 1u;
+            ws.rinc[tslot * T + tid] = h ? S.rowval[tid] : S.carry[tid];
+        }
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) st_relaxed_u32(ws.rflag + tslot, 2u);
+    }
+
+    // ---- copy-forward and store
+    if (rowthr) {
+        uint32_t om = (ehas ? (uint32_t)evl : (uint32_t)S.carry[r]);
+#pragma unroll
+        for (int i = 0; i < 16; i++) {
+            const int wi = i >> 2, sh8 = 8 * (i & 3);
+            const uint32_t px8 = (xw[wi] >> sh8) & 0xFFu;
+            if ((lw[wi] >> sh8) & 1u) om = px8 & mask;
+            else xw[wi] = (xw[wi] & ~(0xFFu << sh8)) | (((px8 & ~mask) | om) << sh8);
+        }
+        *reinterpret_cast<uint4 *>(O + (size_t)(ty * T + r) * g.W + (size_t)tx * T + seg * 16) =
+            make_uint4(xw[0], xw[1], xw[2], xw[3]);
+    }
+}
+
+// ======================================================================================
+// The fused kernels
+// ======================================================================================
+template <int TP, int METHOD>
+__global__ void __launch_bounds__(256) encode_kernel(Geo g, FusedSched sc, const uint8_t *__restrict__ images,
+                                                     const uint8_t *__restrict__ keys, TileWS ws,
+                                                     uint8_t *__restrict__ enc, uint8_t *__restrict__ ceta,
+                                                     int32_t *__restrict__ b_out, int64_t *__restrict__ cap_out,
+                                                     int32_t *__restrict__ status) {
+    constexpr int T = 1 << TP, TPC = 256 / T;
+    constexpr size_t KB = TPC * kRecSlots * 8, PB = sizeof(PermSmem<TP, METHOD>);
+    __shared__ __align__(128) uint8_t smem[KB > PB ? KB : PB];
+    const Role ro = role_of(sc, blockIdx.x);
+    if (ro.img >= g.B) return;
+    if (ro.key) key_role<TP, true>(g, ro.img, ro.idx, keys, images, ws, smem);
+    else perm_role<TP, METHOD>(g, ro.img, ro.idx, sc.nK, images, ws, enc, ceta, b_out, cap_out, status, smem);
+}
+
+template <int TP, int METHOD>
+__global__ void __launch_bounds__(256) recover_kernel(Geo g, FusedSched sc, const uint8_t *__restrict__ marked,
+                                                      const uint8_t *__restrict__ keys, TileWS ws,
+                                                      const uint32_t *__restrict__ eta_bits,
+                                                      const uint32_t *__restrict__ map_bits,
+                                                      const int32_t *__restrict__ lmr_b, uint8_t *__restrict__ out,
+                                                      int32_t *__restrict__ status) {
+    constexpr int T = 1 << TP, TPC = 256 / T;
+    constexpr size_t KB = TPC * kRecSlots * 8, RB = sizeof(RecSmem<TP>);
+    __shared__ __align__(128) uint8_t smem[KB > RB ? KB : RB];
+    const Role ro = role_of(sc, blockIdx.x);
+    if (ro.img >= g.B) return;
+    if (ro.key) key_role<TP, false>(g, ro.img, ro.idx, keys, nullptr, ws, smem);
+    else rec_role<TP, METHOD>(g, ro.img, ro.idx, sc.nK, marked, ws, eta_bits, map_bits, lmr_b, out, status, smem);
+}
+
+// ---------------------------------------------------------------------------- launchers
+FusedSched fused_sched(const Geo &g) {
+    FusedSched sc;
+    const int TPC = 256 / g.T;
+    sc.nK = (g.ntiles + TPC - 1) / TPC;
+    sc.nW = g.ntiles;
+    long long gi = (2ll << 20) / g.HW;                  // ~2 Mpixel per image group
+    if (gi < 1) gi = 1;
+    if (gi > g.B) gi = g.B;
+    sc.GI = (int)gi;
+    sc.ngroups = (g.B + sc.GI - 1) / sc.GI;
+    return sc;
+}
+
+template <int TP>
+static void launch_encode_tp(const Geo &g, const uint8_t *images, const uint8_t *keys, const TileWS &ws, uint8_t *enc,
+                             uint8_t *ceta, int32_t *b_out, int64_t *cap_out, int32_t *status, cudaStream_t st) {
+    const FusedSched sc = fused_sched(g);
+    const unsigned grid = (unsigned)((long long)sc.ngroups * sc.GI * (sc.nK + sc.nW));
+    if (g.method == 0)
+        encode_kernel<TP, 0><<<grid, 256, 0, st>>>(g, sc, images, keys, ws, enc, ceta, b_out, cap_out, status);
+    else
+        encode_kernel<TP, 1><<<grid, 256, 0, st>>>(g, sc, images, keys, ws, enc, ceta, b_out, cap_out, status);
+}
+
+void launch_encode(const Geo &g, const uint8_t *images, const uint8_t *keys, const TileWS &ws, uint8_t *enc,
+                   uint8_t *ceta, int32_t *b_out, int64_t *cap_out, int32_t *status, cudaStream_t st) {
+    switch (g.tp) {
+        case 4: launch_encode_tp<4>(g, images, keys, ws, enc, ceta, b_out, cap_out, status, st); break;
+        case 5: launch_encode_tp<5>(g, images, keys, ws, enc, ceta, b_out, cap_out, status, st); break;
+        default: launch_encode_tp<6>(g, images, keys, ws, enc, ceta, b_out, cap_out, status, st); break;
+    }
+}
+
+template <int TP>
+static void launch_recover_tp(const Geo &g, const uint8_t *marked, const uint8_t *keys, const TileWS &ws,
+                              const uint32_t *eta, const uint32_t *map, const int32_t *lmr_b, uint8_t *out,
+                              int32_t *status, cudaStream_t st) {
+    const FusedSched sc = fused_sched(g);
+    const unsigned grid = (unsigned)((long long)sc.ngroups * sc.GI * (sc.nK + sc.nW));
+    if (g.method == 0)
+        recover_kernel<TP, 0><<<grid, 256, 0, st>>>(g, sc, marked, keys, ws, eta, map, lmr_b, out, status);
+    else
+        recover_kernel<TP, 1><<<grid, 256, 0, st>>>(g, sc, marked, keys, ws, eta, map, lmr_b, out, status);
+}
+
+void launch_recover(const Geo &g, const uint8_t *marked, const uint8_t *keys, const TileWS &ws, const uint32_t *eta,
+                    const uint32_t *map, const int32_t *lmr_b, uint8_t *out, int32_t *status, cudaStream_t st) {
+    switch (g.tp) {
+        case 4: launch_recover_tp<4>(g, marked, keys, ws, eta, map, lmr_b, out, status, st); break;
+        case 5: launch_recover_tp<5>(g, marked, keys, ws, eta, map, lmr_b, out, status, st); break;
+        default: launch_recover_tp<6>(g, marked, keys, ws, eta, map, lmr_b, out, status, st); break;
+    }
+}
+
+}  // namespace mmsb

@@ -16,12 +16,11 @@ namespace mmsb {
 static std::atomic<unsigned long long> g_launches{0};
 
 // ---- live per-kernel timing (CUDA events recorded on the launch stream around each kernel)
-enum KernelId { K_KS_ENC = 0, K_KS_REC, K_PERM_ENC, K_RECOVER, K_EMBED, K_EXTRACT, K_STATS, K_LMR_PLAN,
-                K_CODER_ENC, K_LMR_FIT, K_LMR_MSB, K_LMR_DECODE, K_COUNT };
-static const char *kKernelNames[K_COUNT] = {"ks_tile_kernel<hist>", "ks_tile_kernel", "perm_encode_kernel",
-                                            "recover_strip_kernel", "scan_kernel<embed>+finish", "scan_kernel<extract>+finish",
-                                            "stats_kernel", "lmr_plan_kernel", "coder_encode_kernel",
-                                            "lmr_fit_kernel", "lmr_msb_write_kernel",
+enum KernelId { K_ENCODE = 0, K_RECOVER, K_EMBED, K_EXTRACT, K_STATS, K_LMR_PLAN, K_CODER_ENC, K_LMR_FIT,
+                K_LMR_MSB, K_LMR_DECODE, K_COUNT };
+static const char *kKernelNames[K_COUNT] = {"encode_kernel", "recover_kernel", "scan_kernel<embed>+finish",
+                                            "scan_kernel<extract>+finish", "stats_kernel", "lmr_plan_kernel",
+                                            "coder_encode_kernel", "lmr_fit_kernel", "lmr_msb_write_kernel",
                                             "lmr_pack+header+coder_decode_kernels"};
 struct ProfRec { int id; cudaEvent_t a, b; long long units; };
 static std::mutex g_prof_mu;
@@ -52,53 +51,64 @@ template <class F> static void run_kernel(int id, cudaStream_t st, long long uni
     g_prof.push_back(r);
 }
 
-// Images per tile-kernel group: the group's keystream scratch (1 B/px), its images and
-// their outputs are meant to stay in the 126 MB L2 between the keystream kernel and the
-// permutation kernel that consumes them.
-constexpr long long kGroupBytes = 24ll << 20;
-
 static size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
 
+// Workspace carving.  The keystream scratch and angle records are sized for
+// the whole batch but are transient: each tile is written by one keystream CTA, read by one
+// worker CTA of the same launch shortly after, and then discarded from L2.
 struct Layout {
-    int G;
-    size_t s, rec, fwd, inv, pyr, hist, tdone, tile_zero_end; // per-group tile state
-    size_t states, parts, hdr, scan_zero_end;  // per-call scan state
+    size_t s, rec, pyr, hist, kdone, rflag, tile_zero_end, rhas, ragg, rinc;   // fused tile kernels
+    size_t states, parts, hdr, scan_zero_end;                                  // scan kernels
     size_t ceta, eta_bits, map_bits, lmr_b, lmr_t, plan, streams, sizes, offsets, mbuf, total;
 };
 
 static Layout layout(const Geo &g) {
     Layout L{};
-    long long G = kGroupBytes / g.HW;
-    if (G < 1) G = 1;
-    if (G > g.B) G = g.B;
-    L.G = (int)G;
+    const size_t B = (size_t)g.B, nt = (size_t)g.ntiles;
     size_t o = 0;
-    L.s = o; o = align256(o + (size_t)G * g.HW);
-    L.rec = o; o = align256(o + (size_t)G * g.ntiles * kRecSlots * 8);
-    L.fwd = o; o = align256(o + (size_t)G * g.ntiles * 4);
-    L.inv = o; o = align256(o + (size_t)G * g.ntiles * 4);
-    L.pyr = o; o = align256(o + (size_t)G * (g.npyr > 0 ? g.npyr : 1) * 4);
-    L.hist = o; o = align256(o + (size_t)G * 8 * 4);
-    L.tdone = o; o = align256(o + (size_t)G * 4);
+    L.s = o; o = align256(o + B * g.HW);
+    L.rec = o; o = align256(o + B * nt * kRecSlots * 8);
+    L.pyr = o; o = align256(o + B * (g.npyr > 0 ? g.npyr : 1) * 4);
+    L.hist = o; o = align256(o + B * 8 * 4);
+    L.kdone = o; o = align256(o + B * 4);
+    L.rflag = o; o = align256(o + B * nt * 4);
     L.tile_zero_end = o;
-    L.states = o; o = align256(o + (size_t)g.B * g.nchunks * 8);
-    L.parts = o; o = align256(o + (size_t)g.B * g.nchunks * 16);
-    L.hdr = o; o = align256(o + (size_t)g.B * 4);
+    L.rhas = o; o = align256(o + B * nt * 8);
+    L.ragg = o; o = align256(o + B * nt * g.T);
+    L.rinc = o; o = align256(o + B * nt * g.T);
+    L.states = o; o = align256(o + B * g.nchunks * 8);
+    L.parts = o; o = align256(o + B * g.nchunks * 16);
+    L.hdr = o; o = align256(o + B * 4);
     L.scan_zero_end = o;
-    L.ceta = o; o = align256(o + (g.method == 1 ? (size_t)G * g.HW : 0));
-    L.eta_bits = o; o = align256(o + (g.method == 1 ? (size_t)g.B * g.HW / 8 : 0));
-    L.map_bits = o; o = align256(o + (g.method == 1 ? (size_t)g.B * g.HW / 8 : 0));
-    L.lmr_b = o; o = align256(o + (size_t)g.B * 4);
-    L.lmr_t = o; o = align256(o + (size_t)g.B * 4);
     const bool lmr = g.method == 1;
+    L.ceta = o; o = align256(o + (lmr ? B * g.HW : 0));
+    L.eta_bits = o; o = align256(o + (lmr ? B * g.HW / 8 : 0));
+    L.map_bits = o; o = align256(o + (lmr ? B * g.HW / 8 : 0));
+    L.lmr_b = o; o = align256(o + B * 4);
+    L.lmr_t = o; o = align256(o + B * 4);
     const size_t Tc = (size_t)g.ntiles_coder;
-    L.plan = o; o = align256(o + (lmr ? (size_t)G * sizeof(LmrPlan) : 0));
-    L.streams = o; o = align256(o + (lmr ? (size_t)G * 2 * Tc * lmr_tile_cap_host(g.tile_log2, g.H, g.W) : 0));
-    L.sizes = o; o = align256(o + (lmr ? (size_t)g.B * 2 * Tc * 4 : 0));
-    L.offsets = o; o = align256(o + (lmr ? (size_t)g.B * 2 * Tc * 4 : 0));
-    L.mbuf = o; o = align256(o + (lmr ? (size_t)g.B * g.HW / 8 + 16 : 0));
+    L.plan = o; o = align256(o + (lmr ? B * sizeof(LmrPlan) : 0));
+    L.streams = o; o = align256(o + (lmr ? B * 2 * Tc * lmr_tile_cap_host(g.tile_log2, g.H, g.W) : 0));
+    L.sizes = o; o = align256(o + (lmr ? B * 2 * Tc * 4 : 0));
+    L.offsets = o; o = align256(o + (lmr ? B * 2 * Tc * 4 : 0));
+    L.mbuf = o; o = align256(o + (lmr ? B * g.HW / 8 + 16 : 0));
     L.total = o;
     return L;
+}
+
+static TileWS tile_ws(const Layout &L, void *ws) {
+    char *w = static_cast<char *>(ws);
+    TileWS t;
+    t.s = reinterpret_cast<uint8_t *>(w + L.s);
+    t.rec = reinterpret_cast<uint64_t *>(w + L.rec);
+    t.pyr = reinterpret_cast<uint32_t *>(w + L.pyr);
+    t.hist = reinterpret_cast<uint32_t *>(w + L.hist);
+    t.kdone = reinterpret_cast<uint32_t *>(w + L.kdone);
+    t.rflag = reinterpret_cast<uint32_t *>(w + L.rflag);
+    t.rhas = reinterpret_cast<uint64_t *>(w + L.rhas);
+    t.ragg = reinterpret_cast<uint8_t *>(w + L.ragg);
+    t.rinc = reinterpret_cast<uint8_t *>(w + L.rinc);
+    return t;
 }
 
 static bool geo_of(const mmsb_shape *s, Geo *g) {
@@ -148,42 +158,30 @@ mmsb_status mmsb_content_owner_encode(const mmsb_shape *shape, const uint8_t *im
     const Layout L = layout(g);
     if (ws_bytes < L.total) return MMSB_E_INVAL;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    for (int g0 = 0; g0 < g.B; g0 += L.G) {
-        const int n = g.B - g0 < L.G ? g.B - g0 : L.G;
-        if (cudaMemsetAsync(at<char>(ws, L.pyr), 0, L.tile_zero_end - L.pyr, st) != cudaSuccess) return MMSB_E_CUDA;
-        const long long px = (long long)n * g.HW;
-        run_kernel(K_KS_ENC, st, px, [&] {
-            launch_ks_tile(g, n, k1 + (size_t)g0 * 32, images + (size_t)g0 * g.HW, at<uint8_t>(ws, L.s),
-                           at<uint64_t>(ws, L.rec), at<uint32_t>(ws, L.pyr), at<uint32_t>(ws, L.hist),
-                           at<uint32_t>(ws, L.tdone), at<int32_t>(ws, L.fwd), at<int32_t>(ws, L.inv), st);
-        });
-        run_kernel(K_PERM_ENC, st, px, [&] {
-            launch_perm_encode(g, n, images + (size_t)g0 * g.HW, at<uint8_t>(ws, L.s), at<uint64_t>(ws, L.rec),
-                               at<uint32_t>(ws, L.pyr), at<uint32_t>(ws, L.hist), at<int32_t>(ws, L.inv),
-                               encrypted + (size_t)g0 * g.HW,
-                               at<uint8_t>(ws, L.ceta), b_out + g0, capacity_out + g0, img_status + g0, st);
-        });
-        if (g.method == 1) {
-            // LMR: code eta and the candidate maps until both fit the MSB plane, then write it
-            Geo gg = g;
-            gg.B = n;
-            LmrPlan *plan = at<LmrPlan>(ws, L.plan);
-            run_kernel(K_LMR_PLAN, st, px, [&] { launch_lmr_plan(gg, at<uint32_t>(ws, L.hist), plan, st); });
-            for (int w = 0; w < 7; w++) {
-                run_kernel(K_CODER_ENC, st, px, [&] {
-                    launch_coder_encode(gg, w, at<uint8_t>(ws, L.ceta), plan, at<uint8_t>(ws, L.streams),
-                                        at<int32_t>(ws, L.sizes), st);
-                });
-                run_kernel(K_LMR_FIT, st, px, [&] {
-                    launch_lmr_fit(gg, w, at<int32_t>(ws, L.sizes), plan, at<int32_t>(ws, L.offsets), st);
-                });
-            }
-            run_kernel(K_LMR_MSB, st, px, [&] {
-                launch_lmr_msb_write(gg, plan, at<int32_t>(ws, L.sizes), at<int32_t>(ws, L.offsets),
-                                     at<uint8_t>(ws, L.streams), at<uint32_t>(ws, L.hist),
-                                     encrypted + (size_t)g0 * g.HW, b_out + g0, capacity_out + g0, img_status + g0, st);
+    if (cudaMemsetAsync(at<char>(ws, L.pyr), 0, L.tile_zero_end - L.pyr, st) != cudaSuccess) return MMSB_E_CUDA;
+    const long long px = (long long)g.B * g.HW;
+    run_kernel(K_ENCODE, st, px, [&] {
+        launch_encode(g, images, k1, tile_ws(L, ws), encrypted, at<uint8_t>(ws, L.ceta), b_out, capacity_out,
+                      img_status, st);
+    });
+    if (g.method == 1) {
+        // LMR: code eta and the candidate maps until both fit the MSB plane, then write it
+        LmrPlan *plan = at<LmrPlan>(ws, L.plan);
+        run_kernel(K_LMR_PLAN, st, px, [&] { launch_lmr_plan(g, at<uint32_t>(ws, L.hist), plan, st); });
+        for (int w = 0; w < 7; w++) {
+            run_kernel(K_CODER_ENC, st, px, [&] {
+                launch_coder_encode(g, w, at<uint8_t>(ws, L.ceta), plan, at<uint8_t>(ws, L.streams),
+                                    at<int32_t>(ws, L.sizes), st);
+            });
+            run_kernel(K_LMR_FIT, st, px, [&] {
+                launch_lmr_fit(g, w, at<int32_t>(ws, L.sizes), plan, at<int32_t>(ws, L.offsets), st);
             });
         }
+        run_kernel(K_LMR_MSB, st, px, [&] {
+            launch_lmr_msb_write(g, plan, at<int32_t>(ws, L.sizes), at<int32_t>(ws, L.offsets),
+                                 at<uint8_t>(ws, L.streams), at<uint32_t>(ws, L.hist), encrypted, b_out,
+                                 capacity_out, img_status, st);
+        });
     }
     return check_launch();
 }
@@ -238,22 +236,11 @@ mmsb_status mmsb_receiver_recover(const mmsb_shape *shape, const uint8_t *marked
     if (ws_bytes < L.total) return MMSB_E_INVAL;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (g.method == 1) lmr_decode_all(g, L, true, marked, ws, img_status, nullptr, st);
-    for (int g0 = 0; g0 < g.B; g0 += L.G) {
-        const int n = g.B - g0 < L.G ? g.B - g0 : L.G;
-        if (cudaMemsetAsync(at<char>(ws, L.pyr), 0, L.tile_zero_end - L.pyr, st) != cudaSuccess) return MMSB_E_CUDA;
-        const long long px = (long long)n * g.HW;
-        run_kernel(K_KS_REC, st, px, [&] {
-            launch_ks_tile(g, n, k1 + (size_t)g0 * 32, nullptr, at<uint8_t>(ws, L.s), at<uint64_t>(ws, L.rec),
-                           at<uint32_t>(ws, L.pyr), at<uint32_t>(ws, L.hist), at<uint32_t>(ws, L.tdone),
-                           at<int32_t>(ws, L.fwd), at<int32_t>(ws, L.inv), st);
-        });
-        run_kernel(K_RECOVER, st, px, [&] {
-            launch_recover_strip(g, n, marked + (size_t)g0 * g.HW, at<uint8_t>(ws, L.s), at<uint64_t>(ws, L.rec),
-                                 at<int32_t>(ws, L.fwd), at<uint32_t>(ws, L.eta_bits) + (size_t)g0 * g.HW / 32,
-                                 at<uint32_t>(ws, L.map_bits) + (size_t)g0 * g.HW / 32,
-                                 at<int32_t>(ws, L.lmr_b) + g0, recovered + (size_t)g0 * g.HW, img_status + g0, st);
-        });
-    }
+    if (cudaMemsetAsync(at<char>(ws, L.pyr), 0, L.tile_zero_end - L.pyr, st) != cudaSuccess) return MMSB_E_CUDA;
+    run_kernel(K_RECOVER, st, (long long)g.B * g.HW, [&] {
+        launch_recover(g, marked, k1, tile_ws(L, ws), at<uint32_t>(ws, L.eta_bits), at<uint32_t>(ws, L.map_bits),
+                       at<int32_t>(ws, L.lmr_b), recovered, img_status, st);
+    });
     return check_launch();
 }
 

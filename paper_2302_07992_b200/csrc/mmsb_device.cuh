@@ -187,7 +187,32 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned phase) {
         : "memory");
 }
 
+// shared -> global bulk copy (generic-proxy smem writes must be fenced first)
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void bulk_s2g(void *dst, const void *src, unsigned bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+
+// drop an L2 line (128 B, aligned) without writing it back: transient scratch that exactly one
+// consumer reads (keystream tiles, angle records) never costs HBM write bandwidth
+__device__ __forceinline__ void discard_l2(const void *p) {
+    asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
+}
+
 // ------------------------------------------------------------------- memory ordering
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed_u32(unsigned *p, unsigned v) {
+    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 // relaxed (but coherent at gpu scope) accesses for self-contained flag|value words: no L1
 // invalidation (CCTL.IVALL) per probe, unlike ld.acquire
 __device__ __forceinline__ void st_relaxed(unsigned long long *p, unsigned long long v) {

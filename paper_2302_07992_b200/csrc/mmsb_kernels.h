@@ -33,15 +33,26 @@ void launch_lmr_decode(const Geo &g, bool want_eta, const uint8_t *marked, uint8
                        int32_t *status, int64_t *msg_bits_out, cudaStream_t st);
 int lmr_tile_cap_host(int t, int H, int W);
 
-void launch_ks_tile(const Geo &g, int G, const uint8_t *keys, const uint8_t *images, uint8_t *s, uint64_t *rec,
-                    uint32_t *pyr, uint32_t *hist, uint32_t *done, int32_t *fwd_map, int32_t *inv_map,
-                    cudaStream_t st);
-void launch_perm_encode(const Geo &g, int G, const uint8_t *images, const uint8_t *s, const uint64_t *rec,
-                        const uint32_t *pyr, const uint32_t *hist, const int32_t *inv_map, uint8_t *enc,
-                        uint8_t *ceta, int32_t *b_out, int64_t *cap_out, int32_t *status, cudaStream_t st);
-void launch_recover_strip(const Geo &g, int G, const uint8_t *marked, const uint8_t *s, const uint64_t *rec,
-                          const int32_t *fwd_map, const uint32_t *eta, const uint32_t *map, const int32_t *lmr_b,
-                          uint8_t *out, int32_t *status, cudaStream_t st);
+// per-call device state of the fused encode / recover kernels (k_fused.cu)
+struct TileWS {
+    uint8_t *s;          // [B][ntiles][T*T] K1 keystream, tile-major (transient, discarded from L2)
+    uint64_t *rec;       // [B][ntiles][kRecSlots] in-tile angle records (transient)
+    uint32_t *pyr;       // [B][npyr] upper-level block sums (mod 4 on read)        -- zeroed per call
+    uint32_t *hist;      // [B][8] non-redundant counts for b = 2..8 at index b      -- zeroed per call
+    uint32_t *kdone;     // [B] keystream CTAs finished                               -- zeroed per call
+    uint32_t *rflag;     // [B][ntiles] recover look-back flags (1 agg, 2 inclusive)  -- zeroed per call
+    uint64_t *rhas;      // [B][ntiles] rows with a non-redundant pixel in the tile
+    uint8_t *ragg;       // [B][ntiles][T] per row: last non-redundant masked value in the tile
+    uint8_t *rinc;       // [B][ntiles][T] per row: carry out of the tile
+};
+// blockIdx -> role schedule: groups of GI images, nK keystream and nW worker CTAs per image
+struct FusedSched { int GI, ngroups, nK, nW; };
+FusedSched fused_sched(const Geo &g);
+
+void launch_encode(const Geo &g, const uint8_t *images, const uint8_t *keys, const TileWS &ws, uint8_t *enc,
+                   uint8_t *ceta, int32_t *b_out, int64_t *cap_out, int32_t *status, cudaStream_t st);
+void launch_recover(const Geo &g, const uint8_t *marked, const uint8_t *keys, const TileWS &ws, const uint32_t *eta,
+                    const uint32_t *map, const int32_t *lmr_b, uint8_t *out, int32_t *status, cudaStream_t st);
 void launch_scan(const Geo &g, bool embed, const uint8_t *in, uint8_t *out, const uint8_t *keys, const uint8_t *msg,
                  const int64_t *msg_bits, long long stride, uint8_t *msg_out, int64_t *msg_bits_out, int32_t *status,
                  const ScanWS &ws, const uint32_t *map_bits, const int32_t *lmr_b, cudaStream_t st);
