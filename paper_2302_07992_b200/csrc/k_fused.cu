@@ -27,20 +27,21 @@ struct Role {
     int key, img, idx;
 };
 
-__device__ __forceinline__ Role role_of(const FusedSched &sc, int x) {
-    const int SK = sc.GI * sc.nK, SW = sc.GI * sc.nW;
-    int key, grp, loc;
-    if (x < SK) {
-        key = 1; grp = 0; loc = x;
-    } else {
-        const int x2 = x - SK, pair = x2 / (SK + SW), off = x2 % (SK + SW);
-        if (pair < sc.ngroups - 1 && off < SK) { key = 1; grp = pair + 1; loc = off; }
-        else { key = 0; grp = pair; loc = pair < sc.ngroups - 1 ? off - SK : off; }
-    }
+// grid (SK + SW, ngroups + L): row p holds the keystream CTAs of group p and the worker CTAs
+// of group p - L, so a worker CTA is dispatched L rows after the keystream CTAs it waits for
+__device__ __forceinline__ Role role_of(const FusedSched &sc) {
+    const int x = blockIdx.x, p = blockIdx.y, SK = sc.GI << sc.lgK;
     Role r;
-    r.key = key;
-    r.img = grp * sc.GI + loc / (key ? sc.nK : sc.nW);
-    r.idx = loc % (key ? sc.nK : sc.nW);
+    if (x < SK) {
+        r.key = 1;
+        r.img = p < sc.ngroups ? p * sc.GI + (x >> sc.lgK) : 1 << 30;
+        r.idx = x & ((1 << sc.lgK) - 1);
+    } else {
+        const int loc = x - SK;
+        r.key = 0;
+        r.img = p >= sc.L ? (p - sc.L) * sc.GI + (loc >> sc.lgW) : 1 << 30;
+        r.idx = loc & ((1 << sc.lgW) - 1);
+    }
     return r;
 }
 
@@ -92,7 +93,7 @@ __device__ __forceinline__ int emr_select_b(const uint32_t *hist_img, long long 
 }
 
 __device__ __forceinline__ void wait_keys(const TileWS &ws, int img, int nK) {
-    while (ld_acquire_u32(ws.kdone + img) < (unsigned)nK) __nanosleep(128);
+    while (ld_acquire_u32(ws.kdone + img) < (unsigned)nK) __nanosleep(512);
 }
 
 // ======================================================================================
@@ -170,12 +171,23 @@ __device__ __forceinline__ void key_role(const Geo &g, int img, int kidx, const 
             acc[2] += y & 0x04040404u; acc[3] += y & 0x08080808u;
             acc[4] += y4 & 0x01010101u; acc[5] += y4 & 0x02020202u; acc[6] += y4 & 0x04040404u;
         }
+        // threshold bit k <-> b = 8 - k; per-thread counts <= 64, warp sums <= 2048: two
+        // counts per 32-bit word for the warp reduction
+        uint32_t cnt[7];
 #pragma unroll
-        for (int k = 0; k < 7; k++) {                              // threshold bit k <-> b = 8 - k
-            uint32_t v = valid ? (((acc[k] >> (k & 3)) * 0x01010101u) >> 24) : 0u;
+        for (int k = 0; k < 7; k++) cnt[k] = valid ? (((acc[k] >> (k & 3)) * 0x01010101u) >> 24) : 0u;
+        uint32_t pk[4] = {cnt[0] | (cnt[1] << 16), cnt[2] | (cnt[3] << 16), cnt[4] | (cnt[5] << 16), cnt[6]};
 #pragma unroll
-            for (int s = 16; s > 0; s >>= 1) v += __shfl_xor_sync(0xffffffffu, v, s);
-            if ((tid & 31) == 0 && v) atomicAdd(&ws.hist[img * 8 + 8 - k], v);
+        for (int j = 0; j < 4; j++) {
+#pragma unroll
+            for (int s = 16; s > 0; s >>= 1) pk[j] += __shfl_xor_sync(0xffffffffu, pk[j], s);
+        }
+        if ((tid & 31) == 0) {
+#pragma unroll
+            for (int k = 0; k < 7; k++) {
+                const uint32_t v = (pk[k >> 1] >> (16 * (k & 1))) & 0xFFFFu;
+                if (v) atomicAdd(&ws.hist[img * 8 + 8 - k], v);
+            }
         }
     }
     __syncthreads();
@@ -228,11 +240,12 @@ __device__ __forceinline__ void key_role(const Geo &g, int img, int kidx, const 
 // ======================================================================================
 template <int TP, int METHOD>
 struct PermSmem {
-    static constexpr int T = 1 << TP, RS = T / 4 + 1;
+    static constexpr int T = 1 << TP, RS = T / 4 + 1, NG = T / 8;
     uint8_t ss[T * T];                       // keystream of the destination tile (bulk copy)
     uint32_t src[T * RS];                    // source tile carrier words (row stride RS)
     uint32_t lab[METHOD == 1 ? T * RS : 1];  // LMR: label | eta words
     uint64_t rec[kRecSlots];
+    int gw[NG * NG];                         // per destination 2x2-cell group: source group, turns
     uint64_t bar;
     int sh[4];
 };
@@ -242,7 +255,7 @@ __device__ __forceinline__ void perm_role(const Geo &g, int img, int dtile, int 
                                           const TileWS &ws, uint8_t *__restrict__ enc, uint8_t *__restrict__ ceta_out,
                                           int32_t *__restrict__ b_out, int64_t *__restrict__ cap_out,
                                           int32_t *__restrict__ status, uint8_t *smem) {
-    constexpr int T = 1 << TP, RS = T / 4 + 1, NC = T / 4, NCELL = NC * NC, CPT = T * T / 16;
+    constexpr int T = 1 << TP, RS = T / 4 + 1, NC = T / 4, NCELL = NC * NC, CPT = T * T / 16, NG = NC / 2;
     PermSmem<TP, METHOD> &S = *reinterpret_cast<PermSmem<TP, METHOD> *>(smem);
     const int tid = threadIdx.x;
     const int dty = dtile / g.tilesX, dtx = dtile % g.tilesX;
@@ -310,23 +323,36 @@ __device__ __forceinline__ void perm_role(const Geo &g, int img, int dtile, int 
     // the consumed scratch (this tile's keystream, the source tile's record) leaves L2 unwritten
     if (tid < (T * T) / 128) discard_l2(sg + 128 * tid);
     else if (tid >= 64 && tid < 64 + kRecSlots * 8 / 128) discard_l2(recg + 16 * (tid - 64));
-
-    // cells: destination cell -> source cell (levels 3..tp), then in-cell levels 1, 2
-    for (int c = tid; c < NCELL; c += 256) {
-        const int cy = c / NC, cx = c % NC;
-        int py = cy, px = cx;
-        inv_turn(q_up, NC - 1, py, px);
+    // 2x2-cell groups (8x8 pixels) move rigidly under the levels >= 4 and under the tile's own
+    // turn q_up: one inverse walk per destination group, shared by its 4 cells
+    if (tid < NG * NG) {
+        int gy = tid / NG, gx = tid % NG;
+        inv_turn(q_up, NG - 1, gy, gx);
         int q = q_up;
-        for (int e = TP; e >= 3 && e >= g.emin; e--) {
-            const int k = e - 2, m1 = (1 << k) - 1;
-            const int by = py >> k, bx = px >> k;
+        for (int e = TP; e >= 4 && e >= g.emin; e--) {
+            const int k = e - 3, m1 = (1 << k) - 1;
+            const int by = gy >> k, bx = gx >> k;
             const int a = rec_angle(S.rec, g, e, by, bx);
-            int oy = py & m1, ox = px & m1;
+            int oy = gy & m1, ox = gx & m1;
             inv_turn(a, m1, oy, ox);
-            py = (by << k) | oy;
-            px = (bx << k) | ox;
+            gy = (by << k) | oy;
+            gx = (bx << k) | ox;
             q += a;
         }
+        S.gw[tid] = (gy << 16) | (gx << 8) | (q & 3);
+    }
+    __syncthreads();
+
+    // cells: destination cell -> source cell, then in-cell levels 1, 2
+    for (int c = tid; c < NCELL; c += 256) {
+        const int gi = c >> 2, sub = c & 3;
+        const int cy = 2 * (gi / NG) + (sub >> 1), cx = 2 * (gi % NG) + (sub & 1);
+        const int gw = S.gw[gi], sgy = gw >> 16, sgx = (gw >> 8) & 0xFF;
+        int q = gw & 3;
+        if (g.emin <= 3) q += rec_angle(S.rec, g, 3, sgy, sgx);     // level 3 = the group itself
+        int sy = sub >> 1, sx = sub & 1;
+        inv_turn(q & 3, 1, sy, sx);
+        const int py = 2 * sgy + sy, px = 2 * sgx + sx;
         Cell v = {S.src[(4 * py) * RS + px], S.src[(4 * py + 1) * RS + px], S.src[(4 * py + 2) * RS + px],
                   S.src[(4 * py + 3) * RS + px]};
         Cell cl;
@@ -411,6 +437,7 @@ struct RecSmem {
     uint32_t mbits[T][2], ebits[T][2];       // LMR: decoded map / eta bits of the destination rows
     uint8_t rowval[T], carry[T];
     uint32_t rowhas[2];
+    int gw[(T / 8) * (T / 8)];               // per original 2x2-cell group: destination group, turns
     uint64_t bar;
     int sh[4];
 };
@@ -421,6 +448,7 @@ __device__ __forceinline__ void rec_role(const Geo &g, int img, int otile, int n
                                          const uint32_t *__restrict__ map_bits, const int32_t *__restrict__ lmr_b,
                                          uint8_t *__restrict__ out, int32_t *__restrict__ status, uint8_t *smem) {
     constexpr int T = 1 << TP, RS = T / 4 + 1, NC = T / 4, NCELL = NC * NC, CPT = T * T / 16, SEGS = T / 16;
+    constexpr int NG = NC / 2;
     RecSmem<TP> &S = *reinterpret_cast<RecSmem<TP> *>(smem);
     const int tid = threadIdx.x, lane = tid & 31;
     const int ty = otile / g.tilesX, tx = otile % g.tilesX;
@@ -512,22 +540,34 @@ __device__ __forceinline__ void rec_role(const Geo &g, int img, int otile, int n
         }
     }
     __syncthreads();
-    // cells: original cell -> destination cell, inverse content transform
-    for (int c = tid; c < NCELL; c += 256) {
-        const int cy = c / NC, cx = c % NC;
-        int py = cy, px = cx, q = 0;
-        for (int e = (g.emin > 3 ? g.emin : 3); e <= TP; e++) {
-            const int k = e - 2, m1 = (1 << k) - 1;
-            const int by = py >> k, bx = px >> k;
+    // cells: original cell -> destination cell, inverse content transform.  2x2-cell groups
+    // move rigidly under levels >= 4 and the tile turn: one forward walk per original group.
+    if (tid < NG * NG) {
+        int gy = tid / NG, gx = tid % NG, q = 0;
+        for (int e = (g.emin > 4 ? g.emin : 4); e <= TP; e++) {
+            const int k = e - 3, m1 = (1 << k) - 1;
+            const int by = gy >> k, bx = gx >> k;
             const int a = rec_angle(S.rec, g, e, by, bx);
-            int oy = py & m1, ox = px & m1;
+            int oy = gy & m1, ox = gx & m1;
             fwd_turn(a, m1, oy, ox);
-            py = (by << k) | oy;
-            px = (bx << k) | ox;
+            gy = (by << k) | oy;
+            gx = (bx << k) | ox;
             q += a;
         }
-        fwd_turn(q_up, NC - 1, py, px);
-        q += q_up;
+        fwd_turn(q_up, NG - 1, gy, gx);
+        S.gw[tid] = (gy << 16) | (gx << 8) | ((q + q_up) & 3);
+    }
+    __syncthreads();
+    for (int c = tid; c < NCELL; c += 256) {
+        const int gi = c >> 2, sub = c & 3;
+        const int ogy = gi / NG, ogx = gi % NG;
+        const int cy = 2 * ogy + (sub >> 1), cx = 2 * ogx + (sub & 1);
+        const int gw = S.gw[gi];
+        int q = gw & 3;
+        if (g.emin <= 3) q += rec_angle(S.rec, g, 3, ogy, ogx);     // level 3 = the group itself
+        int sy = sub >> 1, sx = sub & 1;
+        fwd_turn(q & 3, 1, sy, sx);
+        const int py = 2 * (gw >> 16) + sy, px = 2 * ((gw >> 8) & 0xFF) + sx;
         if (g.emin <= 2) q += rec_angle(S.rec, g, 2, cy, cx);
         Cell x = {S.xin[(4 * py) * RS + px], S.xin[(4 * py + 1) * RS + px], S.xin[(4 * py + 2) * RS + px],
                   S.xin[(4 * py + 3) * RS + px]};
@@ -663,10 +703,10 @@ __global__ void __launch_bounds__(256) encode_kernel(Geo g, FusedSched sc, const
     constexpr int T = 1 << TP, TPC = 256 / T;
     constexpr size_t KB = TPC * kRecSlots * 8, PB = sizeof(PermSmem<TP, METHOD>);
     __shared__ __align__(128) uint8_t smem[KB > PB ? KB : PB];
-    const Role ro = role_of(sc, blockIdx.x);
+    const Role ro = role_of(sc);
     if (ro.img >= g.B) return;
     if (ro.key) key_role<TP, true>(g, ro.img, ro.idx, keys, images, ws, smem);
-    else perm_role<TP, METHOD>(g, ro.img, ro.idx, sc.nK, images, ws, enc, ceta, b_out, cap_out, status, smem);
+    else perm_role<TP, METHOD>(g, ro.img, ro.idx, 1 << sc.lgK, images, ws, enc, ceta, b_out, cap_out, status, smem);
 }
 
 template <int TP, int METHOD>
@@ -679,31 +719,36 @@ __global__ void __launch_bounds__(256) recover_kernel(Geo g, FusedSched sc, cons
     constexpr int T = 1 << TP, TPC = 256 / T;
     constexpr size_t KB = TPC * kRecSlots * 8, RB = sizeof(RecSmem<TP>);
     __shared__ __align__(128) uint8_t smem[KB > RB ? KB : RB];
-    const Role ro = role_of(sc, blockIdx.x);
+    const Role ro = role_of(sc);
     if (ro.img >= g.B) return;
     if (ro.key) key_role<TP, false>(g, ro.img, ro.idx, keys, nullptr, ws, smem);
-    else rec_role<TP, METHOD>(g, ro.img, ro.idx, sc.nK, marked, ws, eta_bits, map_bits, lmr_b, out, status, smem);
+    else rec_role<TP, METHOD>(g, ro.img, ro.idx, 1 << sc.lgK, marked, ws, eta_bits, map_bits, lmr_b, out, status, smem);
 }
 
 // ---------------------------------------------------------------------------- launchers
 FusedSched fused_sched(const Geo &g) {
     FusedSched sc;
     const int TPC = 256 / g.T;
-    sc.nK = (g.ntiles + TPC - 1) / TPC;
-    sc.nW = g.ntiles;
-    long long gi = (2ll << 20) / g.HW;                  // ~2 Mpixel per image group
-    if (gi < 1) gi = 1;
-    if (gi > g.B) gi = g.B;
-    sc.GI = (int)gi;
-    sc.ngroups = (g.B + sc.GI - 1) / sc.GI;
+    const int nK = g.ntiles >= TPC ? g.ntiles / TPC : 1;       // powers of two
+    sc.lgK = ilog2(nK);
+    sc.lgW = ilog2(g.ntiles);
+    int gi = 1;
+    while ((long long)(gi * 2) * g.HW <= (2ll << 20) && gi < g.B) gi *= 2;   // ~2 Mpixel per group
+    sc.GI = gi;
+    sc.ngroups = (g.B + gi - 1) / gi;
+    sc.L = 2;
     return sc;
+}
+
+static dim3 fused_grid(const FusedSched &sc) {
+    return dim3((unsigned)((sc.GI << sc.lgK) + (sc.GI << sc.lgW)), (unsigned)(sc.ngroups + sc.L));
 }
 
 template <int TP>
 static void launch_encode_tp(const Geo &g, const uint8_t *images, const uint8_t *keys, const TileWS &ws, uint8_t *enc,
                              uint8_t *ceta, int32_t *b_out, int64_t *cap_out, int32_t *status, cudaStream_t st) {
     const FusedSched sc = fused_sched(g);
-    const unsigned grid = (unsigned)((long long)sc.ngroups * sc.GI * (sc.nK + sc.nW));
+    const dim3 grid = fused_grid(sc);
     if (g.method == 0)
         encode_kernel<TP, 0><<<grid, 256, 0, st>>>(g, sc, images, keys, ws, enc, ceta, b_out, cap_out, status);
     else
@@ -724,7 +769,7 @@ static void launch_recover_tp(const Geo &g, const uint8_t *marked, const uint8_t
                               const uint32_t *eta, const uint32_t *map, const int32_t *lmr_b, uint8_t *out,
                               int32_t *status, cudaStream_t st) {
     const FusedSched sc = fused_sched(g);
-    const unsigned grid = (unsigned)((long long)sc.ngroups * sc.GI * (sc.nK + sc.nW));
+    const dim3 grid = fused_grid(sc);
     if (g.method == 0)
         recover_kernel<TP, 0><<<grid, 256, 0, st>>>(g, sc, marked, keys, ws, eta, map, lmr_b, out, status);
     else

@@ -82,19 +82,22 @@ __device__ __forceinline__ uint32_t bswap32(uint32_t v) { return __byte_perm(v, 
 // and 2 act inside a cell on bytes held in registers (PRMT).
 // --------------------------------------------------------------------------------------
 
-// destination offset -> source offset under `a` clockwise turns of an (m1+1)-block
+// destination offset -> source offset under `a` clockwise turns of an (m1+1)-block,
+// m1 = 2^k - 1 so that m1 - v == v ^ m1.  Branch-free: a = 1: (m1-x, y), 2: (m1-y, m1-x),
+// 3: (x, m1-y).
 __device__ __forceinline__ void inv_turn(int a, int m1, int &y, int &x) {
-    int oy = y, ox = x;
-    if (a == 1) { y = m1 - ox; x = oy; }
-    else if (a == 2) { y = m1 - oy; x = m1 - ox; }
-    else if (a == 3) { y = ox; x = m1 - oy; }
+    const int sw = a & 1, fy = (a ^ (a >> 1)) & 1, fx = (a >> 1) & 1;
+    const int t = sw ? x : y, u = sw ? y : x;
+    y = t ^ (-fy & m1);
+    x = u ^ (-fx & m1);
 }
-// source offset -> destination offset under `a` clockwise turns
+// source offset -> destination offset under `a` clockwise turns: a = 1: (x, m1-y),
+// 2: (m1-y, m1-x), 3: (m1-x, y)
 __device__ __forceinline__ void fwd_turn(int a, int m1, int &y, int &x) {
-    int oy = y, ox = x;
-    if (a == 1) { y = ox; x = m1 - oy; }
-    else if (a == 2) { y = m1 - oy; x = m1 - ox; }
-    else if (a == 3) { y = m1 - ox; x = oy; }
+    const int sw = a & 1, fy = (a >> 1) & 1, fx = (a ^ (a >> 1)) & 1;
+    const int t = sw ? x : y, u = sw ? y : x;
+    y = t ^ (-fy & m1);
+    x = u ^ (-fx & m1);
 }
 
 // A 4x4 cell of bytes: r[i] = row i, byte j = column j (little-endian).

@@ -45,8 +45,9 @@ struct TileWS {
     uint8_t *ragg;       // [B][ntiles][T] per row: last non-redundant masked value in the tile
     uint8_t *rinc;       // [B][ntiles][T] per row: carry out of the tile
 };
-// blockIdx -> role schedule: groups of GI images, nK keystream and nW worker CTAs per image
-struct FusedSched { int GI, ngroups, nK, nW; };
+// blockIdx -> role schedule: groups of GI images (a power of two), 2^lgK keystream and 2^lgW
+// worker CTAs per image, worker CTAs of group g dispatched L grid rows after its keystream CTAs
+struct FusedSched { int GI, ngroups, lgK, lgW, L; };
 FusedSched fused_sched(const Geo &g);
 
 void launch_encode(const Geo &g, const uint8_t *images, const uint8_t *keys, const TileWS &ws, uint8_t *enc,
