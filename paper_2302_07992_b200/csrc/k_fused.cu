@@ -108,7 +108,7 @@ __device__ __forceinline__ void key_role(const Geo &g, int img, int kidx, const 
     const int tid = threadIdx.x, lt = tid / T, row = tid % T;
     const int tile = kidx * TPC + lt;
     const bool valid = tile < g.ntiles;
-    const int ty = valid ? tile / g.tilesX : 0, tx = valid ? tile % g.tilesX : 0;
+    const int ty = valid ? (tile >> g.tlog) : 0, tx = valid ? (tile & (g.tilesX - 1)) : 0;
     const long long o = (long long)(ty * T + row) * g.W + (long long)tx * T;
 
     uint32_t key[8];
@@ -225,10 +225,13 @@ __device__ __forceinline__ void key_role(const Geo &g, int img, int kidx, const 
         const int tl = kidx * TPC + l2;
         if (tl < g.ntiles) ws.rec[((size_t)img * g.ntiles + tl) * kRecSlots + slot] = rec[l2][slot];
     }
-    // publish: every thread's writes fenced, then one arrival per CTA
-    __threadfence();
+    // publish: the barrier orders the CTA's writes before thread 0's gpu-scope fence (cumulative)
+    // and its arrival on the image's counter
     __syncthreads();
-    if (tid == 0) atomicAdd(ws.kdone + img, 1u);
+    if (tid == 0) {
+        __threadfence();
+        atomicAdd(ws.kdone + img, 1u);
+    }
 }
 
 // ======================================================================================
@@ -258,7 +261,7 @@ __device__ __forceinline__ void perm_role(const Geo &g, int img, int dtile, int 
     constexpr int T = 1 << TP, RS = T / 4 + 1, NC = T / 4, NCELL = NC * NC, CPT = T * T / 16, NG = NC / 2;
     PermSmem<TP, METHOD> &S = *reinterpret_cast<PermSmem<TP, METHOD> *>(smem);
     const int tid = threadIdx.x;
-    const int dty = dtile / g.tilesX, dtx = dtile % g.tilesX;
+    const int dty = (dtile >> g.tlog), dtx = (dtile & (g.tilesX - 1));
     const uint8_t *I = images + (size_t)img * g.HW;
     const uint8_t *sg = ws.s + ((size_t)img * g.ntiles + dtile) * (T * T);
 
@@ -269,13 +272,13 @@ __device__ __forceinline__ void perm_role(const Geo &g, int img, int dtile, int 
         bulk_g2s(S.ss, sg, T * T, &S.bar);
         int sty, stx, q;
         upper_walk_inverse(g, ws.pyr + (size_t)img * g.npyr, dty, dtx, sty, stx, q);
-        S.sh[0] = sty * g.tilesX + stx;
+        S.sh[0] = (sty << g.tlog) + stx;
         S.sh[1] = q;
         S.sh[2] = METHOD == 0 ? emr_select_b(ws.hist + img * 8, g.HW) : 0;
     }
     __syncthreads();
     const int stile = S.sh[0], q_up = S.sh[1], b = S.sh[2];
-    const int sty = stile / g.tilesX, stx = stile % g.tilesX;
+    const int sty = (stile >> g.tlog), stx = (stile & (g.tilesX - 1));
     const uint64_t *recg = ws.rec + ((size_t)img * g.ntiles + stile) * kRecSlots;
     if (tid < kRecSlots) S.rec[tid] = __ldcg(recg + tid);
 
@@ -451,7 +454,7 @@ __device__ __forceinline__ void rec_role(const Geo &g, int img, int otile, int n
     constexpr int NG = NC / 2;
     RecSmem<TP> &S = *reinterpret_cast<RecSmem<TP> *>(smem);
     const int tid = threadIdx.x, lane = tid & 31;
-    const int ty = otile / g.tilesX, tx = otile % g.tilesX;
+    const int ty = (otile >> g.tlog), tx = (otile & (g.tilesX - 1));
     const uint8_t *Em = marked + (size_t)img * g.HW;
     uint8_t *O = out + (size_t)img * g.HW;
     const size_t tslot = (size_t)img * g.ntiles + otile;
@@ -471,7 +474,7 @@ __device__ __forceinline__ void rec_role(const Geo &g, int img, int otile, int n
             wait_keys(ws, img, nK);
             int dty, dtx, q;
             upper_walk_forward(g, ws.pyr + (size_t)img * g.npyr, ty, tx, dty, dtx, q);
-            S.sh[0] = dty * g.tilesX + dtx;
+            S.sh[0] = (dty << g.tlog) + dtx;
             S.sh[1] = q;
             mbar_init(&S.bar, 1);
             mbar_expect_tx(&S.bar, T * T);
@@ -489,7 +492,7 @@ __device__ __forceinline__ void rec_role(const Geo &g, int img, int otile, int n
         return;
     }
     const int dt = S.sh[0], q_up = S.sh[1];
-    const int dty = dt / g.tilesX, dtx = dt % g.tilesX;
+    const int dty = (dt >> g.tlog), dtx = (dt & (g.tilesX - 1));
     const uint32_t mask = METHOD == 0 ? ((0xFFu << (8 - b)) & 0xFFu) : (0x7Fu & ~(0xFFu >> b));
     for (int c = tid; c < CPT; c += 256) {
         const int r = c / SEGS, seg = c % SEGS;
@@ -640,9 +643,11 @@ __device__ __forceinline__ void rec_role(const Geo &g, int img, int otile, int n
         if (first_tile) ws.rinc[tslot * T + tid] = S.rowval[tid];
     }
     if (tid == 0) ws.rhas[tslot] = (uint64_t)S.rowhas[0] | ((uint64_t)S.rowhas[1] << 32);
-    __threadfence();
     __syncthreads();
-    if (tid == 0) st_relaxed_u32(ws.rflag + tslot, first_tile ? 2u : 1u);
+    if (tid == 0) {
+        __threadfence();
+        st_relaxed_u32(ws.rflag + tslot, first_tile ? 2u : 1u);
+    }
 
     // ---- look-back for the carry into each row (warp 0; lane owns rows lane, lane + 32)
     if (!first_tile && tid < 32) {
@@ -671,9 +676,11 @@ __device__ __forceinline__ void rec_role(const Geo &g, int img, int otile, int n
             const bool h = (S.rowhas[tid >> 5] >> (tid & 31)) & 1u;
             ws.rinc[tslot * T + tid] = h ? S.rowval[tid] : S.carry[tid];
         }
-        __threadfence();
         __syncthreads();
-        if (tid == 0) st_relaxed_u32(ws.rflag + tslot, 2u);
+        if (tid == 0) {
+            __threadfence();
+            st_relaxed_u32(ws.rflag + tslot, 2u);
+        }
     }
 
     // ---- copy-forward and store
@@ -736,7 +743,7 @@ FusedSched fused_sched(const Geo &g) {
     while ((long long)(gi * 2) * g.HW <= (2ll << 20) && gi < g.B) gi *= 2;   // ~2 Mpixel per group
     sc.GI = gi;
     sc.ngroups = (g.B + gi - 1) / gi;
-    sc.L = 2;
+    sc.L = 6;
     return sc;
 }
 

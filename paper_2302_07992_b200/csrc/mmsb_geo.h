@@ -18,7 +18,7 @@ struct Geo {
     int emin;            // 1 (EMR), min(4, emax) (LMR)            (Q10)
     int tp;              // tile side 2^tp = min(64, min(H, W))
     int T;
-    int tilesY, tilesX, ntiles;
+    int tilesY, tilesX, ntiles, tlog;   // tlog = log2(tilesX)
     int lvl_off[8];      // record slot of level e's first row (e = 1..tp)
     int pyr_off[16];     // upper pyramid: counter offset of level e (tp < e <= emax), per image
     int npyr;            // counters per image
@@ -51,6 +51,7 @@ inline bool make_geo(int method, int B, int H, int W, int tile_log2, Geo *g) {
     g->tilesY = H >> g->tp;
     g->tilesX = W >> g->tp;
     g->ntiles = g->tilesY * g->tilesX;
+    g->tlog = ilog2(g->tilesX);
     int off = 0;
     for (int e = 0; e < 8; e++) g->lvl_off[e] = 0;
     for (int e = 1; e <= g->tp; e++) { g->lvl_off[e] = off; off += g->T >> e; }
