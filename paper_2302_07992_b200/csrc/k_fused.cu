@@ -53,7 +53,7 @@ __device__ __forceinline__ void upper_walk_inverse(const Geo &g, const uint32_t 
     for (int e = g.emax; e > g.tp; e--) {
         const int k = e - g.tp, m1 = (1 << k) - 1;
         const int by = y >> k, bx = x >> k;
-        const int a = (int)(__ldcg(pyr_img + g.pyr_off[e] + by * (g.W >> e) + bx) & 3u);
+        const int a = (int)(pyr_img[g.pyr_off[e] + by * (g.W >> e) + bx] & 3u);
         int oy = y & m1, ox = x & m1;
         inv_turn(a, m1, oy, ox);
         y = (by << k) | oy;
@@ -71,7 +71,7 @@ __device__ __forceinline__ void upper_walk_forward(const Geo &g, const uint32_t 
     for (int e = g.tp + 1; e <= g.emax; e++) {
         const int k = e - g.tp, m1 = (1 << k) - 1;
         const int by = y >> k, bx = x >> k;
-        const int a = (int)(__ldcg(pyr_img + g.pyr_off[e] + by * (g.W >> e) + bx) & 3u);
+        const int a = (int)(pyr_img[g.pyr_off[e] + by * (g.W >> e) + bx] & 3u);
         int oy = y & m1, ox = x & m1;
         fwd_turn(a, m1, oy, ox);
         y = (by << k) | oy;
@@ -94,6 +94,22 @@ __device__ __forceinline__ int emr_select_b(const uint32_t *hist_img, long long 
 
 __device__ __forceinline__ void wait_keys(const TileWS &ws, int img, int nK) {
     while (ld_acquire_u32(ws.kdone + img) < (unsigned)nK) __nanosleep(512);
+}
+
+// Warp 0 of a worker CTA: wait for the image's keystream CTAs, then make the upper angle
+// pyramid walkable -- copied into shared memory in one parallel load when it is small
+// (<= kPyrSmem counters: images up to 2048^2), else walked in L2.  Returns the pointer.
+constexpr int kPyrSmem = 1536;
+__device__ __forceinline__ const uint32_t *warp0_ready(const Geo &g, const TileWS &ws, int img, int nK,
+                                                       uint32_t *spyr) {
+    const int lane = threadIdx.x & 31;
+    if (lane == 0) wait_keys(ws, img, nK);
+    __syncwarp();
+    const uint32_t *pyr_img = ws.pyr + (size_t)img * g.npyr;
+    if (g.npyr > kPyrSmem) return pyr_img;
+    for (int i = lane; i < g.npyr; i += 32) spyr[i] = __ldcg(pyr_img + i);
+    __syncwarp();
+    return spyr;
 }
 
 // ======================================================================================
@@ -225,13 +241,10 @@ __device__ __forceinline__ void key_role(const Geo &g, int img, int kidx, const 
         const int tl = kidx * TPC + l2;
         if (tl < g.ntiles) ws.rec[((size_t)img * g.ntiles + tl) * kRecSlots + slot] = rec[l2][slot];
     }
-    // publish: the barrier orders the CTA's writes before thread 0's gpu-scope fence (cumulative)
-    // and its arrival on the image's counter
+    // publish: the barrier orders the CTA's writes before thread 0's release arrival on the
+    // image's counter (release is cumulative)
     __syncthreads();
-    if (tid == 0) {
-        __threadfence();
-        atomicAdd(ws.kdone + img, 1u);
-    }
+    if (tid == 0) red_release_add_u32(ws.kdone + img, 1u);
 }
 
 // ======================================================================================
@@ -248,6 +261,7 @@ struct PermSmem {
     uint32_t src[T * RS];                    // source tile carrier words (row stride RS)
     uint32_t lab[METHOD == 1 ? T * RS : 1];  // LMR: label | eta words
     uint64_t rec[kRecSlots];
+    uint32_t pyr[kPyrSmem];                  // upper angle pyramid of the image (small images)
     int gw[NG * NG];                         // per destination 2x2-cell group: source group, turns
     uint64_t bar;
     int sh[4];
@@ -265,16 +279,18 @@ __device__ __forceinline__ void perm_role(const Geo &g, int img, int dtile, int 
     const uint8_t *I = images + (size_t)img * g.HW;
     const uint8_t *sg = ws.s + ((size_t)img * g.ntiles + dtile) * (T * T);
 
-    if (tid == 0) {
-        wait_keys(ws, img, nK);
+    if (tid < 32) {
+        const uint32_t *pyr = warp0_ready(g, ws, img, nK, S.pyr);
+        if (tid == 0) {
         mbar_init(&S.bar, 1);
         mbar_expect_tx(&S.bar, T * T);
         bulk_g2s(S.ss, sg, T * T, &S.bar);
         int sty, stx, q;
-        upper_walk_inverse(g, ws.pyr + (size_t)img * g.npyr, dty, dtx, sty, stx, q);
+        upper_walk_inverse(g, pyr, dty, dtx, sty, stx, q);
         S.sh[0] = (sty << g.tlog) + stx;
         S.sh[1] = q;
         S.sh[2] = METHOD == 0 ? emr_select_b(ws.hist + img * 8, g.HW) : 0;
+        }
     }
     __syncthreads();
     const int stile = S.sh[0], q_up = S.sh[1], b = S.sh[2];
@@ -432,14 +448,21 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 template <int TP>
 struct RecSmem {
     static constexpr int T = 1 << TP, RS = T / 4 + 1;
-    uint8_t ss[T * T];                       // keystream of the destination tile (bulk copy)
-    uint8_t es[T * T];                       // marked destination tile (cp.async)
+    union {
+        struct {
+            uint8_t ss[T * T];               // keystream of the destination tile (bulk copy)
+            uint8_t es[T * T];               // marked destination tile (cp.async)
+        };
+        struct {
+            uint32_t xo[T * RS], lo[T * RS]; // original domain (written after ss/es are consumed)
+        };
+    };
     uint32_t xin[T * RS], lin[T * RS];       // destination domain: decrypted words, map bytes
-    uint32_t xo[T * RS], lo[T * RS];         // original domain
     uint64_t rec[kRecSlots];
     uint32_t mbits[T][2], ebits[T][2];       // LMR: decoded map / eta bits of the destination rows
     uint8_t rowval[T], carry[T];
     uint32_t rowhas[2];
+    uint32_t pyr[kPyrSmem];                  // upper angle pyramid of the image (small images)
     int gw[(T / 8) * (T / 8)];               // per original 2x2-cell group: destination group, turns
     uint64_t bar;
     int sh[4];
@@ -459,8 +482,9 @@ __device__ __forceinline__ void rec_role(const Geo &g, int img, int otile, int n
     uint8_t *O = out + (size_t)img * g.HW;
     const size_t tslot = (size_t)img * g.ntiles + otile;
 
-    if (tid == 0) {
-        int b;
+    if (tid < 32) {
+        int b = 0;
+        if (tid == 0) {
         if constexpr (METHOD == 0) {
             const int field = ((Em[0] & 1) << 2) | ((Em[1] & 1) << 1) | (Em[2] & 1);
             b = field > 5 ? -1 : field + 2;
@@ -470,15 +494,19 @@ __device__ __forceinline__ void rec_role(const Geo &g, int img, int otile, int n
             if (otile == 0 && b > 0) status[img] = 0;
         }
         S.sh[2] = b;
+        }
+        b = __shfl_sync(0xffffffffu, b, 0);
         if (b > 0) {
-            wait_keys(ws, img, nK);
+            const uint32_t *pyr = warp0_ready(g, ws, img, nK, S.pyr);
+            if (tid == 0) {
             int dty, dtx, q;
-            upper_walk_forward(g, ws.pyr + (size_t)img * g.npyr, ty, tx, dty, dtx, q);
+            upper_walk_forward(g, pyr, ty, tx, dty, dtx, q);
             S.sh[0] = (dty << g.tlog) + dtx;
             S.sh[1] = q;
             mbar_init(&S.bar, 1);
             mbar_expect_tx(&S.bar, T * T);
             bulk_g2s(S.ss, ws.s + ((size_t)img * g.ntiles + S.sh[0]) * (T * T), T * T, &S.bar);
+            }
         }
     }
     __syncthreads();
@@ -610,16 +638,17 @@ __device__ __forceinline__ void rec_role(const Geo &g, int img, int otile, int n
         for (int i = 0; i < 4; i++) m16 |= bytes_to_bits4(lw[i]) << (4 * i);
         has = m16 != 0;
         if (has) {
-            const int li = 31 - __clz(m16);
-            val = (int)((xw[li >> 2] >> (8 * (li & 3))) & mask);
+            const int li = 31 - __clz(m16), wi = li >> 2;
+            const uint32_t wsel = wi == 0 ? xw[0] : wi == 1 ? xw[1] : wi == 2 ? xw[2] : xw[3];
+            val = (int)((wsel >> (8 * (li & 3))) & mask);
         }
     }
     // exclusive "last non-redundant" across the row's segments (without the tile carry-in)
-    const unsigned gm = SEGS >= 32 ? 0xffffffffu : (((1u << SEGS) - 1u) << (lane & ~(SEGS - 1)));
     int ehas = 0, evl = 0;
-    for (int s2 = 0; s2 < SEGS; s2++) {
-        const int oh = __shfl_sync(gm, has, (lane & ~(SEGS - 1)) + s2, 32);
-        const int ov = __shfl_sync(gm, val, (lane & ~(SEGS - 1)) + s2, 32);
+#pragma unroll
+    for (int s2 = 0; s2 < SEGS - 1; s2++) {                 // whole-warp shuffles within SEGS lanes
+        const int oh = __shfl_sync(0xffffffffu, has, s2, SEGS);
+        const int ov = __shfl_sync(0xffffffffu, val, s2, SEGS);
         if (s2 < seg && oh) { ehas = 1; evl = ov; }
     }
     const int rval = has ? val : evl;                   // last non-redundant value of the row so far
@@ -644,10 +673,7 @@ __device__ __forceinline__ void rec_role(const Geo &g, int img, int otile, int n
     }
     if (tid == 0) ws.rhas[tslot] = (uint64_t)S.rowhas[0] | ((uint64_t)S.rowhas[1] << 32);
     __syncthreads();
-    if (tid == 0) {
-        __threadfence();
-        st_relaxed_u32(ws.rflag + tslot, first_tile ? 2u : 1u);
-    }
+    if (tid == 0) st_release_u32(ws.rflag + tslot, first_tile ? 2u : 1u);
 
     // ---- look-back for the carry into each row (warp 0; lane owns rows lane, lane + 32)
     if (!first_tile && tid < 32) {
@@ -677,10 +703,7 @@ __device__ __forceinline__ void rec_role(const Geo &g, int img, int otile, int n
             ws.rinc[tslot * T + tid] = h ? S.rowval[tid] : S.carry[tid];
         }
         __syncthreads();
-        if (tid == 0) {
-            __threadfence();
-            st_relaxed_u32(ws.rflag + tslot, 2u);
-        }
+        if (tid == 0) st_release_u32(ws.rflag + tslot, 2u);
     }
 
     // ---- copy-forward and store
@@ -702,7 +725,7 @@ __device__ __forceinline__ void rec_role(const Geo &g, int img, int otile, int n
 // The fused kernels
 // ======================================================================================
 template <int TP, int METHOD>
-__global__ void __launch_bounds__(256) encode_kernel(Geo g, FusedSched sc, const uint8_t *__restrict__ images,
+__global__ void __launch_bounds__(256, 8) encode_kernel(Geo g, FusedSched sc, const uint8_t *__restrict__ images,
                                                      const uint8_t *__restrict__ keys, TileWS ws,
                                                      uint8_t *__restrict__ enc, uint8_t *__restrict__ ceta,
                                                      int32_t *__restrict__ b_out, int64_t *__restrict__ cap_out,
@@ -717,7 +740,7 @@ __global__ void __launch_bounds__(256) encode_kernel(Geo g, FusedSched sc, const
 }
 
 template <int TP, int METHOD>
-__global__ void __launch_bounds__(256) recover_kernel(Geo g, FusedSched sc, const uint8_t *__restrict__ marked,
+__global__ void __launch_bounds__(256, 8) recover_kernel(Geo g, FusedSched sc, const uint8_t *__restrict__ marked,
                                                       const uint8_t *__restrict__ keys, TileWS ws,
                                                       const uint32_t *__restrict__ eta_bits,
                                                       const uint32_t *__restrict__ map_bits,

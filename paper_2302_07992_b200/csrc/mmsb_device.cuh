@@ -117,24 +117,21 @@ __device__ __forceinline__ Cell cell_transpose(Cell c) {
     return o;
 }
 
-// rotate the cell clockwise by 90 deg * r:  r odd = transpose + ...; built from transpose,
-// column reversal (byte reverse) and row reversal.
-//   r=1: out[i][j] = in[3-j][i]  = transpose, then reverse columns
-//   r=2: out[i][j] = in[3-i][3-j] = reverse rows and columns
-//   r=3: out[i][j] = in[j][3-i]  = transpose, then reverse rows
+// rotate the cell clockwise by 90 deg * r, branch-free (r differs between lanes):
+//   r=0: out_i = in_i            r=1: out_i = rev(T_i)      (out[i][j] = in[3-j][i])
+//   r=2: out_i = rev(in_{3-i})   r=3: out_i = T_{3-i}       (out[i][j] = in[j][3-i])
+// with T = transpose(in) and rev = byte reversal.
 __device__ __forceinline__ Cell cell_rot_cw(Cell c, int r) {
-    if (r & 1) c = cell_transpose(c);
-    const bool rev_cols = (r == 1) || (r == 2);
-    const bool rev_rows = (r == 2) || (r == 3);
-    if (rev_cols) {
-        c.r0 = __byte_perm(c.r0, 0, 0x0123); c.r1 = __byte_perm(c.r1, 0, 0x0123);
-        c.r2 = __byte_perm(c.r2, 0, 0x0123); c.r3 = __byte_perm(c.r3, 0, 0x0123);
-    }
-    if (rev_rows) {
-        uint32_t t = c.r0; c.r0 = c.r3; c.r3 = t;
-        t = c.r1; c.r1 = c.r2; c.r2 = t;
-    }
-    return c;
+    const Cell t = cell_transpose(c);
+    const bool odd = r & 1, flip = r >= 2;
+    const uint32_t sel = (r == 1 || r == 2) ? 0x0123u : 0x3210u;
+    const uint32_t a0 = odd ? t.r0 : c.r0, a1 = odd ? t.r1 : c.r1, a2 = odd ? t.r2 : c.r2, a3 = odd ? t.r3 : c.r3;
+    Cell o;
+    o.r0 = __byte_perm(flip ? a3 : a0, 0, sel);
+    o.r1 = __byte_perm(flip ? a2 : a1, 0, sel);
+    o.r2 = __byte_perm(flip ? a1 : a2, 0, sel);
+    o.r3 = __byte_perm(flip ? a0 : a3, 0, sel);
+    return o;
 }
 
 // Level-1 (2x2) clockwise rotations of the two 2x2 blocks held in a row pair (top, bot):
@@ -211,6 +208,12 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {
     unsigned v;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned *p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_release_add_u32(unsigned *p, unsigned v) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ void st_relaxed_u32(unsigned *p, unsigned v) {
     asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
