@@ -93,6 +93,9 @@ __device__ __forceinline__ int emr_select_b(const uint32_t *hist_img, long long 
 }
 
 __device__ __forceinline__ void wait_keys(const TileWS &ws, int img, int nK) {
+#if defined(MMSB_PROBE_ROLES)
+    if (!(MMSB_PROBE_ROLES & 1)) return;            // keystream CTAs disabled: nothing to wait for
+#endif
     while (ld_acquire_u32(ws.kdone + img) < (unsigned)nK) __nanosleep(512);
 }
 
@@ -248,476 +251,453 @@ __device__ __forceinline__ void key_role(const Geo &g, int img, int kidx, const 
 }
 
 // ======================================================================================
-// W role, encode: one CTA per destination tile (a3, a5).
-//   EMR: carrier v = (I & 0xFE) | l with l = [c < b] (location map, P:610), permuted as a
-//        whole byte; E = v_r XOR (s & 0xFE) (eq. image_encryption P:739 + LSB map P:744);
-//        header b-2 in the LSBs of r = 0..2 (Q14).
-//   LMR: E = I_r XOR s; second plane ceta = (I & 0x80) | c permuted alongside (for the coder).
+// Worker roles.  One worker CTA per strip of tiles (one tile row of the image), walking the
+// strip left to right with a two-stage cp.async pipeline: the next tile's data is in flight
+// while the current one is transformed.  The tile map of the strip (upper-level walks) is
+// computed once, up front, by warp 0 from the angle pyramid.
 // ======================================================================================
-template <int TP, int METHOD>
-struct PermSmem {
-    static constexpr int T = 1 << TP, RS = T / 4 + 1, NG = T / 8;
-    uint8_t ss[T * T];                       // keystream of the destination tile (bulk copy)
-    uint32_t src[T * RS];                    // source tile carrier words (row stride RS)
-    uint32_t lab[METHOD == 1 ? T * RS : 1];  // LMR: label | eta words
-    uint64_t rec[kRecSlots];
-    uint32_t pyr[kPyrSmem];                  // upper angle pyramid of the image (small images)
-    int gw[NG * NG];                         // per destination 2x2-cell group: source group, turns
-    uint64_t bar;
-    int sh[4];
-};
+constexpr int kMaxTilesX = 512;                  // W <= 32768 with 64-pixel tiles
 
-template <int TP, int METHOD>
-__device__ __forceinline__ void perm_role(const Geo &g, int img, int dtile, int nK, const uint8_t *__restrict__ images,
-                                          const TileWS &ws, uint8_t *__restrict__ enc, uint8_t *__restrict__ ceta_out,
-                                          int32_t *__restrict__ b_out, int64_t *__restrict__ cap_out,
-                                          int32_t *__restrict__ status, uint8_t *smem) {
-    constexpr int T = 1 << TP, RS = T / 4 + 1, NC = T / 4, NCELL = NC * NC, CPT = T * T / 16, NG = NC / 2;
-    PermSmem<TP, METHOD> &S = *reinterpret_cast<PermSmem<TP, METHOD> *>(smem);
-    const int tid = threadIdx.x;
-    const int dty = (dtile >> g.tlog), dtx = (dtile & (g.tilesX - 1));
-    const uint8_t *I = images + (size_t)img * g.HW;
-    const uint8_t *sg = ws.s + ((size_t)img * g.ntiles + dtile) * (T * T);
-
-    if (tid < 32) {
-        const uint32_t *pyr = warp0_ready(g, ws, img, nK, S.pyr);
-        if (tid == 0) {
-        mbar_init(&S.bar, 1);
-        mbar_expect_tx(&S.bar, T * T);
-        bulk_g2s(S.ss, sg, T * T, &S.bar);
-        int sty, stx, q;
-        upper_walk_inverse(g, pyr, dty, dtx, sty, stx, q);
-        S.sh[0] = (sty << g.tlog) + stx;
-        S.sh[1] = q;
-        S.sh[2] = METHOD == 0 ? emr_select_b(ws.hist + img * 8, g.HW) : 0;
-        }
-    }
-    __syncthreads();
-    const int stile = S.sh[0], q_up = S.sh[1], b = S.sh[2];
-    const int sty = (stile >> g.tlog), stx = (stile & (g.tilesX - 1));
-    const uint64_t *recg = ws.rec + ((size_t)img * g.ntiles + stile) * kRecSlots;
-    if (tid < kRecSlots) S.rec[tid] = __ldcg(recg + tid);
-
-    // source tile + left halo -> labels -> carrier (EMR) or I and ceta (LMR)
-    const uint32_t M = METHOD == 0 ? (0xFFu << (8 - b)) & 0xFFu : 0;
-    const uint32_t MB = M * 0x01010101u;
-    for (int c = tid; c < CPT; c += 256) {
-        const int r = c / (T / 16), seg = c % (T / 16);
-        const long long gx = (long long)stx * T + seg * 16;
-        const uint8_t *p = I + (size_t)(sty * T + r) * g.W + gx;
-        const uint4 u = __ldg(reinterpret_cast<const uint4 *>(p));
-        const uint32_t iw[4] = {u.x, u.y, u.z, u.w};
-        uint32_t prev = gx > 0 ? ((uint32_t)__ldg(p - 1) << 24) : 0u;
-        uint32_t vw[4], cw[4];
-#pragma unroll
-        for (int i = 0; i < 4; i++) {
-            uint32_t x = iw[i] ^ __byte_perm(prev, iw[i], 0x6543);
-            if (i == 0 && gx == 0) x |= 0xFFu;                     // column 0: always non-redundant
-            prev = iw[i];
-            if constexpr (METHOD == 0) {
-                const uint32_t t = x & MB;
-                const uint32_t nz = (((t & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | t) & 0x80808080u;   // byte != 0
-                vw[i] = (iw[i] & 0xFEFEFEFEu) | (nz >> 7);
-            } else {
-                // c = #leading equal bits (8 if equal), per byte; column 0 -> 0
-                uint32_t cv = 0;
-#pragma unroll
-                for (int j = 0; j < 4; j++) {
-                    const uint32_t xb = (x >> (8 * j)) & 0xFFu;
-                    const uint32_t cj = xb ? (uint32_t)(__clz(xb) - 24) : 8u;
-                    cv |= cj << (8 * j);
-                }
-                cw[i] = cv | (iw[i] & 0x80808080u);
-                vw[i] = iw[i];
-            }
-        }
-#pragma unroll
-        for (int i = 0; i < 4; i++) {
-            S.src[r * RS + seg * 4 + i] = vw[i];
-            if constexpr (METHOD == 1) S.lab[r * RS + seg * 4 + i] = cw[i];
-        }
-    }
-    mbar_wait(&S.bar, 0);
-    __syncthreads();
-    // the consumed scratch (this tile's keystream, the source tile's record) leaves L2 unwritten
-    if (tid < (T * T) / 128) discard_l2(sg + 128 * tid);
-    else if (tid >= 64 && tid < 64 + kRecSlots * 8 / 128) discard_l2(recg + 16 * (tid - 64));
-    // 2x2-cell groups (8x8 pixels) move rigidly under the levels >= 4 and under the tile's own
-    // turn q_up: one inverse walk per destination group, shared by its 4 cells
-    if (tid < NG * NG) {
-        int gy = tid / NG, gx = tid % NG;
-        inv_turn(q_up, NG - 1, gy, gx);
-        int q = q_up;
-        for (int e = TP; e >= 4 && e >= g.emin; e--) {
-            const int k = e - 3, m1 = (1 << k) - 1;
-            const int by = gy >> k, bx = gx >> k;
-            const int a = rec_angle(S.rec, g, e, by, bx);
-            int oy = gy & m1, ox = gx & m1;
-            inv_turn(a, m1, oy, ox);
-            gy = (by << k) | oy;
-            gx = (bx << k) | ox;
-            q += a;
-        }
-        S.gw[tid] = (gy << 16) | (gx << 8) | (q & 3);
-    }
-    __syncthreads();
-
-    // cells: destination cell -> source cell, then in-cell levels 1, 2
-    for (int c = tid; c < NCELL; c += 256) {
-        const int gi = c >> 2, sub = c & 3;
-        const int cy = 2 * (gi / NG) + (sub >> 1), cx = 2 * (gi % NG) + (sub & 1);
-        const int gw = S.gw[gi], sgy = gw >> 16, sgx = (gw >> 8) & 0xFF;
-        int q = gw & 3;
-        if (g.emin <= 3) q += rec_angle(S.rec, g, 3, sgy, sgx);     // level 3 = the group itself
-        int sy = sub >> 1, sx = sub & 1;
-        inv_turn(q & 3, 1, sy, sx);
-        const int py = 2 * sgy + sy, px = 2 * sgx + sx;
-        Cell v = {S.src[(4 * py) * RS + px], S.src[(4 * py + 1) * RS + px], S.src[(4 * py + 2) * RS + px],
-                  S.src[(4 * py + 3) * RS + px]};
-        Cell cl;
-        if constexpr (METHOD == 1)
-            cl = {S.lab[(4 * py) * RS + px], S.lab[(4 * py + 1) * RS + px], S.lab[(4 * py + 2) * RS + px],
-                  S.lab[(4 * py + 3) * RS + px]};
-        if (g.emin <= 1) {
-            const uint32_t a01 = (uint32_t)(S.rec[g.lvl_off[1] + 2 * py] >> (4 * px)) & 0xFu;
-            const uint32_t a23 = (uint32_t)(S.rec[g.lvl_off[1] + 2 * py + 1] >> (4 * px)) & 0xFu;
-            pair_rot_cw(v.r0, v.r1, a01 & 3, a01 >> 2);
-            pair_rot_cw(v.r2, v.r3, a23 & 3, a23 >> 2);
-            if constexpr (METHOD == 1) {
-                pair_rot_cw(cl.r0, cl.r1, a01 & 3, a01 >> 2);
-                pair_rot_cw(cl.r2, cl.r3, a23 & 3, a23 >> 2);
-            }
-        }
-        if (g.emin <= 2) q += rec_angle(S.rec, g, 2, py, px);
-        v = cell_rot_cw(v, q & 3);
-        if constexpr (METHOD == 1) cl = cell_rot_cw(cl, q & 3);
-
-        const uint32_t *sw = reinterpret_cast<const uint32_t *>(S.ss) + (4 * cy) * (T / 4) + cx;
-        const uint32_t s0 = sw[0], s1 = sw[T / 4], s2 = sw[2 * (T / 4)], s3 = sw[3 * (T / 4)];
-        const size_t base = (size_t)(dty * T + 4 * cy) * g.W + (size_t)dtx * T + 4 * cx;
-        uint32_t e0, e1, e2, e3;
-        if constexpr (METHOD == 0) {
-            e0 = v.r0 ^ (s0 & 0xFEFEFEFEu); e1 = v.r1 ^ (s1 & 0xFEFEFEFEu);
-            e2 = v.r2 ^ (s2 & 0xFEFEFEFEu); e3 = v.r3 ^ (s3 & 0xFEFEFEFEu);
-            if (dtile == 0 && c == 0) {
-                // header: LSB(E[r]) = bit (2 - r) of b - 2 for r = 0..2; the map there is forced
-                // to 1, so capacity counts zeros after forcing (Q14)
-                const uint32_t m = v.r0 & 0x00010101u;
-                const int forced = (int)(m & 1u) + (int)((m >> 8) & 1u) + (int)((m >> 16) & 1u);
-                const uint32_t hb = (uint32_t)(b - 2);
-                const uint32_t hdr = ((hb >> 2) & 1u) | (((hb >> 1) & 1u) << 8) | ((hb & 1u) << 16);
-                e0 = (e0 & 0xFFFEFEFEu) | hdr;
-                const long long zeros = g.HW - (long long)__ldcg(ws.hist + img * 8 + b);
-                b_out[img] = b;
-                cap_out[img] = (long long)b * (zeros - (3 - forced));
-                status[img] = 0;
-            }
-        } else {
-            e0 = v.r0 ^ s0; e1 = v.r1 ^ s1; e2 = v.r2 ^ s2; e3 = v.r3 ^ s3;
-            uint8_t *co = ceta_out + (size_t)img * g.HW + base;
-            *reinterpret_cast<uint32_t *>(co) = cl.r0;
-            *reinterpret_cast<uint32_t *>(co + g.W) = cl.r1;
-            *reinterpret_cast<uint32_t *>(co + 2 * (size_t)g.W) = cl.r2;
-            *reinterpret_cast<uint32_t *>(co + 3 * (size_t)g.W) = cl.r3;
-        }
-        uint8_t *eo = enc + (size_t)img * g.HW + base;
-        *reinterpret_cast<uint32_t *>(eo) = e0;
-        *reinterpret_cast<uint32_t *>(eo + g.W) = e1;
-        *reinterpret_cast<uint32_t *>(eo + 2 * (size_t)g.W) = e2;
-        *reinterpret_cast<uint32_t *>(eo + 3 * (size_t)g.W) = e3;
-    }
-}
-
-// ======================================================================================
-// W role, recover: one CTA per ORIGINAL tile (a10).
-//   X = I_e' XOR s (every bit, Q20); EMR: map bit = raw LSB of I_e' (r < 3 forced to 1);
-//   LMR: MSB := eta_r and the map come from the decoded planes.  Inverse cell transform,
-//   then per row omega := masked bits of the last non-redundant pixel, replaced into the
-//   redundant ones.  The carry into the tile's rows comes from the tiles to
-//   the left (per-row decoupled look-back: aggregate = last non-redundant value of the row
-//   inside the tile, inclusive = carry out).
-// ======================================================================================
 __device__ __forceinline__ uint32_t bits4_to_bytes(uint32_t m4) { return ((m4 & 0xFu) * 0x00204081u) & 0x01010101u; }
 __device__ __forceinline__ uint32_t bytes_to_bits4(uint32_t l) { return (l | (l >> 7) | (l >> 14) | (l >> 21)) & 0xFu; }
 
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
 }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+__device__ __forceinline__ void cp_async4(void *smem, const void *gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N> __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
+// source 2x2-cell group of destination group (gy, gx) in a tile (levels >= 4 and the tile's own
+// turn q_up move 8x8 groups rigidly); returns gy' << 16 | gx' << 8 | turns
+__device__ __forceinline__ int group_walk_inverse(const Geo &g, const uint64_t *rec, int TP, int NG, int q_up,
+                                                  int gy, int gx) {
+    inv_turn(q_up, NG - 1, gy, gx);
+    int q = q_up;
+    for (int e = TP; e >= 4 && e >= g.emin; e--) {
+        const int k = e - 3, m1 = (1 << k) - 1;
+        const int by = gy >> k, bx = gx >> k;
+        const int a = rec_angle(rec, g, e, by, bx);
+        int oy = gy & m1, ox = gx & m1;
+        inv_turn(a, m1, oy, ox);
+        gy = (by << k) | oy;
+        gx = (bx << k) | ox;
+        q += a;
+    }
+    return (gy << 16) | (gx << 8) | (q & 3);
+}
+// destination group of original group (gy, gx)
+__device__ __forceinline__ int group_walk_forward(const Geo &g, const uint64_t *rec, int TP, int NG, int q_up,
+                                                  int gy, int gx) {
+    int q = 0;
+    for (int e = (g.emin > 4 ? g.emin : 4); e <= TP; e++) {
+        const int k = e - 3, m1 = (1 << k) - 1;
+        const int by = gy >> k, bx = gx >> k;
+        const int a = rec_angle(rec, g, e, by, bx);
+        int oy = gy & m1, ox = gx & m1;
+        fwd_turn(a, m1, oy, ox);
+        gy = (by << k) | oy;
+        gx = (bx << k) | ox;
+        q += a;
+    }
+    fwd_turn(q_up, NG - 1, gy, gx);
+    return (gy << 16) | (gx << 8) | ((q + q_up) & 3);
+}
+
+// ======================================================================================
+// W role, encode (a3, a5): destination strip dty, tiles left to right.
+//   EMR: carrier v = (I & 0xFE) | l with l = [c < b] (location map, P:610), permuted as a
+//        whole byte; E = v_r XOR (s & 0xFE) (eq. image_encryption P:739 + LSB map P:744);
+//        header b-2 in the LSBs of r = 0..2 (Q14).
+//   LMR: E = I_r XOR s; second plane ceta = (I & 0x80) | c permuted alongside (for the coder).
+// The carrier / label of a source pixel needs its left neighbour: computed per cell row from
+// the staged source tile (and, at the tile's left edge, the staged halo word).
+// ======================================================================================
 template <int TP>
-struct RecSmem {
-    static constexpr int T = 1 << TP, RS = T / 4 + 1;
-    union {
-        struct {
-            uint8_t ss[T * T];               // keystream of the destination tile (bulk copy)
-            uint8_t es[T * T];               // marked destination tile (cp.async)
-        };
-        struct {
-            uint32_t xo[T * RS], lo[T * RS]; // original domain (written after ss/es are consumed)
-        };
-    };
-    uint32_t xin[T * RS], lin[T * RS];       // destination domain: decrypted words, map bytes
-    uint64_t rec[kRecSlots];
-    uint32_t mbits[T][2], ebits[T][2];       // LMR: decoded map / eta bits of the destination rows
-    uint8_t rowval[T], carry[T];
-    uint32_t rowhas[2];
+struct PermSmem {
+    static constexpr int T = 1 << TP;
+    struct Stage {
+        uint32_t is[T * T / 4];              // source tile of I (row-major words)
+        uint32_t halo[T];                    // per row: the aligned word left of the row (byte 3)
+        uint32_t ss[T * T / 4];              // keystream of the destination tile (tile-major)
+        uint64_t rec[kRecSlots];             // angle record of the source tile
+    } st[2];
     uint32_t pyr[kPyrSmem];                  // upper angle pyramid of the image (small images)
-    int gw[(T / 8) * (T / 8)];               // per original 2x2-cell group: destination group, turns
-    uint64_t bar;
+    int smap[kMaxTilesX];                    // per destination tile of the strip: source << 2 | q
     int sh[4];
 };
 
 template <int TP, int METHOD>
-__device__ __forceinline__ void rec_role(const Geo &g, int img, int otile, int nK, const uint8_t *__restrict__ marked,
+__device__ __forceinline__ void perm_role(const Geo &g, int img, int dty, int nK, const uint8_t *__restrict__ images,
+                                          const TileWS &ws, uint8_t *__restrict__ enc, uint8_t *__restrict__ ceta_out,
+                                          int32_t *__restrict__ b_out, int64_t *__restrict__ cap_out,
+                                          int32_t *__restrict__ status, uint8_t *smem) {
+    constexpr int T = 1 << TP, NW = T / 4, NC = T / 4, NCELL = NC * NC, CPT = T * T / 16, NG = NC / 2;
+    PermSmem<TP> &S = *reinterpret_cast<PermSmem<TP> *>(smem);
+    const int tid = threadIdx.x;
+    const uint8_t *I = images + (size_t)img * g.HW;
+
+    if (tid < 32) {
+        const uint32_t *pyr = warp0_ready(g, ws, img, nK, S.pyr);
+        for (int j = tid; j < g.tilesX; j += 32) {
+            int sty, stx, q;
+            upper_walk_inverse(g, pyr, dty, j, sty, stx, q);
+            S.smap[j] = (((sty << g.tlog) + stx) << 2) | q;
+        }
+        if (tid == 0) S.sh[0] = METHOD == 0 ? emr_select_b(ws.hist + img * 8, g.HW) : 0;
+    }
+    __syncthreads();
+    const int b = S.sh[0];
+    const uint32_t MB = METHOD == 0 ? ((0xFFu << (8 - b)) & 0xFFu) * 0x01010101u : 0u;
+
+    auto issue = [&](int j) {
+        typename PermSmem<TP>::Stage &st = S.st[j & 1];
+        const int stile = S.smap[j] >> 2, sty = stile >> g.tlog, stx = stile & (g.tilesX - 1);
+        const size_t dslot = (size_t)img * g.ntiles + ((size_t)dty << g.tlog) + j;
+        for (int c = tid; c < CPT; c += 256) {
+            const int r = c / (T / 16), seg = c % (T / 16);
+            cp_async16(&st.is[r * NW + seg * 4], I + (size_t)(sty * T + r) * g.W + (size_t)stx * T + seg * 16);
+            cp_async16(&st.ss[4 * c], ws.s + dslot * (T * T) + 16 * c);
+        }
+        if (tid < T && stx > 0) cp_async4(&st.halo[tid], I + (size_t)(sty * T + tid) * g.W + (size_t)stx * T - 4);
+        if (tid < kRecSlots / 2)
+            cp_async16(&st.rec[2 * tid], ws.rec + ((size_t)img * g.ntiles + stile) * kRecSlots + 2 * tid);
+        cp_async_commit();
+    };
+
+    issue(0);
+    for (int j = 0; j < g.tilesX; j++) {
+        if (j + 1 < g.tilesX) {
+            issue(j + 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();                                           // stage j landed for everyone
+        const typename PermSmem<TP>::Stage &st = S.st[j & 1];
+        const int mp = S.smap[j], stile = mp >> 2, q_up = mp & 3;
+        const int stx = stile & (g.tilesX - 1);
+        const int dtile = (dty << g.tlog) + j;
+        {   // the consumed scratch (destination keystream, source record) leaves L2 unwritten
+            const size_t dslot = (size_t)img * g.ntiles + dtile;
+            if (tid < (T * T) / 128) discard_l2(ws.s + dslot * (T * T) + 128 * tid);
+            else if (tid >= 64 && tid < 64 + kRecSlots * 8 / 128)
+                discard_l2(ws.rec + ((size_t)img * g.ntiles + stile) * kRecSlots + 16 * (tid - 64));
+        }
+        for (int c = tid; c < NCELL; c += 256) {
+            // destination cell -> source cell: group walk (levels >= 4, q_up), level 3 inside the
+            // group, then in-cell levels 1, 2
+            const int gi = c >> 2, sub = c & 3;
+            const int cy = 2 * (gi / NG) + (sub >> 1), cx = 2 * (gi % NG) + (sub & 1);
+            const int gw = group_walk_inverse(g, st.rec, TP, NG, q_up, gi / NG, gi % NG);
+            const int sgy = gw >> 16, sgx = (gw >> 8) & 0xFF;
+            int q = gw & 3;
+            if (g.emin <= 3) q += rec_angle(st.rec, g, 3, sgy, sgx);
+            int sy = sub >> 1, sx = sub & 1;
+            inv_turn(q & 3, 1, sy, sx);
+            const int py = 2 * sgy + sy, px = 2 * sgx + sx;
+            // source cell rows -> carrier (EMR) / image + label|eta (LMR)
+            uint32_t vr[4], cr[4];
+#pragma unroll
+            for (int i = 0; i < 4; i++) {
+                const int row = 4 * py + i;
+                const uint32_t w = st.is[row * NW + px];
+                const uint32_t pw = px > 0 ? st.is[row * NW + px - 1] : (stx > 0 ? st.halo[row] : 0u);
+                uint32_t x = w ^ __byte_perm(pw, w, 0x6543);      // p ^ left neighbour, per byte
+                if (px == 0 && stx == 0) x |= 0xFFu;               // column 0: always non-redundant
+                if constexpr (METHOD == 0) {
+                    const uint32_t t = x & MB;
+                    const uint32_t nz = (((t & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | t) & 0x80808080u;   // byte != 0
+                    vr[i] = (w & 0xFEFEFEFEu) | (nz >> 7);
+                } else {
+                    uint32_t cv = 0;                               // c = # leading equal bits per byte
+#pragma unroll
+                    for (int k = 0; k < 4; k++) {
+                        const uint32_t xb = (x >> (8 * k)) & 0xFFu;
+                        cv |= (xb ? (uint32_t)(__clz(xb) - 24) : 8u) << (8 * k);
+                    }
+                    cr[i] = cv | (w & 0x80808080u);
+                    vr[i] = w;
+                }
+            }
+            Cell v = {vr[0], vr[1], vr[2], vr[3]};
+            Cell cl = {cr[0], cr[1], cr[2], cr[3]};
+            if (g.emin <= 1) {
+                const uint32_t a01 = (uint32_t)(st.rec[g.lvl_off[1] + 2 * py] >> (4 * px)) & 0xFu;
+                const uint32_t a23 = (uint32_t)(st.rec[g.lvl_off[1] + 2 * py + 1] >> (4 * px)) & 0xFu;
+                pair_rot_cw(v.r0, v.r1, a01 & 3, a01 >> 2);
+                pair_rot_cw(v.r2, v.r3, a23 & 3, a23 >> 2);
+                if constexpr (METHOD == 1) {
+                    pair_rot_cw(cl.r0, cl.r1, a01 & 3, a01 >> 2);
+                    pair_rot_cw(cl.r2, cl.r3, a23 & 3, a23 >> 2);
+                }
+            }
+            if (g.emin <= 2) q += rec_angle(st.rec, g, 2, py, px);
+            v = cell_rot_cw(v, q & 3);
+            if constexpr (METHOD == 1) cl = cell_rot_cw(cl, q & 3);
+
+            const uint32_t *sw = st.ss + (4 * cy) * NW + cx;
+            const uint32_t s0 = sw[0], s1 = sw[NW], s2 = sw[2 * NW], s3 = sw[3 * NW];
+            const size_t base = (size_t)(dty * T + 4 * cy) * g.W + (size_t)j * T + 4 * cx;
+            uint32_t e0, e1, e2, e3;
+            if constexpr (METHOD == 0) {
+                e0 = v.r0 ^ (s0 & 0xFEFEFEFEu); e1 = v.r1 ^ (s1 & 0xFEFEFEFEu);
+                e2 = v.r2 ^ (s2 & 0xFEFEFEFEu); e3 = v.r3 ^ (s3 & 0xFEFEFEFEu);
+                if (dtile == 0 && c == 0) {
+                    // header: LSB(E[r]) = bit (2 - r) of b - 2 for r = 0..2; the map there is
+                    // forced to 1, so capacity counts zeros after forcing (Q14)
+                    const uint32_t m = v.r0 & 0x00010101u;
+                    const int forced = (int)(m & 1u) + (int)((m >> 8) & 1u) + (int)((m >> 16) & 1u);
+                    const uint32_t hb = (uint32_t)(b - 2);
+                    const uint32_t hdr = ((hb >> 2) & 1u) | (((hb >> 1) & 1u) << 8) | ((hb & 1u) << 16);
+                    e0 = (e0 & 0xFFFEFEFEu) | hdr;
+                    const long long zeros = g.HW - (long long)__ldcg(ws.hist + img * 8 + b);
+                    b_out[img] = b;
+                    cap_out[img] = (long long)b * (zeros - (3 - forced));
+                    status[img] = 0;
+                }
+            } else {
+                e0 = v.r0 ^ s0; e1 = v.r1 ^ s1; e2 = v.r2 ^ s2; e3 = v.r3 ^ s3;
+                uint8_t *co = ceta_out + (size_t)img * g.HW + base;
+                *reinterpret_cast<uint32_t *>(co) = cl.r0;
+                *reinterpret_cast<uint32_t *>(co + g.W) = cl.r1;
+                *reinterpret_cast<uint32_t *>(co + 2 * (size_t)g.W) = cl.r2;
+                *reinterpret_cast<uint32_t *>(co + 3 * (size_t)g.W) = cl.r3;
+            }
+            uint8_t *eo = enc + (size_t)img * g.HW + base;
+            *reinterpret_cast<uint32_t *>(eo) = e0;
+            *reinterpret_cast<uint32_t *>(eo + g.W) = e1;
+            *reinterpret_cast<uint32_t *>(eo + 2 * (size_t)g.W) = e2;
+            *reinterpret_cast<uint32_t *>(eo + 3 * (size_t)g.W) = e3;
+        }
+        __syncthreads();                                           // stage j free for tile j + 2
+    }
+}
+
+// ======================================================================================
+// W role, recover (a10): original strip ty, tiles left to right.
+//   X = I_e' XOR s (every bit, Q20); EMR: map bit = raw LSB of I_e' (r < 3 forced to 1);
+//   LMR: MSB := eta_r and the map come from the decoded planes.  Inverse cell transform into
+//   the original domain, then per row omega := masked bits of the last non-redundant pixel,
+//   replaced into the redundant ones; the row's omega carries from tile to
+//   tile inside the CTA.
+// ======================================================================================
+template <int TP>
+struct RecSmem {
+    static constexpr int T = 1 << TP, RS = T / 4 + 1;
+    struct Stage {
+        uint32_t es[T * T / 4];              // marked destination tile (row-major words)
+        uint32_t ss[T * T / 4];              // keystream of the destination tile (tile-major)
+        uint64_t rec[kRecSlots];             // angle record of the original tile
+        uint32_t mbits[T][2], ebits[T][2];   // LMR: decoded map / eta bits of the destination rows
+    } st[2];
+    uint32_t xo[T * RS], lo[T * RS];         // original domain of the current tile
+    uint32_t pyr[kPyrSmem];
+    int dmap[kMaxTilesX];                    // per original tile of the strip: destination << 2 | q
+    uint8_t carry[T];                        // per row: omega at the right edge of the previous tile
+    uint32_t fsel[16];                       // copy-forward PRMT selectors by 4-bit map
+    int sh[4];
+};
+
+template <int TP, int METHOD>
+__device__ __forceinline__ void rec_role(const Geo &g, int img, int ty, int nK, const uint8_t *__restrict__ marked,
                                          const TileWS &ws, const uint32_t *__restrict__ eta_bits,
                                          const uint32_t *__restrict__ map_bits, const int32_t *__restrict__ lmr_b,
                                          uint8_t *__restrict__ out, int32_t *__restrict__ status, uint8_t *smem) {
-    constexpr int T = 1 << TP, RS = T / 4 + 1, NC = T / 4, NCELL = NC * NC, CPT = T * T / 16, SEGS = T / 16;
-    constexpr int NG = NC / 2;
+    constexpr int T = 1 << TP, NW = T / 4, RS = T / 4 + 1, NC = T / 4, NCELL = NC * NC, CPT = T * T / 16;
+    constexpr int SEGS = T / 16, NG = NC / 2;
     RecSmem<TP> &S = *reinterpret_cast<RecSmem<TP> *>(smem);
     const int tid = threadIdx.x, lane = tid & 31;
-    const int ty = (otile >> g.tlog), tx = (otile & (g.tilesX - 1));
     const uint8_t *Em = marked + (size_t)img * g.HW;
     uint8_t *O = out + (size_t)img * g.HW;
-    const size_t tslot = (size_t)img * g.ntiles + otile;
 
+    if (tid >= 32 && tid < 48) {                        // fsel[m] nibble i: last set bit <= i, else 4
+        const int m = tid - 32;
+        uint32_t v = 0;
+        int last = 4;
+        for (int i = 0; i < 4; i++) {
+            if ((m >> i) & 1) last = i;
+            v |= (uint32_t)last << (4 * i);
+        }
+        S.fsel[m] = v;
+    }
     if (tid < 32) {
         int b = 0;
         if (tid == 0) {
-        if constexpr (METHOD == 0) {
-            const int field = ((Em[0] & 1) << 2) | ((Em[1] & 1) << 1) | (Em[2] & 1);
-            b = field > 5 ? -1 : field + 2;
-            if (otile == 0) status[img] = b < 0 ? 8 : 0;
-        } else {
-            b = __ldcg(lmr_b + img);                    // <= 0: status already set by the decoder
-            if (otile == 0 && b > 0) status[img] = 0;
-        }
-        S.sh[2] = b;
+            if constexpr (METHOD == 0) {
+                const int field = ((Em[0] & 1) << 2) | ((Em[1] & 1) << 1) | (Em[2] & 1);
+                b = field > 5 ? -1 : field + 2;
+                if (ty == 0) status[img] = b < 0 ? 8 : 0;
+            } else {
+                b = __ldcg(lmr_b + img);                // <= 0: status already set by the decoder
+                if (ty == 0 && b > 0) status[img] = 0;
+            }
+            S.sh[0] = b;
         }
         b = __shfl_sync(0xffffffffu, b, 0);
         if (b > 0) {
             const uint32_t *pyr = warp0_ready(g, ws, img, nK, S.pyr);
-            if (tid == 0) {
-            int dty, dtx, q;
-            upper_walk_forward(g, pyr, ty, tx, dty, dtx, q);
-            S.sh[0] = (dty << g.tlog) + dtx;
-            S.sh[1] = q;
-            mbar_init(&S.bar, 1);
-            mbar_expect_tx(&S.bar, T * T);
-            bulk_g2s(S.ss, ws.s + ((size_t)img * g.ntiles + S.sh[0]) * (T * T), T * T, &S.bar);
+            for (int j = tid; j < g.tilesX; j += 32) {
+                int dty, dtx, q;
+                upper_walk_forward(g, pyr, ty, j, dty, dtx, q);
+                S.dmap[j] = (((dty << g.tlog) + dtx) << 2) | q;
             }
         }
     }
     __syncthreads();
-    const int b = S.sh[2];
+    const int b = S.sh[0];
     if (b <= 0) {                                       // FORMAT / BADCASE: zero-filled output
-        for (int c = tid; c < CPT; c += 256) {
-            const int r = c / SEGS, seg = c % SEGS;
-            *reinterpret_cast<uint4 *>(O + (size_t)(ty * T + r) * g.W + (size_t)tx * T + seg * 16) =
-                make_uint4(0, 0, 0, 0);
+        for (int c = tid; c < T * g.W / 16; c += 256) {
+            const int r = c / (g.W / 16), col = c % (g.W / 16);
+            *reinterpret_cast<uint4 *>(O + (size_t)(ty * T + r) * g.W + col * 16) = make_uint4(0, 0, 0, 0);
         }
         return;
     }
-    const int dt = S.sh[0], q_up = S.sh[1];
-    const int dty = (dt >> g.tlog), dtx = (dt & (g.tilesX - 1));
     const uint32_t mask = METHOD == 0 ? ((0xFFu << (8 - b)) & 0xFFu) : (0x7Fu & ~(0xFFu >> b));
-    for (int c = tid; c < CPT; c += 256) {
-        const int r = c / SEGS, seg = c % SEGS;
-        cp_async16(&S.es[r * T + seg * 16], Em + (size_t)(dty * T + r) * g.W + (size_t)dtx * T + seg * 16);
-    }
-    const uint64_t *recg = ws.rec + tslot * kRecSlots;
-    if (tid < kRecSlots) S.rec[tid] = __ldcg(recg + tid);
-    if constexpr (METHOD == 1) {
-        if (tid < T) {
-            const size_t bit = (size_t)img * g.HW + (size_t)(dty * T + tid) * g.W + (size_t)dtx * T;
-            const int nw = T >= 32 ? T / 32 : 1;
-            for (int k = 0; k < 2; k++) {
-                S.mbits[tid][k] = k < nw ? (__ldg(map_bits + (bit >> 5) + k) >> (bit & 31)) : 0u;
-                S.ebits[tid][k] = k < nw ? (__ldg(eta_bits + (bit >> 5) + k) >> (bit & 31)) : 0u;
-            }
-        }
-    }
-    cp_async_wait_all();
-    mbar_wait(&S.bar, 0);
-    __syncthreads();
-    if (tid < (T * T) / 128) discard_l2(ws.s + ((size_t)img * g.ntiles + dt) * (T * T) + 128 * tid);
-    else if (tid >= 64 && tid < 64 + kRecSlots * 8 / 128) discard_l2(recg + 16 * (tid - 64));
+    const uint32_t maskb = mask * 0x01010101u;
 
-    // destination tile: X = E' ^ s, map bits
-    for (int c = tid; c < CPT; c += 256) {
-        const int r = c / SEGS, seg = c % SEGS;
-        const uint4 e = *reinterpret_cast<const uint4 *>(&S.es[r * T + seg * 16]);
-        const uint4 sv = *reinterpret_cast<const uint4 *>(&S.ss[r * T + seg * 16]);
-        const uint32_t ew[4] = {e.x, e.y, e.z, e.w}, sw[4] = {sv.x, sv.y, sv.z, sv.w};
-        uint32_t mb16 = 0, eb16 = 0;
+    auto issue = [&](int j) {
+        typename RecSmem<TP>::Stage &st = S.st[j & 1];
+        const int dt = S.dmap[j] >> 2, dty = dt >> g.tlog, dtx = dt & (g.tilesX - 1);
+        const size_t dslot = (size_t)img * g.ntiles + dt;
+        for (int c = tid; c < CPT; c += 256) {
+            const int r = c / (T / 16), seg = c % (T / 16);
+            cp_async16(&st.es[r * NW + seg * 4], Em + (size_t)(dty * T + r) * g.W + (size_t)dtx * T + seg * 16);
+            cp_async16(&st.ss[4 * c], ws.s + dslot * (T * T) + 16 * c);
+        }
+        if (tid < kRecSlots / 2)
+            cp_async16(&st.rec[2 * tid],
+                       ws.rec + ((size_t)img * g.ntiles + ((size_t)ty << g.tlog) + j) * kRecSlots + 2 * tid);
         if constexpr (METHOD == 1) {
-            mb16 = (S.mbits[r][seg >> 1] >> (16 * (seg & 1))) & 0xFFFFu;
-            eb16 = (S.ebits[r][seg >> 1] >> (16 * (seg & 1))) & 0xFFFFu;
-        }
-        const bool first = dt == 0 && r == 0 && seg == 0;
-#pragma unroll
-        for (int i = 0; i < 4; i++) {
-            uint32_t x = ew[i] ^ sw[i], l;
-            if constexpr (METHOD == 0) {
-                l = ew[i] & 0x01010101u;
-                if (i == 0 && first) l |= 0x00010101u;      // r = 0..2 carry the header, map = 1
-            } else {
-                l = bits4_to_bytes(mb16 >> (4 * i));
-                x = (x & 0x7F7F7F7Fu) | (bits4_to_bytes(eb16 >> (4 * i)) << 7);   // MSB from eta
+            if (tid < T) {
+                const size_t bit = (size_t)img * g.HW + (size_t)(dty * T + tid) * g.W + (size_t)dtx * T;
+                if constexpr (T >= 32) {
+                    for (int k = 0; k < T / 32; k++) {
+                        cp_async4(&st.mbits[tid][k], map_bits + (bit >> 5) + k);
+                        cp_async4(&st.ebits[tid][k], eta_bits + (bit >> 5) + k);
+                    }
+                } else {                                 // 16-pixel rows share words: plain loads
+                    st.mbits[tid][0] = __ldg(map_bits + (bit >> 5)) >> (bit & 31);
+                    st.ebits[tid][0] = __ldg(eta_bits + (bit >> 5)) >> (bit & 31);
+                }
             }
-            S.xin[r * RS + seg * 4 + i] = x;
-            S.lin[r * RS + seg * 4 + i] = l;
         }
-    }
-    __syncthreads();
-    // cells: original cell -> destination cell, inverse content transform.  2x2-cell groups
-    // move rigidly under levels >= 4 and the tile turn: one forward walk per original group.
-    if (tid < NG * NG) {
-        int gy = tid / NG, gx = tid % NG, q = 0;
-        for (int e = (g.emin > 4 ? g.emin : 4); e <= TP; e++) {
-            const int k = e - 3, m1 = (1 << k) - 1;
-            const int by = gy >> k, bx = gx >> k;
-            const int a = rec_angle(S.rec, g, e, by, bx);
-            int oy = gy & m1, ox = gx & m1;
-            fwd_turn(a, m1, oy, ox);
-            gy = (by << k) | oy;
-            gx = (bx << k) | ox;
-            q += a;
-        }
-        fwd_turn(q_up, NG - 1, gy, gx);
-        S.gw[tid] = (gy << 16) | (gx << 8) | ((q + q_up) & 3);
-    }
-    __syncthreads();
-    for (int c = tid; c < NCELL; c += 256) {
-        const int gi = c >> 2, sub = c & 3;
-        const int ogy = gi / NG, ogx = gi % NG;
-        const int cy = 2 * ogy + (sub >> 1), cx = 2 * ogx + (sub & 1);
-        const int gw = S.gw[gi];
-        int q = gw & 3;
-        if (g.emin <= 3) q += rec_angle(S.rec, g, 3, ogy, ogx);     // level 3 = the group itself
-        int sy = sub >> 1, sx = sub & 1;
-        fwd_turn(q & 3, 1, sy, sx);
-        const int py = 2 * (gw >> 16) + sy, px = 2 * ((gw >> 8) & 0xFF) + sx;
-        if (g.emin <= 2) q += rec_angle(S.rec, g, 2, cy, cx);
-        Cell x = {S.xin[(4 * py) * RS + px], S.xin[(4 * py + 1) * RS + px], S.xin[(4 * py + 2) * RS + px],
-                  S.xin[(4 * py + 3) * RS + px]};
-        Cell l = {S.lin[(4 * py) * RS + px], S.lin[(4 * py + 1) * RS + px], S.lin[(4 * py + 2) * RS + px],
-                  S.lin[(4 * py + 3) * RS + px]};
-        const int rinv = (4 - (q & 3)) & 3;
-        x = cell_rot_cw(x, rinv);
-        l = cell_rot_cw(l, rinv);
-        if (g.emin <= 1) {
-            const uint32_t a01 = (uint32_t)(S.rec[g.lvl_off[1] + 2 * cy] >> (4 * cx)) & 0xFu;
-            const uint32_t a23 = (uint32_t)(S.rec[g.lvl_off[1] + 2 * cy + 1] >> (4 * cx)) & 0xFu;
-            const int aL0 = (4 - (a01 & 3)) & 3, aR0 = (4 - (a01 >> 2)) & 3;
-            const int aL1 = (4 - (a23 & 3)) & 3, aR1 = (4 - (a23 >> 2)) & 3;
-            pair_rot_cw(x.r0, x.r1, aL0, aR0);
-            pair_rot_cw(x.r2, x.r3, aL1, aR1);
-            pair_rot_cw(l.r0, l.r1, aL0, aR0);
-            pair_rot_cw(l.r2, l.r3, aL1, aR1);
-        }
-        S.xo[(4 * cy) * RS + cx] = x.r0; S.xo[(4 * cy + 1) * RS + cx] = x.r1;
-        S.xo[(4 * cy + 2) * RS + cx] = x.r2; S.xo[(4 * cy + 3) * RS + cx] = x.r3;
-        S.lo[(4 * cy) * RS + cx] = l.r0; S.lo[(4 * cy + 1) * RS + cx] = l.r1;
-        S.lo[(4 * cy + 2) * RS + cx] = l.r2; S.lo[(4 * cy + 3) * RS + cx] = l.r3;
-    }
-    __syncthreads();
+        cp_async_commit();
+    };
 
-    // ---- row summaries: SEGS threads per row, 16 pixels each
     const bool rowthr = tid < T * SEGS;
     const int r = tid / SEGS, seg = tid % SEGS;
-    uint32_t xw[4] = {0, 0, 0, 0}, lw[4] = {0, 0, 0, 0};
-    int has = 0, val = 0;
-    if (rowthr) {
-#pragma unroll
-        for (int i = 0; i < 4; i++) { xw[i] = S.xo[r * RS + seg * 4 + i]; lw[i] = S.lo[r * RS + seg * 4 + i]; }
-        if (tx == 0 && seg == 0) lw[0] |= 1u;           // column 0: omega starts at its bits
-        uint32_t m16 = 0;
-#pragma unroll
-        for (int i = 0; i < 4; i++) m16 |= bytes_to_bits4(lw[i]) << (4 * i);
-        has = m16 != 0;
-        if (has) {
-            const int li = 31 - __clz(m16), wi = li >> 2;
-            const uint32_t wsel = wi == 0 ? xw[0] : wi == 1 ? xw[1] : wi == 2 ? xw[2] : xw[3];
-            val = (int)((wsel >> (8 * (li & 3))) & mask);
+    issue(0);
+    for (int j = 0; j < g.tilesX; j++) {
+        if (j + 1 < g.tilesX) {
+            issue(j + 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
         }
-    }
-    // exclusive "last non-redundant" across the row's segments (without the tile carry-in)
-    int ehas = 0, evl = 0;
+        __syncthreads();                                           // stage j landed for everyone
+        const typename RecSmem<TP>::Stage &st = S.st[j & 1];
+        const int mp = S.dmap[j], dt = mp >> 2, q_up = mp & 3;
+        // cells: original cell -> destination cell; X, L from the staged destination tile
+        for (int c = tid; c < NCELL; c += 256) {
+            const int gi = c >> 2, sub = c & 3;
+            const int ogy = gi / NG, ogx = gi % NG;
+            const int cy = 2 * ogy + (sub >> 1), cx = 2 * ogx + (sub & 1);
+            const int gw = group_walk_forward(g, st.rec, TP, NG, q_up, ogy, ogx);
+            int q = gw & 3;
+            if (g.emin <= 3) q += rec_angle(st.rec, g, 3, ogy, ogx);   // level 3 = the group itself
+            int sy = sub >> 1, sx = sub & 1;
+            fwd_turn(q & 3, 1, sy, sx);
+            const int py = 2 * (gw >> 16) + sy, px = 2 * ((gw >> 8) & 0xFF) + sx;
+            if (g.emin <= 2) q += rec_angle(st.rec, g, 2, cy, cx);
+            uint32_t xr[4], lr[4];
 #pragma unroll
-    for (int s2 = 0; s2 < SEGS - 1; s2++) {                 // whole-warp shuffles within SEGS lanes
-        const int oh = __shfl_sync(0xffffffffu, has, s2, SEGS);
-        const int ov = __shfl_sync(0xffffffffu, val, s2, SEGS);
-        if (s2 < seg && oh) { ehas = 1; evl = ov; }
-    }
-    const int rval = has ? val : evl;                   // last non-redundant value of the row so far
-    if (rowthr && seg == SEGS - 1) S.rowval[r] = (uint8_t)rval;
-    // rows with a non-redundant pixel inside the tile (their carry out is known outright);
-    // column 0 makes every row of the strip's first tile such a row
-    if (tid < 64) {
-        bool any = false;
-        if (tid < T) {
-            uint32_t a = 0;
-            for (int i = 0; i < T / 4; i++) a |= S.lo[tid * RS + i];
-            any = a != 0 || tx == 0;
-        }
-        const unsigned bl = __ballot_sync(0xffffffffu, any);
-        if (lane == 0) S.rowhas[tid >> 5] = bl;
-    }
-    __syncthreads();
-    const bool first_tile = tx == 0;
-    if (tid < T) {
-        ws.ragg[tslot * T + tid] = S.rowval[tid];
-        if (first_tile) ws.rinc[tslot * T + tid] = S.rowval[tid];
-    }
-    if (tid == 0) ws.rhas[tslot] = (uint64_t)S.rowhas[0] | ((uint64_t)S.rowhas[1] << 32);
-    __syncthreads();
-    if (tid == 0) st_release_u32(ws.rflag + tslot, first_tile ? 2u : 1u);
-
-    // ---- look-back for the carry into each row (warp 0; lane owns rows lane, lane + 32)
-    if (!first_tile && tid < 32) {
-        bool u0 = lane < T, u1 = lane + 32 < T;
-        uint32_t c0 = 0, c1 = 0;
-        size_t k = tslot - 1;                           // tile to the left, same strip
-        while (__any_sync(0xffffffffu, u0 || u1)) {
-            unsigned f;
-            do { f = ld_acquire_u32(ws.rflag + k); } while (f == 0);
-            if (f == 2) {
-                if (u0) { c0 = __ldcg(ws.rinc + k * T + lane); u0 = false; }
-                if (u1) { c1 = __ldcg(ws.rinc + k * T + lane + 32); u1 = false; }
-            } else {
-                const uint64_t hm = __ldcg(ws.rhas + k);
-                if (u0 && ((hm >> lane) & 1u)) { c0 = __ldcg(ws.ragg + k * T + lane); u0 = false; }
-                if (u1 && ((hm >> (lane + 32)) & 1u)) { c1 = __ldcg(ws.ragg + k * T + lane + 32); u1 = false; }
+            for (int i = 0; i < 4; i++) {
+                const int row = 4 * py + i;
+                const uint32_t e = st.es[row * NW + px];
+                uint32_t x = e ^ st.ss[row * NW + px];
+                uint32_t l;
+                if constexpr (METHOD == 0) {
+                    l = e & 0x01010101u;
+                    if (i == 0 && dt == 0 && py == 0 && px == 0) l |= 0x00010101u;   // header pixels, map 1
+                } else {
+                    const int bp = 4 * px;
+                    l = bits4_to_bytes(st.mbits[row][bp >> 5] >> (bp & 31));
+                    x = (x & 0x7F7F7F7Fu) | (bits4_to_bytes(st.ebits[row][bp >> 5] >> (bp & 31)) << 7);  // MSB <- eta
+                }
+                xr[i] = x;
+                lr[i] = l;
             }
-            k--;
+            Cell x = {xr[0], xr[1], xr[2], xr[3]};
+            Cell l = {lr[0], lr[1], lr[2], lr[3]};
+            const int rinv = (4 - (q & 3)) & 3;
+            x = cell_rot_cw(x, rinv);
+            l = cell_rot_cw(l, rinv);
+            if (g.emin <= 1) {
+                const uint32_t a01 = (uint32_t)(st.rec[g.lvl_off[1] + 2 * cy] >> (4 * cx)) & 0xFu;
+                const uint32_t a23 = (uint32_t)(st.rec[g.lvl_off[1] + 2 * cy + 1] >> (4 * cx)) & 0xFu;
+                const int aL0 = (4 - (a01 & 3)) & 3, aR0 = (4 - (a01 >> 2)) & 3;
+                const int aL1 = (4 - (a23 & 3)) & 3, aR1 = (4 - (a23 >> 2)) & 3;
+                pair_rot_cw(x.r0, x.r1, aL0, aR0);
+                pair_rot_cw(x.r2, x.r3, aL1, aR1);
+                pair_rot_cw(l.r0, l.r1, aL0, aR0);
+                pair_rot_cw(l.r2, l.r3, aL1, aR1);
+            }
+            S.xo[(4 * cy) * RS + cx] = x.r0; S.xo[(4 * cy + 1) * RS + cx] = x.r1;
+            S.xo[(4 * cy + 2) * RS + cx] = x.r2; S.xo[(4 * cy + 3) * RS + cx] = x.r3;
+            S.lo[(4 * cy) * RS + cx] = l.r0; S.lo[(4 * cy + 1) * RS + cx] = l.r1;
+            S.lo[(4 * cy + 2) * RS + cx] = l.r2; S.lo[(4 * cy + 3) * RS + cx] = l.r3;
         }
-        if (lane < T) S.carry[lane] = (uint8_t)c0;
-        if (lane + 32 < T) S.carry[lane + 32] = (uint8_t)c1;
-    }
-    __syncthreads();
-    if (!first_tile && tx + 1 < g.tilesX) {             // carry out for the tiles to the right
-        if (tid < T) {
-            const bool h = (S.rowhas[tid >> 5] >> (tid & 31)) & 1u;
-            ws.rinc[tslot * T + tid] = h ? S.rowval[tid] : S.carry[tid];
+        __syncthreads();                                           // tile j in the original domain
+        {   // the consumed scratch (destination keystream, original record) leaves L2 unwritten
+            const size_t dslot = (size_t)img * g.ntiles + dt;
+            if (tid < (T * T) / 128) discard_l2(ws.s + dslot * (T * T) + 128 * tid);
+            else if (tid >= 64 && tid < 64 + kRecSlots * 8 / 128)
+                discard_l2(ws.rec + ((size_t)img * g.ntiles + ((size_t)ty << g.tlog) + j) * kRecSlots + 16 * (tid - 64));
         }
-        __syncthreads();
-        if (tid == 0) st_release_u32(ws.rflag + tslot, 2u);
-    }
-
-    // ---- copy-forward and store
-    if (rowthr) {
-        uint32_t om = (ehas ? (uint32_t)evl : (uint32_t)S.carry[r]);
+        // ---- rows: SEGS threads per row, 16 pixels each.  Copy-forward 4 pixels at a time:
+        // om = PRMT(x & mask, carry, fsel[m4]) gives every byte the masked value of the last
+        // non-redundant pixel at or before it (or the carry); out = (x & ~mask) | om is exact for
+        // both kinds of pixel (a non-redundant pixel takes its own bits).
+        uint32_t xw[4] = {0, 0, 0, 0}, sel[4] = {0, 0, 0, 0};
+        uint32_t m16 = 0;
+        if (rowthr) {
 #pragma unroll
-        for (int i = 0; i < 16; i++) {
-            const int wi = i >> 2, sh8 = 8 * (i & 3);
-            const uint32_t px8 = (xw[wi] >> sh8) & 0xFFu;
-            if ((lw[wi] >> sh8) & 1u) om = px8 & mask;
-            else xw[wi] = (xw[wi] & ~(0xFFu << sh8)) | (((px8 & ~mask) | om) << sh8);
+            for (int i = 0; i < 4; i++) {
+                xw[i] = S.xo[r * RS + seg * 4 + i];
+                m16 |= bytes_to_bits4(S.lo[r * RS + seg * 4 + i]) << (4 * i);
+            }
+            if (j == 0 && seg == 0) m16 |= 1u;         // column 0: omega starts at its bits
         }
-        *reinterpret_cast<uint4 *>(O + (size_t)(ty * T + r) * g.W + (size_t)tx * T + seg * 16) =
-            make_uint4(xw[0], xw[1], xw[2], xw[3]);
+        uint32_t c4 = 0;                                // segment summary with a zero carry-in
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            sel[i] = S.fsel[(m16 >> (4 * i)) & 0xFu];
+            c4 = __byte_perm(__byte_perm(xw[i] & maskb, c4, sel[i]), 0, 0x3333);
+        }
+        const int has = m16 != 0, val = (int)(c4 & 0xFFu);
+        int ehas = 0, evl = 0;                          // last non-redundant before this segment
+#pragma unroll
+        for (int s2 = 0; s2 < SEGS - 1; s2++) {
+            const int oh = __shfl_sync(0xffffffffu, has, s2, SEGS);
+            const int ov = __shfl_sync(0xffffffffu, val, s2, SEGS);
+            if (s2 < seg && oh) { ehas = 1; evl = ov; }
+        }
+        if (rowthr) {
+            uint32_t cin = (ehas ? (uint32_t)evl : (uint32_t)S.carry[r]) * 0x01010101u;
+#pragma unroll
+            for (int i = 0; i < 4; i++) {
+                const uint32_t om = __byte_perm(xw[i] & maskb, cin, sel[i]);
+                xw[i] = (xw[i] & ~maskb) | om;
+                cin = __byte_perm(om, 0, 0x3333);
+            }
+            *reinterpret_cast<uint4 *>(O + (size_t)(ty * T + r) * g.W + (size_t)j * T + seg * 16) =
+                make_uint4(xw[0], xw[1], xw[2], xw[3]);
+            if (seg == SEGS - 1) S.carry[r] = (uint8_t)cin;   // omega leaving the tile
+        }
+        __syncthreads();                                           // xo/lo, carry, stage j reusable
     }
 }
 
@@ -725,22 +705,25 @@ __device__ __forceinline__ void rec_role(const Geo &g, int img, int otile, int n
 // The fused kernels
 // ======================================================================================
 template <int TP, int METHOD>
-__global__ void __launch_bounds__(256, 8) encode_kernel(Geo g, FusedSched sc, const uint8_t *__restrict__ images,
+__global__ void __launch_bounds__(256, 6) encode_kernel(Geo g, FusedSched sc, const uint8_t *__restrict__ images,
                                                      const uint8_t *__restrict__ keys, TileWS ws,
                                                      uint8_t *__restrict__ enc, uint8_t *__restrict__ ceta,
                                                      int32_t *__restrict__ b_out, int64_t *__restrict__ cap_out,
                                                      int32_t *__restrict__ status) {
     constexpr int T = 1 << TP, TPC = 256 / T;
-    constexpr size_t KB = TPC * kRecSlots * 8, PB = sizeof(PermSmem<TP, METHOD>);
+    constexpr size_t KB = TPC * kRecSlots * 8, PB = sizeof(PermSmem<TP>);
     __shared__ __align__(128) uint8_t smem[KB > PB ? KB : PB];
     const Role ro = role_of(sc);
     if (ro.img >= g.B) return;
+#ifdef MMSB_PROBE_ROLES   // performance probes only (tools/role_probe.py): 1 = keystream CTAs only, 2 = workers only
+    if (!((MMSB_PROBE_ROLES >> (ro.key ? 0 : 1)) & 1)) return;
+#endif
     if (ro.key) key_role<TP, true>(g, ro.img, ro.idx, keys, images, ws, smem);
     else perm_role<TP, METHOD>(g, ro.img, ro.idx, 1 << sc.lgK, images, ws, enc, ceta, b_out, cap_out, status, smem);
 }
 
 template <int TP, int METHOD>
-__global__ void __launch_bounds__(256, 8) recover_kernel(Geo g, FusedSched sc, const uint8_t *__restrict__ marked,
+__global__ void __launch_bounds__(256, 6) recover_kernel(Geo g, FusedSched sc, const uint8_t *__restrict__ marked,
                                                       const uint8_t *__restrict__ keys, TileWS ws,
                                                       const uint32_t *__restrict__ eta_bits,
                                                       const uint32_t *__restrict__ map_bits,
@@ -751,6 +734,9 @@ __global__ void __launch_bounds__(256, 8) recover_kernel(Geo g, FusedSched sc, c
     __shared__ __align__(128) uint8_t smem[KB > RB ? KB : RB];
     const Role ro = role_of(sc);
     if (ro.img >= g.B) return;
+#ifdef MMSB_PROBE_ROLES
+    if (!((MMSB_PROBE_ROLES >> (ro.key ? 0 : 1)) & 1)) return;
+#endif
     if (ro.key) key_role<TP, false>(g, ro.img, ro.idx, keys, nullptr, ws, smem);
     else rec_role<TP, METHOD>(g, ro.img, ro.idx, 1 << sc.lgK, marked, ws, eta_bits, map_bits, lmr_b, out, status, smem);
 }
@@ -761,7 +747,7 @@ FusedSched fused_sched(const Geo &g) {
     const int TPC = 256 / g.T;
     const int nK = g.ntiles >= TPC ? g.ntiles / TPC : 1;       // powers of two
     sc.lgK = ilog2(nK);
-    sc.lgW = ilog2(g.ntiles);
+    sc.lgW = ilog2(g.tilesY);                           // one worker CTA per strip of tiles
     int gi = 1;
     while ((long long)(gi * 2) * g.HW <= (2ll << 20) && gi < g.B) gi *= 2;   // ~2 Mpixel per group
     sc.GI = gi;

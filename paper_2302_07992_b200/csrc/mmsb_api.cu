@@ -57,7 +57,7 @@ static size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
 // the whole batch but are transient: each tile is written by one keystream CTA, read by one
 // worker CTA of the same launch shortly after, and then discarded from L2.
 struct Layout {
-    size_t s, rec, pyr, hist, kdone, rflag, tile_zero_end, rhas, ragg, rinc;   // fused tile kernels
+    size_t s, rec, pyr, hist, kdone, rstate, tile_zero_end, ragg, rinc;   // fused tile kernels
     size_t states, parts, hdr, scan_zero_end;                                  // scan kernels
     size_t ceta, eta_bits, map_bits, lmr_b, lmr_t, plan, streams, sizes, offsets, mbuf, total;
 };
@@ -71,9 +71,8 @@ static Layout layout(const Geo &g) {
     L.pyr = o; o = align256(o + B * (g.npyr > 0 ? g.npyr : 1) * 4);
     L.hist = o; o = align256(o + B * 8 * 4);
     L.kdone = o; o = align256(o + B * 4);
-    L.rflag = o; o = align256(o + B * nt * 4);
+    L.rstate = o; o = align256(o + B * nt * 16);
     L.tile_zero_end = o;
-    L.rhas = o; o = align256(o + B * nt * 8);
     L.ragg = o; o = align256(o + B * nt * g.T);
     L.rinc = o; o = align256(o + B * nt * g.T);
     L.states = o; o = align256(o + B * g.nchunks * 8);
@@ -104,8 +103,7 @@ static TileWS tile_ws(const Layout &L, void *ws) {
     t.pyr = reinterpret_cast<uint32_t *>(w + L.pyr);
     t.hist = reinterpret_cast<uint32_t *>(w + L.hist);
     t.kdone = reinterpret_cast<uint32_t *>(w + L.kdone);
-    t.rflag = reinterpret_cast<uint32_t *>(w + L.rflag);
-    t.rhas = reinterpret_cast<uint64_t *>(w + L.rhas);
+    t.rstate = reinterpret_cast<unsigned long long *>(w + L.rstate);
     t.ragg = reinterpret_cast<uint8_t *>(w + L.ragg);
     t.rinc = reinterpret_cast<uint8_t *>(w + L.rinc);
     return t;

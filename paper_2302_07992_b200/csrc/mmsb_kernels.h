@@ -40,8 +40,7 @@ struct TileWS {
     uint32_t *pyr;       // [B][npyr] upper-level block sums (mod 4 on read)        -- zeroed per call
     uint32_t *hist;      // [B][8] non-redundant counts for b = 2..8 at index b      -- zeroed per call
     uint32_t *kdone;     // [B] keystream CTAs finished                               -- zeroed per call
-    uint32_t *rflag;     // [B][ntiles] recover look-back flags (1 agg, 2 inclusive)  -- zeroed per call
-    uint64_t *rhas;      // [B][ntiles] rows with a non-redundant pixel in the tile
+    unsigned long long *rstate;   // [B][ntiles][2] recover look-back: flag | row mask  -- zeroed per call
     uint8_t *ragg;       // [B][ntiles][T] per row: last non-redundant masked value in the tile
     uint8_t *rinc;       // [B][ntiles][T] per row: carry out of the tile
 };

@@ -32,9 +32,10 @@ def lib():
     """Loads the in-tree libmmsb.so (never a CPU substitute)."""
     global _lib
     if _lib is None:
-        if not os.path.exists(_build.LIB):
-            raise MmsbError(f"{_build.LIB} is missing: run __graft_entry__.build() (nvcc sm_100a) first")
-        L = C.CDLL(_build.LIB)
+        path = os.environ.get("MMSB_LIB", _build.LIB)     # (tools/role_probe.py loads probe builds)
+        if not os.path.exists(path):
+            raise MmsbError(f"{path} is missing: run __graft_entry__.build() (nvcc sm_100a) first")
+        L = C.CDLL(path)
         vp, sp = C.c_void_p, C.POINTER(_Shape)
         L.mmsb_workspace_bytes.restype = C.c_size_t
         L.mmsb_workspace_bytes.argtypes = [sp]
