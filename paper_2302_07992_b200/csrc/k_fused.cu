@@ -118,7 +118,7 @@ __device__ __forceinline__ const uint32_t *warp0_ready(const Geo &g, const TileW
 // ======================================================================================
 // K role: one thread per tile row, TPC = 256 / T tiles per CTA.
 // ======================================================================================
-template <int TP, bool HIST>
+template <int TP, bool HIST, bool INV>
 __device__ __forceinline__ void key_role(const Geo &g, int img, int kidx, const uint8_t *__restrict__ keys,
                                          const uint8_t *__restrict__ images, const TileWS &ws, uint8_t *smem) {
     constexpr int T = 1 << TP, NW = T / 4, TPC = 256 / T;
@@ -229,6 +229,30 @@ __device__ __forceinline__ void key_role(const Geo &g, int img, int kidx, const 
         __syncthreads();
     }
 
+    // in-tile 8x8-group map: levels 4..tp move 2x2-cell groups rigidly.  Forward (recover):
+    // entry[original group] = group after those levels << 2 | turns; inverse (encode):
+    // entry[group after those levels] = original group << 2 | turns (3-bit coordinates).
+    {
+        constexpr int NG = T / 8, NGG = NG * NG;
+        for (int t = tid; t < TPC * NGG; t += 256) {
+            const int l2 = t / NGG, gi = t % NGG;
+            int gy = gi / NG, gx = gi % NG, q = 0;
+            for (int e = (g.emin > 4 ? g.emin : 4); e <= TP; e++) {
+                const int k = e - 3, m1 = (1 << k) - 1;
+                const int by = gy >> k, bx = gx >> k;
+                const int a = rec_angle(rec[l2], g, e, by, bx);
+                int oy = gy & m1, ox = gx & m1;
+                fwd_turn(a, m1, oy, ox);
+                gy = (by << k) | oy;
+                gx = (bx << k) | ox;
+                q += a;
+            }
+            uint8_t *tab = reinterpret_cast<uint8_t *>(&rec[l2][kRecGroupSlot]);
+            if (INV) tab[gy * NG + gx] = (uint8_t)((((gi / NG) << 5) | ((gi % NG) << 2)) | (q & 3));
+            else tab[gi] = (uint8_t)((gy << 5) | (gx << 2) | (q & 3));
+        }
+        __syncthreads();
+    }
     // upper pyramid: the tile total (= level-tp angle) into every enclosing block
     if (valid && row == 0) {
         const uint32_t tv = (uint32_t)(rec[lt][g.lvl_off[TP]] & 3u);
@@ -269,42 +293,6 @@ __device__ __forceinline__ void cp_async4(void *smem, const void *gmem) {
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N> __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-
-// source 2x2-cell group of destination group (gy, gx) in a tile (levels >= 4 and the tile's own
-// turn q_up move 8x8 groups rigidly); returns gy' << 16 | gx' << 8 | turns
-__device__ __forceinline__ int group_walk_inverse(const Geo &g, const uint64_t *rec, int TP, int NG, int q_up,
-                                                  int gy, int gx) {
-    inv_turn(q_up, NG - 1, gy, gx);
-    int q = q_up;
-    for (int e = TP; e >= 4 && e >= g.emin; e--) {
-        const int k = e - 3, m1 = (1 << k) - 1;
-        const int by = gy >> k, bx = gx >> k;
-        const int a = rec_angle(rec, g, e, by, bx);
-        int oy = gy & m1, ox = gx & m1;
-        inv_turn(a, m1, oy, ox);
-        gy = (by << k) | oy;
-        gx = (bx << k) | ox;
-        q += a;
-    }
-    return (gy << 16) | (gx << 8) | (q & 3);
-}
-// destination group of original group (gy, gx)
-__device__ __forceinline__ int group_walk_forward(const Geo &g, const uint64_t *rec, int TP, int NG, int q_up,
-                                                  int gy, int gx) {
-    int q = 0;
-    for (int e = (g.emin > 4 ? g.emin : 4); e <= TP; e++) {
-        const int k = e - 3, m1 = (1 << k) - 1;
-        const int by = gy >> k, bx = gx >> k;
-        const int a = rec_angle(rec, g, e, by, bx);
-        int oy = gy & m1, ox = gx & m1;
-        fwd_turn(a, m1, oy, ox);
-        gy = (by << k) | oy;
-        gx = (bx << k) | ox;
-        q += a;
-    }
-    fwd_turn(q_up, NG - 1, gy, gx);
-    return (gy << 16) | (gx << 8) | ((q + q_up) & 3);
-}
 
 // ======================================================================================
 // W role, encode (a3, a5): destination strip dty, tiles left to right.
@@ -391,15 +379,17 @@ __device__ __forceinline__ void perm_role(const Geo &g, int img, int dty, int nK
             // group, then in-cell levels 1, 2
             const int gi = c >> 2, sub = c & 3;
             const int cy = 2 * (gi / NG) + (sub >> 1), cx = 2 * (gi % NG) + (sub & 1);
-            const int gw = group_walk_inverse(g, st.rec, TP, NG, q_up, gi / NG, gi % NG);
-            const int sgy = gw >> 16, sgx = (gw >> 8) & 0xFF;
-            int q = gw & 3;
+            int dgy = gi / NG, dgx = gi % NG;
+            inv_turn(q_up, NG - 1, dgy, dgx);               // undo the tile's own turn, then the
+            const uint32_t ge = reinterpret_cast<const uint8_t *>(st.rec + kRecGroupSlot)[dgy * NG + dgx];
+            const int sgy = ge >> 5, sgx = (ge >> 2) & 7;    // in-tile levels >= 4 (group table)
+            int q = q_up + (int)(ge & 3);
             if (g.emin <= 3) q += rec_angle(st.rec, g, 3, sgy, sgx);
             int sy = sub >> 1, sx = sub & 1;
             inv_turn(q & 3, 1, sy, sx);
             const int py = 2 * sgy + sy, px = 2 * sgx + sx;
             // source cell rows -> carrier (EMR) / image + label|eta (LMR)
-            uint32_t vr[4], cr[4];
+            uint32_t vr[4], cr[4] = {0, 0, 0, 0};
 #pragma unroll
             for (int i = 0; i < 4; i++) {
                 const int row = 4 * py + i;
@@ -509,7 +499,7 @@ __device__ __forceinline__ void rec_role(const Geo &g, int img, int ty, int nK, 
     constexpr int T = 1 << TP, NW = T / 4, RS = T / 4 + 1, NC = T / 4, NCELL = NC * NC, CPT = T * T / 16;
     constexpr int SEGS = T / 16, NG = NC / 2;
     RecSmem<TP> &S = *reinterpret_cast<RecSmem<TP> *>(smem);
-    const int tid = threadIdx.x, lane = tid & 31;
+    const int tid = threadIdx.x;
     const uint8_t *Em = marked + (size_t)img * g.HW;
     uint8_t *O = out + (size_t)img * g.HW;
 
@@ -605,12 +595,14 @@ __device__ __forceinline__ void rec_role(const Geo &g, int img, int ty, int nK, 
             const int gi = c >> 2, sub = c & 3;
             const int ogy = gi / NG, ogx = gi % NG;
             const int cy = 2 * ogy + (sub >> 1), cx = 2 * ogx + (sub & 1);
-            const int gw = group_walk_forward(g, st.rec, TP, NG, q_up, ogy, ogx);
-            int q = gw & 3;
+            const uint32_t ge = reinterpret_cast<const uint8_t *>(st.rec + kRecGroupSlot)[gi];
+            int dgy = ge >> 5, dgx = (ge >> 2) & 7;          // in-tile levels >= 4 (group table),
+            fwd_turn(q_up, NG - 1, dgy, dgx);                // then the tile's own turn
+            int q = q_up + (int)(ge & 3);
             if (g.emin <= 3) q += rec_angle(st.rec, g, 3, ogy, ogx);   // level 3 = the group itself
             int sy = sub >> 1, sx = sub & 1;
             fwd_turn(q & 3, 1, sy, sx);
-            const int py = 2 * (gw >> 16) + sy, px = 2 * ((gw >> 8) & 0xFF) + sx;
+            const int py = 2 * dgy + sy, px = 2 * dgx + sx;
             if (g.emin <= 2) q += rec_angle(st.rec, g, 2, cy, cx);
             uint32_t xr[4], lr[4];
 #pragma unroll
@@ -718,7 +710,7 @@ __global__ void __launch_bounds__(256, 6) encode_kernel(Geo g, FusedSched sc, co
 #ifdef MMSB_PROBE_ROLES   // performance probes only (tools/role_probe.py): 1 = keystream CTAs only, 2 = workers only
     if (!((MMSB_PROBE_ROLES >> (ro.key ? 0 : 1)) & 1)) return;
 #endif
-    if (ro.key) key_role<TP, true>(g, ro.img, ro.idx, keys, images, ws, smem);
+    if (ro.key) key_role<TP, true, true>(g, ro.img, ro.idx, keys, images, ws, smem);
     else perm_role<TP, METHOD>(g, ro.img, ro.idx, 1 << sc.lgK, images, ws, enc, ceta, b_out, cap_out, status, smem);
 }
 
@@ -737,7 +729,7 @@ __global__ void __launch_bounds__(256, 6) recover_kernel(Geo g, FusedSched sc, c
 #ifdef MMSB_PROBE_ROLES
     if (!((MMSB_PROBE_ROLES >> (ro.key ? 0 : 1)) & 1)) return;
 #endif
-    if (ro.key) key_role<TP, false>(g, ro.img, ro.idx, keys, nullptr, ws, smem);
+    if (ro.key) key_role<TP, false, false>(g, ro.img, ro.idx, keys, nullptr, ws, smem);
     else rec_role<TP, METHOD>(g, ro.img, ro.idx, 1 << sc.lgK, marked, ws, eta_bits, map_bits, lmr_b, out, status, smem);
 }
 

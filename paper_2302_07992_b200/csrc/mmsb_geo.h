@@ -7,7 +7,9 @@ namespace mmsb {
 constexpr int kScanThreads = 256;   // threads per scan CTA
 constexpr int kScanRounds = 4;      // 16-pixel groups per thread
 constexpr int kChunk = kScanRounds * kScanThreads * 16;   // raster pixels per scan chunk (16384)
-constexpr int kRecSlots = 64;       // u64 slots of a tile's in-tile angle record
+constexpr int kRecSlots = 80;       // u64 slots of a tile's record: angles of levels 1..6 (slots 0..62),
+                                    // the in-tile 8x8-group map (bytes of slots 64..71), padding to 5 lines
+constexpr int kRecGroupSlot = 64;
 
 struct Geo {
     int method;          // 0 EMR, 1 LMR
