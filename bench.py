@@ -408,38 +408,48 @@ def load_peaks():
         return {}
 
 
-# algorithmic work per pixel of each kernel class: HBM bytes and int32 ops
-CHACHA_OPS_PER_BYTE = 976 / 64          # 80 quarter-rounds x 12 ops + 16 adds per 64-byte block
+# Algorithmic work per pixel of each kernel class.  bytes: compulsory HBM bytes
+# (inputs read + outputs written once; the keystream scratch lives in L2).  alu: the ChaCha20
+# ALU-pipe operations that cannot be avoided -- XOR and rotate, 640 per 64-byte block = 10 per
+# keystream byte (the adds may issue on the FMA pipe as IMAD); everything else is overhead.
+CHACHA_ALU_PER_BYTE = 640 / 64
 
 
 def kernel_model(name, der):
     d8 = der / 8.0
     return {
-        "ks_tile_kernel<hist>": dict(bytes=1.0, ops=CHACHA_OPS_PER_BYTE * 1.0),
-        "ks_tile_kernel": dict(bytes=0.0, ops=CHACHA_OPS_PER_BYTE * 1.0),
-        "perm_encode_kernel": dict(bytes=2.0, ops=0.0),
-        "recover_strip_kernel": dict(bytes=2.0, ops=0.0),
-        "scan_kernel<embed>+finish": dict(bytes=2.0 + d8, ops=CHACHA_OPS_PER_BYTE * d8),
-        "scan_kernel<extract>+finish": dict(bytes=1.0 + d8, ops=CHACHA_OPS_PER_BYTE * d8),
-        "stats_kernel": dict(bytes=2.0, ops=0.0),
-    }.get(name, dict(bytes=0.0, ops=0.0))
+        "encode_kernel": dict(bytes=2.0, alu=CHACHA_ALU_PER_BYTE * 1.0),
+        "recover_kernel": dict(bytes=2.0, alu=CHACHA_ALU_PER_BYTE * 1.0),
+        "scan_kernel<embed>+finish": dict(bytes=2.0 + d8, alu=CHACHA_ALU_PER_BYTE * d8),
+        "scan_kernel<extract>+finish": dict(bytes=1.0 + d8, alu=CHACHA_ALU_PER_BYTE * d8),
+        "stats_kernel": dict(bytes=2.0, alu=0.0),
+    }.get(name, dict(bytes=0.0, alu=0.0))
+
+
+def load_traffic():
+    """dram bytes per pixel per kernel from the committed ncu --set full capture (profiles/)."""
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))["bytes_per_px"]
+    except Exception:
+        return {}
 
 
 def roofline(prof, peaks, B, HW, cap, method):
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
-    alu_peak = 148 * 128 * sm_mhz * 1e6 / 1e12        # Tops/s: 148 SMs x (ALU 64 + FMA/IMAD 64) lanes/clk
+    alu_peak = 148 * 64 * sm_mhz * 1e6 / 1e12         # Tops/s: 148 SMs x 64 ALU-pipe lanes/clk
     der = float(np.mean(cap)) / HW
+    traffic = load_traffic()
     kern = {}
     for name, p in prof.items():
         m = kernel_model(name, der)
         sec = p["ms"] / 1e3
         gbs = m["bytes"] * p["pixels"] / sec / 1e9
-        tops = m["ops"] * p["pixels"] / sec / 1e12
+        tops = m["alu"] * p["pixels"] / sec / 1e12
         kern[name] = {"ms_total": p["ms"], "launches": p["launches"], "ms_per_launch": p["ms"] / p["launches"],
                       "algorithmic_GBps": gbs, "hbm_frac": gbs / hbm_peak,
-                      "algorithmic_int_Tops": tops, "alu_frac": tops / alu_peak,
-                      "bytes_per_px": m["bytes"], "ops_per_px": m["ops"]}
+                      "chacha_alu_Tops": tops, "alu_frac": tops / alu_peak,
+                      "bytes_per_px": m["bytes"], "chacha_alu_ops_per_px": m["alu"]}
     total = sum(p["ms"] for p in prof.values()) or 1.0
     for k in kern:
         kern[k]["share"] = kern[k]["ms_total"] / total
@@ -451,11 +461,16 @@ def roofline(prof, peaks, B, HW, cap, method):
         d = {"kernel": dom, "bound": "hbm", "achieved": k["algorithmic_GBps"], "peak": hbm_peak, "unit": "GB/s",
              "frac": k["hbm_frac"], "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)"}
     else:
-        d = {"kernel": dom, "bound": "alu", "achieved": k["algorithmic_int_Tops"], "peak": alu_peak,
+        d = {"kernel": dom, "bound": "alu", "achieved": k["chacha_alu_Tops"], "peak": alu_peak,
              "unit": "Tops/s", "frac": k["alu_frac"],
-             "peak_source": "148 SMs x 128 int32 lanes/clk (ALU+FMA pipes) x sm_max_mhz (DESIGN.md §6)"}
+             "peak_source": "148 SMs x 64 ALU-pipe int32 lanes/clk x sm_max_mhz (B300_MICROARCH pipe rates; "
+                            "DESIGN.md §5.4)",
+             "hbm": {"achieved_GBps": k["algorithmic_GBps"], "peak": hbm_peak, "frac": k["hbm_frac"]}}
     d["share_of_step"] = k["share"]
-    d["traffic"] = None
+    px_launch = prof[dom]["pixels"] / prof[dom]["launches"]
+    d["traffic"] = traffic[dom] * px_launch if dom in traffic else None
+    d["traffic_note"] = ("dram__bytes_read.sum + dram__bytes_write.sum per pixel from profiles/traffic.json "
+                         "(ncu --set full), scaled to this launch's pixels")
     d["per_launch_ms"] = k["ms_per_launch"]
     return {"dominant": d, "kernels": kern}
 

@@ -102,18 +102,19 @@ __device__ __forceinline__ void embed16(uint32_t w[4], uint32_t mm, const uint32
 // embed, general path (the group reaches the frame end `fend`): bit by bit, bits at or past
 // fend untouched (a partially filled last pixel keeps its remaining bits, reading Q19)
 template <int BP, int SHIFT>
-__device__ __noinline__ void embed16_tail(uint32_t w[4], uint32_t mm, const uint32_t *kbuf, long long rel,
-                                          long long fend) {
+__device__ __noinline__ uint4 embed16_tail(uint4 u, uint32_t mm, const uint32_t *kbuf, long long rel, long long fend) {
+    uint32_t w[4] = {u.x, u.y, u.z, u.w};
     long long k = rel;
     for (int i = 0; i < 16; i++) {
         if (!((mm >> i) & 1u)) continue;
         for (int t = 0; t < BP; t++, k++) {
-            if (k >= fend) return;
+            if (k >= fend) return make_uint4(w[0], w[1], w[2], w[3]);
             const uint32_t bit = (kbuf[k >> 5] >> (31 - (k & 31))) & 1u;
             const int pos = 8 * (i & 3) + SHIFT + BP - 1 - t;
             w[i >> 2] = (w[i >> 2] & ~(1u << pos)) | (bit << pos);
         }
     }
+    return make_uint4(w[0], w[1], w[2], w[3]);
 }
 
 // extract: the set pixels' BP-bit fields appended in raster order, ORed into kbuf from bit
@@ -172,7 +173,7 @@ __device__ __forceinline__ int image_b(const uint8_t *img0, const int32_t *lmr_b
 }
 
 template <int METHOD, bool EMBED>
-__global__ void __launch_bounds__(kScanThreads, 4) scan_kernel(Geo g, const uint8_t *__restrict__ in,
+__global__ void __launch_bounds__(kScanThreads, 5) scan_kernel(Geo g, const uint8_t *__restrict__ in,
                                                             uint8_t *__restrict__ out, const uint8_t *__restrict__ keys,
                                                             const uint8_t *__restrict__ msg,
                                                             const int64_t *__restrict__ msg_bits, long long stride,
@@ -183,8 +184,9 @@ __global__ void __launch_bounds__(kScanThreads, 4) scan_kernel(Geo g, const uint
     __shared__ __align__(16) uint32_t smap[METHOD == 1 ? kChunk / 32 : 4];
     __shared__ __align__(16) uint32_t kbuf[kKbufWords];
     __shared__ __align__(8) uint64_t bar;
-    __shared__ uint32_t wtot[kScanThreads / 32][kScanRounds];
+    __shared__ uint32_t wtot[kScanRounds][kScanThreads / 32], woff[kScanRounds][kScanThreads / 32];
     __shared__ long long sh_prefix;
+    __shared__ uint32_t sh_agg;
     __shared__ uint32_t esel[16], csel[16];
 
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -247,25 +249,23 @@ __global__ void __launch_bounds__(kScanThreads, 4) scan_kernel(Geo g, const uint
         if (lane >= s) { i01 += t01; i23 += t23; }
     }
     if (lane == 31) {
-        wtot[wid][0] = i01 & 0xFFFFu; wtot[wid][1] = i01 >> 16;
-        wtot[wid][2] = i23 & 0xFFFFu; wtot[wid][3] = i23 >> 16;
+        wtot[0][wid] = i01 & 0xFFFFu; wtot[1][wid] = i01 >> 16;
+        wtot[2][wid] = i23 & 0xFFFFu; wtot[3][wid] = i23 >> 16;
     }
     __syncthreads();
-    // exclusive offset of each of this thread's groups inside the chunk, and the chunk total
-    uint32_t excl[kScanRounds];
+    // warp 0: exclusive scan of the 32 warp totals in raster order (round-major), which also
+    // gives the chunk's aggregate for the look-back below; the offsets are read back after it
     uint32_t agg = 0;
-    {
-        const uint32_t e01 = i01 - c01, e23 = i23 - c23;
-        const uint32_t ein[4] = {e01 & 0xFFFFu, e01 >> 16, e23 & 0xFFFFu, e23 >> 16};
+    if (wid == 0) {
+        const uint32_t v = (&wtot[0][0])[lane];
+        uint32_t incl = v;
 #pragma unroll
-        for (int r = 0; r < kScanRounds; r++) {
-            uint32_t before = 0;
-#pragma unroll
-            for (int w = 0; w < kScanThreads / 32; w++) before += w < wid ? wtot[w][r] : 0u;
-            excl[r] = agg + before + ein[r];
-#pragma unroll
-            for (int w = 0; w < kScanThreads / 32; w++) agg += wtot[w][r];
+        for (int s2 = 1; s2 < 32; s2 <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, incl, s2);
+            if (lane >= s2) incl += t;
         }
+        (&woff[0][0])[lane] = incl - v;
+        agg = __shfl_sync(0xffffffffu, incl, 31);
     }
 
     // ---- single-pass decoupled look-back over the image's chunks (blockIdx order).  Warp 0
@@ -299,8 +299,18 @@ __global__ void __launch_bounds__(kScanThreads, 4) scan_kernel(Geo g, const uint
         }
         if (lane == 0) sh_prefix = (long long)prefix;
     }
+    if (wid == 0 && lane == 0) sh_agg = agg;
     __syncthreads();
     const long long prefix = sh_prefix;
+    agg = sh_agg;
+    uint32_t excl[kScanRounds];                              // this thread's groups inside the chunk
+    {
+        const uint32_t e01 = i01 - c01, e23 = i23 - c23;
+        excl[0] = woff[0][wid] + (e01 & 0xFFFFu);
+        excl[1] = woff[1][wid] + (e01 >> 16);
+        excl[2] = woff[2][wid] + (e23 & 0xFFFFu);
+        excl[3] = woff[3][wid] + (e23 >> 16);
+    }
     const long long lo = prefix * bp, hi = (prefix + (long long)agg) * bp;
 
     if constexpr (EMBED) {
@@ -341,7 +351,10 @@ __global__ void __launch_bounds__(kScanThreads, 4) scan_kernel(Geo g, const uint
                 const int cnt = __popc(m[r]);
                 if (cnt && rel < fend) {
                     if (rel + (long long)cnt * BP <= fend) embed16<BP, SH>(w, m[r], kbuf, (int)rel, esel);
-                    else embed16_tail<BP, SH>(w, m[r], kbuf, rel, fend);
+                    else {
+                        const uint4 t = embed16_tail<BP, SH>(make_uint4(w[0], w[1], w[2], w[3]), m[r], kbuf, rel, fend);
+                        w[0] = t.x; w[1] = t.y; w[2] = t.z; w[3] = t.w;
+                    }
                 }
                 *reinterpret_cast<uint4 *>(dst + 16 * q) = make_uint4(w[0], w[1], w[2], w[3]);
             }
