@@ -118,7 +118,7 @@ __device__ __forceinline__ const uint32_t *warp0_ready(const Geo &g, const TileW
 // ======================================================================================
 // K role: one thread per tile row, TPC = 256 / T tiles per CTA.
 // ======================================================================================
-template <int TP, bool HIST, bool INV>
+template <int TP, bool HIST, bool INV, bool LMR8 = true>
 __device__ __forceinline__ void key_role(const Geo &g, int img, int kidx, const uint8_t *__restrict__ keys,
                                          const uint8_t *__restrict__ images, const TileWS &ws, uint8_t *smem) {
     constexpr int T = 1 << TP, NW = T / 4, TPC = 256 / T;
@@ -175,20 +175,27 @@ __device__ __forceinline__ void key_role(const Geo &g, int img, int kidx, const 
             iw[i] = u.x; iw[i + 1] = u.y; iw[i + 2] = u.z; iw[i + 3] = u.w;
         }
         uint32_t prev = (valid && tx > 0) ? ((uint32_t)__ldg(src - 1) << 24) : 0u;
+        // The shifts (as multiply-high) and the counter adds (as multiply-add) go through the
+        // opaque g.one so that they issue on the FMA pipe: the ALU pipe is busy with ChaCha.
         uint32_t acc[7] = {0, 0, 0, 0, 0, 0, 0};
+        const uint32_t one = g.one, h1 = one << 31, h2 = one << 30, h4 = one << 28;
 #pragma unroll
         for (int i = 0; i < NW; i++) {
             const uint32_t left = __byte_perm(prev, iw[i], 0x6543);   // [prev.b3, w.b0, w.b1, w.b2]
             uint32_t x = iw[i] ^ left;
             if (i == 0 && tx == 0) x |= 0xFFu;                     // column 0 is non-redundant
             prev = iw[i];
-            uint32_t y = x | ((x >> 1) & 0x7F7F7F7Fu);
-            y |= (y >> 2) & 0x3F3F3F3Fu;
-            y |= (y >> 4) & 0x0F0F0F0Fu;                           // byte = 2^bitlen(x) - 1
-            const uint32_t y4 = (y >> 4) & 0x0F0F0F0Fu;
-            acc[0] += y & 0x01010101u; acc[1] += y & 0x02020202u;
-            acc[2] += y & 0x04040404u; acc[3] += y & 0x08080808u;
-            acc[4] += y4 & 0x01010101u; acc[5] += y4 & 0x02020202u; acc[6] += y4 & 0x04040404u;
+            uint32_t y = x | (__umulhi(x, h1) & 0x7F7F7F7Fu);
+            y |= __umulhi(y, h2) & 0x3F3F3F3Fu;
+            y |= __umulhi(y, h4) & 0x0F0F0F0Fu;                    // byte = 2^bitlen(x) - 1
+            const uint32_t y4 = __umulhi(y, h4) & 0x0F0F0F0Fu;
+            if (LMR8) acc[0] = (y & 0x01010101u) * one + acc[0];   // b = 8: LMR only
+            acc[1] = (y & 0x02020202u) * one + acc[1];
+            acc[2] = (y & 0x04040404u) * one + acc[2];
+            acc[3] = (y & 0x08080808u) * one + acc[3];
+            acc[4] = (y4 & 0x01010101u) * one + acc[4];
+            acc[5] = (y4 & 0x02020202u) * one + acc[5];
+            acc[6] = (y4 & 0x04040404u) * one + acc[6];
         }
         // threshold bit k <-> b = 8 - k; per-thread counts <= 64, warp sums <= 2048: two
         // counts per 32-bit word for the warp reduction
@@ -710,7 +717,7 @@ __global__ void __launch_bounds__(256, 6) encode_kernel(Geo g, FusedSched sc, co
 #ifdef MMSB_PROBE_ROLES   // performance probes only (tools/role_probe.py): 1 = keystream CTAs only, 2 = workers only
     if (!((MMSB_PROBE_ROLES >> (ro.key ? 0 : 1)) & 1)) return;
 #endif
-    if (ro.key) key_role<TP, true, true>(g, ro.img, ro.idx, keys, images, ws, smem);
+    if (ro.key) key_role<TP, true, true, METHOD == 1>(g, ro.img, ro.idx, keys, images, ws, smem);
     else perm_role<TP, METHOD>(g, ro.img, ro.idx, 1 << sc.lgK, images, ws, enc, ceta, b_out, cap_out, status, smem);
 }
 

@@ -27,6 +27,7 @@ struct Geo {
     int nchunks;         // scan chunks per image
     int tile_log2;       // LMR coder tile side 2^t
     int ntiles_coder;    // LMR coder tiles per plane
+    uint32_t one;        // = 1, opaque to the compiler: multiplies that keep adds / shifts on the FMA pipe
 };
 
 inline int ilog2(long long v) {
@@ -63,6 +64,7 @@ inline bool make_geo(int method, int B, int H, int W, int tile_log2, Geo *g) {
     g->npyr = p;
     g->nchunks = (int)((g->HW + kChunk - 1) / kChunk);
     g->tile_log2 = tile_log2;
+    g->one = 1;
     {
         const int th = (1 << tile_log2) < H ? (1 << tile_log2) : H, tw = (1 << tile_log2) < W ? (1 << tile_log2) : W;
         g->ntiles_coder = ((H + th - 1) / th) * ((W + tw - 1) / tw);
