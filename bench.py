@@ -216,6 +216,7 @@ def run_ours(args):
 
     from paper_2302_07992_b200 import build as BLD
     from paper_2302_07992_b200 import mmsb as G
+    from paper_2302_07992_b200 import parallel as P
     from paper_2302_07992_b200 import synth as S
 
     rank = int(os.environ.get("RANK", "0"))
@@ -256,8 +257,8 @@ def run_ours(args):
     NB = torch.from_numpy(nbits_np).to(dev)
     MOUT = torch.zeros(B, stride, dtype=torch.uint8, device=dev)
     SSE = torch.empty(B, dtype=torch.int64, device=dev)
-    records = torch.empty(B, 4, dtype=torch.int64, device=dev)
-    gathered = torch.empty(world * B, 4, dtype=torch.int64, device=dev) if world > 1 else None
+    records = torch.empty(B, P.REC_COLS, dtype=torch.int64, device=dev)
+    gathered = [records]
 
     def step(I_, K1_, K2_, MSG_, NB_):
         _, b, c, _ = G.encode(mid, I_, K1_, ws, out=enc)
@@ -265,13 +266,13 @@ def run_ours(args):
         _, nb_out, st_x = G.extract(mid, marked, K2_, stride, ws, out=MOUT)
         _, st_r = G.recover(mid, marked, K1_, ws, out=rec)
         G.stats(I_, rec, out=SSE)
+        last[:] = [b, c, st_r]
         if world > 1:   # the path's one exchange: per-image records to every rank (NCCL)
-            records[:, 0] = b
-            records[:, 1] = c
-            records[:, 2] = SSE
-            records[:, 3] = st_r
-            dist.all_gather_into_tensor(gathered, records)
+            records.copy_(P.make_records(b, c, SSE, st_r))
+            gathered[0] = P.gather_records(records, world)
         return b, c
+
+    last = [None, None, None]
 
     # warm-up
     for _ in range(args.warmup):
@@ -302,10 +303,7 @@ def run_ours(args):
     ms = e0.elapsed_time(e1)
     prof = read_profile(G)
     G.lib().mmsb_profile_enable(0)
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
+    ms_max = P.max_over_ranks(ms, dev, world)
     px_total = world * B * HW * args.steps
     value = px_total / (ms_max / 1e3) / 1e6
 
@@ -359,10 +357,7 @@ def run_ours(args):
                 _, st_ = G.recover(mid, L.marked, L.K1, L.ws, out=L.rec)
                 G.stats(L.I, L.rec, out=L.SSE)
                 if world > 1:
-                    records[a:z, 0] = b_
-                    records[a:z, 1] = c_
-                    records[a:z, 2] = L.SSE
-                    records[a:z, 3] = st_
+                    records[a:z] = P.make_records(b_, c_, L.SSE, st_)
                 hREC[a:z].copy_(L.rec, non_blocking=True)
                 hMOUT[a:z].copy_(L.MOUT, non_blocking=True)
                 hSSE[a:z].copy_(L.SSE, non_blocking=True)
@@ -370,7 +365,7 @@ def run_ours(args):
         for L in lanes:
             stream.wait_event(L.done)
         if world > 1:
-            dist.all_gather_into_tensor(gathered, records)
+            gathered[0] = P.gather_records(records, world)
 
     e2e_step()
     torch.cuda.synchronize()
@@ -382,10 +377,8 @@ def run_ours(args):
         e2e_step()
     f1.record(stream)
     torch.cuda.synchronize()
-    te = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_value = world * B * HW * e2e_steps / (float(te.item()) / 1e3) / 1e6
+    te_ms = P.max_over_ranks(f0.elapsed_time(f1), dev, world)
+    e2e_value = world * B * HW * e2e_steps / (te_ms / 1e3) / 1e6
     ok_e2e = bool(np.array_equal(hREC.numpy(), rec.cpu().numpy())) and bool(
         np.array_equal(hSSE.numpy(), SSE.cpu().numpy()))
 
@@ -406,7 +399,8 @@ def run_ours(args):
                 "kernels": roof["kernels"],
                 "checks": {"payload_round_trip": ok_rt, "e2e_matches_device": ok_e2e,
                            "statuses_ok": bool((st0 == 0).all().item())},
-                "mean_der_bpp": float(cap.mean() / HW), "gen_s": gen_s}
+                "mean_der_bpp": float(cap.mean() / HW), "gen_s": gen_s,
+                "stats": P.aggregate(gathered[0] if world > 1 else P.make_records(last[0], last[1], SSE, last[2]), H, W)}
         if world == 1 and not args.no_cpu_baseline:
             import oracle as O
 
