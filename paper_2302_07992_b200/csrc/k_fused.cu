@@ -751,7 +751,10 @@ FusedSched fused_sched(const Geo &g) {
     while ((long long)(gi * 2) * g.HW <= (2ll << 20) && gi < g.B) gi *= 2;   // ~2 Mpixel per group
     sc.GI = gi;
     sc.ngroups = (g.B + gi - 1) / gi;
-    sc.L = 6;
+    // keystream rows run L rows ahead of their workers: enough to hide the keystream latency,
+    // few enough that the scratch (1 B/px) and the re-read images of L groups stay in L2
+    long long lag = (12ll << 20) / ((long long)gi * g.HW);
+    sc.L = (int)(lag < 1 ? 1 : lag > 6 ? 6 : lag);
     return sc;
 }
 

@@ -223,27 +223,26 @@ __global__ void lmr_fit_kernel(Geo g, int wave, const int32_t *__restrict__ size
 //   remaining MSBs keep I_r XOR s.  Bad case: the b-field 7 (bits r = 0..2 set).
 // One thread per 16 pixels; the stream bits of its pixels are gathered from the tile slots.
 // ======================================================================================
-__device__ __forceinline__ uint32_t stream_bit(const Geo &g, int Tc, const LmrPlan &pl, const int32_t *sz,
-                                               const int32_t *off, const uint8_t *slots, int cap, long long r) {
-    if (r < 3) return ((uint32_t)(pl.b - 2) >> (2 - r)) & 1u;
-    if (r < 7) return ((uint32_t)g.tile_log2 >> (6 - r)) & 1u;
-    const long long hdr = 7 + 32ll * Tc;
-    if (r < hdr) {
-        const int k = (int)((r - 7) >> 4), bi = (int)((r - 7) & 15);
-        return ((uint32_t)sz[k] >> (15 - bi)) & 1u;
-    }
-    const long long q = r - hdr;
-    const long long byte = q >> 3;
-    // locate the stream holding `byte` (binary search over the exclusive offsets)
+// bytes [q0, q0 + 2) of the MSB-plane stream (header excluded) for the 16 pixels of a thread:
+// one binary search for the stream holding byte q0, the next byte from the same or next stream
+__device__ __forceinline__ uint32_t stream_bytes2(int Tc, const int32_t *sz, const int32_t *off, const uint8_t *slots,
+                                                  int cap, long long q0, long long total) {
     int lo = 0, hi = 2 * Tc - 1;
     while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
-        if (off[mid] <= byte) lo = mid; else hi = mid - 1;
+        if (off[mid] <= q0) lo = mid; else hi = mid - 1;
     }
-    const int k = lo;
-    const int slot = k < Tc ? 0 : 1, tile = k < Tc ? k : k - Tc;
-    const uint8_t v = slots[((size_t)slot * Tc + tile) * cap + (byte - off[k])];
-    return (v >> (7 - (q & 7))) & 1u;
+    uint32_t v = 0;
+    int k = lo;
+    for (int i = 0; i < 2; i++) {
+        const long long q = q0 + i;
+        if (q >= total) break;
+        while (k + 1 < 2 * Tc && off[k + 1] <= q) k++;         // (empty streams are skipped)
+        const int slot = k < Tc ? 0 : 1, tile = k < Tc ? k : k - Tc;
+        v = (v << 8) | slots[((size_t)slot * Tc + tile) * cap + (q - off[k])];
+        if (i == 0 && q0 + 1 >= total) v <<= 8;
+    }
+    return v;                                                   // 16 bits, stream order MSB first
 }
 
 __global__ void __launch_bounds__(256) lmr_msb_write_kernel(Geo g, const LmrPlan *__restrict__ plan,
@@ -275,15 +274,39 @@ __global__ void __launch_bounds__(256) lmr_msb_write_kernel(Geo g, const LmrPlan
     const int32_t *sz = sizes + (size_t)img * 2 * Tc;
     const int32_t *off = offsets + (size_t)img * 2 * Tc;
     const uint8_t *slots = streams + (size_t)img * 2 * Tc * cap;
+    const long long hdr = 7 + 32ll * Tc;                        // header bits before the stream bytes
+    const long long total = (pl.K - hdr) / 8;                   // stream bytes
     for (long long p = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * 16; p < pl.K;
          p += (long long)gridDim.x * blockDim.x * 16) {
+        // the 16 plane bits of pixels [p, p+16), MSB first
+        uint32_t bits16 = 0;
+        if (p >= hdr) {
+            const long long q = p - hdr, q0 = q >> 3;
+            const int sh = (int)(q & 7);                        // bit offset inside byte q0
+            const uint32_t b3 = (stream_bytes2(Tc, sz, off, slots, cap, q0, total) << 8) |
+                                (q0 + 2 < total ? stream_bytes2(Tc, sz, off, slots, cap, q0 + 2, total) >> 8 : 0u);
+            bits16 = (b3 >> (8 - sh)) & 0xFFFFu;
+        } else {
+            for (int i = 0; i < 16; i++) {
+                const long long r = p + i;
+                uint32_t bit = 0;
+                if (r < 3) bit = ((uint32_t)(pl.b - 2) >> (2 - r)) & 1u;
+                else if (r < 7) bit = ((uint32_t)g.tile_log2 >> (6 - r)) & 1u;
+                else if (r < hdr) bit = ((uint32_t)sz[(r - 7) >> 4] >> (15 - ((r - 7) & 15))) & 1u;
+                else {
+                    const long long q = r - hdr;
+                    const uint32_t by = stream_bytes2(Tc, sz, off, slots, cap, q >> 3, total) >> 8;
+                    bit = (by >> (7 - (q & 7))) & 1u;
+                }
+                bits16 |= bit << (15 - i);
+            }
+        }
         uint4 u = *reinterpret_cast<const uint4 *>(E + p);
         uint32_t wv[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
         for (int i = 0; i < 16; i++) {
-            const long long r = p + i;
-            if (r < pl.K) {
-                const uint32_t bit = stream_bit(g, Tc, pl, sz, off, slots, cap, r);
+            if (p + i < pl.K) {
+                const uint32_t bit = (bits16 >> (15 - i)) & 1u;
                 const int sh = 8 * (i & 3) + 7;
                 wv[i >> 2] = (wv[i >> 2] & ~(1u << sh)) | (bit << sh);
             }
