@@ -208,12 +208,18 @@ __device__ __forceinline__ void key_role(const Geo &g, int img, int kidx, const 
 #pragma unroll
             for (int s = 16; s > 0; s >>= 1) pk[j] += __shfl_xor_sync(0xffffffffu, pk[j], s);
         }
+        // per-CTA sum, then one atomic per count: a 4096^2 image has 1024 keystream CTAs, and
+        // per-warp atomics on the image's 7 counters serialised at L2
+        uint32_t *hsum = reinterpret_cast<uint32_t *>(&rec[TPC][0]);       // [8 warps][4]
         if ((tid & 31) == 0) {
 #pragma unroll
-            for (int k = 0; k < 7; k++) {
-                const uint32_t v = (pk[k >> 1] >> (16 * (k & 1))) & 0xFFFFu;
-                if (v) atomicAdd(&ws.hist[img * 8 + 8 - k], v);
-            }
+            for (int j = 0; j < 4; j++) hsum[(tid >> 5) * 4 + j] = pk[j];
+        }
+        __syncthreads();
+        if (tid < 7) {
+            uint32_t v = 0;
+            for (int w = 0; w < 8; w++) v += (hsum[w * 4 + (tid >> 1)] >> (16 * (tid & 1))) & 0xFFFFu;
+            if (v) atomicAdd(&ws.hist[img * 8 + 8 - tid], v);
         }
     }
     __syncthreads();
@@ -260,14 +266,26 @@ __device__ __forceinline__ void key_role(const Geo &g, int img, int kidx, const 
         }
         __syncthreads();
     }
-    // upper pyramid: the tile total (= level-tp angle) into every enclosing block
-    if (valid && row == 0) {
-        const uint32_t tv = (uint32_t)(rec[lt][g.lvl_off[TP]] & 3u);
-        if (tv)
-            for (int e = TP + 1; e <= g.emax; e++) {
-                const int k = e - TP;
-                atomicAdd(&ws.pyr[(size_t)img * g.npyr + g.pyr_off[e] + (ty >> k) * (g.W >> e) + (tx >> k)], tv);
+    // upper pyramid: the tile totals (= level-tp angles) into every enclosing block, summed over
+    // the CTA's tiles first (neighbouring tiles share the upper blocks: fewer contended atomics)
+    if (tid < 32) {
+        for (int e = TP + 1 + tid; e <= g.emax; e += 32) {
+            const int k = e - TP;
+            int cur = -1;
+            uint32_t acc = 0;
+            for (int l2 = 0; l2 < TPC; l2++) {
+                const int tl = kidx * TPC + l2;
+                if (tl >= g.ntiles) break;
+                const int blk = ((tl >> g.tlog) >> k) * (g.W >> e) + ((tl & (g.tilesX - 1)) >> k);
+                if (blk != cur) {
+                    if (acc) atomicAdd(&ws.pyr[(size_t)img * g.npyr + g.pyr_off[e] + cur], acc);
+                    cur = blk;
+                    acc = 0;
+                }
+                acc += (uint32_t)(rec[l2][g.lvl_off[TP]] & 3u);
             }
+            if (acc) atomicAdd(&ws.pyr[(size_t)img * g.npyr + g.pyr_off[e] + cur], acc);
+        }
     }
     // records out
     for (int t = tid; t < TPC * kRecSlots; t += 256) {
@@ -710,7 +728,7 @@ __global__ void __launch_bounds__(256, 6) encode_kernel(Geo g, FusedSched sc, co
                                                      int32_t *__restrict__ b_out, int64_t *__restrict__ cap_out,
                                                      int32_t *__restrict__ status) {
     constexpr int T = 1 << TP, TPC = 256 / T;
-    constexpr size_t KB = TPC * kRecSlots * 8, PB = sizeof(PermSmem<TP>);
+    constexpr size_t KB = (TPC + 1) * kRecSlots * 8, PB = sizeof(PermSmem<TP>);
     __shared__ __align__(128) uint8_t smem[KB > PB ? KB : PB];
     const Role ro = role_of(sc);
     if (ro.img >= g.B) return;
@@ -729,7 +747,7 @@ __global__ void __launch_bounds__(256, 6) recover_kernel(Geo g, FusedSched sc, c
                                                       const int32_t *__restrict__ lmr_b, uint8_t *__restrict__ out,
                                                       int32_t *__restrict__ status) {
     constexpr int T = 1 << TP, TPC = 256 / T;
-    constexpr size_t KB = TPC * kRecSlots * 8, RB = sizeof(RecSmem<TP>);
+    constexpr size_t KB = (TPC + 1) * kRecSlots * 8, RB = sizeof(RecSmem<TP>);
     __shared__ __align__(128) uint8_t smem[KB > RB ? KB : RB];
     const Role ro = role_of(sc);
     if (ro.img >= g.B) return;

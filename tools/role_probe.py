@@ -27,16 +27,16 @@ def build_variant(mask):
     return out
 
 
-def run(mask, batch, reps=10):
+def run(mask, batch, config=2, reps=10):
     import numpy as np
     import torch
 
     from paper_2302_07992_b200 import mmsb as G
     from paper_2302_07992_b200 import synth as S
 
-    imgs, k1, k2 = S.batch(2, n=batch)
+    imgs, k1, k2 = S.batch(config, n=batch)
     I, K1 = torch.from_numpy(imgs).cuda(), torch.from_numpy(k1).cuda()
-    ws = G.Workspace(G.EMR, batch, 512, 512)
+    ws = G.Workspace(G.EMR, batch, imgs.shape[1], imgs.shape[2])
     enc = torch.empty_like(I)
     rec = torch.empty_like(I)
     res = {}
@@ -60,13 +60,14 @@ if __name__ == "__main__":
     ap.add_argument("--build", action="store_true")
     ap.add_argument("--batch", type=int, default=1000)
     ap.add_argument("--mask", type=int, default=None)
+    ap.add_argument("--config", type=int, default=2)
     a = ap.parse_args()
     if a.build:
         for m in (1, 2, 6, 10, 14):
             print(build_variant(m))
         sys.exit(0)
     if a.mask is not None:
-        run(a.mask, a.batch)
+        run(a.mask, a.batch, a.config)
         sys.exit(0)
     from paper_2302_07992_b200 import build as B
 
@@ -74,4 +75,4 @@ if __name__ == "__main__":
         env = dict(os.environ)
         if m != 3:
             env["MMSB_LIB"] = os.path.join(B.PKG, f"libmmsb_probe{m}.so")
-        subprocess.run([sys.executable, __file__, "--mask", str(m), "--batch", str(a.batch)], env=env, timeout=120)
+        subprocess.run([sys.executable, __file__, "--mask", str(m), "--batch", str(a.batch), "--config", str(a.config)], env=env, timeout=120)
