@@ -485,6 +485,253 @@ __global__ void __launch_bounds__(kCoderThreads) coder_decode_kernel(Geo g, int 
     }
 }
 
+// ======================================================================================
+// Fast coder kernels for tiles at least 32 pixels wide (every configured shape).  Same bit
+// stream as coder_encode_kernel / coder_decode_kernel: the tile's two previous
+// rows are kept in registers as MSB-first words, the 10-pixel context of a symbol comes from
+// funnel shifts, and the probability of the NEXT symbol is loaded from the shared-memory model
+// while the current one is coded -- for the encoder from its known context, for the decoder
+// for both values of the bit being decoded -- with a forward of the freshly updated
+// probability when the two contexts coincide.  What is left on the serial chain per symbol is
+// the range update itself.
+// ======================================================================================
+__device__ __forceinline__ uint32_t nib4(uint32_t t) { return ((t * 0x08040201u) >> 24) & 0xFu; }   // bytes' bit 0 -> MSB-first nibble
+
+// context bits 7..0 of pixel x = 32 K + j from the two previous rows (MSB-first words; pixels
+// outside the tile read as 0): 5 pixels x-2..x+2 of row y-1, 3 pixels x-1..x+1 of row y-2
+template <int NW, int K>
+__device__ __forceinline__ uint32_t rows_ctx(const uint32_t (&p1)[NW], const uint32_t (&p2)[NW], int j) {
+    const uint32_t a0 = K > 0 ? p1[K > 0 ? K - 1 : 0] : 0u, a2 = K + 1 < NW ? p1[K + 1 < NW ? K + 1 : K] : 0u;
+    const uint32_t b0 = K > 0 ? p2[K > 0 ? K - 1 : 0] : 0u, b2 = K + 1 < NW ? p2[K + 1 < NW ? K + 1 : K] : 0u;
+    const uint32_t w5 = __funnelshift_l(j >= 2 ? a2 : p1[K], j >= 2 ? p1[K] : a0, (j - 2) & 31) >> 27;
+    const uint32_t w3 = __funnelshift_l(j >= 1 ? b2 : p2[K], j >= 1 ? p2[K] : b0, (j - 1) & 31) >> 29;
+    return (w5 << 3) | w3;
+}
+
+template <int NW, int K>
+__device__ __forceinline__ void enc_row(RcEnc &e, uint16_t *mdl, const uint32_t (&cw)[NW], const uint32_t (&p1)[NW],
+                                        const uint32_t (&p2)[NW], uint32_t &ctx, uint32_t &p, uint32_t &hist2) {
+    // context of the first pixel of the next word (loop invariant); unused after the row's end
+    const uint32_t first_next = K + 1 < NW ? rows_ctx<NW, (K + 1 < NW ? K + 1 : K)>(p1, p2, 0) : 0u;
+    const uint32_t word = cw[K];
+#pragma unroll 2
+    for (int j = 0; j < 32; j++) {
+        const uint32_t bit = (word >> (31 - j)) & 1u;
+        const uint32_t nh = ((hist2 << 1) | bit) & 3u;
+        const bool last = (K == NW - 1) && j == 31;
+        // next symbol's context and probability (prefetched before this symbol's store)
+        const uint32_t nrows = j < 31 ? rows_ctx<NW, K>(p1, p2, j + 1) : first_next;
+        const uint32_t nctx = ((nh & 1u) << 9) | ((nh >> 1) << 8) | nrows;
+        const uint32_t np = last ? 0u : (uint32_t)mdl[nctx * 32];
+        const uint32_t bound = (e.range >> 16) * p;
+        uint32_t pu;
+        if (bit == 0) {
+            e.range = bound;
+            pu = p + ((65536u - p) >> 4);
+        } else {
+            e.low += bound;
+            e.range -= bound;
+            pu = p - (p >> 4);
+        }
+        mdl[ctx * 32] = (uint16_t)pu;
+        while (e.range < (1u << 24)) {
+            e.range <<= 8;
+            e.shift_low();
+        }
+        p = nctx == ctx ? pu : np;
+        ctx = nctx;
+        hist2 = nh;
+    }
+    if constexpr (K + 1 < NW) enc_row<NW, K + 1>(e, mdl, cw, p1, p2, ctx, p, hist2);
+}
+
+template <int NW>
+__global__ void __launch_bounds__(kCoderThreads) coder_encode_fast_kernel(Geo g, int wave, const uint8_t *__restrict__ ceta,
+                                                                          const LmrPlan *__restrict__ plan,
+                                                                          uint8_t *__restrict__ streams,
+                                                                          int32_t *__restrict__ sizes) {
+    extern __shared__ uint16_t p0s[];                                  // [1024][32]
+    const int lane = threadIdx.x;
+    const int Tc = lmr_tile_count(g.H, g.W, g.tile_log2);
+    const int nslots = wave == 0 ? 2 : 1;
+    const long long gid = (long long)blockIdx.x * kCoderThreads + lane;
+    const long long total = (long long)g.B * nslots * Tc;
+    const bool active0 = gid < total;
+    const int img = active0 ? (int)(gid / ((long long)nslots * Tc)) : 0;
+    const int rem = active0 ? (int)(gid % ((long long)nslots * Tc)) : 0;
+    const int slot = wave == 0 ? rem / Tc : 1;
+    const int tile = rem % Tc;
+    const LmrPlan pl = plan[img];
+    const bool active = active0 && pl.state == 0;
+    if (!__any_sync(0xffffffffu, active)) return;
+    for (int c = 0; c < 1024; c++) p0s[c * 32 + lane] = 32768;
+    if (!active) return;
+
+    const int th = lmr_tile_side(g.tile_log2, g.H);
+    constexpr int w = 32 * NW;
+    const int TN = g.W / w;
+    const int y0 = (tile / TN) * th, x0 = (tile % TN) * w;
+    const int h = g.H - y0 < th ? g.H - y0 : th;
+    const uint32_t bsub = slot == 0 ? 0u : (uint32_t)(0x80 - pl.order[wave]) * 0x01010101u;
+    const int cap = lmr_tile_cap(g.tile_log2, g.H, g.W);
+    uint16_t *mdl = p0s + lane;
+
+    RcEnc e{0, 0xFFFFFFFFu, 0, 1, streams + (((size_t)img * 2 + slot) * Tc + tile) * cap, 0, cap};
+    const uint8_t *src = ceta + (size_t)img * g.HW + x0;
+    uint32_t p1[NW], p2[NW];
+#pragma unroll
+    for (int k = 0; k < NW; k++) { p1[k] = 0; p2[k] = 0; }
+    // the row's bits, MSB-first: eta = byte >> 7 (eq. MSB_map), map = [(byte & 15) < b];
+    // the next row's bytes are loaded while the current row is coded
+    uint4 raw[2 * NW];
+    auto load_row = [&](int y) {
+        const uint4 *rp = reinterpret_cast<const uint4 *>(src + (size_t)(y0 + y) * g.W);
+#pragma unroll
+        for (int q = 0; q < 2 * NW; q++) raw[q] = __ldg(rp + q);
+    };
+    load_row(0);
+    for (int y = 0; y < h; y++) {
+        uint32_t cw[NW];
+#pragma unroll
+        for (int k = 0; k < NW; k++) {
+            uint32_t wv = 0;
+#pragma unroll
+            for (int q = 0; q < 2; q++) {
+                const uint32_t v[4] = {raw[2 * k + q].x, raw[2 * k + q].y, raw[2 * k + q].z, raw[2 * k + q].w};
+#pragma unroll
+                for (int i = 0; i < 4; i++) {
+                    const uint32_t t = slot == 0 ? (v[i] >> 7) & 0x01010101u
+                                                 : (~((v[i] & 0x0F0F0F0Fu) + bsub) >> 7) & 0x01010101u;
+                    wv |= nib4(t) << (28 - 4 * (4 * q + i));
+                }
+            }
+            cw[k] = wv;
+        }
+        if (y + 1 < h) load_row(y + 1);
+        uint32_t hist2 = 0;
+        uint32_t ctx = rows_ctx<NW, 0>(p1, p2, 0);
+        uint32_t p = mdl[ctx * 32];
+        enc_row<NW, 0>(e, mdl, cw, p1, p2, ctx, p, hist2);
+#pragma unroll
+        for (int k = 0; k < NW; k++) { p2[k] = p1[k]; p1[k] = cw[k]; }
+    }
+    for (int i = 0; i < 5; i++) e.shift_low();
+    sizes[((size_t)img * 2 + slot) * Tc + tile] = (e.n <= cap && e.n <= 65535) ? e.n : -1;
+}
+
+// decoder input: stream byte `pos` of a tile (bit-aligned inside the MSB-plane bytes); 0 past the end
+struct RcIn {
+    const uint8_t *m;
+    long long bit0;
+    int nbytes, pos;
+    __device__ __forceinline__ uint32_t next() {
+        uint32_t v = 0;
+        if (pos < nbytes) {
+            const long long bb = bit0 + 8ll * pos;
+            const uint32_t hi = __ldg(m + (bb >> 3)), lo = __ldg(m + (bb >> 3) + 1);
+            v = (((hi << 8) | lo) >> (8 - (bb & 7))) & 0xFFu;
+        }
+        pos++;
+        return v;
+    }
+};
+
+template <int NW, int K>
+__device__ __forceinline__ void dec_row(RcIn &in, uint32_t &range, uint32_t &code, uint16_t *mdl, uint32_t (&cw)[NW],
+                                        const uint32_t (&p1)[NW], const uint32_t (&p2)[NW], uint32_t &ctx, uint32_t &p,
+                                        uint32_t &hist2, uint32_t *orow) {
+    const uint32_t first_next = K + 1 < NW ? rows_ctx<NW, (K + 1 < NW ? K + 1 : K)>(p1, p2, 0) : 0u;
+    uint32_t acc = 0, word = 0;
+#pragma unroll 2
+    for (int j = 0; j < 32; j++) {
+        const bool last = (K == NW - 1) && j == 31;
+        // both candidate contexts of the next symbol (its (0,-1) bit is the one decoded now)
+        const uint32_t nbase = ((hist2 & 1u) << 8) | (j < 31 ? rows_ctx<NW, K>(p1, p2, j + 1) : first_next);
+        const uint32_t np0 = last ? 0u : (uint32_t)mdl[nbase * 32];
+        const uint32_t np1 = last ? 0u : (uint32_t)mdl[(nbase | 512u) * 32];
+        const uint32_t bound = (range >> 16) * p;
+        uint32_t bit, pu;
+        if (code < bound) {
+            range = bound;
+            bit = 0;
+            pu = p + ((65536u - p) >> 4);
+        } else {
+            code -= bound;
+            range -= bound;
+            bit = 1;
+            pu = p - (p >> 4);
+        }
+        mdl[ctx * 32] = (uint16_t)pu;
+        while (range < (1u << 24)) {
+            range <<= 8;
+            code = (code << 8) | in.next();
+        }
+        word |= bit << (31 - j);
+        acc |= bit << j;
+        hist2 = ((hist2 << 1) | bit) & 3u;
+        const uint32_t nctx = nbase | (bit << 9);
+        p = nctx == ctx ? pu : (bit ? np1 : np0);
+        ctx = nctx;
+    }
+    cw[K] = word;
+    orow[K] = acc;                                           // plane words: bit x & 31 = pixel x
+    if constexpr (K + 1 < NW) dec_row<NW, K + 1>(in, range, code, mdl, cw, p1, p2, ctx, p, hist2, orow);
+}
+
+template <int NW>
+__global__ void __launch_bounds__(kCoderThreads) coder_decode_fast_kernel(Geo g, int want_eta, const uint8_t *__restrict__ mbuf,
+                                                                          const int32_t *__restrict__ lmr_b,
+                                                                          const int32_t *__restrict__ lmr_t,
+                                                                          const int32_t *__restrict__ offsets,
+                                                                          const int32_t *__restrict__ sizes,
+                                                                          uint32_t *__restrict__ eta_bits,
+                                                                          uint32_t *__restrict__ map_bits) {
+    extern __shared__ uint16_t p0s[];
+    const int lane = threadIdx.x;
+    const int TcM = g.ntiles_coder;
+    const int nplanes = want_eta ? 2 : 1;
+    const long long gid = (long long)blockIdx.x * kCoderThreads + lane;
+    const long long total = (long long)g.B * nplanes * TcM;
+    bool active = gid < total;
+    const int img = active ? (int)(gid / ((long long)nplanes * TcM)) : 0;
+    const int rem = active ? (int)(gid % ((long long)nplanes * TcM)) : 0;
+    const int plane = want_eta ? rem / TcM : 1;
+    const int tile = rem % TcM;
+    const int b = lmr_b[img];
+    const int Tc = TcM;                                       // header t == g.tile_log2 (else FORMAT)
+    active = active && b >= 2;
+    if (!__any_sync(0xffffffffu, active)) return;
+    for (int c = 0; c < 1024; c++) p0s[c * 32 + lane] = 32768;
+    if (!active) return;
+
+    const int th = lmr_tile_side(g.tile_log2, g.H);
+    constexpr int w = 32 * NW;
+    const int TN = g.W / w;
+    const int y0 = (tile / TN) * th, x0 = (tile % TN) * w;
+    const int h = g.H - y0 < th ? g.H - y0 : th;
+    uint16_t *mdl = p0s + lane;
+
+    const int k = (plane == 0 ? 0 : Tc) + tile;
+    RcIn in{mbuf + (size_t)img * (g.HW / 8), 7 + 32ll * Tc + 8ll * offsets[(size_t)img * 2 * TcM + k],
+            sizes[(size_t)img * 2 * TcM + k], 0};
+    uint32_t range = 0xFFFFFFFFu, code = 0;
+    for (int i = 0; i < 5; i++) code = (code << 8) | in.next();
+    uint32_t *plane_out = plane == 0 ? eta_bits : map_bits;
+    uint32_t p1[NW], p2[NW];
+#pragma unroll
+    for (int q = 0; q < NW; q++) { p1[q] = 0; p2[q] = 0; }
+    for (int y = 0; y < h; y++) {
+        uint32_t cw[NW];
+        uint32_t hist2 = 0;
+        uint32_t ctx = rows_ctx<NW, 0>(p1, p2, 0);
+        uint32_t p = mdl[ctx * 32];
+        uint32_t *orow = plane_out + (((size_t)img * g.HW + (size_t)(y0 + y) * g.W + x0) >> 5);
+        dec_row<NW, 0>(in, range, code, mdl, cw, p1, p2, ctx, p, hist2, orow);
+#pragma unroll
+        for (int q = 0; q < NW; q++) { p2[q] = p1[q]; p1[q] = cw[q]; }
+    }
+}
+
 // ---------------------------------------------------------------------------- launchers
 int lmr_tile_cap_host(int t, int H, int W) { return lmr_tile_cap(t, H, W); }
 
@@ -495,6 +742,12 @@ void lmr_set_smem_attrs() {
     if (done) return;
     cudaFuncSetAttribute(coder_encode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)coder_smem());
     cudaFuncSetAttribute(coder_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)coder_smem());
+    cudaFuncSetAttribute(coder_encode_fast_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)coder_smem());
+    cudaFuncSetAttribute(coder_encode_fast_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)coder_smem());
+    cudaFuncSetAttribute(coder_encode_fast_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)coder_smem());
+    cudaFuncSetAttribute(coder_decode_fast_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)coder_smem());
+    cudaFuncSetAttribute(coder_decode_fast_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)coder_smem());
+    cudaFuncSetAttribute(coder_decode_fast_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)coder_smem());
     done = true;
 }
 
@@ -508,7 +761,12 @@ void launch_coder_encode(const Geo &g, int wave, const uint8_t *ceta, const LmrP
     const int Tc = lmr_tile_count(g.H, g.W, g.tile_log2);
     const long long total = (long long)g.B * (wave == 0 ? 2 : 1) * Tc;
     const unsigned grid = (unsigned)((total + kCoderThreads - 1) / kCoderThreads);
-    coder_encode_kernel<<<grid, kCoderThreads, coder_smem(), st>>>(g, wave, ceta, plan, streams, sizes);
+    switch (lmr_tile_side(g.tile_log2, g.W)) {
+        case 32: coder_encode_fast_kernel<1><<<grid, kCoderThreads, coder_smem(), st>>>(g, wave, ceta, plan, streams, sizes); break;
+        case 64: coder_encode_fast_kernel<2><<<grid, kCoderThreads, coder_smem(), st>>>(g, wave, ceta, plan, streams, sizes); break;
+        case 128: coder_encode_fast_kernel<4><<<grid, kCoderThreads, coder_smem(), st>>>(g, wave, ceta, plan, streams, sizes); break;
+        default: coder_encode_kernel<<<grid, kCoderThreads, coder_smem(), st>>>(g, wave, ceta, plan, streams, sizes);
+    }
 }
 
 void launch_lmr_fit(const Geo &g, int wave, const int32_t *sizes, LmrPlan *plan, int32_t *offsets, cudaStream_t st) {
@@ -534,8 +792,17 @@ void launch_lmr_decode(const Geo &g, bool want_eta, const uint8_t *marked, uint8
         g.HW, g.B, marked, mbuf);
     lmr_header_kernel<<<g.B, 32, 0, st>>>(g, mbuf, lmr_b, lmr_t, offsets, sizes, status, msg_bits_out);
     const long long total = (long long)g.B * (want_eta ? 2 : 1) * g.ntiles_coder;
-    coder_decode_kernel<<<(unsigned)((total + kCoderThreads - 1) / kCoderThreads), kCoderThreads, coder_smem(), st>>>(
-        g, want_eta ? 1 : 0, mbuf, lmr_b, lmr_t, offsets, sizes, eta_bits, map_bits);
+    const unsigned dgrid = (unsigned)((total + kCoderThreads - 1) / kCoderThreads);
+    switch (lmr_tile_side(g.tile_log2, g.W)) {
+        case 32: coder_decode_fast_kernel<1><<<dgrid, kCoderThreads, coder_smem(), st>>>(
+                     g, want_eta ? 1 : 0, mbuf, lmr_b, lmr_t, offsets, sizes, eta_bits, map_bits); break;
+        case 64: coder_decode_fast_kernel<2><<<dgrid, kCoderThreads, coder_smem(), st>>>(
+                     g, want_eta ? 1 : 0, mbuf, lmr_b, lmr_t, offsets, sizes, eta_bits, map_bits); break;
+        case 128: coder_decode_fast_kernel<4><<<dgrid, kCoderThreads, coder_smem(), st>>>(
+                     g, want_eta ? 1 : 0, mbuf, lmr_b, lmr_t, offsets, sizes, eta_bits, map_bits); break;
+        default: coder_decode_kernel<<<dgrid, kCoderThreads, coder_smem(), st>>>(
+                     g, want_eta ? 1 : 0, mbuf, lmr_b, lmr_t, offsets, sizes, eta_bits, map_bits);
+    }
 }
 
 }  // namespace mmsb
