@@ -341,7 +341,7 @@ __global__ void __launch_bounds__(kScanThreads, 5) scan_kernel(Geo g, const uint
         const long long fend = hie - base;
         uint8_t *dst = out + (size_t)img * g.HW + p0;
         MMSB_BP_SWITCH(bp, METHOD, ({
-            _Pragma("unroll 1")
+            _Pragma("unroll")
             for (int r = 0; r < kScanRounds; r++) {
                 const int q = r * kScanThreads + tid;
                 if (16 * q >= cpx) continue;
@@ -367,7 +367,7 @@ __global__ void __launch_bounds__(kScanThreads, 5) scan_kernel(Geo g, const uint
         for (int t = tid; t < nblk * 16 + 1; t += kScanThreads) kbuf[t] = 0;
         __syncthreads();
         MMSB_BP_SWITCH(bp, METHOD, ({
-            _Pragma("unroll 1")
+            _Pragma("unroll")
             for (int r = 0; r < kScanRounds; r++) {
                 if (!m[r]) continue;
                 const uint4 u = spx[r * kScanThreads + tid];
