@@ -106,6 +106,18 @@ mmsb_status mmsb_receiver_recover(const mmsb_shape *shape, const uint8_t *marked
                                   uint8_t *recovered, int32_t *img_status, void *ws, size_t ws_bytes,
                                   void *stream);
 
+/*
+ * Receiver holding both keys (EMR: P:842-843; LMR: P:1066-1067): extraction
+ * with K2 and recovery with K1 in one call.  Outputs are those of mmsb_receiver_extract and
+ * mmsb_receiver_recover on the same arguments; LMR decodes the coded maps (eta and the location
+ * map) from the MSB plane once for both steps instead of once per call.  img_status: the
+ * extraction's status if it is not OK (INTEGRITY, FORMAT, BADCASE, E_INVAL region), else the
+ * recovery's.
+ */
+mmsb_status mmsb_receiver_both(const mmsb_shape *shape, const uint8_t *marked, const uint8_t *k1, const uint8_t *k2,
+                               uint8_t *msg_out, int64_t stride_bytes, int64_t *msg_bits_out, uint8_t *recovered,
+                               int32_t *img_status, void *ws, size_t ws_bytes, void *stream);
+
 /* Per-image sum of squared differences (int64) of two image batches (P:746 PSNR numerator). */
 mmsb_status mmsb_stats(const mmsb_shape *shape, const uint8_t *original, const uint8_t *recovered,
                        int64_t *sse_out, void *stream);

@@ -548,6 +548,16 @@ __global__ void __launch_bounds__(256) stats_kernel(long long HW, const uint8_t 
     }
 }
 
+// both-keys receiver: the image's status is the extraction's unless that was OK
+__global__ void status_merge_kernel(int B, const int32_t *__restrict__ second, int32_t *__restrict__ status) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < B && status[i] == 0) status[i] = second[i];
+}
+
+void launch_status_merge(int B, const int32_t *second, int32_t *status, cudaStream_t st) {
+    status_merge_kernel<<<(B + 255) / 256, 256, 0, st>>>(B, second, status);
+}
+
 void launch_stats(long long HW, int B, const uint8_t *a, const uint8_t *b, int64_t *sse, cudaStream_t st) {
     const long long n16 = HW / 16;
     int bx = (int)((n16 + 256 * 8 - 1) / (256 * 8));

@@ -59,7 +59,7 @@ static size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
 struct Layout {
     size_t s, rec, pyr, hist, kdone, rstate, tile_zero_end, ragg, rinc;   // fused tile kernels
     size_t states, parts, hdr, scan_zero_end;                                  // scan kernels
-    size_t ceta, eta_bits, map_bits, lmr_b, lmr_t, plan, streams, sizes, offsets, mbuf, total;
+    size_t ceta, eta_bits, map_bits, lmr_b, lmr_t, plan, streams, sizes, offsets, mbuf, rstat, total;
 };
 
 static Layout layout(const Geo &g) {
@@ -91,6 +91,7 @@ static Layout layout(const Geo &g) {
     L.sizes = o; o = align256(o + (lmr ? B * 2 * Tc * 4 : 0));
     L.offsets = o; o = align256(o + (lmr ? B * 2 * Tc * 4 : 0));
     L.mbuf = o; o = align256(o + (lmr ? B * g.HW / 8 + 16 : 0));
+    L.rstat = o; o = align256(o + B * 4);
     L.total = o;
     return L;
 }
@@ -239,6 +240,36 @@ mmsb_status mmsb_receiver_recover(const mmsb_shape *shape, const uint8_t *marked
         launch_recover(g, marked, k1, tile_ws(L, ws), at<uint32_t>(ws, L.eta_bits), at<uint32_t>(ws, L.map_bits),
                        at<int32_t>(ws, L.lmr_b), recovered, img_status, st);
     });
+    return check_launch();
+}
+
+mmsb_status mmsb_receiver_both(const mmsb_shape *shape, const uint8_t *marked, const uint8_t *k1, const uint8_t *k2,
+                               uint8_t *msg_out, int64_t stride_bytes, int64_t *msg_bits_out, uint8_t *recovered,
+                               int32_t *img_status, void *ws, size_t ws_bytes, void *stream) {
+    Geo g;
+    if (!geo_of(shape, &g) || !marked || !k1 || !k2 || !msg_out || !msg_bits_out || !recovered || !img_status || !ws)
+        return MMSB_E_INVAL;
+    if (stride_bytes <= 0 || stride_bytes % 16) return MMSB_E_INVAL;
+    const Layout L = layout(g);
+    if (ws_bytes < L.total) return MMSB_E_INVAL;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    int32_t *rstat = at<int32_t>(ws, L.rstat);
+    if (cudaMemsetAsync(at<char>(ws, L.states), 0, L.scan_zero_end - L.states, st) != cudaSuccess) return MMSB_E_CUDA;
+    if (cudaMemsetAsync(rstat, 0, (size_t)g.B * 4, st) != cudaSuccess) return MMSB_E_CUDA;
+    // LMR: the coded maps (eta and the location map) are decoded once for both parties' steps
+    if (g.method == 1) lmr_decode_all(g, L, true, marked, ws, img_status, msg_bits_out, st);
+    ScanWS sw{at<unsigned long long>(ws, L.states), at<unsigned long long>(ws, L.parts), at<uint32_t>(ws, L.hdr)};
+    run_kernel(K_EXTRACT, st, (long long)g.B * g.HW, [&] {
+        launch_scan(g, false, marked, nullptr, k2, nullptr, nullptr, stride_bytes, msg_out, msg_bits_out,
+                    img_status, sw, at<uint32_t>(ws, L.map_bits), at<int32_t>(ws, L.lmr_b), st);
+    }, 2);
+    if (cudaMemsetAsync(at<char>(ws, L.pyr), 0, L.tile_zero_end - L.pyr, st) != cudaSuccess) return MMSB_E_CUDA;
+    run_kernel(K_RECOVER, st, (long long)g.B * g.HW, [&] {
+        launch_recover(g, marked, k1, tile_ws(L, ws), at<uint32_t>(ws, L.eta_bits), at<uint32_t>(ws, L.map_bits),
+                       at<int32_t>(ws, L.lmr_b), recovered, rstat, st);
+    });
+    g_launches += 1;
+    launch_status_merge(g.B, rstat, img_status, st);
     return check_launch();
 }
 

@@ -47,6 +47,8 @@ def lib():
         L.mmsb_receiver_extract.argtypes = [sp, vp, vp, vp, C.c_int64, vp, vp, vp, C.c_size_t, vp]
         L.mmsb_receiver_recover.restype = C.c_int
         L.mmsb_receiver_recover.argtypes = [sp, vp, vp, vp, vp, vp, C.c_size_t, vp]
+        L.mmsb_receiver_both.restype = C.c_int
+        L.mmsb_receiver_both.argtypes = [sp, vp, vp, vp, vp, C.c_int64, vp, vp, vp, vp, C.c_size_t, vp]
         L.mmsb_stats.restype = C.c_int
         L.mmsb_stats.argtypes = [sp, vp, vp, vp, vp]
         L.mmsb_der_psnr_host.restype = None
@@ -158,6 +160,22 @@ def recover(method: int, marked: torch.Tensor, k1: torch.Tensor, ws: Workspace |
                                      ws.nbytes, _stream())
     _check(rc, "mmsb_receiver_recover")
     return rec, st
+
+
+def receive_both(method: int, marked: torch.Tensor, k1: torch.Tensor, k2: torch.Tensor, stride: int,
+                 ws: Workspace | None = None, tile_log2: int = 7, msg_out: torch.Tensor | None = None,
+                 rec_out: torch.Tensor | None = None):
+    """Receiver with both keys: returns (msg_bytes, msg_bits, recovered, status) -- mmsb_receiver_both."""
+    B, H, W = marked.shape
+    ws = _ws(ws, method, B, H, W, tile_log2, marked.device)
+    msg = msg_out if msg_out is not None else torch.zeros(B, stride, dtype=torch.uint8, device=marked.device)
+    rec = rec_out if rec_out is not None else torch.empty_like(marked)
+    nb = torch.empty(B, dtype=torch.int64, device=marked.device)
+    st = torch.empty(B, dtype=torch.int32, device=marked.device)
+    rc = lib().mmsb_receiver_both(C.byref(ws.shape), _ptr(marked), _ptr(k1), _ptr(k2), _ptr(msg), stride, _ptr(nb),
+                                  _ptr(rec), _ptr(st), _ptr(ws.buf), ws.nbytes, _stream())
+    _check(rc, "mmsb_receiver_both")
+    return msg, nb, rec, st
 
 
 def stats(original: torch.Tensor, recovered: torch.Tensor, out: torch.Tensor | None = None):
