@@ -69,6 +69,10 @@ def lib():
                 "orc_sse": (C.c_int64, [u8p, u8p, C.c_int64]),
                 "orc_der_psnr": (None, [C.c_int, C.c_int, C.c_int64, C.c_int64,
                                         C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+                "orc_entropy": (C.c_double, [u8p, C.c_int64]),
+                "orc_chi2": (C.c_double, [u8p, C.c_int64]),
+                "orc_npcr_uaci": (None, [u8p, u8p, C.c_int64, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+                "orc_ssim": (C.c_double, [u8p, u8p, C.c_int, C.c_int]),
             }
             for name, (res, args) in sig.items():
                 f = getattr(L, name)
@@ -233,3 +237,27 @@ def der_psnr(M: int, N: int, capacity_bits: int, sse_: int):
     d, p = C.c_double(0), C.c_double(0)
     lib().orc_der_psnr(M, N, capacity_bits, sse_, C.byref(d), C.byref(p))
     return d.value, p.value
+
+
+def entropy(img: np.ndarray) -> float:
+    img = _u8(img)
+    return lib().orc_entropy(_p(img), img.size)
+
+
+def chi2(img: np.ndarray) -> float:
+    img = _u8(img)
+    return lib().orc_chi2(_p(img), img.size)
+
+
+def npcr_uaci(a: np.ndarray, b: np.ndarray):
+    a, b = _u8(a), _u8(b)
+    assert a.shape == b.shape
+    n_, u_ = C.c_double(0), C.c_double(0)
+    lib().orc_npcr_uaci(_p(a), _p(b), a.size, C.byref(n_), C.byref(u_))
+    return n_.value, u_.value
+
+
+def ssim(a: np.ndarray, b: np.ndarray) -> float:
+    a, b = _u8(a), _u8(b)
+    assert a.shape == b.shape
+    return lib().orc_ssim(_p(a), _p(b), a.shape[0], a.shape[1])

@@ -729,3 +729,80 @@ void orc_der_psnr(int M, int N, int64_t capacity_bits, int64_t sse, double *der,
     *der = (double)capacity_bits / MN;
     *psnr = sse == 0 ? INFINITY : 10.0 * log10(255.0 * 255.0 * MN / (double)sse);
 }
+
+/* ===================================================================================
+ * Security / quality statistics (P:1437-1467 Shannon entropy, chi^2, NPCR, UACI; SSIM
+ * P:1071, P:1235 with the window of S:524).  Plain definitions, fp64.
+ * =================================================================================== */
+static void histogram(const uint8_t *img, int64_t n, int64_t h[256])
+{
+    for (int i = 0; i < 256; i++) h[i] = 0;
+    for (int64_t k = 0; k < n; k++) h[img[k]]++;
+}
+
+double orc_entropy(const uint8_t *img, int64_t n)
+{
+    int64_t h[256];
+    histogram(img, n, h);
+    double H = 0.0;
+    for (int i = 0; i < 256; i++) {
+        if (h[i] == 0) continue;                       /* 0 log 0 = 0 */
+        double P = (double)h[i] / (double)n;
+        H -= P * log2(P);
+    }
+    return H;
+}
+
+double orc_chi2(const uint8_t *img, int64_t n)
+{
+    int64_t h[256];
+    histogram(img, n, h);
+    double s = 0.0;
+    for (int i = 0; i < 256; i++) {
+        double d = (double)h[i] / (double)n - 1.0 / 256.0;
+        s += d * d;
+    }
+    return 256.0 * (double)n * s;
+}
+
+void orc_npcr_uaci(const uint8_t *a, const uint8_t *b, int64_t n, double *npcr, double *uaci)
+{
+    int64_t diff = 0, absum = 0;
+    for (int64_t k = 0; k < n; k++) {
+        if (a[k] != b[k]) diff++;
+        absum += a[k] > b[k] ? a[k] - b[k] : b[k] - a[k];
+    }
+    *npcr = 100.0 * (double)diff / (double)n;
+    *uaci = 100.0 * (double)absum / (255.0 * (double)n);
+}
+
+double orc_ssim(const uint8_t *a, const uint8_t *b, int M, int N)
+{
+    const double C1 = (0.01 * 255.0) * (0.01 * 255.0), C2 = (0.03 * 255.0) * (0.03 * 255.0);
+    double w[11][11], tot = 0.0;
+    for (int i = 0; i < 11; i++)
+        for (int j = 0; j < 11; j++) {
+            w[i][j] = exp(-((i - 5) * (i - 5) + (j - 5) * (j - 5)) / (2.0 * 1.5 * 1.5));
+            tot += w[i][j];
+        }
+    for (int i = 0; i < 11; i++)
+        for (int j = 0; j < 11; j++) w[i][j] /= tot;
+    if (M < 11 || N < 11) return 0.0;
+    double sum = 0.0;
+    for (int y = 0; y + 11 <= M; y++)
+        for (int x = 0; x + 11 <= N; x++) {
+            double ma = 0, mb = 0, saa = 0, sbb = 0, sab = 0;
+            for (int i = 0; i < 11; i++)
+                for (int j = 0; j < 11; j++) {
+                    double va = a[(size_t)(y + i) * N + x + j], vb = b[(size_t)(y + i) * N + x + j];
+                    ma += w[i][j] * va;
+                    mb += w[i][j] * vb;
+                    saa += w[i][j] * va * va;
+                    sbb += w[i][j] * vb * vb;
+                    sab += w[i][j] * va * vb;
+                }
+            double va2 = saa - ma * ma, vb2 = sbb - mb * mb, cov = sab - ma * mb;
+            sum += ((2 * ma * mb + C1) * (2 * cov + C2)) / ((ma * ma + mb * mb + C1) * (va2 + vb2 + C2));
+        }
+    return sum / ((double)(M - 10) * (double)(N - 10));
+}

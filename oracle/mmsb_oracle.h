@@ -79,6 +79,17 @@ int orc_capacity(int method, const uint8_t *marked, int M, int N, int tile_log2,
 
 /* ---- statistics (P:630 DER, P:746 PSNR; Q23) ---- */
 int64_t orc_sse(const uint8_t *a, const uint8_t *b, int64_t n);
+
+/* ---- security / quality statistics ---- */
+/* Shannon entropy H = -sum P(a_i) log2 P(a_i) over the 256 grey levels */
+double orc_entropy(const uint8_t *img, int64_t n);
+/* chi^2 = 256 (h w) sum (P(a_i) - 1/256)^2 */
+double orc_chi2(const uint8_t *img, int64_t n);
+/* NPCR = 100 * #{a != b} / n (reading Q26: sigma = 1 where the pixels DIFFER), UACI = 100 * mean(|a-b|) / 255 */
+void orc_npcr_uaci(const uint8_t *a, const uint8_t *b, int64_t n, double *npcr, double *uaci);
+/* mean local SSIM, 11x11 Gaussian window sigma 1.5 (normalised), K1 = 0.01, K2 = 0.03, L = 255,
+ * over the windows lying fully inside the image ("valid" positions, reading in DESIGN.md) */
+double orc_ssim(const uint8_t *a, const uint8_t *b, int M, int N);
 void orc_der_psnr(int M, int N, int64_t capacity_bits, int64_t sse, double *der, double *psnr);
 
 #endif
