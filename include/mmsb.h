@@ -127,6 +127,27 @@ mmsb_status mmsb_stats(const mmsb_shape *shape, const uint8_t *original, const u
 void mmsb_der_psnr_host(int32_t batch, int32_t height, int32_t width, const int64_t *capacity_bits,
                         const int64_t *sse, double *der_out, double *psnr_out);
 
+/*
+ * The paper's security / quality statistics.
+ * Device arrays in, device arrays out, asynchronous on `stream`; integer counts are exact, SSIM is
+ * computed in fp64.  The host functions turn the counts into the paper's quantities.
+ *   mmsb_histogram   hist_out [B][256] int64: grey-level counts of each image (overwritten)
+ *   mmsb_diff_stats  per image: sse = sum (a-b)^2, ndiff = #{a != b}, absdiff = sum |a-b|
+ *   mmsb_ssim        ssim_out [B] double: mean local SSIM, 11x11 Gaussian window sigma 1.5,
+ *                    K1 = 0.01, K2 = 0.03, L = 255, over the (H-10)(W-10) windows inside
+ *                    the image (reading in DESIGN.md §3)
+ */
+mmsb_status mmsb_histogram(const mmsb_shape *shape, const uint8_t *images, int64_t *hist_out, void *stream);
+mmsb_status mmsb_diff_stats(const mmsb_shape *shape, const uint8_t *a, const uint8_t *b, int64_t *sse_out,
+                            int64_t *ndiff_out, int64_t *absdiff_out, void *stream);
+mmsb_status mmsb_ssim(const mmsb_shape *shape, const uint8_t *a, const uint8_t *b, double *ssim_out, void *stream);
+/* HOST: Shannon entropy H = -sum P log2 P and chi^2 = 256 (H W) sum (P - 1/256)^2
+ * from the histograms; NPCR = 100 ndiff / (H W), UACI = 100 absdiff / (255 H W) (Q26) */
+void mmsb_entropy_chi2_host(int32_t batch, int32_t height, int32_t width, const int64_t *hist, double *entropy_out,
+                            double *chi2_out);
+void mmsb_npcr_uaci_host(int32_t batch, int32_t height, int32_t width, const int64_t *ndiff, const int64_t *absdiff,
+                         double *npcr_out, double *uaci_out);
+
 const char *mmsb_status_string(mmsb_status status);
 
 /* Number of kernels the library launched since load (for the bench's gpu_launches claim). */

@@ -292,6 +292,63 @@ void mmsb_der_psnr_host(int32_t batch, int32_t height, int32_t width, const int6
     }
 }
 
+mmsb_status mmsb_histogram(const mmsb_shape *shape, const uint8_t *images, int64_t *hist_out, void *stream) {
+    Geo g;
+    if (!geo_of(shape, &g) || !images || !hist_out) return MMSB_E_INVAL;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (cudaMemsetAsync(hist_out, 0, (size_t)g.B * 256 * 8, st) != cudaSuccess) return MMSB_E_CUDA;
+    g_launches += 1;
+    launch_histogram(g.HW, g.B, images, hist_out, st);
+    return check_launch();
+}
+
+mmsb_status mmsb_diff_stats(const mmsb_shape *shape, const uint8_t *a, const uint8_t *b, int64_t *sse_out,
+                            int64_t *ndiff_out, int64_t *absdiff_out, void *stream) {
+    Geo g;
+    if (!geo_of(shape, &g) || !a || !b || !sse_out || !ndiff_out || !absdiff_out) return MMSB_E_INVAL;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    for (int64_t *p : {sse_out, ndiff_out, absdiff_out})
+        if (cudaMemsetAsync(p, 0, (size_t)g.B * 8, st) != cudaSuccess) return MMSB_E_CUDA;
+    g_launches += 1;
+    launch_diff_stats(g.HW, g.B, a, b, sse_out, ndiff_out, absdiff_out, st);
+    return check_launch();
+}
+
+mmsb_status mmsb_ssim(const mmsb_shape *shape, const uint8_t *a, const uint8_t *b, double *ssim_out, void *stream) {
+    Geo g;
+    if (!geo_of(shape, &g) || !a || !b || !ssim_out) return MMSB_E_INVAL;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (cudaMemsetAsync(ssim_out, 0, (size_t)g.B * 8, st) != cudaSuccess) return MMSB_E_CUDA;
+    g_launches += 2;
+    launch_ssim(g.B, g.H, g.W, a, b, ssim_out, st);
+    return check_launch();
+}
+
+void mmsb_entropy_chi2_host(int32_t batch, int32_t height, int32_t width, const int64_t *hist, double *entropy_out,
+                            double *chi2_out) {
+    const double n = (double)height * (double)width;
+    for (int i = 0; i < batch; i++) {
+        double H = 0.0, s = 0.0;
+        for (int v = 0; v < 256; v++) {
+            const double P = (double)hist[(size_t)i * 256 + v] / n;
+            if (P > 0) H -= P * std::log2(P);
+            const double d = P - 1.0 / 256.0;
+            s += d * d;
+        }
+        if (entropy_out) entropy_out[i] = H;
+        if (chi2_out) chi2_out[i] = 256.0 * n * s;
+    }
+}
+
+void mmsb_npcr_uaci_host(int32_t batch, int32_t height, int32_t width, const int64_t *ndiff, const int64_t *absdiff,
+                         double *npcr_out, double *uaci_out) {
+    const double n = (double)height * (double)width;
+    for (int i = 0; i < batch; i++) {
+        if (npcr_out) npcr_out[i] = 100.0 * (double)ndiff[i] / n;
+        if (uaci_out) uaci_out[i] = 100.0 * (double)absdiff[i] / (255.0 * n);
+    }
+}
+
 const char *mmsb_status_string(mmsb_status s) {
     switch (s) {
         case MMSB_OK: return "ok";

@@ -56,6 +56,10 @@ void launch_recover(const Geo &g, const uint8_t *marked, const uint8_t *keys, co
 void launch_scan(const Geo &g, bool embed, const uint8_t *in, uint8_t *out, const uint8_t *keys, const uint8_t *msg,
                  const int64_t *msg_bits, long long stride, uint8_t *msg_out, int64_t *msg_bits_out, int32_t *status,
                  const ScanWS &ws, const uint32_t *map_bits, const int32_t *lmr_b, cudaStream_t st);
+void launch_histogram(long long HW, int B, const uint8_t *img, int64_t *hist, cudaStream_t st);
+void launch_diff_stats(long long HW, int B, const uint8_t *a, const uint8_t *b, int64_t *sse, int64_t *ndiff,
+                       int64_t *absd, cudaStream_t st);
+void launch_ssim(int B, int H, int W, const uint8_t *a, const uint8_t *b, double *ssim, cudaStream_t st);
 void launch_status_merge(int B, const int32_t *second, int32_t *status, cudaStream_t st);
 void launch_stats(long long HW, int B, const uint8_t *a, const uint8_t *b, int64_t *sse, cudaStream_t st);
 

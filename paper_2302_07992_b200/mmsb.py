@@ -49,6 +49,16 @@ def lib():
         L.mmsb_receiver_recover.argtypes = [sp, vp, vp, vp, vp, vp, C.c_size_t, vp]
         L.mmsb_receiver_both.restype = C.c_int
         L.mmsb_receiver_both.argtypes = [sp, vp, vp, vp, vp, C.c_int64, vp, vp, vp, vp, C.c_size_t, vp]
+        L.mmsb_histogram.restype = C.c_int
+        L.mmsb_histogram.argtypes = [sp, vp, vp, vp]
+        L.mmsb_diff_stats.restype = C.c_int
+        L.mmsb_diff_stats.argtypes = [sp, vp, vp, vp, vp, vp, vp]
+        L.mmsb_ssim.restype = C.c_int
+        L.mmsb_ssim.argtypes = [sp, vp, vp, vp, vp]
+        L.mmsb_entropy_chi2_host.restype = None
+        L.mmsb_entropy_chi2_host.argtypes = [C.c_int32, C.c_int32, C.c_int32, vp, vp, vp]
+        L.mmsb_npcr_uaci_host.restype = None
+        L.mmsb_npcr_uaci_host.argtypes = [C.c_int32, C.c_int32, C.c_int32, vp, vp, vp, vp]
         L.mmsb_stats.restype = C.c_int
         L.mmsb_stats.argtypes = [sp, vp, vp, vp, vp]
         L.mmsb_der_psnr_host.restype = None
@@ -198,3 +208,50 @@ def der_psnr(H: int, W: int, capacity_bits, sse):
     psnr = np.zeros(len(cap), np.float64)
     lib().mmsb_der_psnr_host(len(cap), H, W, cap.ctypes.data, s.ctypes.data, der.ctypes.data, psnr.ctypes.data)
     return der, psnr
+
+
+# ---------------------------------------------------------------- the paper's statistics (NEXT 2)
+def histogram(images: torch.Tensor, out: torch.Tensor | None = None):
+    """[B, 256] int64 grey-level counts -- mmsb_histogram."""
+    B, H, W = images.shape
+    h = out if out is not None else torch.empty(B, 256, dtype=torch.int64, device=images.device)
+    _check(lib().mmsb_histogram(C.byref(_shape(EMR, B, H, W)), _ptr(images), _ptr(h), _stream()), "mmsb_histogram")
+    return h
+
+
+def diff_stats(a: torch.Tensor, b: torch.Tensor):
+    """(sse, ndiff, absdiff) int64 per image -- mmsb_diff_stats."""
+    B, H, W = a.shape
+    sse, nd, ad = (torch.empty(B, dtype=torch.int64, device=a.device) for _ in range(3))
+    _check(lib().mmsb_diff_stats(C.byref(_shape(EMR, B, H, W)), _ptr(a), _ptr(b), _ptr(sse), _ptr(nd), _ptr(ad),
+                                 _stream()), "mmsb_diff_stats")
+    return sse, nd, ad
+
+
+def ssim(a: torch.Tensor, b: torch.Tensor):
+    """[B] float64 mean windowed SSIM -- mmsb_ssim."""
+    B, H, W = a.shape
+    out = torch.empty(B, dtype=torch.float64, device=a.device)
+    _check(lib().mmsb_ssim(C.byref(_shape(EMR, B, H, W)), _ptr(a), _ptr(b), _ptr(out), _stream()), "mmsb_ssim")
+    return out
+
+
+def entropy_chi2(H: int, W: int, hist):
+    """Host entropy / chi^2 from [B, 256] counts (mmsb_entropy_chi2_host)."""
+    import numpy as np
+
+    h = np.ascontiguousarray(np.asarray(hist, dtype=np.int64))
+    ent, chi = np.zeros(h.shape[0]), np.zeros(h.shape[0])
+    lib().mmsb_entropy_chi2_host(h.shape[0], H, W, h.ctypes.data, ent.ctypes.data, chi.ctypes.data)
+    return ent, chi
+
+
+def npcr_uaci(H: int, W: int, ndiff, absdiff):
+    """Host NPCR / UACI in percent (mmsb_npcr_uaci_host)."""
+    import numpy as np
+
+    nd = np.ascontiguousarray(np.asarray(ndiff, dtype=np.int64))
+    ad = np.ascontiguousarray(np.asarray(absdiff, dtype=np.int64))
+    npcr, uaci = np.zeros(len(nd)), np.zeros(len(nd))
+    lib().mmsb_npcr_uaci_host(len(nd), H, W, nd.ctypes.data, ad.ctypes.data, npcr.ctypes.data, uaci.ctypes.data)
+    return npcr, uaci
