@@ -44,6 +44,7 @@ def parse():
     ap.add_argument("--e2e-chunks", type=int, default=None, help="sub-batches of the pipelined e2e leg")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-security", action="store_true", help="skip the untimed statistics table")
     return ap.parse_args()
 
 
@@ -382,6 +383,30 @@ def run_ours(args):
     ok_e2e = bool(np.array_equal(hREC.numpy(), rec.cpu().numpy())) and bool(
         np.array_equal(hSSE.numpy(), SSE.cpu().numpy()))
 
+    # the paper's security / quality table (Tab. analysis, Tab. EMR_results) on
+    # this rank's batch, outside the timed region: entropy / chi^2 of I, I_e, I_e'; NPCR / UACI and
+    # PSNR of I vs I_e and I vs I_e'; SSIM of I vs I' (all through the library's statistics calls)
+    security = None
+    if rank == 0 and not args.no_security:
+        def _mean(x):
+            return float(np.mean(x))
+
+        sec = {}
+        for name, X in (("I", I), ("I_e", enc), ("I_e_marked", marked)):
+            ent, chi = G.entropy_chi2(H, W, G.histogram(X).cpu().numpy())
+            sec[f"entropy_{name}"] = _mean(ent)
+            sec[f"chi2_{name}"] = _mean(chi)
+        for name, X in (("I_e", enc), ("I_e_marked", marked)):
+            sse_, nd, ad = (t.cpu().numpy() for t in G.diff_stats(I, X))
+            npcr, uaci = G.npcr_uaci(H, W, nd, ad)
+            _, psnr = G.der_psnr(H, W, np.zeros_like(sse_), sse_)
+            sec[f"npcr_I_vs_{name}"], sec[f"uaci_I_vs_{name}"] = _mean(npcr), _mean(uaci)
+            sec[f"psnr_I_vs_{name}"] = _mean(psnr)
+        ss = G.ssim(I, rec).cpu().numpy()
+        sec["ssim_I_vs_recovered_mean"], sec["ssim_I_vs_recovered_min"] = _mean(ss), float(ss.min())
+        sec["note"] = "means over this rank's batch; synthetic images (the paper's Lena / BOWS-2 are not available)"
+        security = sec
+
     if rank == 0:
         peaks = load_peaks()
         roof = roofline(prof, peaks, B, HW, cap, method)
@@ -400,7 +425,8 @@ def run_ours(args):
                 "checks": {"payload_round_trip": ok_rt, "e2e_matches_device": ok_e2e,
                            "statuses_ok": bool((st0 == 0).all().item())},
                 "mean_der_bpp": float(cap.mean() / HW), "gen_s": gen_s,
-                "stats": P.aggregate(gathered[0] if world > 1 else P.make_records(last[0], last[1], SSE, last[2]), H, W)}
+                "stats": P.aggregate(gathered[0] if world > 1 else P.make_records(last[0], last[1], SSE, last[2]), H, W),
+                "security": security}
         if world == 1 and not args.no_cpu_baseline:
             import oracle as O
 
