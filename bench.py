@@ -45,6 +45,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-security", action="store_true", help="skip the untimed statistics table")
+    ap.add_argument("--lmr-emin", type=int, default=0, help="LMR rotation schedule {2^e..} (Tab. LMR_block_size)")
     return ap.parse_args()
 
 
@@ -65,7 +66,8 @@ def config_json(args, cfg, method, B, world):
             "height": cfg["H"], "width": cfg["W"], "parallelism": f"dp{world} (image shards, weak scaling)",
             "l2": "inputs larger than L2 (batch bytes >> 126 MB); no flush needed" if B * cfg["H"] * cfg["W"] > 126e6
             else "inputs smaller than L2",
-            "keys": "ChaCha20 K = k128||k128 per image (reading Q13)"}
+            "keys": "ChaCha20 K = k128||k128 per image (reading Q13)",
+            "lmr_emin": (args.lmr_emin or 4) if method == "lmr" else None}
 
 
 # ------------------------------------------------------------------------------ clocks
@@ -244,7 +246,7 @@ def run_ours(args):
     I = torch.from_numpy(imgs).to(dev)
     K1 = torch.from_numpy(k1).to(dev)
     K2 = torch.from_numpy(k2).to(dev)
-    ws = G.Workspace(mid, B, H, W, device=dev)
+    ws = G.Workspace(mid, B, H, W, device=dev, lmr_emin=args.lmr_emin)
     enc = torch.empty_like(I)
     marked = torch.empty_like(I)
     rec = torch.empty_like(I)
@@ -326,7 +328,7 @@ def run_ours(args):
     class Lane:
         def __init__(self):
             self.stream = torch.cuda.Stream(device=dev)
-            self.ws = G.Workspace(mid, sub, H, W, device=dev)
+            self.ws = G.Workspace(mid, sub, H, W, device=dev, lmr_emin=args.lmr_emin)
             self.I = torch.empty(sub, H, W, dtype=torch.uint8, device=dev)
             self.K1 = torch.empty(sub, 32, dtype=torch.uint8, device=dev)
             self.K2 = torch.empty(sub, 32, dtype=torch.uint8, device=dev)

@@ -53,6 +53,9 @@ typedef struct {
     int32_t height;      /* M (power of two, 16..32768)                                        */
     int32_t width;       /* N (power of two, 16..32768)                                        */
     int32_t tile_log2;   /* LMR map-coder tile side 2^t, t in [3, 7] (0 = default 7)           */
+    int32_t lmr_emin;    /* LMR rotation blocks {2^e_min .. 2^e_max}: 0 = the paper's e_min = 4;
+                            1..3 = the schedules of Tab. LMR_block_size.  Shared
+                            protocol knowledge like the method (not stored in the image).  EMR: 1.  */
 } mmsb_shape;
 
 /* Bytes of device workspace the four calls need for this shape. 0 if the shape is invalid. */

@@ -65,6 +65,8 @@ def lib():
                 "orc_hide": (C.c_int, [C.c_int, u8p, C.c_int, C.c_int, C.c_int, u8p, u8p, C.c_int64, u8p]),
                 "orc_extract": (C.c_int, [C.c_int, u8p, C.c_int, C.c_int, C.c_int, u8p, u8p, C.c_int64, i64p]),
                 "orc_recover": (C.c_int, [C.c_int, u8p, C.c_int, C.c_int, C.c_int, u8p, u8p]),
+                "orc_encode_s": (C.c_int, [C.c_int, u8p, C.c_int, C.c_int, u8p, C.c_int, C.c_int, u8p, i32p, i64p]),
+                "orc_recover_s": (C.c_int, [C.c_int, u8p, C.c_int, C.c_int, C.c_int, C.c_int, u8p, u8p]),
                 "orc_capacity": (C.c_int, [C.c_int, u8p, C.c_int, C.c_int, C.c_int, i32p, i64p]),
                 "orc_sse": (C.c_int64, [u8p, u8p, C.c_int64]),
                 "orc_der_psnr": (None, [C.c_int, C.c_int, C.c_int64, C.c_int64,
@@ -180,13 +182,13 @@ def tile_count(M: int, N: int, t: int) -> int:
 
 
 # ---------------------------------------------------------------- the four calls
-def encode(method: int, img: np.ndarray, k1: bytes, tile_log2: int = 7):
+def encode(method: int, img: np.ndarray, k1: bytes, tile_log2: int = 7, lmr_emin: int = 0):
     img = _u8(img)
     M, N = img.shape
     E = np.zeros_like(img)
     b, cap = C.c_int32(0), C.c_int64(0)
     k = _u8(bytearray(k1))
-    st = lib().orc_encode(method, _p(img), M, N, _p(k), tile_log2, _p(E), C.byref(b), C.byref(cap))
+    st = lib().orc_encode_s(method, _p(img), M, N, _p(k), tile_log2, lmr_emin, _p(E), C.byref(b), C.byref(cap))
     return st, E, b.value, cap.value
 
 
@@ -210,12 +212,12 @@ def extract(method: int, marked: np.ndarray, k2: bytes, stride_bytes: int, fill:
     return st, out, nb.value
 
 
-def recover(method: int, marked: np.ndarray, k1: bytes, tile_log2: int = 7):
+def recover(method: int, marked: np.ndarray, k1: bytes, tile_log2: int = 7, lmr_emin: int = 0):
     marked = _u8(marked)
     M, N = marked.shape
     out = np.zeros_like(marked)
     k = _u8(bytearray(k1))
-    st = lib().orc_recover(method, _p(marked), M, N, tile_log2, _p(k), _p(out))
+    st = lib().orc_recover_s(method, _p(marked), M, N, tile_log2, lmr_emin, _p(k), _p(out))
     return st, out
 
 

@@ -205,10 +205,10 @@ void orc_rotate_all(uint8_t *grid, int M, int N, const uint8_t *s, int emin, int
 }
 
 static int emr_emin(int M, int N) { (void)M; (void)N; return 1; }          /* P:1073 {2^1..2^n} */
-static int lmr_emin(int M, int N)                                          /* P:985 {2^4..}, Q10 */
+static int lmr_emin(int M, int N, int req)           /* P:985 {2^4..}, Q10; Tab. LMR_block_size variants */
 {
-    int emax = orc_emax(M, N);
-    return emax < 4 ? emax : 4;
+    int emax = orc_emax(M, N), e = (req >= 1 && req <= 4) ? req : 4;
+    return emax < e ? emax : e;
 }
 
 /* ===================================================================================
@@ -443,12 +443,12 @@ static int code_plane(const uint8_t *plane, int M, int N, int t, int *sizes, uin
     return 0;
 }
 
-static int lmr_encode(const uint8_t *I, int M, int N, const uint8_t k1[32], int t, uint8_t *E, int32_t *b_out,
-                      int64_t *cap_out)
+static int lmr_encode(const uint8_t *I, int M, int N, const uint8_t k1[32], int t, int emin_req, uint8_t *E,
+                      int32_t *b_out, int64_t *cap_out)
 {
     size_t MN = (size_t)M * N;
     if (t < 3 || t > 9) return ORC_E_INVAL;
-    int emin = lmr_emin(M, N);
+    int emin = lmr_emin(M, N, emin_req);
     /* (1) location map candidates and first MSB map eta = (I AND 128) mod 127 (eq. MSB_map, Q21) */
     int64_t zeros[9];
     int order[7];
@@ -559,13 +559,19 @@ static int lmr_read_maps(const uint8_t *Em, int M, int N, int t_expected, int *b
 /* ===================================================================================
  * The four calls.
  * =================================================================================== */
-int orc_encode(int method, const uint8_t *I, int M, int N, const uint8_t k1[32], int tile_log2, uint8_t *E,
-               int32_t *b_out, int64_t *capacity_out)
+int orc_encode_s(int method, const uint8_t *I, int M, int N, const uint8_t k1[32], int tile_log2, int lmr_emin_req,
+                 uint8_t *E, int32_t *b_out, int64_t *capacity_out)
 {
     if (M < 4 || N < 4) return ORC_E_INVAL;
     if (method == ORC_EMR) return emr_encode(I, M, N, k1, E, b_out, capacity_out);
-    if (method == ORC_LMR) return lmr_encode(I, M, N, k1, tile_log2, E, b_out, capacity_out);
+    if (method == ORC_LMR) return lmr_encode(I, M, N, k1, tile_log2, lmr_emin_req, E, b_out, capacity_out);
     return ORC_E_INVAL;
+}
+
+int orc_encode(int method, const uint8_t *I, int M, int N, const uint8_t k1[32], int tile_log2, uint8_t *E,
+               int32_t *b_out, int64_t *capacity_out)
+{
+    return orc_encode_s(method, I, M, N, k1, tile_log2, 0, E, b_out, capacity_out);
 }
 
 static int read_map(int method, const uint8_t *Em, int M, int N, int t, int *b, uint8_t *l, uint8_t *eta)
@@ -677,6 +683,12 @@ int orc_extract(int method, const uint8_t *marked, int M, int N, int tile_log2, 
  * (EMR) or bits 2..b (LMR) row by row from omega = the last non-redundant pixel. */
 int orc_recover(int method, const uint8_t *marked, int M, int N, int tile_log2, const uint8_t k1[32], uint8_t *out)
 {
+    return orc_recover_s(method, marked, M, N, tile_log2, 0, k1, out);
+}
+
+int orc_recover_s(int method, const uint8_t *marked, int M, int N, int tile_log2, int lmr_emin_req, const uint8_t k1[32],
+                  uint8_t *out)
+{
     size_t MN = (size_t)M * N;
     uint8_t *l = (uint8_t *)malloc(MN), *eta = (uint8_t *)malloc(MN);
     int b = 0;
@@ -689,7 +701,7 @@ int orc_recover(int method, const uint8_t *marked, int M, int N, int tile_log2, 
     uint8_t *s = (uint8_t *)malloc(MN);
     orc_keystream(k1, 0, MN, s);
     for (size_t r = 0; r < MN; r++) out[r] = (uint8_t)(marked[r] ^ s[r]);
-    int emin = method == ORC_EMR ? emr_emin(M, N) : lmr_emin(M, N);
+    int emin = method == ORC_EMR ? emr_emin(M, N) : lmr_emin(M, N, lmr_emin_req);
     orc_rotate_all(out, M, N, s, emin, 1);
     orc_rotate_all(l, M, N, s, emin, 1);
     if (method == ORC_LMR) {

@@ -74,6 +74,12 @@ int orc_hide(int method, const uint8_t *E, int M, int N, int tile_log2, const ui
 int orc_extract(int method, const uint8_t *marked, int M, int N, int tile_log2, const uint8_t k2[32],
                 uint8_t *msg_out, int64_t stride_bytes, int64_t *msg_bits_out);
 int orc_recover(int method, const uint8_t *marked, int M, int N, int tile_log2, const uint8_t k1[32], uint8_t *out);
+/* LMR rotation-schedule variants of Tab. LMR_block_size: blocks {2^e_min .. 2^e_max} with
+ * e_min = lmr_emin_req in 1..4 (0 = the paper's default 4), shared protocol knowledge like the method */
+int orc_encode_s(int method, const uint8_t *I, int M, int N, const uint8_t k1[32], int tile_log2, int lmr_emin_req,
+                 uint8_t *E, int32_t *b_out, int64_t *capacity_out);
+int orc_recover_s(int method, const uint8_t *marked, int M, int N, int tile_log2, int lmr_emin_req, const uint8_t k1[32],
+                  uint8_t *out);
 /* capacity C that the hider/receiver derive from a marked image (header + map) */
 int orc_capacity(int method, const uint8_t *marked, int M, int N, int tile_log2, int32_t *b_out, int64_t *capacity_out);
 

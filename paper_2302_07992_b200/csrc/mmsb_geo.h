@@ -36,10 +36,11 @@ inline int ilog2(long long v) {
     return e;
 }
 
-inline bool make_geo(int method, int B, int H, int W, int tile_log2, Geo *g) {
+inline bool make_geo(int method, int B, int H, int W, int tile_log2, int lmr_emin, Geo *g) {
     if (B < 1 || H < 16 || W < 16 || H > 32768 || W > 32768) return false;
     if ((H & (H - 1)) || (W & (W - 1))) return false;
     if (method != 0 && method != 1) return false;
+    if (lmr_emin < 0 || lmr_emin > 4) return false;
     if (tile_log2 == 0) tile_log2 = 7;
     if (tile_log2 < 3 || tile_log2 > 7) return false;   // GPU coder rows hold <= 128 pixels
     g->method = method;
@@ -48,7 +49,10 @@ inline bool make_geo(int method, int B, int H, int W, int tile_log2, Geo *g) {
     g->hlog = ilog2(H); g->wlog = ilog2(W);
     g->HW = (long long)H * W;
     g->emax = g->hlog < g->wlog ? g->hlog : g->wlog;
-    g->emin = method == 0 ? 1 : (g->emax < 4 ? g->emax : 4);
+    {
+        const int e = lmr_emin ? lmr_emin : 4;                // Tab. LMR_block_size schedules
+        g->emin = method == 0 ? 1 : (g->emax < e ? g->emax : e);
+    }
     g->tp = g->emax < 6 ? g->emax : 6;
     g->T = 1 << g->tp;
     g->tilesY = H >> g->tp;

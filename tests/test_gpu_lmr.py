@@ -90,3 +90,30 @@ def test_lmr_partial_and_capacity():
     out = _run(imgs, k1, k2, msgs, 7, nbits)
     assert out["st_h"][2] == O.E_CAPACITY
     _check(imgs, k1, k2, msgs, 7, out)
+
+
+@pytest.mark.parametrize("emin", [1, 2, 3])
+def test_lmr_schedule_variants_parity(emin):
+    """Tab. LMR_block_size schedules: rotation blocks {2^e_min..}, bit-exact with the oracle."""
+    H = W = 128
+    kinds = ["smooth", "textured", "smooth", "constant"]
+    imgs = np.stack([S.random_image(9100 + j, H, W, k) for j, k in enumerate(kinds)])
+    k1 = np.stack([np.frombuffer(S.key(9100 + j, 1), np.uint8) for j in range(len(kinds))])
+    k2 = np.stack([np.frombuffer(S.key(9100 + j, 2), np.uint8) for j in range(len(kinds))])
+    stride = S.msg_stride(H, W)
+    msgs = np.stack([S.payload(j, stride) for j in range(len(kinds))])
+    ws = G.Workspace(G.LMR, len(kinds), H, W, lmr_emin=emin)
+    enc, b, cap, st_e = G.encode(G.LMR, _dev(imgs), _dev(k1), ws)
+    marked, st_h = G.embed(G.LMR, enc, _dev(k2), _dev(msgs), (cap - 32).clamp(min=0), ws)
+    rec, st_r = G.recover(G.LMR, marked, _dev(k1), ws)
+    torch.cuda.synchronize()
+    for j in range(len(kinds)):
+        st, E, bo, Co = O.encode(O.LMR, imgs[j], k1[j].tobytes(), lmr_emin=emin)
+        assert int(st_e[j]) == st and int(b[j]) == bo and int(cap[j]) == Co
+        assert np.array_equal(enc[j].cpu().numpy(), E)
+        if st != O.OK:
+            continue
+        _, Em = O.hide(O.LMR, E, k2[j].tobytes(), msgs[j], Co - 32)
+        assert np.array_equal(marked[j].cpu().numpy(), Em)
+        _, R = O.recover(O.LMR, Em, k1[j].tobytes(), lmr_emin=emin)
+        assert np.array_equal(rec[j].cpu().numpy(), R) and np.array_equal(R, imgs[j])

@@ -318,3 +318,29 @@ def test_statistics_closed_forms():
     assert O.der_psnr(512, 512, 0, 0)[1] == math.inf
     # expected EMR PSNR, half of the LSBs wrong
     assert O.der_psnr(512, 512, 0, 512 * 512 // 2)[1] == pytest.approx(51.1411, abs=5e-5)
+
+
+@pytest.mark.parametrize("emin", [1, 2, 3, 4])
+def test_lmr_schedule_variants_round_trip(emin):
+    """Tab. LMR_block_size: LMR with rotation blocks {2^e_min..2^e_max} stays lossless and
+    separable for every schedule; e_min = 4 is the default."""
+    for j, kind in enumerate(["smooth", "smooth", "textured"]):
+        img = S.random_image(600 + j, 64, 64, kind)
+        k1, k2 = S.key(600 + j, 1), S.key(600 + j, 2)
+        st, E, b, C = O.encode(O.LMR, img, k1, lmr_emin=emin)
+        if st != O.OK:
+            continue
+        if emin == 4:
+            st0, E0, b0, C0 = O.encode(O.LMR, img, k1)
+            assert (st0, b0, C0) == (st, b, C) and np.array_equal(E0, E)
+        stride = S.msg_stride(64, 64)
+        msg = S.payload(j, stride)
+        _, Em = O.hide(O.LMR, E, k2, msg, C - 32)
+        _, mo, nb = O.extract(O.LMR, Em, k2, stride)
+        assert nb == C - 32
+        assert np.array_equal(np.unpackbits(mo)[:nb], np.unpackbits(msg)[:nb])
+        str_, R = O.recover(O.LMR, Em, k1, lmr_emin=emin)
+        assert str_ == O.OK and np.array_equal(R, img)
+        if emin != 4:            # the schedule is shared knowledge: the default schedule cannot decrypt it
+            _, Rw = O.recover(O.LMR, Em, k1)
+            assert not np.array_equal(Rw, img)
