@@ -53,7 +53,8 @@ struct RcEnc {
         if ((uint32_t)low < 0xFF000000u || (low >> 32) != 0) {
             const uint32_t carry = (uint32_t)(low >> 32);
             uint32_t temp = cache;
-            do {
+#pragma unroll 1
+            do {                                      // (a pending 0xFF run is rare: keep it a plain loop)
                 put((temp + carry) & 0xFFu);
                 temp = 0xFFu;
             } while (--cache_size != 0);
@@ -621,17 +622,33 @@ __global__ void __launch_bounds__(kCoderThreads) coder_encode_fast_kernel(Geo g,
 
 // decoder input: stream byte `pos` of a tile (bit-aligned inside the MSB-plane bytes); 0 past the end
 struct RcIn {
-    const uint8_t *m;
-    long long bit0;
+    // 64-bit look-ahead window (cur:nxt, big-endian words of the MSB-plane bytes) over the tile's
+    // stream: a byte is two funnel shifts away, and the word after the window is loaded 32 bits
+    // before it is needed, so the renormalisation never waits on memory
+    const uint32_t *w;                        // word-aligned base of the image's plane bytes
+    long long wb;                             // bit index of cur's MSB (multiple of 32)
+    long long bb;                             // bit index of the next stream byte
     int nbytes, pos;
+    uint32_t cur, nxt;
+    __device__ __forceinline__ void init(const uint8_t *m, long long bit0, int n) {
+        w = reinterpret_cast<const uint32_t *>(m);
+        bb = bit0;
+        wb = bit0 & ~31ll;
+        nbytes = n;
+        pos = 0;
+        cur = bswap32(__ldg(w + (wb >> 5)));
+        nxt = bswap32(__ldg(w + (wb >> 5) + 1));
+    }
     __device__ __forceinline__ uint32_t next() {
-        uint32_t v = 0;
-        if (pos < nbytes) {
-            const long long bb = bit0 + 8ll * pos;
-            const uint32_t hi = __ldg(m + (bb >> 3)), lo = __ldg(m + (bb >> 3) + 1);
-            v = (((hi << 8) | lo) >> (8 - (bb & 7))) & 0xFFu;
-        }
+        const int off = (int)(bb - wb);                                  // 0..31
+        const uint32_t v = pos < nbytes ? (__funnelshift_l(nxt, cur, off) >> 24) : 0u;
         pos++;
+        bb += 8;
+        if (bb - wb >= 32) {
+            cur = nxt;
+            wb += 32;
+            nxt = bswap32(__ldg(w + (wb >> 5) + 1));
+        }
         return v;
     }
 };
@@ -712,8 +729,9 @@ __global__ void __launch_bounds__(kCoderThreads) coder_decode_fast_kernel(Geo g,
     uint16_t *mdl = p0s + lane;
 
     const int k = (plane == 0 ? 0 : Tc) + tile;
-    RcIn in{mbuf + (size_t)img * (g.HW / 8), 7 + 32ll * Tc + 8ll * offsets[(size_t)img * 2 * TcM + k],
-            sizes[(size_t)img * 2 * TcM + k], 0};
+    RcIn in;
+    in.init(mbuf + (size_t)img * (g.HW / 8), 7 + 32ll * Tc + 8ll * offsets[(size_t)img * 2 * TcM + k],
+            sizes[(size_t)img * 2 * TcM + k]);
     uint32_t range = 0xFFFFFFFFu, code = 0;
     for (int i = 0; i < 5; i++) code = (code << 8) | in.next();
     uint32_t *plane_out = plane == 0 ? eta_bits : map_bits;
