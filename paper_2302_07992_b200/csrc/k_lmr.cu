@@ -488,96 +488,158 @@ __global__ void __launch_bounds__(kCoderThreads) coder_decode_kernel(Geo g, int 
 
 // ======================================================================================
 // Fast coder kernels for tiles at least 32 pixels wide (every configured shape).  Same bit
-// stream as coder_encode_kernel / coder_decode_kernel: the tile's two previous
-// rows are kept in registers as MSB-first words, the 10-pixel context of a symbol comes from
-// funnel shifts, and the probability of the NEXT symbol is loaded from the shared-memory model
-// while the current one is coded -- for the encoder from its known context, for the decoder
-// for both values of the bit being decoded -- with a forward of the freshly updated
-// probability when the two contexts coincide.  What is left on the serial chain per symbol is
-// the range update itself.
+// stream as coder_encode_kernel / coder_decode_kernel, restructured for a
+// serial chain that has only a few warps per SM to hide its latency (the models, 2 KB per
+// tile, bound residency at ~112 tiles per SM):
+//  * CTAs of kFastThreads = 112 threads (3.5 warps: all four SM sub-partitions busy) holding
+//    224 KB of models, one CTA per SM;
+//  * the row is walked in half-words of 16 pixels with the 16 symbols fully unrolled: the
+//    10-pixel context of every symbol comes from two pre-aligned 32-bit slices of the rows
+//    above with immediate shifts;
+//  * the next symbol's probability is loaded while the current one is coded -- the decoder
+//    loads both candidates and forwards the freshly updated probability when the contexts
+//    coincide, so after the bit is known only one select remains;
+//  * renormalisation is branch-free: the number of bytes to shift is clz(range) >> 3 (0..2:
+//    range >= 3840 after any symbol), the decoder reads through a 64-bit MSB-aligned bit
+//    buffer refilled from funnel-shifted stream words (bytes past the end read as 0), the
+//    encoder's byte output is predicated (only a pending 0xFF run takes a branch).
 // ======================================================================================
+constexpr int kFastThreads = 112;
+constexpr int kHalfCtx = 512;                                  // contexts with (0,-1) = 0; the rest at +kHiOff
+constexpr uint32_t kHiOff = kFastThreads * kHalfCtx * 2;      // bytes: models of contexts 512..1023
+static constexpr size_t fast_smem() { return 2 * (size_t)kHiOff; }
+
+// Model layout (224 KB): context ctx of thread tid at byte
+//   (ctx >> 9) * kHiOff + warp * 512 * 64 + (ctx & 511) * sbytes + lane * 2,
+// sbytes = 2 * (lanes of the warp): warp-interleaved (<= 2-way bank conflicts), and the two
+// contexts that differ only in the (0,-1) bit a fixed immediate offset apart.
+__device__ __forceinline__ void fast_model_init(uint16_t *p0s) {
+    uint4 *q = reinterpret_cast<uint4 *>(p0s);
+    const uint4 v = make_uint4(0x80008000u, 0x80008000u, 0x80008000u, 0x80008000u);   // p0 = 32768
+    for (int i = threadIdx.x; i < (int)(fast_smem() / 16); i += kFastThreads) q[i] = v;
+    __syncthreads();
+}
+__device__ __forceinline__ uint32_t fast_model_base(const uint16_t *p0s, int tid, uint32_t &sbytes) {
+    const int w = tid >> 5;
+    sbytes = 2u * ((w == kFastThreads / 32) ? (kFastThreads & 31) : 32);
+    return (uint32_t)__cvta_generic_to_shared(p0s) + w * kHalfCtx * 64 + (tid & 31) * 2;
+}
+// shared-memory model accesses keep program order (asm volatile): a probability loaded for the
+// next symbol is read before the current symbol's update, which is forwarded explicitly
+__device__ __forceinline__ uint32_t lds_u16(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts_u16(uint32_t a, uint32_t v) {
+    asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((unsigned short)v));
+}
+
 __device__ __forceinline__ uint32_t nib4(uint32_t t) { return ((t * 0x08040201u) >> 24) & 0xFu; }   // bytes' bit 0 -> MSB-first nibble
 
-// context bits 7..0 of pixel x = 32 K + j from the two previous rows (MSB-first words; pixels
-// outside the tile read as 0): 5 pixels x-2..x+2 of row y-1, 3 pixels x-1..x+1 of row y-2
-template <int NW, int K>
-__device__ __forceinline__ uint32_t rows_ctx(const uint32_t (&p1)[NW], const uint32_t (&p2)[NW], int j) {
-    const uint32_t a0 = K > 0 ? p1[K > 0 ? K - 1 : 0] : 0u, a2 = K + 1 < NW ? p1[K + 1 < NW ? K + 1 : K] : 0u;
-    const uint32_t b0 = K > 0 ? p2[K > 0 ? K - 1 : 0] : 0u, b2 = K + 1 < NW ? p2[K + 1 < NW ? K + 1 : K] : 0u;
-    const uint32_t w5 = __funnelshift_l(j >= 2 ? a2 : p1[K], j >= 2 ? p1[K] : a0, (j - 2) & 31) >> 27;
-    const uint32_t w3 = __funnelshift_l(j >= 1 ? b2 : p2[K], j >= 1 ? p2[K] : b0, (j - 1) & 31) >> 29;
-    return (w5 << 3) | w3;
+template <int NW>
+__device__ __forceinline__ uint32_t pick(const uint32_t (&r)[NW], int k) {       // r[k], 0 outside the row
+    uint32_t v = 0;
+#pragma unroll
+    for (int i = 0; i < NW; i++) v = k == i ? r[i] : v;
+    return v;
 }
 
-template <int NW, int K>
-__device__ __forceinline__ void enc_row(RcEnc &e, uint16_t *mdl, const uint32_t (&cw)[NW], const uint32_t (&p1)[NW],
-                                        const uint32_t (&p2)[NW], uint32_t &ctx, uint32_t &p, uint32_t &hist2) {
-    // context of the first pixel of the next word (loop invariant); unused after the row's end
-    const uint32_t first_next = K + 1 < NW ? rows_ctx<NW, (K + 1 < NW ? K + 1 : K)>(p1, p2, 0) : 0u;
-    const uint32_t word = cw[K];
-#pragma unroll 2
-    for (int j = 0; j < 32; j++) {
-        const uint32_t bit = (word >> (31 - j)) & 1u;
-        const uint32_t nh = ((hist2 << 1) | bit) & 3u;
-        const bool last = (K == NW - 1) && j == 31;
-        // next symbol's context and probability (prefetched before this symbol's store)
-        const uint32_t nrows = j < 31 ? rows_ctx<NW, K>(p1, p2, j + 1) : first_next;
-        const uint32_t nctx = ((nh & 1u) << 9) | ((nh >> 1) << 8) | nrows;
-        const uint32_t np = last ? 0u : (uint32_t)mdl[nctx * 32];
-        const uint32_t bound = (e.range >> 16) * p;
-        uint32_t pu;
-        if (bit == 0) {
-            e.range = bound;
-            pu = p + ((65536u - p) >> 4);
-        } else {
-            e.low += bound;
-            e.range -= bound;
-            pu = p - (p >> 4);
-        }
-        mdl[ctx * 32] = (uint16_t)pu;
-        while (e.range < (1u << 24)) {
-            e.range <<= 8;
-            e.shift_low();
-        }
-        p = nctx == ctx ? pu : np;
-        ctx = nctx;
-        hist2 = nh;
+// context slices of half-word q (pixels 16q .. 16q+15 of the tile row; MSB-first words):
+// s1 = row y-1 from pixel 16q-2, s2 = row y-2 from pixel 16q-1 (pixels outside the tile = 0).
+template <int NW>
+__device__ __forceinline__ void half_slices(const uint32_t (&p1)[NW], const uint32_t (&p2)[NW], int q, uint32_t &s1,
+                                            uint32_t &s2) {
+    const int K = q >> 1;
+    const uint32_t a1 = pick(p1, K - 1), c1 = pick(p1, K), n1 = pick(p1, K + 1);
+    const uint32_t a2 = pick(p2, K - 1), c2 = pick(p2, K), n2 = pick(p2, K + 1);
+    if (q & 1) {
+        s1 = __funnelshift_l(n1, c1, 14);
+        s2 = __funnelshift_l(n2, c2, 15);
+    } else {
+        s1 = __funnelshift_l(c1, a1, 30);
+        s2 = __funnelshift_l(c2, a2, 31);
     }
-    if constexpr (K + 1 < NW) enc_row<NW, K + 1>(e, mdl, cw, p1, p2, ctx, p, hist2);
 }
+// rows part (bits 7..0) of the context of symbol J of a half: 5 pixels x-2..x+2 of row y-1,
+// 3 pixels x-1..x+1 of row y-2 (J is a constant after unrolling)
+__device__ __forceinline__ uint32_t slice_ctx(uint32_t s1, uint32_t s2, int J) {
+    return ((s1 >> (24 - J)) & 0xF8u) | ((s2 >> (29 - J)) & 7u);
+}
+
+__device__ __forceinline__ void st_u8_if(bool c, uint8_t *p, uint32_t v) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %0, 0;\n\t@q st.global.u8 [%1], %2;\n\t}" ::"r"((uint32_t)c), "l"(p),
+                 "r"(v));
+}
+
+struct FastEnc {
+    uint64_t low;
+    uint32_t range, cache, cache_size;
+    uint8_t *out;
+    int n, cap;
+    int run_n, run_len;                       // pending 0xFF run of the current symbol: reserved, written later
+    uint32_t run_val;
+    // one byte shift of low (a no-op unless take), branch-free: the common case writes one byte
+    // (a write past cap lands on byte cap-1 of a tile whose stream is over cap, i.e. discarded);
+    // a released 0xFF run (at most one per symbol) only reserves its bytes
+    __device__ __forceinline__ void shift_low(bool take) {
+        const uint32_t lo = (uint32_t)low, hi = (uint32_t)(low >> 32);
+        const bool emit = take && (lo < 0xFF000000u || hi != 0);
+        st_u8_if(emit, out + (n < cap ? n : cap - 1), cache + hi);
+        const int run = emit ? (int)cache_size - 1 : 0;
+        if (run) {
+            run_n = n + 1;
+            run_len = run;
+            run_val = 0xFFu + hi;
+        }
+        n += emit ? 1 + run : 0;
+        cache = emit ? lo >> 24 : cache;
+        cache_size = emit ? 1u : cache_size + (take ? 1u : 0u);
+        low = take ? (uint64_t)(lo << 8) : low;
+    }
+    __device__ __forceinline__ void write_run() {
+        if (__builtin_expect(run_len != 0, 0)) {
+#pragma unroll 1
+            for (int i = 0; i < run_len; i++)
+                if (run_n + i < cap) out[run_n + i] = (uint8_t)run_val;
+            run_len = 0;
+        }
+    }
+};
 
 template <int NW>
-__global__ void __launch_bounds__(kCoderThreads) coder_encode_fast_kernel(Geo g, int wave, const uint8_t *__restrict__ ceta,
-                                                                          const LmrPlan *__restrict__ plan,
-                                                                          uint8_t *__restrict__ streams,
-                                                                          int32_t *__restrict__ sizes) {
-    extern __shared__ uint16_t p0s[];                                  // [1024][32]
-    const int lane = threadIdx.x;
+__global__ void __launch_bounds__(kFastThreads, 1) coder_encode_fast_kernel(Geo g, int wave, const uint8_t *__restrict__ ceta,
+                                                                         const LmrPlan *__restrict__ plan,
+                                                                         uint8_t *__restrict__ streams,
+                                                                         int32_t *__restrict__ sizes) {
+    extern __shared__ __align__(16) uint16_t p0s[];
+    const int tid = threadIdx.x;
     const int Tc = lmr_tile_count(g.H, g.W, g.tile_log2);
     const int nslots = wave == 0 ? 2 : 1;
-    const long long gid = (long long)blockIdx.x * kCoderThreads + lane;
+    const long long gid = (long long)blockIdx.x * kFastThreads + tid;
     const long long total = (long long)g.B * nslots * Tc;
     const bool active0 = gid < total;
     const int img = active0 ? (int)(gid / ((long long)nslots * Tc)) : 0;
     const int rem = active0 ? (int)(gid % ((long long)nslots * Tc)) : 0;
     const int slot = wave == 0 ? rem / Tc : 1;
     const int tile = rem % Tc;
-    const LmrPlan pl = plan[img];
-    const bool active = active0 && pl.state == 0;
-    if (!__any_sync(0xffffffffu, active)) return;
-    for (int c = 0; c < 1024; c++) p0s[c * 32 + lane] = 32768;
+    const bool active = active0 && plan[img].state == 0;
+    if (!__syncthreads_or(active)) return;
+    fast_model_init(p0s);
     if (!active) return;
+    const unsigned am = __activemask();
+    uint32_t sbytes;
+    const uint32_t mbase = fast_model_base(p0s, tid, sbytes);
 
     const int th = lmr_tile_side(g.tile_log2, g.H);
     constexpr int w = 32 * NW;
     const int TN = g.W / w;
     const int y0 = (tile / TN) * th, x0 = (tile % TN) * w;
     const int h = g.H - y0 < th ? g.H - y0 : th;
-    const uint32_t bsub = slot == 0 ? 0u : (uint32_t)(0x80 - pl.order[wave]) * 0x01010101u;
+    const uint32_t bsub = slot == 0 ? 0u : (uint32_t)(0x80 - plan[img].order[wave]) * 0x01010101u;
     const int cap = lmr_tile_cap(g.tile_log2, g.H, g.W);
-    uint16_t *mdl = p0s + lane;
 
-    RcEnc e{0, 0xFFFFFFFFu, 0, 1, streams + (((size_t)img * 2 + slot) * Tc + tile) * cap, 0, cap};
+    FastEnc e{0, 0xFFFFFFFFu, 0, 1, streams + (((size_t)img * 2 + slot) * Tc + tile) * cap, 0, cap, 0, 0, 0};
     const uint8_t *src = ceta + (size_t)img * g.HW + x0;
     uint32_t p1[NW], p2[NW];
 #pragma unroll
@@ -591,6 +653,7 @@ __global__ void __launch_bounds__(kCoderThreads) coder_encode_fast_kernel(Geo g,
         for (int q = 0; q < 2 * NW; q++) raw[q] = __ldg(rp + q);
     };
     load_row(0);
+#pragma unroll 1
     for (int y = 0; y < h; y++) {
         uint32_t cw[NW];
 #pragma unroll
@@ -609,105 +672,104 @@ __global__ void __launch_bounds__(kCoderThreads) coder_encode_fast_kernel(Geo g,
             cw[k] = wv;
         }
         if (y + 1 < h) load_row(y + 1);
-        uint32_t hist2 = 0;
-        uint32_t ctx = rows_ctx<NW, 0>(p1, p2, 0);
-        uint32_t p = mdl[ctx * 32];
-        enc_row<NW, 0>(e, mdl, cw, p1, p2, ctx, p, hist2);
+        uint32_t s1, s2;
+        half_slices(p1, p2, 0, s1, s2);
+        uint32_t actx = mbase + slice_ctx(s1, s2, 0) * sbytes;         // hist bits 0 at the row start
+        uint32_t p = lds_u16(actx);
+        uint32_t prev8 = 0;                                            // previous bit << 8
+#pragma unroll 1
+        for (int q = 0; q < 2 * NW; q++) {
+            uint32_t t1, t2;
+            half_slices(p1, p2, q + 1, t1, t2);                        // next half (unused past the row)
+            const uint32_t cb = pick(cw, q >> 1) << (16 * (q & 1));
+#pragma unroll
+            for (int J = 0; J < 16; J++) {
+                const bool bit = (cb >> (31 - J)) & 1u;
+                const uint32_t nrows = J < 15 ? slice_ctx(s1, s2, J + 1) : slice_ctx(t1, t2, 0);
+                const uint32_t anctx = mbase + (prev8 | nrows) * sbytes + (bit ? kHiOff : 0u);
+                const uint32_t np = lds_u16(anctx);
+                const uint32_t bound = (e.range >> 16) * p;
+                const uint32_t pu = bit ? p - (p >> 4) : p + ((65536u - p) >> 4);
+                e.low += bit ? bound : 0u;
+                e.range = bit ? e.range - bound : bound;
+                sts_u16(actx, pu);
+                const int s = __clz(e.range) >> 3;                     // 0..2 bytes to shift out
+                if (__any_sync(am, s != 0)) {
+                    e.shift_low(s >= 1);
+                    e.shift_low(s >= 2);
+                    e.write_run();
+                    e.range <<= 8 * s;
+                }
+                p = anctx == actx ? pu : np;
+                actx = anctx;
+                prev8 = bit ? 256u : 0u;
+            }
+            s1 = t1;
+            s2 = t2;
+        }
 #pragma unroll
         for (int k = 0; k < NW; k++) { p2[k] = p1[k]; p1[k] = cw[k]; }
     }
-    for (int i = 0; i < 5; i++) e.shift_low();
+#pragma unroll 1
+    for (int i = 0; i < 5; i++) {
+        e.shift_low(true);
+        e.write_run();
+    }
     sizes[((size_t)img * 2 + slot) * Tc + tile] = (e.n <= cap && e.n <= 65535) ? e.n : -1;
 }
 
-// decoder input: stream byte `pos` of a tile (bit-aligned inside the MSB-plane bytes); 0 past the end
-struct RcIn {
-    // 64-bit look-ahead window (cur:nxt, big-endian words of the MSB-plane bytes) over the tile's
-    // stream: a byte is two funnel shifts away, and the word after the window is loaded 32 bits
-    // before it is needed, so the renormalisation never waits on memory
-    const uint32_t *w;                        // word-aligned base of the image's plane bytes
-    long long wb;                             // bit index of cur's MSB (multiple of 32)
-    long long bb;                             // bit index of the next stream byte
-    int nbytes, pos;
-    uint32_t cur, nxt;
-    __device__ __forceinline__ void init(const uint8_t *m, long long bit0, int n) {
-        w = reinterpret_cast<const uint32_t *>(m);
-        bb = bit0;
-        wb = bit0 & ~31ll;
-        nbytes = n;
-        pos = 0;
-        cur = bswap32(__ldg(w + (wb >> 5)));
-        nxt = bswap32(__ldg(w + (wb >> 5) + 1));
+// decoder input: the tile's stream as a 64-bit MSB-aligned bit buffer (nb valid bits, >= 32 at
+// every symbol), refilled from stream words funnel-shifted out of the big-endian words of the
+// MSB-plane bytes (the stream starts at an arbitrary bit); stream bytes past nbytes read as 0
+struct FastIn {
+    const uint32_t *w;                        // aligned word holding the next stream word's first bit
+    uint32_t wa, wb, wc;                      // w[0], w[1], w[2] (big-endian)
+    int sh;                                   // stream bit 0 = bit sh of the first word
+    int valid;                                // stream bits left to deliver (8 nbytes - delivered)
+    uint64_t buf;
+    int nb;
+    __device__ __forceinline__ uint32_t word() {                      // next 32 stream bits, masked
+        const uint32_t v = __funnelshift_l(wb, wa, sh);
+        const uint32_t keep = valid >= 32 ? 0xFFFFFFFFu : (valid <= 0 ? 0u : ~(0xFFFFFFFFu >> valid));
+        valid -= 32;
+        wa = wb;
+        wb = wc;
+        ++w;
+        wc = bswap32(__ldg(w + 2));
+        return v & keep;
     }
-    __device__ __forceinline__ uint32_t next() {
-        const int off = (int)(bb - wb);                                  // 0..31
-        const uint32_t v = pos < nbytes ? (__funnelshift_l(nxt, cur, off) >> 24) : 0u;
-        pos++;
-        bb += 8;
-        if (bb - wb >= 32) {
-            cur = nxt;
-            wb += 32;
-            nxt = bswap32(__ldg(w + (wb >> 5) + 1));
+    __device__ __forceinline__ void init(const uint8_t *m, long long bit0, int nbytes) {
+        w = reinterpret_cast<const uint32_t *>(m) + (bit0 >> 5);
+        sh = (int)(bit0 & 31);
+        valid = 8 * nbytes;
+        wa = bswap32(__ldg(w));
+        wb = bswap32(__ldg(w + 1));
+        wc = bswap32(__ldg(w + 2));
+        const uint32_t hi = word(), lo = word();
+        buf = ((uint64_t)hi << 32) | lo;
+        nb = 64;
+    }
+    __device__ __forceinline__ void refill() {
+        if (nb < 32) {
+            buf |= (uint64_t)word() << (32 - nb);
+            nb += 32;
         }
-        return v;
     }
 };
 
-template <int NW, int K>
-__device__ __forceinline__ void dec_row(RcIn &in, uint32_t &range, uint32_t &code, uint16_t *mdl, uint32_t (&cw)[NW],
-                                        const uint32_t (&p1)[NW], const uint32_t (&p2)[NW], uint32_t &ctx, uint32_t &p,
-                                        uint32_t &hist2, uint32_t *orow) {
-    const uint32_t first_next = K + 1 < NW ? rows_ctx<NW, (K + 1 < NW ? K + 1 : K)>(p1, p2, 0) : 0u;
-    uint32_t acc = 0, word = 0;
-#pragma unroll 2
-    for (int j = 0; j < 32; j++) {
-        const bool last = (K == NW - 1) && j == 31;
-        // both candidate contexts of the next symbol (its (0,-1) bit is the one decoded now)
-        const uint32_t nbase = ((hist2 & 1u) << 8) | (j < 31 ? rows_ctx<NW, K>(p1, p2, j + 1) : first_next);
-        const uint32_t np0 = last ? 0u : (uint32_t)mdl[nbase * 32];
-        const uint32_t np1 = last ? 0u : (uint32_t)mdl[(nbase | 512u) * 32];
-        const uint32_t bound = (range >> 16) * p;
-        uint32_t bit, pu;
-        if (code < bound) {
-            range = bound;
-            bit = 0;
-            pu = p + ((65536u - p) >> 4);
-        } else {
-            code -= bound;
-            range -= bound;
-            bit = 1;
-            pu = p - (p >> 4);
-        }
-        mdl[ctx * 32] = (uint16_t)pu;
-        while (range < (1u << 24)) {
-            range <<= 8;
-            code = (code << 8) | in.next();
-        }
-        word |= bit << (31 - j);
-        acc |= bit << j;
-        hist2 = ((hist2 << 1) | bit) & 3u;
-        const uint32_t nctx = nbase | (bit << 9);
-        p = nctx == ctx ? pu : (bit ? np1 : np0);
-        ctx = nctx;
-    }
-    cw[K] = word;
-    orow[K] = acc;                                           // plane words: bit x & 31 = pixel x
-    if constexpr (K + 1 < NW) dec_row<NW, K + 1>(in, range, code, mdl, cw, p1, p2, ctx, p, hist2, orow);
-}
-
 template <int NW>
-__global__ void __launch_bounds__(kCoderThreads) coder_decode_fast_kernel(Geo g, int want_eta, const uint8_t *__restrict__ mbuf,
-                                                                          const int32_t *__restrict__ lmr_b,
-                                                                          const int32_t *__restrict__ lmr_t,
-                                                                          const int32_t *__restrict__ offsets,
-                                                                          const int32_t *__restrict__ sizes,
-                                                                          uint32_t *__restrict__ eta_bits,
-                                                                          uint32_t *__restrict__ map_bits) {
-    extern __shared__ uint16_t p0s[];
-    const int lane = threadIdx.x;
+__global__ void __launch_bounds__(kFastThreads, 1) coder_decode_fast_kernel(Geo g, int want_eta, const uint8_t *__restrict__ mbuf,
+                                                                         const int32_t *__restrict__ lmr_b,
+                                                                         const int32_t *__restrict__ lmr_t,
+                                                                         const int32_t *__restrict__ offsets,
+                                                                         const int32_t *__restrict__ sizes,
+                                                                         uint32_t *__restrict__ eta_bits,
+                                                                         uint32_t *__restrict__ map_bits) {
+    extern __shared__ __align__(16) uint16_t p0s[];
+    const int tid = threadIdx.x;
     const int TcM = g.ntiles_coder;
     const int nplanes = want_eta ? 2 : 1;
-    const long long gid = (long long)blockIdx.x * kCoderThreads + lane;
+    const long long gid = (long long)blockIdx.x * kFastThreads + tid;
     const long long total = (long long)g.B * nplanes * TcM;
     bool active = gid < total;
     const int img = active ? (int)(gid / ((long long)nplanes * TcM)) : 0;
@@ -717,34 +779,90 @@ __global__ void __launch_bounds__(kCoderThreads) coder_decode_fast_kernel(Geo g,
     const int b = lmr_b[img];
     const int Tc = TcM;                                       // header t == g.tile_log2 (else FORMAT)
     active = active && b >= 2;
-    if (!__any_sync(0xffffffffu, active)) return;
-    for (int c = 0; c < 1024; c++) p0s[c * 32 + lane] = 32768;
+    if (!__syncthreads_or(active)) return;
+    fast_model_init(p0s);
     if (!active) return;
+    const unsigned am = __activemask();
+    uint32_t sbytes;
+    const uint32_t mbase = fast_model_base(p0s, tid, sbytes);
 
     const int th = lmr_tile_side(g.tile_log2, g.H);
     constexpr int w = 32 * NW;
     const int TN = g.W / w;
     const int y0 = (tile / TN) * th, x0 = (tile % TN) * w;
     const int h = g.H - y0 < th ? g.H - y0 : th;
-    uint16_t *mdl = p0s + lane;
 
     const int k = (plane == 0 ? 0 : Tc) + tile;
-    RcIn in;
+    FastIn in;
     in.init(mbuf + (size_t)img * (g.HW / 8), 7 + 32ll * Tc + 8ll * offsets[(size_t)img * 2 * TcM + k],
             sizes[(size_t)img * 2 * TcM + k]);
-    uint32_t range = 0xFFFFFFFFu, code = 0;
-    for (int i = 0; i < 5; i++) code = (code << 8) | in.next();
+    // the encoder's first byte is the initial cache byte: code = stream bytes 1..4
+    uint32_t range = 0xFFFFFFFFu, code = (uint32_t)(in.buf >> 24);
+    in.buf <<= 40;
+    in.nb = 24;
+    in.refill();
     uint32_t *plane_out = plane == 0 ? eta_bits : map_bits;
     uint32_t p1[NW], p2[NW];
 #pragma unroll
     for (int q = 0; q < NW; q++) { p1[q] = 0; p2[q] = 0; }
+#pragma unroll 1
     for (int y = 0; y < h; y++) {
         uint32_t cw[NW];
-        uint32_t hist2 = 0;
-        uint32_t ctx = rows_ctx<NW, 0>(p1, p2, 0);
-        uint32_t p = mdl[ctx * 32];
+#pragma unroll
+        for (int q = 0; q < NW; q++) cw[q] = 0;
+        uint32_t s1, s2;
+        half_slices(p1, p2, 0, s1, s2);
+        uint32_t actx = mbase + slice_ctx(s1, s2, 0) * sbytes;
+        uint32_t p = lds_u16(actx);
+        uint32_t prev8 = 0, word = 0, acc = 0;
         uint32_t *orow = plane_out + (((size_t)img * g.HW + (size_t)(y0 + y) * g.W + x0) >> 5);
-        dec_row<NW, 0>(in, range, code, mdl, cw, p1, p2, ctx, p, hist2, orow);
+#pragma unroll 1
+        for (int q = 0; q < 2 * NW; q++) {
+            uint32_t t1, t2;
+            half_slices(p1, p2, q + 1, t1, t2);
+            uint32_t hw = 0, lw = 0;
+#pragma unroll
+            for (int J = 0; J < 16; J++) {
+                // both candidate contexts of the next symbol (its (0,-1) bit is the one decoded now)
+                const uint32_t nrows = J < 15 ? slice_ctx(s1, s2, J + 1) : slice_ctx(t1, t2, 0);
+                const uint32_t a0 = mbase + (prev8 | nrows) * sbytes, a1 = a0 + kHiOff;
+                const uint32_t np0 = lds_u16(a0), np1 = lds_u16(a1);
+                const uint32_t pu0 = p + ((65536u - p) >> 4), pu1 = p - (p >> 4);
+                const uint32_t f0 = a0 == actx ? pu0 : np0, f1 = a1 == actx ? pu1 : np1;
+                const uint32_t bound = (range >> 16) * p;
+                const bool bit = code >= bound;
+                range = bit ? range - bound : bound;
+                code = bit ? code - bound : code;
+                sts_u16(actx, bit ? pu1 : pu0);
+                const int s = __clz(range) >> 3;                      // 0..2 bytes to shift in
+                if (__any_sync(am, s != 0)) {
+                    const uint32_t top = (uint32_t)(in.buf >> 48);
+                    code = (code << (8 * s)) | (top >> (16 - 8 * s));
+                    range <<= 8 * s;
+                    in.buf <<= 8 * s;
+                    in.nb -= 8 * s;
+                    in.refill();
+                }
+                hw |= bit ? 1u << (15 - J) : 0u;
+                lw |= bit ? 1u << J : 0u;
+                actx = bit ? a1 : a0;
+                p = bit ? f1 : f0;
+                prev8 = bit ? 256u : 0u;
+            }
+            s1 = t1;
+            s2 = t2;
+            if (q & 1) {
+                const int K = q >> 1;
+                word |= hw;
+                acc |= lw << 16;
+#pragma unroll
+                for (int i = 0; i < NW; i++) cw[i] = i == K ? word : cw[i];
+                orow[K] = acc;                                          // plane words: bit x & 31 = pixel x
+            } else {
+                word = hw << 16;
+                acc = lw;
+            }
+        }
 #pragma unroll
         for (int q = 0; q < NW; q++) { p2[q] = p1[q]; p1[q] = cw[q]; }
     }
@@ -760,12 +878,12 @@ void lmr_set_smem_attrs() {
     if (done) return;
     cudaFuncSetAttribute(coder_encode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)coder_smem());
     cudaFuncSetAttribute(coder_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)coder_smem());
-    cudaFuncSetAttribute(coder_encode_fast_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)coder_smem());
-    cudaFuncSetAttribute(coder_encode_fast_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)coder_smem());
-    cudaFuncSetAttribute(coder_encode_fast_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)coder_smem());
-    cudaFuncSetAttribute(coder_decode_fast_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)coder_smem());
-    cudaFuncSetAttribute(coder_decode_fast_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)coder_smem());
-    cudaFuncSetAttribute(coder_decode_fast_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)coder_smem());
+    cudaFuncSetAttribute(coder_encode_fast_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fast_smem());
+    cudaFuncSetAttribute(coder_encode_fast_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fast_smem());
+    cudaFuncSetAttribute(coder_encode_fast_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fast_smem());
+    cudaFuncSetAttribute(coder_decode_fast_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fast_smem());
+    cudaFuncSetAttribute(coder_decode_fast_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fast_smem());
+    cudaFuncSetAttribute(coder_decode_fast_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fast_smem());
     done = true;
 }
 
@@ -779,10 +897,11 @@ void launch_coder_encode(const Geo &g, int wave, const uint8_t *ceta, const LmrP
     const int Tc = lmr_tile_count(g.H, g.W, g.tile_log2);
     const long long total = (long long)g.B * (wave == 0 ? 2 : 1) * Tc;
     const unsigned grid = (unsigned)((total + kCoderThreads - 1) / kCoderThreads);
+    const unsigned fgrid = (unsigned)((total + kFastThreads - 1) / kFastThreads);
     switch (lmr_tile_side(g.tile_log2, g.W)) {
-        case 32: coder_encode_fast_kernel<1><<<grid, kCoderThreads, coder_smem(), st>>>(g, wave, ceta, plan, streams, sizes); break;
-        case 64: coder_encode_fast_kernel<2><<<grid, kCoderThreads, coder_smem(), st>>>(g, wave, ceta, plan, streams, sizes); break;
-        case 128: coder_encode_fast_kernel<4><<<grid, kCoderThreads, coder_smem(), st>>>(g, wave, ceta, plan, streams, sizes); break;
+        case 32: coder_encode_fast_kernel<1><<<fgrid, kFastThreads, fast_smem(), st>>>(g, wave, ceta, plan, streams, sizes); break;
+        case 64: coder_encode_fast_kernel<2><<<fgrid, kFastThreads, fast_smem(), st>>>(g, wave, ceta, plan, streams, sizes); break;
+        case 128: coder_encode_fast_kernel<4><<<fgrid, kFastThreads, fast_smem(), st>>>(g, wave, ceta, plan, streams, sizes); break;
         default: coder_encode_kernel<<<grid, kCoderThreads, coder_smem(), st>>>(g, wave, ceta, plan, streams, sizes);
     }
 }
@@ -811,12 +930,13 @@ void launch_lmr_decode(const Geo &g, bool want_eta, const uint8_t *marked, uint8
     lmr_header_kernel<<<g.B, 32, 0, st>>>(g, mbuf, lmr_b, lmr_t, offsets, sizes, status, msg_bits_out);
     const long long total = (long long)g.B * (want_eta ? 2 : 1) * g.ntiles_coder;
     const unsigned dgrid = (unsigned)((total + kCoderThreads - 1) / kCoderThreads);
+    const unsigned fgrid = (unsigned)((total + kFastThreads - 1) / kFastThreads);
     switch (lmr_tile_side(g.tile_log2, g.W)) {
-        case 32: coder_decode_fast_kernel<1><<<dgrid, kCoderThreads, coder_smem(), st>>>(
+        case 32: coder_decode_fast_kernel<1><<<fgrid, kFastThreads, fast_smem(), st>>>(
                      g, want_eta ? 1 : 0, mbuf, lmr_b, lmr_t, offsets, sizes, eta_bits, map_bits); break;
-        case 64: coder_decode_fast_kernel<2><<<dgrid, kCoderThreads, coder_smem(), st>>>(
+        case 64: coder_decode_fast_kernel<2><<<fgrid, kFastThreads, fast_smem(), st>>>(
                      g, want_eta ? 1 : 0, mbuf, lmr_b, lmr_t, offsets, sizes, eta_bits, map_bits); break;
-        case 128: coder_decode_fast_kernel<4><<<dgrid, kCoderThreads, coder_smem(), st>>>(
+        case 128: coder_decode_fast_kernel<4><<<fgrid, kFastThreads, fast_smem(), st>>>(
                      g, want_eta ? 1 : 0, mbuf, lmr_b, lmr_t, offsets, sizes, eta_bits, map_bits); break;
         default: coder_decode_kernel<<<dgrid, kCoderThreads, coder_smem(), st>>>(
                      g, want_eta ? 1 : 0, mbuf, lmr_b, lmr_t, offsets, sizes, eta_bits, map_bits);
