@@ -572,38 +572,38 @@ __device__ __forceinline__ void st_u8_if(bool c, uint8_t *p, uint32_t v) {
                  "r"(v));
 }
 
+// Encoder output as exact base-256 digits.  The reference coder (coder_encode_kernel) keeps a
+// cache byte and a count of pending 0xFF bytes so that a carry out of low can still reach them;
+// its output is the digit string of the exact code value (a carry never reaches a byte it has
+// already written -- the nested intervals never leave the initial one), one digit per shift.
+// Here a 40-bit window [cache digit | 32-bit low] shifts its top digit straight to memory and a
+// carry out of the window (rare) is added into the written bytes (0xFF -> 0x00 backwards, +1 on
+// the first byte below 0xFF): the same bytes, with no per-shift cache / run bookkeeping.
 struct FastEnc {
-    uint64_t low;
-    uint32_t range, cache, cache_size;
+    uint64_t acc;                             // bits 39..32: next digit to leave; 31..0: low; >= 40: carries
+    uint32_t range;
     uint8_t *out;
     int n, cap;
-    int run_n, run_len;                       // pending 0xFF run of the current symbol: reserved, written later
-    uint32_t run_val;
-    // one byte shift of low (a no-op unless take), branch-free: the common case writes one byte
-    // (a write past cap lands on byte cap-1 of a tile whose stream is over cap, i.e. discarded);
-    // a released 0xFF run (at most one per symbol) only reserves its bytes
-    __device__ __forceinline__ void shift_low(bool take) {
-        const uint32_t lo = (uint32_t)low, hi = (uint32_t)(low >> 32);
-        const bool emit = take && (lo < 0xFF000000u || hi != 0);
-        st_u8_if(emit, out + (n < cap ? n : cap - 1), cache + hi);
-        const int run = emit ? (int)cache_size - 1 : 0;
-        if (run) {
-            run_n = n + 1;
-            run_len = run;
-            run_val = 0xFFu + hi;
-        }
-        n += emit ? 1 + run : 0;
-        cache = emit ? lo >> 24 : cache;
-        cache_size = emit ? 1u : cache_size + (take ? 1u : 0u);
-        low = take ? (uint64_t)(lo << 8) : low;
-    }
-    __device__ __forceinline__ void write_run() {
-        if (__builtin_expect(run_len != 0, 0)) {
+    __device__ __forceinline__ void carry_fix() {                    // pending carries into written digits
+        if (__builtin_expect((acc >> 40) != 0, 0)) {
+            uint32_t c = (uint32_t)(acc >> 40);
+            acc &= (1ull << 40) - 1;
 #pragma unroll 1
-            for (int i = 0; i < run_len; i++)
-                if (run_n + i < cap) out[run_n + i] = (uint8_t)run_val;
-            run_len = 0;
+            for (int i = (n < cap ? n : cap) - 1; i >= 0 && c; i--) {   // (asm: ordered after the stores)
+                uint32_t v;
+                asm volatile("ld.global.u8 %0, [%1];" : "=r"(v) : "l"(out + i));
+                v += c;
+                st_u8_if(true, out + i, v);
+                c = v >> 8;
+            }
         }
+    }
+    __device__ __forceinline__ void shift(int s) {                   // s = 0..2 digits out
+        carry_fix();
+        st_u8_if(s >= 1, out + (n < cap ? n : cap - 1), (uint32_t)(acc >> 32));
+        st_u8_if(s >= 2, out + (n + 1 < cap ? n + 1 : cap - 1), (uint32_t)acc >> 24);
+        n += s;
+        acc = (acc << (8 * s)) & ((1ull << 40) - 1);
     }
 };
 
@@ -639,7 +639,7 @@ __global__ void __launch_bounds__(kFastThreads, 1) coder_encode_fast_kernel(Geo 
     const uint32_t bsub = slot == 0 ? 0u : (uint32_t)(0x80 - plan[img].order[wave]) * 0x01010101u;
     const int cap = lmr_tile_cap(g.tile_log2, g.H, g.W);
 
-    FastEnc e{0, 0xFFFFFFFFu, 0, 1, streams + (((size_t)img * 2 + slot) * Tc + tile) * cap, 0, cap, 0, 0, 0};
+    FastEnc e{0, 0xFFFFFFFFu, streams + (((size_t)img * 2 + slot) * Tc + tile) * cap, 0, cap};
     const uint8_t *src = ceta + (size_t)img * g.HW + x0;
     uint32_t p1[NW], p2[NW];
 #pragma unroll
@@ -690,14 +690,12 @@ __global__ void __launch_bounds__(kFastThreads, 1) coder_encode_fast_kernel(Geo 
                 const uint32_t np = lds_u16(anctx);
                 const uint32_t bound = (e.range >> 16) * p;
                 const uint32_t pu = bit ? p - (p >> 4) : p + ((65536u - p) >> 4);
-                e.low += bit ? bound : 0u;
+                e.acc += bit ? bound : 0u;
                 e.range = bit ? e.range - bound : bound;
                 sts_u16(actx, pu);
                 const int s = __clz(e.range) >> 3;                     // 0..2 bytes to shift out
                 if (__any_sync(am, s != 0)) {
-                    e.shift_low(s >= 1);
-                    e.shift_low(s >= 2);
-                    e.write_run();
+                    e.shift(s);
                     e.range <<= 8 * s;
                 }
                 p = anctx == actx ? pu : np;
@@ -711,10 +709,7 @@ __global__ void __launch_bounds__(kFastThreads, 1) coder_encode_fast_kernel(Geo 
         for (int k = 0; k < NW; k++) { p2[k] = p1[k]; p1[k] = cw[k]; }
     }
 #pragma unroll 1
-    for (int i = 0; i < 5; i++) {
-        e.shift_low(true);
-        e.write_run();
-    }
+    for (int i = 0; i < 5; i++) e.shift(1);                           // flush: the window's 5 digits
     sizes[((size_t)img * 2 + slot) * Tc + tile] = (e.n <= cap && e.n <= 65535) ? e.n : -1;
 }
 
