@@ -718,7 +718,7 @@ __global__ void __launch_bounds__(kFastThreads, 1) coder_encode_fast_kernel(Geo 
 // MSB-plane bytes (the stream starts at an arbitrary bit); stream bytes past nbytes read as 0
 struct FastIn {
     const uint32_t *w;                        // aligned word holding the next stream word's first bit
-    uint32_t wa, wb, wc;                      // w[0], w[1], w[2] (big-endian)
+    uint32_t wa, wb, wc;                      // w[0], w[1] (big-endian), w[2] (raw)
     int sh;                                   // stream bit 0 = bit sh of the first word
     int valid;                                // stream bits left to deliver (8 nbytes - delivered)
     uint64_t buf;
@@ -728,9 +728,9 @@ struct FastIn {
         const uint32_t keep = valid >= 32 ? 0xFFFFFFFFu : (valid <= 0 ? 0u : ~(0xFFFFFFFFu >> valid));
         valid -= 32;
         wa = wb;
-        wb = wc;
+        wb = bswap32(wc);                     // (wc is kept raw: its load is not waited on here)
         ++w;
-        wc = bswap32(__ldg(w + 2));
+        wc = __ldg(w + 2);
         return v & keep;
     }
     __device__ __forceinline__ void init(const uint8_t *m, long long bit0, int nbytes) {
@@ -739,7 +739,7 @@ struct FastIn {
         valid = 8 * nbytes;
         wa = bswap32(__ldg(w));
         wb = bswap32(__ldg(w + 1));
-        wc = bswap32(__ldg(w + 2));
+        wc = __ldg(w + 2);
         const uint32_t hi = word(), lo = word();
         buf = ((uint64_t)hi << 32) | lo;
         nb = 64;
