@@ -477,6 +477,10 @@ def load_peaks():
 # ALU-pipe operations that cannot be avoided -- XOR and rotate, 640 per 64-byte block = 10 per
 # keystream byte (the adds may issue on the FMA pipe as IMAD); everything else is overhead.
 CHACHA_ALU_PER_BYTE = 640 / 64
+# LMR tile coder: integer ops of one coded / decoded symbol -- context 4 (two
+# row windows shifted and masked, merged with the two history bits), bound = (range>>16)*p0 2,
+# interval update 2, model update 3, renormalisation test 1; its units are symbols, not pixels
+CODER_ALU_PER_SYMBOL = 12.0
 
 
 def kernel_model(name, der):
@@ -487,6 +491,8 @@ def kernel_model(name, der):
         "scan_kernel<embed>+finish": dict(bytes=2.0 + d8, alu=CHACHA_ALU_PER_BYTE * d8),
         "scan_kernel<extract>+finish": dict(bytes=1.0 + d8, alu=CHACHA_ALU_PER_BYTE * d8),
         "stats_kernel": dict(bytes=2.0, alu=0.0),
+        "coder_encode_kernel": dict(bytes=1.0, alu=CODER_ALU_PER_SYMBOL),   # per symbol: its byte of ceta
+        "lmr_pack+header+coder_decode_kernels": dict(bytes=0.125, alu=CODER_ALU_PER_SYMBOL),  # per symbol: its bit
     }.get(name, dict(bytes=0.0, alu=0.0))
 
 
@@ -512,8 +518,8 @@ def roofline(prof, peaks, B, HW, cap, method):
         tops = m["alu"] * p["pixels"] / sec / 1e12
         kern[name] = {"ms_total": p["ms"], "launches": p["launches"], "ms_per_launch": p["ms"] / p["launches"],
                       "algorithmic_GBps": gbs, "hbm_frac": gbs / hbm_peak,
-                      "chacha_alu_Tops": tops, "alu_frac": tops / alu_peak,
-                      "bytes_per_px": m["bytes"], "chacha_alu_ops_per_px": m["alu"]}
+                      "alu_Tops": tops, "alu_frac": tops / alu_peak,
+                      "bytes_per_px": m["bytes"], "alu_ops_per_unit": m["alu"]}
     total = sum(p["ms"] for p in prof.values()) or 1.0
     for k in kern:
         kern[k]["share"] = kern[k]["ms_total"] / total
@@ -525,10 +531,13 @@ def roofline(prof, peaks, B, HW, cap, method):
         d = {"kernel": dom, "bound": "hbm", "achieved": k["algorithmic_GBps"], "peak": hbm_peak, "unit": "GB/s",
              "frac": k["hbm_frac"], "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)"}
     else:
-        d = {"kernel": dom, "bound": "alu", "achieved": k["chacha_alu_Tops"], "peak": alu_peak,
+        d = {"kernel": dom, "bound": "alu", "achieved": k["alu_Tops"], "peak": alu_peak,
              "unit": "Tops/s", "frac": k["alu_frac"],
              "peak_source": "148 SMs x 64 ALU-pipe int32 lanes/clk x sm_max_mhz (B300_MICROARCH pipe rates; "
                             "DESIGN.md §5.4)",
+             "ops_model": ("ChaCha20: 10 ALU ops per keystream byte" if "coder" not in dom else
+                           f"tile coder: {CODER_ALU_PER_SYMBOL:.0f} integer ops per coded symbol (DESIGN.md §5.6); "
+                           "a serial chain per tile, ~112 tiles in flight per SM"),
              "hbm": {"achieved_GBps": k["algorithmic_GBps"], "peak": hbm_peak, "frac": k["hbm_frac"]}}
     d["share_of_step"] = k["share"]
     px_launch = prof[dom]["pixels"] / prof[dom]["launches"]

@@ -159,8 +159,9 @@ uint64_t mmsb_kernel_launches(void);
 /* Live per-kernel timing.  mmsb_profile_enable(1) clears the record and brackets every later
  * kernel launch with CUDA events on its launch stream; mmsb_profile_enable(0) stops.  After the
  * caller synchronises, mmsb_profile_read(k, ...) returns, for kernel class k in [0, K), its name,
- * the summed event time in ms, the number of launches and the pixels they processed; the return
- * value is K (the number of kernel classes), or < 0 for an invalid k / unfinished events. */
+ * the summed event time in ms, the number of launches and the pixels they processed (for the LMR
+ * tile coder classes: the symbols coded / decoded, counted on the device); the return value is K
+ * (the number of kernel classes), or < 0 for an invalid k / unfinished events. */
 void mmsb_profile_enable(int on);
 int mmsb_profile_read(int kernel, const char **name, double *total_ms, int64_t *launches, int64_t *units);
 

@@ -611,7 +611,8 @@ template <int NW>
 __global__ void __launch_bounds__(kFastThreads, 1) coder_encode_fast_kernel(Geo g, int wave, const uint8_t *__restrict__ ceta,
                                                                          const LmrPlan *__restrict__ plan,
                                                                          uint8_t *__restrict__ streams,
-                                                                         int32_t *__restrict__ sizes) {
+                                                                         int32_t *__restrict__ sizes,
+                                                                         unsigned long long *__restrict__ sym_count) {
     extern __shared__ __align__(16) uint16_t p0s[];
     const int tid = threadIdx.x;
     const int Tc = lmr_tile_count(g.H, g.W, g.tile_log2);
@@ -636,6 +637,10 @@ __global__ void __launch_bounds__(kFastThreads, 1) coder_encode_fast_kernel(Geo 
     const int TN = g.W / w;
     const int y0 = (tile / TN) * th, x0 = (tile % TN) * w;
     const int h = g.H - y0 < th ? g.H - y0 : th;
+    if (sym_count) {                                                   // profiling: coded symbols
+        const unsigned v = __reduce_add_sync(am, (unsigned)(h * w));
+        if ((tid & 31) == __ffs(am) - 1) atomicAdd(sym_count, (unsigned long long)v);
+    }
     const uint32_t bsub = slot == 0 ? 0u : (uint32_t)(0x80 - plan[img].order[wave]) * 0x01010101u;
     const int cap = lmr_tile_cap(g.tile_log2, g.H, g.W);
 
@@ -759,7 +764,8 @@ __global__ void __launch_bounds__(kFastThreads, 1) coder_decode_fast_kernel(Geo 
                                                                          const int32_t *__restrict__ offsets,
                                                                          const int32_t *__restrict__ sizes,
                                                                          uint32_t *__restrict__ eta_bits,
-                                                                         uint32_t *__restrict__ map_bits) {
+                                                                         uint32_t *__restrict__ map_bits,
+                                                                         unsigned long long *__restrict__ sym_count) {
     extern __shared__ __align__(16) uint16_t p0s[];
     const int tid = threadIdx.x;
     const int TcM = g.ntiles_coder;
@@ -786,6 +792,10 @@ __global__ void __launch_bounds__(kFastThreads, 1) coder_decode_fast_kernel(Geo 
     const int TN = g.W / w;
     const int y0 = (tile / TN) * th, x0 = (tile % TN) * w;
     const int h = g.H - y0 < th ? g.H - y0 : th;
+    if (sym_count) {                                                   // profiling: decoded symbols
+        const unsigned v = __reduce_add_sync(am, (unsigned)(h * w));
+        if ((tid & 31) == __ffs(am) - 1) atomicAdd(sym_count, (unsigned long long)v);
+    }
 
     const int k = (plane == 0 ? 0 : Tc) + tile;
     FastIn in;
@@ -887,16 +897,16 @@ void launch_lmr_plan(const Geo &g, const uint32_t *hist, LmrPlan *plan, cudaStre
 }
 
 void launch_coder_encode(const Geo &g, int wave, const uint8_t *ceta, const LmrPlan *plan, uint8_t *streams,
-                         int32_t *sizes, cudaStream_t st) {
+                         int32_t *sizes, unsigned long long *sym_count, cudaStream_t st) {
     lmr_set_smem_attrs();
     const int Tc = lmr_tile_count(g.H, g.W, g.tile_log2);
     const long long total = (long long)g.B * (wave == 0 ? 2 : 1) * Tc;
     const unsigned grid = (unsigned)((total + kCoderThreads - 1) / kCoderThreads);
     const unsigned fgrid = (unsigned)((total + kFastThreads - 1) / kFastThreads);
     switch (lmr_tile_side(g.tile_log2, g.W)) {
-        case 32: coder_encode_fast_kernel<1><<<fgrid, kFastThreads, fast_smem(), st>>>(g, wave, ceta, plan, streams, sizes); break;
-        case 64: coder_encode_fast_kernel<2><<<fgrid, kFastThreads, fast_smem(), st>>>(g, wave, ceta, plan, streams, sizes); break;
-        case 128: coder_encode_fast_kernel<4><<<fgrid, kFastThreads, fast_smem(), st>>>(g, wave, ceta, plan, streams, sizes); break;
+        case 32: coder_encode_fast_kernel<1><<<fgrid, kFastThreads, fast_smem(), st>>>(g, wave, ceta, plan, streams, sizes, sym_count); break;
+        case 64: coder_encode_fast_kernel<2><<<fgrid, kFastThreads, fast_smem(), st>>>(g, wave, ceta, plan, streams, sizes, sym_count); break;
+        case 128: coder_encode_fast_kernel<4><<<fgrid, kFastThreads, fast_smem(), st>>>(g, wave, ceta, plan, streams, sizes, sym_count); break;
         default: coder_encode_kernel<<<grid, kCoderThreads, coder_smem(), st>>>(g, wave, ceta, plan, streams, sizes);
     }
 }
@@ -917,7 +927,7 @@ void launch_lmr_msb_write(const Geo &g, const LmrPlan *plan, const int32_t *size
 
 void launch_lmr_decode(const Geo &g, bool want_eta, const uint8_t *marked, uint8_t *mbuf, int32_t *lmr_b,
                        int32_t *lmr_t, int32_t *offsets, int32_t *sizes, uint32_t *eta_bits, uint32_t *map_bits,
-                       int32_t *status, int64_t *msg_bits_out, cudaStream_t st) {
+                       int32_t *status, int64_t *msg_bits_out, unsigned long long *sym_count, cudaStream_t st) {
     lmr_set_smem_attrs();
     const long long n16 = (long long)g.B * g.HW / 16;
     lmr_pack_kernel<<<(unsigned)((n16 + 255) / 256 < 148 * 16 ? (n16 + 255) / 256 : 148 * 16), 256, 0, st>>>(
@@ -928,11 +938,11 @@ void launch_lmr_decode(const Geo &g, bool want_eta, const uint8_t *marked, uint8
     const unsigned fgrid = (unsigned)((total + kFastThreads - 1) / kFastThreads);
     switch (lmr_tile_side(g.tile_log2, g.W)) {
         case 32: coder_decode_fast_kernel<1><<<fgrid, kFastThreads, fast_smem(), st>>>(
-                     g, want_eta ? 1 : 0, mbuf, lmr_b, lmr_t, offsets, sizes, eta_bits, map_bits); break;
+                     g, want_eta ? 1 : 0, mbuf, lmr_b, lmr_t, offsets, sizes, eta_bits, map_bits, sym_count); break;
         case 64: coder_decode_fast_kernel<2><<<fgrid, kFastThreads, fast_smem(), st>>>(
-                     g, want_eta ? 1 : 0, mbuf, lmr_b, lmr_t, offsets, sizes, eta_bits, map_bits); break;
+                     g, want_eta ? 1 : 0, mbuf, lmr_b, lmr_t, offsets, sizes, eta_bits, map_bits, sym_count); break;
         case 128: coder_decode_fast_kernel<4><<<fgrid, kFastThreads, fast_smem(), st>>>(
-                     g, want_eta ? 1 : 0, mbuf, lmr_b, lmr_t, offsets, sizes, eta_bits, map_bits); break;
+                     g, want_eta ? 1 : 0, mbuf, lmr_b, lmr_t, offsets, sizes, eta_bits, map_bits, sym_count); break;
         default: coder_decode_kernel<<<dgrid, kCoderThreads, coder_smem(), st>>>(
                      g, want_eta ? 1 : 0, mbuf, lmr_b, lmr_t, offsets, sizes, eta_bits, map_bits);
     }

@@ -27,6 +27,11 @@ static std::mutex g_prof_mu;
 static bool g_prof_on = false;
 static std::vector<ProfRec> g_prof;
 static std::vector<cudaEvent_t> g_event_pool;
+// profiling: symbols coded / decoded by the tile coder (device counters, read by mmsb_profile_read)
+static unsigned long long *g_sym = nullptr;
+static unsigned long long *sym_counter(int which) {   // (called inside run_kernel, which holds g_prof_mu)
+    return g_prof_on && g_sym ? g_sym + which : nullptr;
+}
 
 static cudaEvent_t prof_event() {
     if (!g_event_pool.empty()) { cudaEvent_t e = g_event_pool.back(); g_event_pool.pop_back(); return e; }
@@ -132,7 +137,8 @@ static void lmr_decode_all(const Geo &g, const Layout &L, bool want_eta, const u
     run_kernel(K_LMR_DECODE, st, (long long)g.B * g.HW, [&] {
         launch_lmr_decode(g, want_eta, marked, at<uint8_t>(ws, L.mbuf), at<int32_t>(ws, L.lmr_b),
                           at<int32_t>(ws, L.lmr_t), at<int32_t>(ws, L.offsets), at<int32_t>(ws, L.sizes),
-                          at<uint32_t>(ws, L.eta_bits), at<uint32_t>(ws, L.map_bits), img_status, msg_bits_out, st);
+                          at<uint32_t>(ws, L.eta_bits), at<uint32_t>(ws, L.map_bits), img_status, msg_bits_out,
+                          sym_counter(1), st);
     }, 3);
 }
 
@@ -170,7 +176,7 @@ mmsb_status mmsb_content_owner_encode(const mmsb_shape *shape, const uint8_t *im
         for (int w = 0; w < 7; w++) {
             run_kernel(K_CODER_ENC, st, px, [&] {
                 launch_coder_encode(g, w, at<uint8_t>(ws, L.ceta), plan, at<uint8_t>(ws, L.streams),
-                                    at<int32_t>(ws, L.sizes), st);
+                                    at<int32_t>(ws, L.sizes), sym_counter(0), st);
             });
             run_kernel(K_LMR_FIT, st, px, [&] {
                 launch_lmr_fit(g, w, at<int32_t>(ws, L.sizes), plan, at<int32_t>(ws, L.offsets), st);
@@ -370,6 +376,10 @@ void mmsb_profile_enable(int on) {
     for (auto &r : g_prof) { g_event_pool.push_back(r.a); g_event_pool.push_back(r.b); }
     g_prof.clear();
     g_prof_on = on != 0;
+    if (g_prof_on) {
+        if (!g_sym && cudaMalloc(&g_sym, 2 * sizeof(unsigned long long)) != cudaSuccess) g_sym = nullptr;
+        if (g_sym) cudaMemset(g_sym, 0, 2 * sizeof(unsigned long long));
+    }
 }
 
 int mmsb_profile_read(int kernel, const char **name, double *total_ms, int64_t *launches, int64_t *units) {
@@ -384,6 +394,11 @@ int mmsb_profile_read(int kernel, const char **name, double *total_ms, int64_t *
         t += ms;
         n++;
         u += r.units;
+    }
+    if ((kernel == K_CODER_ENC || kernel == K_LMR_DECODE) && g_sym && n) {   // coded symbols, not pixels
+        unsigned long long c = 0;
+        if (cudaMemcpy(&c, g_sym + (kernel == K_CODER_ENC ? 0 : 1), sizeof c, cudaMemcpyDeviceToHost) == cudaSuccess)
+            u = (int64_t)c;
     }
     if (name) *name = kKernelNames[kernel];
     if (total_ms) *total_ms = t;

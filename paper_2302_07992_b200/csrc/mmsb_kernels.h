@@ -23,14 +23,15 @@ struct LmrPlan {
 
 void launch_lmr_plan(const Geo &g, const uint32_t *hist, LmrPlan *plan, cudaStream_t st);
 void launch_coder_encode(const Geo &g, int wave, const uint8_t *ceta, const LmrPlan *plan, uint8_t *streams,
-                         int32_t *sizes, cudaStream_t st);
+                         int32_t *sizes, unsigned long long *sym_count, cudaStream_t st);
 void launch_lmr_fit(const Geo &g, int wave, const int32_t *sizes, LmrPlan *plan, int32_t *offsets, cudaStream_t st);
 void launch_lmr_msb_write(const Geo &g, const LmrPlan *plan, const int32_t *sizes, const int32_t *offsets,
                           const uint8_t *streams, const uint32_t *hist, uint8_t *enc, int32_t *b_out, int64_t *cap_out,
                           int32_t *status, cudaStream_t st);
 void launch_lmr_decode(const Geo &g, bool want_eta, const uint8_t *marked, uint8_t *mbuf, int32_t *lmr_b,
                        int32_t *lmr_t, int32_t *offsets, int32_t *sizes, uint32_t *eta_bits, uint32_t *map_bits,
-                       int32_t *status, int64_t *msg_bits_out, cudaStream_t st);
+                       int32_t *status, int64_t *msg_bits_out,
+                       unsigned long long *sym_count, cudaStream_t st);
 int lmr_tile_cap_host(int t, int H, int W);
 
 // per-call device state of the fused encode / recover kernels (k_fused.cu)
