@@ -31,6 +31,8 @@ __host__ __device__ inline int lmr_tile_cap(int t, int H, int W) {   // >= 1.1 *
     const int n = lmr_tile_side(t, H) * lmr_tile_side(t, W);
     return n / 8 + n / 64 + 64;
 }
+// stream slot stride: cap + slack for the fast encoder's unchecked digit stores (<= 32 per half-word)
+__host__ __device__ inline int lmr_tile_stride(int t, int H, int W) { return lmr_tile_cap(t, H, W) + 48; }
 
 // context bits from the two previous rows: rows are MSB-first with pixel x at padded bit x+2
 __device__ __forceinline__ uint32_t row_window(const uint32_t *row, int pos, int nbits) {
@@ -103,7 +105,7 @@ __global__ void __launch_bounds__(kCoderThreads) coder_encode_kernel(Geo g, int 
     for (int r = 0; r < 3; r++)
         for (int k = 0; k < kRowWords; k++) R[r][k] = 0;
 
-    RcEnc e{0, 0xFFFFFFFFu, 0, 1, streams + (((size_t)img * 2 + slot) * Tc + tile) * cap, 0, cap};
+    RcEnc e{0, 0xFFFFFFFFu, 0, 1, streams + (((size_t)img * 2 + slot) * Tc + tile) * lmr_tile_stride(g.tile_log2, g.H, g.W), 0, cap};
     const uint8_t *src = ceta + (size_t)img * g.HW;
     if (active) {
         for (int y = 0; y < h; y++) {
@@ -274,7 +276,8 @@ __global__ void __launch_bounds__(256) lmr_msb_write_kernel(Geo g, const LmrPlan
     if (pl.state != 1) return;
     const int32_t *sz = sizes + (size_t)img * 2 * Tc;
     const int32_t *off = offsets + (size_t)img * 2 * Tc;
-    const uint8_t *slots = streams + (size_t)img * 2 * Tc * cap;
+    const int stride = lmr_tile_stride(g.tile_log2, g.H, g.W);
+    const uint8_t *slots = streams + (size_t)img * 2 * Tc * stride;
     const long long hdr = 7 + 32ll * Tc;                        // header bits before the stream bytes
     const long long total = (pl.K - hdr) / 8;                   // stream bytes
     for (long long p = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * 16; p < pl.K;
@@ -284,8 +287,8 @@ __global__ void __launch_bounds__(256) lmr_msb_write_kernel(Geo g, const LmrPlan
         if (p >= hdr) {
             const long long q = p - hdr, q0 = q >> 3;
             const int sh = (int)(q & 7);                        // bit offset inside byte q0
-            const uint32_t b3 = (stream_bytes2(Tc, sz, off, slots, cap, q0, total) << 8) |
-                                (q0 + 2 < total ? stream_bytes2(Tc, sz, off, slots, cap, q0 + 2, total) >> 8 : 0u);
+            const uint32_t b3 = (stream_bytes2(Tc, sz, off, slots, stride, q0, total) << 8) |
+                                (q0 + 2 < total ? stream_bytes2(Tc, sz, off, slots, stride, q0 + 2, total) >> 8 : 0u);
             bits16 = (b3 >> (8 - sh)) & 0xFFFFu;
         } else {
             for (int i = 0; i < 16; i++) {
@@ -296,7 +299,7 @@ __global__ void __launch_bounds__(256) lmr_msb_write_kernel(Geo g, const LmrPlan
                 else if (r < hdr) bit = ((uint32_t)sz[(r - 7) >> 4] >> (15 - ((r - 7) & 15))) & 1u;
                 else {
                     const long long q = r - hdr;
-                    const uint32_t by = stream_bytes2(Tc, sz, off, slots, cap, q >> 3, total) >> 8;
+                    const uint32_t by = stream_bytes2(Tc, sz, off, slots, stride, q >> 3, total) >> 8;
                     bit = (by >> (7 - (q & 7))) & 1u;
                 }
                 bits16 |= bit << (15 - i);
@@ -576,34 +579,49 @@ __device__ __forceinline__ void st_u8_if(bool c, uint8_t *p, uint32_t v) {
 // cache byte and a count of pending 0xFF bytes so that a carry out of low can still reach them;
 // its output is the digit string of the exact code value (a carry never reaches a byte it has
 // already written -- the nested intervals never leave the initial one), one digit per shift.
-// Here a 40-bit window [cache digit | 32-bit low] shifts its top digit straight to memory and a
-// carry out of the window (rare) is added into the written bytes (0xFF -> 0x00 backwards, +1 on
-// the first byte below 0xFF): the same bytes, with no per-shift cache / run bookkeeping.
+// Here the window [hi = cache digit (+ carry in bit 8) | lo = low] shifts its top digits straight
+// to memory with predicated stores, branch-free; a carry out of the window is recorded in a
+// per-half-word mask (bit k: into the digit before the k-th digit of the half) and added into
+// the written bytes after the half (0xFF -> 0x00 backwards, +1 on the first byte below 0xFF).
+// Stores go to the tile's slot while n <= cap at the half's start, else into the slot's slack
+// (the stream is then over cap and discarded), so none needs a bound check.
 struct FastEnc {
-    uint64_t acc;                             // bits 39..32: next digit to leave; 31..0: low; >= 40: carries
-    uint32_t range;
-    uint8_t *out;
-    int n, cap;
-    __device__ __forceinline__ void carry_fix() {                    // pending carries into written digits
-        if (__builtin_expect((acc >> 40) != 0, 0)) {
-            uint32_t c = (uint32_t)(acc >> 40);
-            acc &= (1ull << 40) - 1;
+    uint32_t hi, lo, range;
+    uint8_t *out, *obase;                     // slot; base of this half's stores (out, or shifted into the slack)
+    int n, cap, n0;                           // digits so far; n at the half's start
+    uint32_t cm;                              // carries of this half
+    __device__ __forceinline__ void begin_half() {
+        obase = n <= cap ? out : out + (cap - n);
+        n0 = n;
+        cm = 0;
+    }
+    __device__ __forceinline__ void emit(int s) {                    // s = 0..2 digits out
+        cm |= (hi >> 8) << (n - n0);
+        const uint32_t h8 = hi & 0xFFu;
+        uint8_t *op = obase + n;
+        st_u8_if(s >= 1, op, h8);
+        st_u8_if(s >= 2, op + 1, lo >> 24);
+        hi = __funnelshift_l(lo, h8, 8 * s) & 0xFFu;
+        lo <<= 8 * s;
+        n += s;
+    }
+    __device__ __forceinline__ void end_half(unsigned am) {
+        if (__any_sync(am, cm != 0)) {
 #pragma unroll 1
-            for (int i = (n < cap ? n : cap) - 1; i >= 0 && c; i--) {   // (asm: ordered after the stores)
-                uint32_t v;
-                asm volatile("ld.global.u8 %0, [%1];" : "=r"(v) : "l"(out + i));
-                v += c;
-                st_u8_if(true, out + i, v);
-                c = v >> 8;
+            while (cm) {
+                const int k = __ffs(cm) - 1;
+                cm &= cm - 1;
+                uint32_t c = 1;
+#pragma unroll 1
+                for (int i = n0 + k - 1; i >= 0 && c && i < cap; i--) {      // (asm: ordered after the stores)
+                    uint32_t v;
+                    asm volatile("ld.global.u8 %0, [%1];" : "=r"(v) : "l"(out + i));
+                    v += c;
+                    st_u8_if(true, out + i, v);
+                    c = v >> 8;
+                }
             }
         }
-    }
-    __device__ __forceinline__ void shift(int s) {                   // s = 0..2 digits out
-        carry_fix();
-        st_u8_if(s >= 1, out + (n < cap ? n : cap - 1), (uint32_t)(acc >> 32));
-        st_u8_if(s >= 2, out + (n + 1 < cap ? n + 1 : cap - 1), (uint32_t)acc >> 24);
-        n += s;
-        acc = (acc << (8 * s)) & ((1ull << 40) - 1);
     }
 };
 
@@ -644,7 +662,8 @@ __global__ void __launch_bounds__(kFastThreads, 1) coder_encode_fast_kernel(Geo 
     const uint32_t bsub = slot == 0 ? 0u : (uint32_t)(0x80 - plan[img].order[wave]) * 0x01010101u;
     const int cap = lmr_tile_cap(g.tile_log2, g.H, g.W);
 
-    FastEnc e{0, 0xFFFFFFFFu, streams + (((size_t)img * 2 + slot) * Tc + tile) * cap, 0, cap};
+    uint8_t *slot_out = streams + (((size_t)img * 2 + slot) * Tc + tile) * lmr_tile_stride(g.tile_log2, g.H, g.W);
+    FastEnc e{0, 0, 0xFFFFFFFFu, slot_out, slot_out, 0, cap, 0, 0};
     const uint8_t *src = ceta + (size_t)img * g.HW + x0;
     uint32_t p1[NW], p2[NW];
 #pragma unroll
@@ -687,6 +706,7 @@ __global__ void __launch_bounds__(kFastThreads, 1) coder_encode_fast_kernel(Geo 
             uint32_t t1, t2;
             half_slices(p1, p2, q + 1, t1, t2);                        // next half (unused past the row)
             const uint32_t cb = pick(cw, q >> 1) << (16 * (q & 1));
+            e.begin_half();
 #pragma unroll
             for (int J = 0; J < 16; J++) {
                 const bool bit = (cb >> (31 - J)) & 1u;
@@ -695,26 +715,29 @@ __global__ void __launch_bounds__(kFastThreads, 1) coder_encode_fast_kernel(Geo 
                 const uint32_t np = lds_u16(anctx);
                 const uint32_t bound = (e.range >> 16) * p;
                 const uint32_t pu = bit ? p - (p >> 4) : p + ((65536u - p) >> 4);
-                e.acc += bit ? bound : 0u;
+                const uint64_t a = (uint64_t)e.lo + (bit ? bound : 0u);       // low += bound (carry into hi)
+                e.lo = (uint32_t)a;
+                e.hi += (uint32_t)(a >> 32);
                 e.range = bit ? e.range - bound : bound;
                 sts_u16(actx, pu);
                 const int s = __clz(e.range) >> 3;                     // 0..2 bytes to shift out
-                if (__any_sync(am, s != 0)) {
-                    e.shift(s);
-                    e.range <<= 8 * s;
-                }
+                e.emit(s);
+                e.range <<= 8 * s;
                 p = anctx == actx ? pu : np;
                 actx = anctx;
                 prev8 = bit ? 256u : 0u;
             }
+            e.end_half(am);
             s1 = t1;
             s2 = t2;
         }
 #pragma unroll
         for (int k = 0; k < NW; k++) { p2[k] = p1[k]; p1[k] = cw[k]; }
     }
+    e.begin_half();                                                    // flush: the window's 5 digits
 #pragma unroll 1
-    for (int i = 0; i < 5; i++) e.shift(1);                           // flush: the window's 5 digits
+    for (int i = 0; i < 5; i++) e.emit(1);
+    e.end_half(am);
     sizes[((size_t)img * 2 + slot) * Tc + tile] = (e.n <= cap && e.n <= 65535) ? e.n : -1;
 }
 
@@ -875,6 +898,7 @@ __global__ void __launch_bounds__(kFastThreads, 1) coder_decode_fast_kernel(Geo 
 
 // ---------------------------------------------------------------------------- launchers
 int lmr_tile_cap_host(int t, int H, int W) { return lmr_tile_cap(t, H, W); }
+int lmr_tile_stride_host(int t, int H, int W) { return lmr_tile_stride(t, H, W); }
 
 static size_t coder_smem() { return 1024 * 32 * sizeof(uint16_t); }
 

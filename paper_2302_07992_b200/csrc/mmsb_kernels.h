@@ -33,6 +33,7 @@ void launch_lmr_decode(const Geo &g, bool want_eta, const uint8_t *marked, uint8
                        int32_t *status, int64_t *msg_bits_out,
                        unsigned long long *sym_count, cudaStream_t st);
 int lmr_tile_cap_host(int t, int H, int W);
+int lmr_tile_stride_host(int t, int H, int W);
 
 // per-call device state of the fused encode / recover kernels (k_fused.cu)
 struct TileWS {
