@@ -741,15 +741,17 @@ __global__ void __launch_bounds__(kFastThreads, 1) coder_encode_fast_kernel(Geo 
     sizes[((size_t)img * 2 + slot) * Tc + tile] = (e.n <= cap && e.n <= 65535) ? e.n : -1;
 }
 
-// decoder input: the tile's stream as a 64-bit MSB-aligned bit buffer (nb valid bits, >= 32 at
-// every symbol), refilled from stream words funnel-shifted out of the big-endian words of the
-// MSB-plane bytes (the stream starts at an arbitrary bit); stream bytes past nbytes read as 0
+// decoder input: the tile's stream as a 96-bit MSB-aligned bit buffer b0:b1:b2 (nb valid bits),
+// refilled from stream words funnel-shifted out of the big-endian words of the MSB-plane bytes
+// (the stream starts at an arbitrary bit); stream bytes past nbytes read as 0.  A symbol takes at
+// most 16 bits, so the buffer is topped up to >= 64 bits once per 4 symbols (behind a warp vote)
+// and the per-symbol shift is branch-free.
 struct FastIn {
     const uint32_t *w;                        // aligned word holding the next stream word's first bit
     uint32_t wa, wb, wc;                      // w[0], w[1] (big-endian), w[2] (raw)
     int sh;                                   // stream bit 0 = bit sh of the first word
     int valid;                                // stream bits left to deliver (8 nbytes - delivered)
-    uint64_t buf;
+    uint32_t b0, b1, b2;
     int nb;
     __device__ __forceinline__ uint32_t word() {                      // next 32 stream bits, masked
         const uint32_t v = __funnelshift_l(wb, wa, sh);
@@ -768,14 +770,29 @@ struct FastIn {
         wa = bswap32(__ldg(w));
         wb = bswap32(__ldg(w + 1));
         wc = __ldg(w + 2);
-        const uint32_t hi = word(), lo = word();
-        buf = ((uint64_t)hi << 32) | lo;
-        nb = 64;
+        b0 = word();
+        b1 = word();
+        b2 = word();
+        nb = 96;
     }
-    __device__ __forceinline__ void refill() {
-        if (nb < 32) {
-            buf |= (uint64_t)word() << (32 - nb);
-            nb += 32;
+    __device__ __forceinline__ void consume(int s8) {                // s8 = 0, 8 or 16 bits
+        b0 = __funnelshift_l(b1, b0, s8);
+        b1 = __funnelshift_l(b2, b1, s8);
+        b2 <<= s8;
+        nb -= s8;
+    }
+    __device__ __forceinline__ void refill() {                       // nb in [0, 96] -> [64, 96]
+#pragma unroll
+        for (int i = 0; i < 2; i++) {
+            if (nb <= 64) {
+                const uint32_t v = word();
+                const int r = nb & 31;
+                const uint32_t hi = v >> r, lo = __funnelshift_lc(0u, v, 32 - r);   // v at bit offset nb
+                if (nb < 32) { b0 |= hi; b1 |= lo; }
+                else if (nb < 64) { b1 |= hi; b2 |= lo; }
+                else b2 |= v;
+                nb += 32;
+            }
         }
     }
 };
@@ -825,9 +842,12 @@ __global__ void __launch_bounds__(kFastThreads, 1) coder_decode_fast_kernel(Geo 
     in.init(mbuf + (size_t)img * (g.HW / 8), 7 + 32ll * Tc + 8ll * offsets[(size_t)img * 2 * TcM + k],
             sizes[(size_t)img * 2 * TcM + k]);
     // the encoder's first byte is the initial cache byte: code = stream bytes 1..4
-    uint32_t range = 0xFFFFFFFFu, code = (uint32_t)(in.buf >> 24);
-    in.buf <<= 40;
-    in.nb = 24;
+    uint32_t range = 0xFFFFFFFFu, code = __funnelshift_l(in.b1, in.b0, 8);
+    in.b0 = in.b1;
+    in.b1 = in.b2;
+    in.b2 = 0;
+    in.nb = 64;
+    in.consume(8);
     in.refill();
     uint32_t *plane_out = plane == 0 ? eta_bits : map_bits;
     uint32_t p1[NW], p2[NW];
@@ -851,6 +871,7 @@ __global__ void __launch_bounds__(kFastThreads, 1) coder_decode_fast_kernel(Geo 
             uint32_t hw = 0, lw = 0;
 #pragma unroll
             for (int J = 0; J < 16; J++) {
+                if ((J & 3) == 0 && __any_sync(am, in.nb < 64)) in.refill();   // >= 64 bits for 4 symbols
                 // both candidate contexts of the next symbol (its (0,-1) bit is the one decoded now)
                 const uint32_t nrows = J < 15 ? slice_ctx(s1, s2, J + 1) : slice_ctx(t1, t2, 0);
                 const uint32_t a0 = mbase + (prev8 | nrows) * sbytes, a1 = a0 + kHiOff;
@@ -862,15 +883,10 @@ __global__ void __launch_bounds__(kFastThreads, 1) coder_decode_fast_kernel(Geo 
                 range = bit ? range - bound : bound;
                 code = bit ? code - bound : code;
                 sts_u16(actx, bit ? pu1 : pu0);
-                const int s = __clz(range) >> 3;                      // 0..2 bytes to shift in
-                if (__any_sync(am, s != 0)) {
-                    const uint32_t top = (uint32_t)(in.buf >> 48);
-                    code = (code << (8 * s)) | (top >> (16 - 8 * s));
-                    range <<= 8 * s;
-                    in.buf <<= 8 * s;
-                    in.nb -= 8 * s;
-                    in.refill();
-                }
+                const int s8 = __clz(range) & 24;                     // 0, 8 or 16 bits to shift in
+                code = __funnelshift_l(in.b0, code, s8);
+                range <<= s8;
+                in.consume(s8);
                 hw |= bit ? 1u << (15 - J) : 0u;
                 lw |= bit ? 1u << J : 0u;
                 actx = bit ? a1 : a0;
