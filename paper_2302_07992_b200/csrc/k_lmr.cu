@@ -748,7 +748,7 @@ __global__ void __launch_bounds__(kFastThreads, 1) coder_encode_fast_kernel(Geo 
 // and the per-symbol shift is branch-free.
 struct FastIn {
     const uint32_t *w;                        // aligned word holding the next stream word's first bit
-    uint32_t wa, wb, wc;                      // w[0], w[1] (big-endian), w[2] (raw)
+    uint32_t wa, wb, wc, wd;                  // w[0], w[1] (big-endian), w[2], w[3] (raw: loads in flight)
     int sh;                                   // stream bit 0 = bit sh of the first word
     int valid;                                // stream bits left to deliver (8 nbytes - delivered)
     uint32_t b0, b1, b2;
@@ -758,9 +758,10 @@ struct FastIn {
         const uint32_t keep = valid >= 32 ? 0xFFFFFFFFu : (valid <= 0 ? 0u : ~(0xFFFFFFFFu >> valid));
         valid -= 32;
         wa = wb;
-        wb = bswap32(wc);                     // (wc is kept raw: its load is not waited on here)
+        wb = bswap32(wc);                     // (loaded two refills ago)
+        wc = wd;
         ++w;
-        wc = __ldg(w + 2);
+        wd = __ldg(w + 3);
         return v & keep;
     }
     __device__ __forceinline__ void init(const uint8_t *m, long long bit0, int nbytes) {
@@ -770,6 +771,7 @@ struct FastIn {
         wa = bswap32(__ldg(w));
         wb = bswap32(__ldg(w + 1));
         wc = __ldg(w + 2);
+        wd = __ldg(w + 3);
         b0 = word();
         b1 = word();
         b2 = word();

@@ -95,7 +95,7 @@ static Layout layout(const Geo &g) {
     L.streams = o; o = align256(o + (lmr ? B * 2 * Tc * lmr_tile_stride_host(g.tile_log2, g.H, g.W) : 0));
     L.sizes = o; o = align256(o + (lmr ? B * 2 * Tc * 4 : 0));
     L.offsets = o; o = align256(o + (lmr ? B * 2 * Tc * 4 : 0));
-    L.mbuf = o; o = align256(o + (lmr ? B * g.HW / 8 + 64 : 0));   // + decoder look-ahead past the last stream
+    L.mbuf = o; o = align256(o + (lmr ? B * g.HW / 8 + 128 : 0));   // + decoder look-ahead past the last stream
     L.rstat = o; o = align256(o + B * 4);
     L.total = o;
     return L;
