@@ -783,19 +783,31 @@ struct FastIn {
         b2 <<= s8;
         nb -= s8;
     }
-    __device__ __forceinline__ void refill() {                       // nb in [0, 96] -> [64, 96]
-#pragma unroll
-        for (int i = 0; i < 2; i++) {
-            if (nb <= 64) {
-                const uint32_t v = word();
-                const int r = nb & 31;
-                const uint32_t hi = v >> r, lo = __funnelshift_lc(0u, v, 32 - r);   // v at bit offset nb
-                if (nb < 32) { b0 |= hi; b1 |= lo; }
-                else if (nb < 64) { b1 |= hi; b2 |= lo; }
-                else b2 |= v;
-                nb += 32;
-            }
+    // one more stream word at bit offset nb (nb <= 64) when `need`, branch-free (predicated load)
+    __device__ __forceinline__ void add_word_if(bool need) {
+        const int vc = valid < 0 ? 0 : (valid > 32 ? 32 : valid);
+        const uint32_t keep = ~__funnelshift_rc(0xFFFFFFFFu, 0u, vc);  // top vc bits: bytes past the end read 0
+        const uint32_t v = need ? __funnelshift_l(wb, wa, sh) & keep : 0u;
+        if (need) {
+            valid -= 32;
+            wa = wb;
+            wb = bswap32(wc);                 // (loaded two words ago)
+            wc = wd;
+            ++w;
+            wd = __ldg(w + 3);
         }
+        const int r = nb & 31;
+        const uint32_t hi = v >> r, lo = __funnelshift_lc(0u, v, 32 - r);
+        b0 |= nb < 32 ? hi : 0u;
+        b1 |= nb < 32 ? lo : (nb < 64 ? hi : 0u);
+        b2 |= nb < 32 ? 0u : (nb < 64 ? lo : v);
+        nb += need ? 32 : 0;
+    }
+    // before each group of 4 symbols (<= 64 bits): nb in [0, 96] -> [64, 96]; the second word is
+    // rarely needed (a group that took more than 32 bits)
+    __device__ __forceinline__ void refill(unsigned am) {
+        add_word_if(nb <= 64);
+        if (__any_sync(am, nb < 64)) add_word_if(nb < 64);
     }
 };
 
@@ -850,7 +862,7 @@ __global__ void __launch_bounds__(kFastThreads, 1) coder_decode_fast_kernel(Geo 
     in.b2 = 0;
     in.nb = 64;
     in.consume(8);
-    in.refill();
+    in.refill(am);
     uint32_t *plane_out = plane == 0 ? eta_bits : map_bits;
     uint32_t p1[NW], p2[NW];
 #pragma unroll
@@ -873,7 +885,7 @@ __global__ void __launch_bounds__(kFastThreads, 1) coder_decode_fast_kernel(Geo 
             uint32_t hw = 0, lw = 0;
 #pragma unroll
             for (int J = 0; J < 16; J++) {
-                if ((J & 3) == 0 && __any_sync(am, in.nb < 64)) in.refill();   // >= 64 bits for 4 symbols
+                if ((J & 3) == 0) in.refill(am);                       // >= 64 bits for 4 symbols
                 // both candidate contexts of the next symbol (its (0,-1) bit is the one decoded now)
                 const uint32_t nrows = J < 15 ? slice_ctx(s1, s2, J + 1) : slice_ctx(t1, t2, 0);
                 const uint32_t a0 = mbase + (prev8 | nrows) * sbytes, a1 = a0 + kHiOff;
