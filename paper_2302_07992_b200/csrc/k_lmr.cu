@@ -587,33 +587,37 @@ __device__ __forceinline__ void st_u8_if(bool c, uint8_t *p, uint32_t v) {
 // (the stream is then over cap and discarded), so none needs a bound check.
 struct FastEnc {
     uint32_t hi, lo, range;
-    uint8_t *out, *obase;                     // slot; base of this half's stores (out, or shifted into the slack)
-    int n, cap, n0;                           // digits so far; n at the half's start
+    uint8_t *out, *obase;                     // slot; this half's stores at obase + k (obase = slot + n0, or in the slack)
+    int n, cap, n0;                           // digits before this half; k = digits in this half
+    int k;
     uint32_t cm;                              // carries of this half
     __device__ __forceinline__ void begin_half() {
-        obase = n <= cap ? out : out + (cap - n);
+        n += k;
+        obase = n <= cap ? out + n : out + cap;
         n0 = n;
+        k = 0;
         cm = 0;
     }
-    __device__ __forceinline__ void emit(int s) {                    // s = 0..2 digits out
-        cm |= (hi >> 8) << (n - n0);
+    // s = 0..2 digits out; p1 = (s >= 1), p2 = (s >= 2)
+    __device__ __forceinline__ void emit(bool p1, bool p2, int s8) {
+        cm |= (hi >> 8) << k;
         const uint32_t h8 = hi & 0xFFu;
-        uint8_t *op = obase + n;
-        st_u8_if(s >= 1, op, h8);
-        st_u8_if(s >= 2, op + 1, lo >> 24);
-        hi = __funnelshift_l(lo, h8, 8 * s) & 0xFFu;
-        lo <<= 8 * s;
-        n += s;
+        uint8_t *op = obase + k;
+        st_u8_if(p1, op, h8);
+        st_u8_if(p2, op + 1, lo >> 24);
+        hi = __funnelshift_l(lo, h8, s8) & 0xFFu;
+        lo <<= s8;
+        k += s8 >> 3;
     }
     __device__ __forceinline__ void end_half(unsigned am) {
         if (__any_sync(am, cm != 0)) {
 #pragma unroll 1
             while (cm) {
-                const int k = __ffs(cm) - 1;
+                const int j = __ffs(cm) - 1;
                 cm &= cm - 1;
                 uint32_t c = 1;
 #pragma unroll 1
-                for (int i = n0 + k - 1; i >= 0 && c && i < cap; i--) {      // (asm: ordered after the stores)
+                for (int i = n0 + j - 1; i >= 0 && c && i < cap; i--) {      // (asm: ordered after the stores)
                     uint32_t v;
                     asm volatile("ld.global.u8 %0, [%1];" : "=r"(v) : "l"(out + i));
                     v += c;
@@ -663,7 +667,7 @@ __global__ void __launch_bounds__(kFastThreads, 1) coder_encode_fast_kernel(Geo 
     const int cap = lmr_tile_cap(g.tile_log2, g.H, g.W);
 
     uint8_t *slot_out = streams + (((size_t)img * 2 + slot) * Tc + tile) * lmr_tile_stride(g.tile_log2, g.H, g.W);
-    FastEnc e{0, 0, 0xFFFFFFFFu, slot_out, slot_out, 0, cap, 0, 0};
+    FastEnc e{0, 0, 0xFFFFFFFFu, slot_out, slot_out, 0, cap, 0, 0, 0};
     const uint8_t *src = ceta + (size_t)img * g.HW + x0;
     uint32_t p1[NW], p2[NW];
 #pragma unroll
@@ -705,11 +709,12 @@ __global__ void __launch_bounds__(kFastThreads, 1) coder_encode_fast_kernel(Geo 
         for (int q = 0; q < 2 * NW; q++) {
             uint32_t t1, t2;
             half_slices(p1, p2, q + 1, t1, t2);                        // next half (unused past the row)
-            const uint32_t cb = pick(cw, q >> 1) << (16 * (q & 1));
+            uint32_t cb = pick(cw, q >> 1) << (16 * (q & 1));          // the half's bits from the MSB, rolled
             e.begin_half();
 #pragma unroll
             for (int J = 0; J < 16; J++) {
-                const bool bit = (cb >> (31 - J)) & 1u;
+                const bool bit = (int)cb < 0;
+                cb <<= 1;
                 const uint32_t nrows = J < 15 ? slice_ctx(s1, s2, J + 1) : slice_ctx(t1, t2, 0);
                 const uint32_t anctx = mbase + (prev8 | nrows) * sbytes + (bit ? kHiOff : 0u);
                 const uint32_t np = lds_u16(anctx);
@@ -720,9 +725,10 @@ __global__ void __launch_bounds__(kFastThreads, 1) coder_encode_fast_kernel(Geo 
                 e.hi += (uint32_t)(a >> 32);
                 e.range = bit ? e.range - bound : bound;
                 sts_u16(actx, pu);
-                const int s = __clz(e.range) >> 3;                     // 0..2 bytes to shift out
-                e.emit(s);
-                e.range <<= 8 * s;
+                const bool r24 = e.range < (1u << 24), r16 = e.range < (1u << 16);   // 1 / 2 digits out
+                const int s8 = (r24 ? 8 : 0) + (r16 ? 8 : 0);
+                e.emit(r24, r16, s8);
+                e.range <<= s8;
                 p = anctx == actx ? pu : np;
                 actx = anctx;
                 prev8 = bit ? 256u : 0u;
@@ -736,8 +742,9 @@ __global__ void __launch_bounds__(kFastThreads, 1) coder_encode_fast_kernel(Geo 
     }
     e.begin_half();                                                    // flush: the window's 5 digits
 #pragma unroll 1
-    for (int i = 0; i < 5; i++) e.emit(1);
+    for (int i = 0; i < 5; i++) e.emit(true, false, 8);
     e.end_half(am);
+    e.n += e.k;
     sizes[((size_t)img * 2 + slot) * Tc + tile] = (e.n <= cap && e.n <= 65535) ? e.n : -1;
 }
 
