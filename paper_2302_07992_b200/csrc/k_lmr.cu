@@ -14,6 +14,8 @@
 // One GPU thread codes one tile (the coder is serial within a tile).  Each thread's model
 // (1024 x u16) lives in shared memory interleaved across the 32 lanes of the warp
 // (entry ctx of lane l at u16 index ctx*32 + l: at most 2-way bank conflicts).
+#include <algorithm>
+
 #include "mmsb_device.cuh"
 #include "mmsb_kernels.h"
 
@@ -67,37 +69,50 @@ struct RcEnc {
     }
 };
 
+// work item gid of candidate wave `wave` (mmsb_kernels.h): image, stream slot (0 = eta,
+// 1 + c = candidate c), candidate index (-1 for eta) and tile; false past the wave's work
+struct WaveItem { int img, slot, cand, tile; };
+__device__ __forceinline__ bool wave_item(const Geo &g, int wave, int R, long long gid, const LmrEncWS &e, WaveItem &it) {
+    const int Tc = lmr_tile_count(g.H, g.W, g.tile_log2);
+    const int A = wave == 0 ? g.B : e.ctl->count[wave];
+    const int nc = wave == 0 ? 0 : e.ctl->nc[wave];
+    const int k = lmr_wave_k(wave, A, Tc, g.B, R, nc);
+    const int per = (wave == 0 ? 1 : 0) + k;                     // slots per image in this wave
+    if (gid >= (long long)A * per * Tc) return false;
+    const int i = (int)(gid / ((long long)per * Tc)), r = (int)(gid % ((long long)per * Tc));
+    const int j = r / Tc;
+    it.tile = r % Tc;
+    it.img = wave == 0 ? i : e.lists[(size_t)wave * g.B + i];
+    it.cand = wave == 0 ? j - 1 : nc + j;
+    it.slot = it.cand + 1;
+    return true;
+}
+
 // ======================================================================================
 // coder_encode_kernel: one thread per (image, plane slot, coder tile).
 //   slot 0 = rotated eta (MSB of I_r, eq. MSB_map) -- wave 0 only;
 //   slot 1 = rotated location map L_b = [c_r < b] of candidate order[wave].
 // Images already decided (state != 0) are skipped.
 // ======================================================================================
-__global__ void __launch_bounds__(kCoderThreads) coder_encode_kernel(Geo g, int wave, const uint8_t *__restrict__ ceta,
-                                                                     const LmrPlan *__restrict__ plan,
-                                                                     uint8_t *__restrict__ streams,
-                                                                     int32_t *__restrict__ sizes) {
+__global__ void __launch_bounds__(kCoderThreads) coder_encode_kernel(Geo g, int wave, int round_tiles, const uint8_t *__restrict__ ceta,
+                                                                     LmrEncWS ew) {
     extern __shared__ uint16_t p0s[];                                  // [1024][32]
     __shared__ uint32_t rows[kCoderThreads][3][kRowWords];
     const int lane = threadIdx.x;
     const int Tc = lmr_tile_count(g.H, g.W, g.tile_log2);
-    const int nslots = wave == 0 ? 2 : 1;
-    const long long gid = (long long)blockIdx.x * kCoderThreads + lane;
-    const long long total = (long long)g.B * nslots * Tc;
-    const bool active0 = gid < total;
-    const int img = active0 ? (int)(gid / ((long long)nslots * Tc)) : 0;
-    const int rem = active0 ? (int)(gid % ((long long)nslots * Tc)) : 0;
-    const int slot = wave == 0 ? rem / Tc : 1;
-    const int tile = rem % Tc;
-    const LmrPlan pl = plan[img];
-    const bool active = active0 && pl.state == 0;
+    WaveItem it{0, 0, -1, 0};
+    const bool active = wave_item(g, wave, round_tiles, (long long)blockIdx.x * kCoderThreads + lane, ew, it);
     if (!__any_sync(0xffffffffu, active)) return;
+    const int img = it.img, slot = it.slot, tile = it.tile;
+    const LmrPlan pl = ew.plan[img];
+    uint8_t *streams = ew.streams;
+    int32_t *sizes = ew.sizes;
 
     const int th = lmr_tile_side(g.tile_log2, g.H), tw = lmr_tile_side(g.tile_log2, g.W);
     const int TN = (g.W + tw - 1) / tw;
     const int y0 = (tile / TN) * th, x0 = (tile % TN) * tw;
     const int h = g.H - y0 < th ? g.H - y0 : th, w = g.W - x0 < tw ? g.W - x0 : tw;
-    const int b = slot == 0 ? 0 : pl.order[wave];
+    const int b = slot == 0 ? 0 : pl.order[it.cand < 0 ? 0 : it.cand];
     const int cap = lmr_tile_cap(g.tile_log2, g.H, g.W);
 
     for (int c = 0; c < 1024; c++) p0s[c * 32 + lane] = 32768;
@@ -105,7 +120,7 @@ __global__ void __launch_bounds__(kCoderThreads) coder_encode_kernel(Geo g, int 
     for (int r = 0; r < 3; r++)
         for (int k = 0; k < kRowWords; k++) R[r][k] = 0;
 
-    RcEnc e{0, 0xFFFFFFFFu, 0, 1, streams + (((size_t)img * 2 + slot) * Tc + tile) * lmr_tile_stride(g.tile_log2, g.H, g.W), 0, cap};
+    RcEnc e{0, 0xFFFFFFFFu, 0, 1, streams + (((size_t)img * kLmrSlots + slot) * Tc + tile) * lmr_tile_stride(g.tile_log2, g.H, g.W), 0, cap};
     const uint8_t *src = ceta + (size_t)img * g.HW;
     if (active) {
         for (int y = 0; y < h; y++) {
@@ -140,7 +155,7 @@ __global__ void __launch_bounds__(kCoderThreads) coder_encode_kernel(Geo g, int 
             // keep the two padding words beyond the row zero for the next rows' windows
         }
         for (int i = 0; i < 5; i++) e.shift_low();
-        sizes[((size_t)img * 2 + slot) * Tc + tile] = (e.n <= cap && e.n <= 65535) ? e.n : -1;
+        sizes[((size_t)img * kLmrSlots + slot) * Tc + tile] = (e.n <= cap && e.n <= 65535) ? e.n : -1;
     }
 }
 
@@ -148,8 +163,12 @@ __global__ void __launch_bounds__(kCoderThreads) coder_encode_kernel(Geo g, int 
 // lmr_plan_kernel: candidate order per image from the label histogram: b in [2,8] ordered by
 // (b-1) * zeros(b) descending, ties -> smaller b (readings Q5, Q22).
 // ======================================================================================
-__global__ void lmr_plan_kernel(Geo g, const uint32_t *__restrict__ hist, LmrPlan *__restrict__ plan) {
+__global__ void lmr_plan_kernel(Geo g, const uint32_t *__restrict__ hist, LmrPlan *__restrict__ plan,
+                                LmrWaveCtl *__restrict__ ctl) {
     const int img = blockIdx.x * blockDim.x + threadIdx.x;
+    if (img == 0) {
+        for (int w = 0; w < 8; w++) { ctl->count[w] = w == 0 ? g.B : 0; ctl->nc[w] = 0; }
+    }
     if (img >= g.B) return;
     LmrPlan p{};
     long long val[9];
@@ -165,6 +184,7 @@ __global__ void lmr_plan_kernel(Geo g, const uint32_t *__restrict__ hist, LmrPla
     for (int k = 0; k < 7; k++) p.order[k] = (int8_t)ord[k];
     p.state = 0;
     p.b = 0;
+    p.dslot = 0;
     p.K = 0;
     plan[img] = p;
 }
@@ -175,47 +195,69 @@ __global__ void lmr_plan_kernel(Geo g, const uint32_t *__restrict__ hist, LmrPla
 // image stays undecided, and after the last candidate it is a bad case.
 // Also produces the exclusive byte offsets of the streams (eta tiles, then map tiles).
 // ======================================================================================
-__global__ void lmr_fit_kernel(Geo g, int wave, const int32_t *__restrict__ sizes, LmrPlan *__restrict__ plan,
-                               int32_t *__restrict__ offsets) {
+__global__ void lmr_fit_kernel(Geo g, int wave, int R, LmrEncWS e) {
     const int img = blockIdx.x, lane = threadIdx.x;
-    if (plan[img].state != 0) return;
     const int Tc = lmr_tile_count(g.H, g.W, g.tile_log2);
-    const int32_t *sz = sizes + (size_t)img * 2 * Tc;
-    long long tot = 0;
-    int bad = 0;
-    for (int k = lane; k < 2 * Tc; k += 32) {
-        const int s = sz[k];
-        if (s < 0) bad = 1;
-        tot += s;
+    const int A = wave == 0 ? g.B : e.ctl->count[wave];
+    const int nc = wave == 0 ? 0 : e.ctl->nc[wave];
+    const int k = lmr_wave_k(wave, A, Tc, g.B, R, nc);
+    if (img == 0 && lane == 0 && wave < 7) e.ctl->nc[wave + 1] = nc + k;
+    if (e.plan[img].state != 0) return;
+    const int32_t *sz = e.sizes + (size_t)img * kLmrSlots * Tc;       // slot 0: eta, slot 1 + c: candidate c
+    long long teta = 0;
+    int bad_eta = 0;
+    for (int t = lane; t < Tc; t += 32) {
+        const int v = sz[t];
+        bad_eta |= v < 0;
+        teta += v;
     }
 #pragma unroll
     for (int s2 = 16; s2 > 0; s2 >>= 1) {
-        tot += __shfl_xor_sync(0xffffffffu, tot, s2);
-        bad |= __shfl_xor_sync(0xffffffffu, bad, s2);
+        teta += __shfl_xor_sync(0xffffffffu, teta, s2);
+        bad_eta |= __shfl_xor_sync(0xffffffffu, bad_eta, s2);
     }
-    const long long K = 7 + 32ll * Tc + 8 * tot;
-    const bool fits = !bad && K <= g.HW;
-    if (fits) {
-        // exclusive prefix of the 2 Tc stream sizes (eta tiles then map tiles), warp-serial chunks
+    int chosen = -1;
+    long long K = 0;
+    for (int c = nc; c < nc + k && chosen < 0; c++) {                  // candidates in order
+        const int32_t *sm = sz + (size_t)(1 + c) * Tc;
+        long long tot = 0;
+        int bad = bad_eta;
+        for (int t = lane; t < Tc; t += 32) {
+            const int v = sm[t];
+            bad |= v < 0;
+            tot += v;
+        }
+#pragma unroll
+        for (int s2 = 16; s2 > 0; s2 >>= 1) {
+            tot += __shfl_xor_sync(0xffffffffu, tot, s2);
+            bad |= __shfl_xor_sync(0xffffffffu, bad, s2);
+        }
+        const long long Kc = 7 + 32ll * Tc + 8 * (teta + tot);
+        if (!bad && Kc <= g.HW) { chosen = c; K = Kc; }
+    }
+    if (chosen >= 0) {
+        // sizes of the decided streams (eta tiles, then map tiles) and their exclusive prefix
+        int32_t *ds = e.dsizes + (size_t)img * 2 * Tc, *off = e.offsets + (size_t)img * 2 * Tc;
         int run = 0;
         for (int k0 = 0; k0 < 2 * Tc; k0 += 32) {
-            const int k = k0 + lane;
-            const int s = k < 2 * Tc ? sz[k] : 0;
-            int v = s;
+            const int q = k0 + lane;
+            const int v = q < 2 * Tc ? (q < Tc ? sz[q] : sz[(size_t)(1 + chosen) * Tc + (q - Tc)]) : 0;
+            int x = v;
 #pragma unroll
             for (int d = 1; d < 32; d <<= 1) {
-                const int t = __shfl_up_sync(0xffffffffu, v, d);
-                if (lane >= d) v += t;
+                const int t = __shfl_up_sync(0xffffffffu, x, d);
+                if (lane >= d) x += t;
             }
-            if (k < 2 * Tc) offsets[(size_t)img * 2 * Tc + k] = run + v - s;
-            run += __shfl_sync(0xffffffffu, v, 31);
+            if (q < 2 * Tc) { ds[q] = v; off[q] = run + x - v; }
+            run += __shfl_sync(0xffffffffu, x, 31);
         }
     }
     if (lane == 0) {
-        LmrPlan p = plan[img];
-        if (fits) { p.state = 1; p.b = p.order[wave]; p.K = K; }
-        else if (wave == 6) { p.state = 2; p.b = 0; p.K = 0; }
-        plan[img] = p;
+        LmrPlan p = e.plan[img];
+        if (chosen >= 0) { p.state = 1; p.b = p.order[chosen]; p.dslot = 1 + chosen; p.K = K; }
+        else if (nc + k >= 7) { p.state = 2; p.b = 0; p.K = 0; }
+        else e.lists[(size_t)(wave + 1) * g.B + atomicAdd(&e.ctl->count[wave + 1], 1)] = img;
+        e.plan[img] = p;
     }
 }
 
@@ -229,7 +271,7 @@ __global__ void lmr_fit_kernel(Geo g, int wave, const int32_t *__restrict__ size
 // bytes [q0, q0 + 2) of the MSB-plane stream (header excluded) for the 16 pixels of a thread:
 // one binary search for the stream holding byte q0, the next byte from the same or next stream
 __device__ __forceinline__ uint32_t stream_bytes2(int Tc, const int32_t *sz, const int32_t *off, const uint8_t *slots,
-                                                  int cap, long long q0, long long total) {
+                                                  int cap, int dslot, long long q0, long long total) {
     int lo = 0, hi = 2 * Tc - 1;
     while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
@@ -241,25 +283,21 @@ __device__ __forceinline__ uint32_t stream_bytes2(int Tc, const int32_t *sz, con
         const long long q = q0 + i;
         if (q >= total) break;
         while (k + 1 < 2 * Tc && off[k + 1] <= q) k++;         // (empty streams are skipped)
-        const int slot = k < Tc ? 0 : 1, tile = k < Tc ? k : k - Tc;
+        const int slot = k < Tc ? 0 : dslot, tile = k < Tc ? k : k - Tc;
         v = (v << 8) | slots[((size_t)slot * Tc + tile) * cap + (q - off[k])];
         if (i == 0 && q0 + 1 >= total) v <<= 8;
     }
     return v;                                                   // 16 bits, stream order MSB first
 }
 
-__global__ void __launch_bounds__(256) lmr_msb_write_kernel(Geo g, const LmrPlan *__restrict__ plan,
-                                                            const int32_t *__restrict__ sizes,
-                                                            const int32_t *__restrict__ offsets,
-                                                            const uint8_t *__restrict__ streams,
+__global__ void __launch_bounds__(256) lmr_msb_write_kernel(Geo g, LmrEncWS ew,
                                                             const uint32_t *__restrict__ hist,
                                                             uint8_t *__restrict__ enc, int32_t *__restrict__ b_out,
                                                             int64_t *__restrict__ cap_out,
                                                             int32_t *__restrict__ status) {
     const int img = blockIdx.y;
-    const LmrPlan pl = plan[img];
+    const LmrPlan pl = ew.plan[img];
     const int Tc = lmr_tile_count(g.H, g.W, g.tile_log2);
-    const int cap = lmr_tile_cap(g.tile_log2, g.H, g.W);
     uint8_t *E = enc + (size_t)img * g.HW;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         if (pl.state == 1) {
@@ -274,10 +312,10 @@ __global__ void __launch_bounds__(256) lmr_msb_write_kernel(Geo g, const LmrPlan
         }
     }
     if (pl.state != 1) return;
-    const int32_t *sz = sizes + (size_t)img * 2 * Tc;
-    const int32_t *off = offsets + (size_t)img * 2 * Tc;
+    const int32_t *sz = ew.dsizes + (size_t)img * 2 * Tc;
+    const int32_t *off = ew.offsets + (size_t)img * 2 * Tc;
     const int stride = lmr_tile_stride(g.tile_log2, g.H, g.W);
-    const uint8_t *slots = streams + (size_t)img * 2 * Tc * stride;
+    const uint8_t *slots = ew.streams + (size_t)img * kLmrSlots * Tc * stride;
     const long long hdr = 7 + 32ll * Tc;                        // header bits before the stream bytes
     const long long total = (pl.K - hdr) / 8;                   // stream bytes
     for (long long p = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * 16; p < pl.K;
@@ -287,8 +325,8 @@ __global__ void __launch_bounds__(256) lmr_msb_write_kernel(Geo g, const LmrPlan
         if (p >= hdr) {
             const long long q = p - hdr, q0 = q >> 3;
             const int sh = (int)(q & 7);                        // bit offset inside byte q0
-            const uint32_t b3 = (stream_bytes2(Tc, sz, off, slots, stride, q0, total) << 8) |
-                                (q0 + 2 < total ? stream_bytes2(Tc, sz, off, slots, stride, q0 + 2, total) >> 8 : 0u);
+            const uint32_t b3 = (stream_bytes2(Tc, sz, off, slots, stride, pl.dslot, q0, total) << 8) |
+                                (q0 + 2 < total ? stream_bytes2(Tc, sz, off, slots, stride, pl.dslot, q0 + 2, total) >> 8 : 0u);
             bits16 = (b3 >> (8 - sh)) & 0xFFFFu;
         } else {
             for (int i = 0; i < 16; i++) {
@@ -299,7 +337,7 @@ __global__ void __launch_bounds__(256) lmr_msb_write_kernel(Geo g, const LmrPlan
                 else if (r < hdr) bit = ((uint32_t)sz[(r - 7) >> 4] >> (15 - ((r - 7) & 15))) & 1u;
                 else {
                     const long long q = r - hdr;
-                    const uint32_t by = stream_bytes2(Tc, sz, off, slots, stride, q >> 3, total) >> 8;
+                    const uint32_t by = stream_bytes2(Tc, sz, off, slots, stride, pl.dslot, q >> 3, total) >> 8;
                     bit = (by >> (7 - (q & 7))) & 1u;
                 }
                 bits16 |= bit << (15 - i);
@@ -630,24 +668,16 @@ struct FastEnc {
 };
 
 template <int NW>
-__global__ void __launch_bounds__(kFastThreads, 1) coder_encode_fast_kernel(Geo g, int wave, const uint8_t *__restrict__ ceta,
-                                                                         const LmrPlan *__restrict__ plan,
-                                                                         uint8_t *__restrict__ streams,
-                                                                         int32_t *__restrict__ sizes,
+__global__ void __launch_bounds__(kFastThreads, 1) coder_encode_fast_kernel(Geo g, int wave, int R,
+                                                                         const uint8_t *__restrict__ ceta, LmrEncWS ew,
                                                                          unsigned long long *__restrict__ sym_count) {
     extern __shared__ __align__(16) uint16_t p0s[];
     const int tid = threadIdx.x;
     const int Tc = lmr_tile_count(g.H, g.W, g.tile_log2);
-    const int nslots = wave == 0 ? 2 : 1;
-    const long long gid = (long long)blockIdx.x * kFastThreads + tid;
-    const long long total = (long long)g.B * nslots * Tc;
-    const bool active0 = gid < total;
-    const int img = active0 ? (int)(gid / ((long long)nslots * Tc)) : 0;
-    const int rem = active0 ? (int)(gid % ((long long)nslots * Tc)) : 0;
-    const int slot = wave == 0 ? rem / Tc : 1;
-    const int tile = rem % Tc;
-    const bool active = active0 && plan[img].state == 0;
+    WaveItem it{0, 0, -1, 0};
+    const bool active = wave_item(g, wave, R, (long long)blockIdx.x * kFastThreads + tid, ew, it);
     if (!__syncthreads_or(active)) return;
+    const int img = it.img, slot = it.slot, tile = it.tile;
     fast_model_init(p0s);
     if (!active) return;
     const unsigned am = __activemask();
@@ -663,10 +693,10 @@ __global__ void __launch_bounds__(kFastThreads, 1) coder_encode_fast_kernel(Geo 
         const unsigned v = __reduce_add_sync(am, (unsigned)(h * w));
         if ((tid & 31) == __ffs(am) - 1) atomicAdd(sym_count, (unsigned long long)v);
     }
-    const uint32_t bsub = slot == 0 ? 0u : (uint32_t)(0x80 - plan[img].order[wave]) * 0x01010101u;
+    const uint32_t bsub = slot == 0 ? 0u : (uint32_t)(0x80 - ew.plan[img].order[it.cand]) * 0x01010101u;
     const int cap = lmr_tile_cap(g.tile_log2, g.H, g.W);
 
-    uint8_t *slot_out = streams + (((size_t)img * 2 + slot) * Tc + tile) * lmr_tile_stride(g.tile_log2, g.H, g.W);
+    uint8_t *slot_out = ew.streams + (((size_t)img * kLmrSlots + slot) * Tc + tile) * lmr_tile_stride(g.tile_log2, g.H, g.W);
     FastEnc e{0, 0, 0xFFFFFFFFu, slot_out, slot_out, 0, cap, 0, 0, 0};
     const uint8_t *src = ceta + (size_t)img * g.HW + x0;
     uint32_t p1[NW], p2[NW];
@@ -745,7 +775,7 @@ __global__ void __launch_bounds__(kFastThreads, 1) coder_encode_fast_kernel(Geo 
     for (int i = 0; i < 5; i++) e.emit(true, false, 8);
     e.end_half(am);
     e.n += e.k;
-    sizes[((size_t)img * 2 + slot) * Tc + tile] = (e.n <= cap && e.n <= 65535) ? e.n : -1;
+    ew.sizes[((size_t)img * kLmrSlots + slot) * Tc + tile] = (e.n <= cap && e.n <= 65535) ? e.n : -1;
 }
 
 // decoder input: the tile's stream as a 96-bit MSB-aligned bit buffer b0:b1:b2 (nb valid bits),
@@ -953,37 +983,55 @@ void lmr_set_smem_attrs() {
     done = true;
 }
 
-void launch_lmr_plan(const Geo &g, const uint32_t *hist, LmrPlan *plan, cudaStream_t st) {
-    lmr_plan_kernel<<<(g.B + 127) / 128, 128, 0, st>>>(g, hist, plan);
+void launch_lmr_plan(const Geo &g, const uint32_t *hist, const LmrEncWS &e, cudaStream_t st) {
+    lmr_plan_kernel<<<(g.B + 127) / 128, 128, 0, st>>>(g, hist, e.plan, e.ctl);
 }
 
-void launch_coder_encode(const Geo &g, int wave, const uint8_t *ceta, const LmrPlan *plan, uint8_t *streams,
-                         int32_t *sizes, unsigned long long *sym_count, cudaStream_t st) {
+static int sm_count() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+// resident coder tiles per round: fast kernel one CTA of kFastThreads per SM, legacy 3 warps per SM
+static int coder_round(const Geo &g) {
+    const int tw = lmr_tile_side(g.tile_log2, g.W);
+    return tw == 32 || tw == 64 || tw == 128 ? sm_count() * kFastThreads : sm_count() * 3 * kCoderThreads;
+}
+
+void launch_coder_encode(const Geo &g, int wave, const uint8_t *ceta, const LmrEncWS &e,
+                         unsigned long long *sym_count, cudaStream_t st) {
     lmr_set_smem_attrs();
     const int Tc = lmr_tile_count(g.H, g.W, g.tile_log2);
-    const long long total = (long long)g.B * (wave == 0 ? 2 : 1) * Tc;
+    const int R = coder_round(g);
+    // most work items of this wave: wave 0 = B (1 + k0) Tc; later waves A k Tc <= max(R, B Tc)
+    const long long total = wave == 0 ? (long long)g.B * (1 + lmr_wave_k(0, g.B, Tc, g.B, R, 0)) * Tc
+                                      : std::max<long long>(R, (long long)g.B * Tc);
     const unsigned grid = (unsigned)((total + kCoderThreads - 1) / kCoderThreads);
     const unsigned fgrid = (unsigned)((total + kFastThreads - 1) / kFastThreads);
     switch (lmr_tile_side(g.tile_log2, g.W)) {
-        case 32: coder_encode_fast_kernel<1><<<fgrid, kFastThreads, fast_smem(), st>>>(g, wave, ceta, plan, streams, sizes, sym_count); break;
-        case 64: coder_encode_fast_kernel<2><<<fgrid, kFastThreads, fast_smem(), st>>>(g, wave, ceta, plan, streams, sizes, sym_count); break;
-        case 128: coder_encode_fast_kernel<4><<<fgrid, kFastThreads, fast_smem(), st>>>(g, wave, ceta, plan, streams, sizes, sym_count); break;
-        default: coder_encode_kernel<<<grid, kCoderThreads, coder_smem(), st>>>(g, wave, ceta, plan, streams, sizes);
+        case 32: coder_encode_fast_kernel<1><<<fgrid, kFastThreads, fast_smem(), st>>>(g, wave, R, ceta, e, sym_count); break;
+        case 64: coder_encode_fast_kernel<2><<<fgrid, kFastThreads, fast_smem(), st>>>(g, wave, R, ceta, e, sym_count); break;
+        case 128: coder_encode_fast_kernel<4><<<fgrid, kFastThreads, fast_smem(), st>>>(g, wave, R, ceta, e, sym_count); break;
+        default: coder_encode_kernel<<<grid, kCoderThreads, coder_smem(), st>>>(g, wave, R, ceta, e);
     }
 }
 
-void launch_lmr_fit(const Geo &g, int wave, const int32_t *sizes, LmrPlan *plan, int32_t *offsets, cudaStream_t st) {
-    lmr_fit_kernel<<<g.B, 32, 0, st>>>(g, wave, sizes, plan, offsets);
+void launch_lmr_fit(const Geo &g, int wave, const LmrEncWS &e, cudaStream_t st) {
+    lmr_fit_kernel<<<g.B, 32, 0, st>>>(g, wave, coder_round(g), e);
 }
 
-void launch_lmr_msb_write(const Geo &g, const LmrPlan *plan, const int32_t *sizes, const int32_t *offsets,
-                          const uint8_t *streams, const uint32_t *hist, uint8_t *enc, int32_t *b_out, int64_t *cap_out,
-                          int32_t *status, cudaStream_t st) {
+void launch_lmr_msb_write(const Geo &g, const LmrEncWS &e, const uint32_t *hist, uint8_t *enc, int32_t *b_out,
+                          int64_t *cap_out, int32_t *status, cudaStream_t st) {
     const long long n16 = g.HW / 16;
     int bx = (int)((n16 + 255) / 256);
     if (bx > 64) bx = 64;
     dim3 grid(bx, g.B);
-    lmr_msb_write_kernel<<<grid, 256, 0, st>>>(g, plan, sizes, offsets, streams, hist, enc, b_out, cap_out, status);
+    lmr_msb_write_kernel<<<grid, 256, 0, st>>>(g, e, hist, enc, b_out, cap_out, status);
 }
 
 void launch_lmr_decode(const Geo &g, bool want_eta, const uint8_t *marked, uint8_t *mbuf, int32_t *lmr_b,

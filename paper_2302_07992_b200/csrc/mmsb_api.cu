@@ -64,7 +64,7 @@ static size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
 struct Layout {
     size_t s, rec, pyr, hist, kdone, rstate, tile_zero_end, ragg, rinc;   // fused tile kernels
     size_t states, parts, hdr, scan_zero_end;                                  // scan kernels
-    size_t ceta, eta_bits, map_bits, lmr_b, lmr_t, plan, streams, sizes, offsets, mbuf, rstat, total;
+    size_t ceta, eta_bits, map_bits, lmr_b, lmr_t, plan, wctl, lists, streams, sizes, dsizes, offsets, mbuf, rstat, total;
 };
 
 static Layout layout(const Geo &g) {
@@ -92,8 +92,11 @@ static Layout layout(const Geo &g) {
     L.lmr_t = o; o = align256(o + B * 4);
     const size_t Tc = (size_t)g.ntiles_coder;
     L.plan = o; o = align256(o + (lmr ? B * sizeof(LmrPlan) : 0));
-    L.streams = o; o = align256(o + (lmr ? B * 2 * Tc * lmr_tile_stride_host(g.tile_log2, g.H, g.W) : 0));
-    L.sizes = o; o = align256(o + (lmr ? B * 2 * Tc * 4 : 0));
+    L.wctl = o; o = align256(o + (lmr ? sizeof(LmrWaveCtl) : 0));
+    L.lists = o; o = align256(o + (lmr ? 8 * B * 4 : 0));
+    L.streams = o; o = align256(o + (lmr ? B * kLmrSlots * Tc * lmr_tile_stride_host(g.tile_log2, g.H, g.W) : 0));
+    L.sizes = o; o = align256(o + (lmr ? B * kLmrSlots * Tc * 4 : 0));
+    L.dsizes = o; o = align256(o + (lmr ? B * 2 * Tc * 4 : 0));
     L.offsets = o; o = align256(o + (lmr ? B * 2 * Tc * 4 : 0));
     L.mbuf = o; o = align256(o + (lmr ? B * g.HW / 8 + 128 : 0));   // + decoder look-ahead past the last stream
     L.rstat = o; o = align256(o + B * 4);
@@ -171,21 +174,18 @@ mmsb_status mmsb_content_owner_encode(const mmsb_shape *shape, const uint8_t *im
     });
     if (g.method == 1) {
         // LMR: code eta and the candidate maps until both fit the MSB plane, then write it
-        LmrPlan *plan = at<LmrPlan>(ws, L.plan);
-        run_kernel(K_LMR_PLAN, st, px, [&] { launch_lmr_plan(g, at<uint32_t>(ws, L.hist), plan, st); });
-        for (int w = 0; w < 7; w++) {
+        const LmrEncWS ew{at<LmrPlan>(ws, L.plan), at<LmrWaveCtl>(ws, L.wctl), at<int32_t>(ws, L.lists),
+                          at<uint8_t>(ws, L.streams), at<int32_t>(ws, L.sizes), at<int32_t>(ws, L.dsizes),
+                          at<int32_t>(ws, L.offsets)};
+        run_kernel(K_LMR_PLAN, st, px, [&] { launch_lmr_plan(g, at<uint32_t>(ws, L.hist), ew, st); });
+        for (int w = 0; w < 7; w++) {      // candidate waves; waves after the last undecided image exit at once
             run_kernel(K_CODER_ENC, st, px, [&] {
-                launch_coder_encode(g, w, at<uint8_t>(ws, L.ceta), plan, at<uint8_t>(ws, L.streams),
-                                    at<int32_t>(ws, L.sizes), sym_counter(0), st);
+                launch_coder_encode(g, w, at<uint8_t>(ws, L.ceta), ew, sym_counter(0), st);
             });
-            run_kernel(K_LMR_FIT, st, px, [&] {
-                launch_lmr_fit(g, w, at<int32_t>(ws, L.sizes), plan, at<int32_t>(ws, L.offsets), st);
-            });
+            run_kernel(K_LMR_FIT, st, px, [&] { launch_lmr_fit(g, w, ew, st); });
         }
         run_kernel(K_LMR_MSB, st, px, [&] {
-            launch_lmr_msb_write(g, plan, at<int32_t>(ws, L.sizes), at<int32_t>(ws, L.offsets),
-                                 at<uint8_t>(ws, L.streams), at<uint32_t>(ws, L.hist), encrypted, b_out,
-                                 capacity_out, img_status, st);
+            launch_lmr_msb_write(g, ew, at<uint32_t>(ws, L.hist), encrypted, b_out, capacity_out, img_status, st);
         });
     }
     return check_launch();

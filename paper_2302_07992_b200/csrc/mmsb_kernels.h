@@ -18,16 +18,44 @@ struct LmrPlan {
     int8_t order[7];
     int8_t state;                    // 0 undecided, 1 fits (b), 2 bad case
     int32_t b;
+    int32_t dslot;                   // stream slot of the decided map (1 + its candidate index)
     long long K;                     // MSB-plane bits used: 7 + 32 T + 8 (bytes_eta + bytes_map)
 };
 
-void launch_lmr_plan(const Geo &g, const uint32_t *hist, LmrPlan *plan, cudaStream_t st);
-void launch_coder_encode(const Geo &g, int wave, const uint8_t *ceta, const LmrPlan *plan, uint8_t *streams,
-                         int32_t *sizes, unsigned long long *sym_count, cudaStream_t st);
-void launch_lmr_fit(const Geo &g, int wave, const int32_t *sizes, LmrPlan *plan, int32_t *offsets, cudaStream_t st);
-void launch_lmr_msb_write(const Geo &g, const LmrPlan *plan, const int32_t *sizes, const int32_t *offsets,
-                          const uint8_t *streams, const uint32_t *hist, uint8_t *enc, int32_t *b_out, int64_t *cap_out,
-                          int32_t *status, cudaStream_t st);
+// Candidate waves: wave w codes, for the count[w] images still undecided
+// (list[w]), candidates nc[w] .. nc[w]+k_w-1 of their order at once, k_w as many as fill one
+// round of resident tiles (wave 0: eta and candidate 0 for every image); the fit then takes the
+// first candidate in order that fits, exactly the serial walk's choice.
+constexpr int kLmrSlots = 8;         // stream slots per image: eta, candidates 0..6
+struct LmrWaveCtl {
+    int count[8];                    // images entering wave w (count[0] = B)
+    int nc[8];                       // candidates tried before wave w
+};
+struct LmrEncWS {
+    LmrPlan *plan;                   // [B]
+    LmrWaveCtl *ctl;
+    int32_t *lists;                  // [8][B] image list of each wave
+    uint8_t *streams;                // [B][kLmrSlots][Tc] slots of lmr_tile_stride bytes
+    int32_t *sizes;                  // [B][kLmrSlots][Tc] stream bytes (-1: over cap)
+    int32_t *dsizes;                 // [B][2][Tc] sizes of the decided eta + map streams
+    int32_t *offsets;                // [B][2][Tc] their exclusive byte offsets
+};
+__host__ __device__ inline int lmr_wave_k(int wave, int A, int Tc, int B, int R, int nc) {
+    if (wave == 0) {                                            // eta + k candidates per image
+        const int k = R / (B * Tc) - 1;
+        return k < 1 ? 1 : (k > 7 ? 7 : k);
+    }
+    if (A <= 0) return 1;
+    const int k = R / (A * Tc), left = 7 - nc;
+    return k < 1 ? 1 : (k > left ? left : k);
+}
+
+void launch_lmr_plan(const Geo &g, const uint32_t *hist, const LmrEncWS &e, cudaStream_t st);
+void launch_coder_encode(const Geo &g, int wave, const uint8_t *ceta, const LmrEncWS &e,
+                         unsigned long long *sym_count, cudaStream_t st);
+void launch_lmr_fit(const Geo &g, int wave, const LmrEncWS &e, cudaStream_t st);
+void launch_lmr_msb_write(const Geo &g, const LmrEncWS &e, const uint32_t *hist, uint8_t *enc, int32_t *b_out,
+                          int64_t *cap_out, int32_t *status, cudaStream_t st);
 void launch_lmr_decode(const Geo &g, bool want_eta, const uint8_t *marked, uint8_t *mbuf, int32_t *lmr_b,
                        int32_t *lmr_t, int32_t *offsets, int32_t *sizes, uint32_t *eta_bits, uint32_t *map_bits,
                        int32_t *status, int64_t *msg_bits_out,
