@@ -319,23 +319,9 @@ __global__ void __launch_bounds__(kScanThreads, 5) scan_kernel(Geo g, const uint
         const long long hie = hi < F ? hi : F;
         const long long blk0 = lo >> 9;
         const int nblk = lo < hie ? (int)(((hie - 1) >> 9) - blk0 + 1) : 0;
-        if (tid < nblk) {
-            // frame words [16 (blk0 + tid), +16): word 0 = n, word i >= 1 = message word i - 1
-            const long long fw0 = (blk0 + tid) * 16;
-            uint32_t ks[16];
-            chacha20_block(key, (uint32_t)(blk0 + tid), ks);
-            const uint32_t *mw = reinterpret_cast<const uint32_t *>(msg + (size_t)img * stride);
-            const long long nmw = stride / 4;                    // message words in the row
-#pragma unroll
-            for (int j = 0; j < 16; j++) {
-                const long long wi = fw0 + j;
-                uint32_t fw;
-                if (wi == 0) fw = (uint32_t)n;
-                else if (wi - 1 < nmw) fw = bswap32(__ldg(mw + (wi - 1)));
-                else fw = 0;
-                kbuf[tid * 16 + j] = fw ^ bswap32(ks[j]);
-            }
-        }
+        // E_F words of the chunk's frame blocks (frame_encrypt_kernel), coalesced into smem
+        const uint32_t *ef = ws.ef + (size_t)img * ws.ef_words + blk0 * 16;
+        for (int t = tid; t < nblk * 16; t += kScanThreads) kbuf[t] = __ldg(ef + t);
         __syncthreads();
         const long long base = blk0 * 512;
         const long long fend = hie - base;
@@ -402,6 +388,43 @@ __global__ void __launch_bounds__(kScanThreads, 5) scan_kernel(Geo g, const uint
             }
         }
     }
+}
+
+// ======================================================================================
+// frame_encrypt_kernel: E_F = F XOR KS2 for every ChaCha20 block of the frame (reading Q17):
+// F = BE32(n) || message, block k = frame words [16k, 16k+16).  Independent of the pixels,
+// so it runs at full occupancy before the chunk kernel, which copies the words it needs.
+// ======================================================================================
+__global__ void __launch_bounds__(128) frame_encrypt_kernel(Geo g, const uint8_t *__restrict__ keys,
+                                                            const uint8_t *__restrict__ msg,
+                                                            const int64_t *__restrict__ msg_bits, long long stride,
+                                                            ScanWS ws) {
+    const int img = blockIdx.y;
+    const long long k = (long long)blockIdx.x * 128 + threadIdx.x;
+    const long long n = msg_bits[img];
+    const bool n_ok = n >= 0 && n <= 8 * stride && n <= 0xFFFFFFFFll;
+    const long long F = n_ok ? 32 + n : 0;
+    const long long nblk = (F + 511) / 512 < ws.ef_words / 16 ? (F + 511) / 512 : ws.ef_words / 16;
+    if (k >= nblk) return;
+    uint32_t key[8];
+    load_key(keys, img, key);
+    uint32_t ks[16];
+    chacha20_block(key, (uint32_t)k, ks);
+    const uint32_t *mw = reinterpret_cast<const uint32_t *>(msg + (size_t)img * stride);
+    const long long nmw = stride / 4;                            // message words in the row
+    uint32_t o[16];
+#pragma unroll
+    for (int j = 0; j < 16; j++) {
+        const long long wi = k * 16 + j;
+        uint32_t fw;
+        if (wi == 0) fw = (uint32_t)n;
+        else if (wi - 1 < nmw) fw = bswap32(__ldg(mw + (wi - 1)));
+        else fw = 0;
+        o[j] = fw ^ bswap32(ks[j]);
+    }
+    uint4 *dst = reinterpret_cast<uint4 *>(ws.ef + (size_t)img * ws.ef_words + k * 16);
+#pragma unroll
+    for (int j = 0; j < 4; j++) dst[j] = make_uint4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
 }
 
 // ======================================================================================
@@ -493,6 +516,11 @@ static void launch_scan_t(const Geo &g, const uint8_t *in, uint8_t *out, const u
                           int32_t *status, const ScanWS &ws, const uint32_t *map_bits, const int32_t *lmr_b,
                           cudaStream_t st) {
     const unsigned grid = (unsigned)((long long)g.B * g.nchunks);
+    if constexpr (EMBED) {
+        const long long fb = (32 + 8 * stride + 511) / 512;     // frame blocks (capped by ef_words in the kernel)
+        const long long nb = fb < ws.ef_words / 16 ? fb : ws.ef_words / 16;
+        frame_encrypt_kernel<<<dim3((unsigned)((nb + 127) / 128), g.B), 128, 0, st>>>(g, keys, msg, msg_bits, stride, ws);
+    }
     scan_kernel<METHOD, EMBED><<<grid, kScanThreads, 0, st>>>(g, in, out, keys, msg, msg_bits, stride, msg_out, ws,
                                                               map_bits, lmr_b);
     scan_finish_kernel<METHOD, EMBED><<<g.B, 256, 0, st>>>(g, in, out, msg_bits, stride, msg_out, msg_bits_out,

@@ -11,7 +11,10 @@ struct ScanWS {
     unsigned long long *states;      // [B][nchunks] flag | value (decoupled look-back)
     unsigned long long *parts;       // [B][nchunks][2] boundary words of the extracted bit string
     uint32_t *hdr;                   // [B] frame length word (extract)
+    uint32_t *ef;                    // [B][ef_words] encrypted frame E_F = F XOR KS2 (embed)
+    long long ef_words;              // words per image: ceil(7 HW / 512) + 1 ChaCha blocks of 16
 };
+__host__ __device__ inline long long ef_words_of(long long HW) { return ((7 * HW + 511) / 512 + 1) * 16; }
 
 // LMR encode state of one image: candidate order (P:985 walk), decision and header length K
 struct LmrPlan {
