@@ -372,18 +372,24 @@ __global__ void __launch_bounds__(kScanThreads, 5) scan_kernel(Geo g, const uint
         uint32_t *mo = reinterpret_cast<uint32_t *>(msg_out + (size_t)img * stride);
         unsigned long long *parts = ws.parts + ((size_t)img * g.nchunks + chunk) * 2;
         if (lo < hi) {
-            const long long w0 = lo >> 5, w1 = (hi - 1) >> 5;
-            for (long long W = w0 + tid; W <= w1; W += kScanThreads) {
-                const long long s0 = W * 32 > lo ? W * 32 : lo;
-                const long long e0 = W * 32 + 32 < hi ? W * 32 + 32 : hi;
-                const uint32_t v = kbuf[W - basew];
-                if (s0 == W * 32 && e0 == W * 32 + 32) {
+            // frame words [w0, w1] (word indices < 7 HW / 32 fit 32 bits); the first and last
+            // may be shared with the neighbouring chunks, the ones in between are this chunk's
+            const int w0 = (int)(lo >> 5), w1 = (int)((hi - 1) >> 5), nw = w1 - w0 + 1;
+            const bool hp = (lo & 31) != 0, tp = (hi & 31) != 0;
+            const int wlim = (int)(stride / 4);                  // message words in the row: W - 1 < wlim
+            const uint32_t *kb = kbuf + (w0 - (int)basew);
+            for (int i = tid; i < nw; i += kScanThreads) {
+                const int W = w0 + i;
+                const uint32_t v = kb[i];
+                if (!((i == 0 && hp) || (i == nw - 1 && tp))) {
                     if (W == 0) ws.hdr[img] = v;
-                    else if (4 * W <= stride) mo[W - 1] = bswap32(v);
+                    else if (W <= wlim) mo[W - 1] = bswap32(v);
                 } else {                                     // shared word: merged by scan_finish
-                    const int len = (int)(e0 - s0), st0 = (int)(s0 - W * 32);
+                    const long long s0 = (long long)W * 32 > lo ? (long long)W * 32 : lo;
+                    const long long e0 = (long long)W * 32 + 32 < hi ? (long long)W * 32 + 32 : hi;
+                    const int len = (int)(e0 - s0), st0 = (int)(s0 - (long long)W * 32);
                     const uint32_t msk = (len == 32 ? 0xFFFFFFFFu : ((1u << len) - 1u)) << (32 - st0 - len);
-                    parts[W == w0 ? 0 : 1] = ((unsigned long long)(W + 1) << 32) | (v & msk);
+                    parts[i == 0 ? 0 : 1] = ((unsigned long long)(W + 1) << 32) | (v & msk);
                 }
             }
         }
