@@ -262,34 +262,29 @@ __global__ void lmr_fit_kernel(Geo g, int wave, int R, LmrEncWS e) {
 }
 
 // ======================================================================================
+// lmr_concat_kernel: the decided eta and map streams of an image, concatenated in order (tile
+// raster, eta first) into one byte string at their exclusive offsets: one CTA per stream,
+// coalesced copies.
+// ======================================================================================
+__global__ void __launch_bounds__(128) lmr_concat_kernel(Geo g, LmrEncWS ew) {
+    const int img = blockIdx.y, k = blockIdx.x;
+    const LmrPlan pl = ew.plan[img];
+    if (pl.state != 1) return;
+    const int Tc = lmr_tile_count(g.H, g.W, g.tile_log2);
+    const int n = ew.dsizes[(size_t)img * 2 * Tc + k], o = ew.offsets[(size_t)img * 2 * Tc + k];
+    const int slot = k < Tc ? 0 : pl.dslot, tile = k < Tc ? k : k - Tc;
+    const uint8_t *src = ew.streams + (((size_t)img * kLmrSlots + slot) * Tc + tile) * lmr_tile_stride(g.tile_log2, g.H, g.W);
+    uint8_t *dst = ew.cat + (size_t)img * (g.HW / 8 + 128) + o;
+    for (int i = threadIdx.x; i < n; i += 128) dst[i] = src[i];
+}
+
+// ======================================================================================
 // lmr_msb_write_kernel: writes the first-MSB plane of I_e (layout reading Q15):
 //   [b-2: 3 bits][t: 4 bits][16-bit byte lengths of the eta tiles][... of the map tiles]
 //   [eta tile bytes][map tile bytes], MSB first, pixel r <- stream bit r for r < K; the
 //   remaining MSBs keep I_r XOR s.  Bad case: the b-field 7 (bits r = 0..2 set).
-// One thread per 16 pixels; the stream bits of its pixels are gathered from the tile slots.
+// One thread per 16 pixels; the stream bits come from the concatenated string (3 bytes).
 // ======================================================================================
-// bytes [q0, q0 + 2) of the MSB-plane stream (header excluded) for the 16 pixels of a thread:
-// one binary search for the stream holding byte q0, the next byte from the same or next stream
-__device__ __forceinline__ uint32_t stream_bytes2(int Tc, const int32_t *sz, const int32_t *off, const uint8_t *slots,
-                                                  int cap, int dslot, long long q0, long long total) {
-    int lo = 0, hi = 2 * Tc - 1;
-    while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (off[mid] <= q0) lo = mid; else hi = mid - 1;
-    }
-    uint32_t v = 0;
-    int k = lo;
-    for (int i = 0; i < 2; i++) {
-        const long long q = q0 + i;
-        if (q >= total) break;
-        while (k + 1 < 2 * Tc && off[k + 1] <= q) k++;         // (empty streams are skipped)
-        const int slot = k < Tc ? 0 : dslot, tile = k < Tc ? k : k - Tc;
-        v = (v << 8) | slots[((size_t)slot * Tc + tile) * cap + (q - off[k])];
-        if (i == 0 && q0 + 1 >= total) v <<= 8;
-    }
-    return v;                                                   // 16 bits, stream order MSB first
-}
-
 __global__ void __launch_bounds__(256) lmr_msb_write_kernel(Geo g, LmrEncWS ew,
                                                             const uint32_t *__restrict__ hist,
                                                             uint8_t *__restrict__ enc, int32_t *__restrict__ b_out,
@@ -313,9 +308,7 @@ __global__ void __launch_bounds__(256) lmr_msb_write_kernel(Geo g, LmrEncWS ew,
     }
     if (pl.state != 1) return;
     const int32_t *sz = ew.dsizes + (size_t)img * 2 * Tc;
-    const int32_t *off = ew.offsets + (size_t)img * 2 * Tc;
-    const int stride = lmr_tile_stride(g.tile_log2, g.H, g.W);
-    const uint8_t *slots = ew.streams + (size_t)img * kLmrSlots * Tc * stride;
+    const uint8_t *cat = ew.cat + (size_t)img * (g.HW / 8 + 128);
     const long long hdr = 7 + 32ll * Tc;                        // header bits before the stream bytes
     const long long total = (pl.K - hdr) / 8;                   // stream bytes
     for (long long p = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * 16; p < pl.K;
@@ -325,8 +318,9 @@ __global__ void __launch_bounds__(256) lmr_msb_write_kernel(Geo g, LmrEncWS ew,
         if (p >= hdr) {
             const long long q = p - hdr, q0 = q >> 3;
             const int sh = (int)(q & 7);                        // bit offset inside byte q0
-            const uint32_t b3 = (stream_bytes2(Tc, sz, off, slots, stride, pl.dslot, q0, total) << 8) |
-                                (q0 + 2 < total ? stream_bytes2(Tc, sz, off, slots, stride, pl.dslot, q0 + 2, total) >> 8 : 0u);
+            uint32_t b3 = 0;
+#pragma unroll
+            for (int i = 0; i < 3; i++) b3 = (b3 << 8) | (q0 + i < total ? (uint32_t)cat[q0 + i] : 0u);
             bits16 = (b3 >> (8 - sh)) & 0xFFFFu;
         } else {
             for (int i = 0; i < 16; i++) {
@@ -337,7 +331,7 @@ __global__ void __launch_bounds__(256) lmr_msb_write_kernel(Geo g, LmrEncWS ew,
                 else if (r < hdr) bit = ((uint32_t)sz[(r - 7) >> 4] >> (15 - ((r - 7) & 15))) & 1u;
                 else {
                     const long long q = r - hdr;
-                    const uint32_t by = stream_bytes2(Tc, sz, off, slots, stride, pl.dslot, q >> 3, total) >> 8;
+                    const uint32_t by = q >> 3 < total ? (uint32_t)cat[q >> 3] : 0u;
                     bit = (by >> (7 - (q & 7))) & 1u;
                 }
                 bits16 |= bit << (15 - i);
@@ -1031,6 +1025,8 @@ void launch_lmr_msb_write(const Geo &g, const LmrEncWS &e, const uint32_t *hist,
     int bx = (int)((n16 + 255) / 256);
     if (bx > 64) bx = 64;
     dim3 grid(bx, g.B);
+    const int Tc = lmr_tile_count(g.H, g.W, g.tile_log2);
+    lmr_concat_kernel<<<dim3(2 * Tc, g.B), 128, 0, st>>>(g, e);
     lmr_msb_write_kernel<<<grid, 256, 0, st>>>(g, e, hist, enc, b_out, cap_out, status);
 }
 

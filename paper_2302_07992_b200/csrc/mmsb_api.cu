@@ -20,7 +20,7 @@ enum KernelId { K_ENCODE = 0, K_RECOVER, K_EMBED, K_EXTRACT, K_STATS, K_LMR_PLAN
                 K_LMR_MSB, K_LMR_DECODE, K_COUNT };
 static const char *kKernelNames[K_COUNT] = {"encode_kernel", "recover_kernel", "frame_encrypt+scan_kernel<embed>+finish",
                                             "scan_kernel<extract>+finish", "stats_kernel", "lmr_plan_kernel",
-                                            "coder_encode_kernel", "lmr_fit_kernel", "lmr_msb_write_kernel",
+                                            "coder_encode_kernel", "lmr_fit_kernel", "lmr_concat+msb_write_kernels",
                                             "lmr_pack+header+coder_decode_kernels"};
 struct ProfRec { int id; cudaEvent_t a, b; long long units; };
 static std::mutex g_prof_mu;
@@ -177,7 +177,7 @@ mmsb_status mmsb_content_owner_encode(const mmsb_shape *shape, const uint8_t *im
         // LMR: code eta and the candidate maps until both fit the MSB plane, then write it
         const LmrEncWS ew{at<LmrPlan>(ws, L.plan), at<LmrWaveCtl>(ws, L.wctl), at<int32_t>(ws, L.lists),
                           at<uint8_t>(ws, L.streams), at<int32_t>(ws, L.sizes), at<int32_t>(ws, L.dsizes),
-                          at<int32_t>(ws, L.offsets)};
+                          at<int32_t>(ws, L.offsets), at<uint8_t>(ws, L.mbuf)};
         run_kernel(K_LMR_PLAN, st, px, [&] { launch_lmr_plan(g, at<uint32_t>(ws, L.hist), ew, st); });
         for (int w = 0; w < 7; w++) {      // candidate waves; waves after the last undecided image exit at once
             run_kernel(K_CODER_ENC, st, px, [&] {
@@ -187,7 +187,7 @@ mmsb_status mmsb_content_owner_encode(const mmsb_shape *shape, const uint8_t *im
         }
         run_kernel(K_LMR_MSB, st, px, [&] {
             launch_lmr_msb_write(g, ew, at<uint32_t>(ws, L.hist), encrypted, b_out, capacity_out, img_status, st);
-        });
+        }, 2);
     }
     return check_launch();
 }

@@ -42,6 +42,7 @@ struct LmrEncWS {
     int32_t *sizes;                  // [B][kLmrSlots][Tc] stream bytes (-1: over cap)
     int32_t *dsizes;                 // [B][2][Tc] sizes of the decided eta + map streams
     int32_t *offsets;                // [B][2][Tc] their exclusive byte offsets
+    uint8_t *cat;                    // [B][HW/8 + 128] the decided streams concatenated (MSB-plane bytes)
 };
 __host__ __device__ inline int lmr_wave_k(int wave, int A, int Tc, int B, int R, int nc) {
     if (wave == 0) {                                            // eta + k candidates per image
