@@ -164,12 +164,13 @@ __global__ void __launch_bounds__(kCoderThreads) coder_encode_kernel(Geo g, int 
 // (b-1) * zeros(b) descending, ties -> smaller b (readings Q5, Q22).
 // ======================================================================================
 __global__ void lmr_plan_kernel(Geo g, const uint32_t *__restrict__ hist, LmrPlan *__restrict__ plan,
-                                LmrWaveCtl *__restrict__ ctl) {
+                                LmrWaveCtl *__restrict__ ctl, int32_t *__restrict__ mapbytes) {
     const int img = blockIdx.x * blockDim.x + threadIdx.x;
     if (img == 0) {
         for (int w = 0; w < 8; w++) { ctl->count[w] = w == 0 ? g.B : 0; ctl->nc[w] = 0; }
     }
     if (img >= g.B) return;
+    for (int c = 0; c < 8; c++) mapbytes[(size_t)img * 8 + c] = 0;
     LmrPlan p{};
     long long val[9];
     for (int b = 2; b <= 8; b++) val[b] = (long long)(b - 1) * (g.HW - (long long)hist[img * 8 + b]);
@@ -185,6 +186,7 @@ __global__ void lmr_plan_kernel(Geo g, const uint32_t *__restrict__ hist, LmrPla
     p.state = 0;
     p.b = 0;
     p.dslot = 0;
+    p.eta_bytes = 0;
     p.K = 0;
     plan[img] = p;
 }
@@ -254,8 +256,10 @@ __global__ void lmr_fit_kernel(Geo g, int wave, int R, LmrEncWS e) {
     }
     if (lane == 0) {
         LmrPlan p = e.plan[img];
+        p.eta_bytes = bad_eta ? -1 : (int32_t)teta;
+        // a bad eta (a tile over cap) fits with no candidate: the walk's outcome is the bad case
         if (chosen >= 0) { p.state = 1; p.b = p.order[chosen]; p.dslot = 1 + chosen; p.K = K; }
-        else if (nc + k >= 7) { p.state = 2; p.b = 0; p.K = 0; }
+        else if (nc + k >= 7 || bad_eta) { p.state = 2; p.b = 0; p.K = 0; }
         else e.lists[(size_t)(wave + 1) * g.B + atomicAdd(&e.ctl->count[wave + 1], 1)] = img;
         e.plan[img] = p;
     }
@@ -690,6 +694,17 @@ __global__ void __launch_bounds__(kFastThreads, 1) coder_encode_fast_kernel(Geo 
     const uint32_t bsub = slot == 0 ? 0u : (uint32_t)(0x80 - ew.plan[img].order[it.cand]) * 0x01010101u;
     const int cap = lmr_tile_cap(g.tile_log2, g.H, g.W);
 
+    // early abort (waves >= 1, eta known): the candidate's map can no longer fit once its tiles'
+    // running byte counts exceed the room left by eta (sizes only grow, so the walk's choice is
+    // unchanged); each tile publishes its count once per row and reads the total a row later
+    int32_t *abort_cnt = nullptr;
+    long long room = 0;
+    if (wave > 0 && it.cand >= 0) {
+        abort_cnt = ew.mapbytes + (size_t)img * 8 + it.cand;
+        room = (g.HW - 7 - 32ll * Tc) / 8 - ew.plan[img].eta_bytes;
+    }
+    int published = 0, seen = 0;
+    bool aborted = false;
     uint8_t *slot_out = ew.streams + (((size_t)img * kLmrSlots + slot) * Tc + tile) * lmr_tile_stride(g.tile_log2, g.H, g.W);
     FastEnc e{0, 0, 0xFFFFFFFFu, slot_out, slot_out, 0, cap, 0, 0, 0};
     const uint8_t *src = ceta + (size_t)img * g.HW + x0;
@@ -763,6 +778,16 @@ __global__ void __launch_bounds__(kFastThreads, 1) coder_encode_fast_kernel(Geo 
         }
 #pragma unroll
         for (int k = 0; k < NW; k++) { p2[k] = p1[k]; p1[k] = cw[k]; }
+        if (abort_cnt) {
+            if (seen > room) { aborted = true; break; }
+            const int cur = e.n + e.k;
+            seen = atomicAdd(abort_cnt, cur - published) + (cur - published);
+            published = cur;
+        }
+    }
+    if (aborted) {                                                     // over the room: does not fit
+        ew.sizes[((size_t)img * kLmrSlots + slot) * Tc + tile] = -1;
+        return;
     }
     e.begin_half();                                                    // flush: the window's 5 digits
 #pragma unroll 1
@@ -978,7 +1003,7 @@ void lmr_set_smem_attrs() {
 }
 
 void launch_lmr_plan(const Geo &g, const uint32_t *hist, const LmrEncWS &e, cudaStream_t st) {
-    lmr_plan_kernel<<<(g.B + 127) / 128, 128, 0, st>>>(g, hist, e.plan, e.ctl);
+    lmr_plan_kernel<<<(g.B + 127) / 128, 128, 0, st>>>(g, hist, e.plan, e.ctl, e.mapbytes);
 }
 
 static int sm_count() {

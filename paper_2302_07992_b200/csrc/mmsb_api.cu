@@ -64,7 +64,7 @@ static size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
 struct Layout {
     size_t s, rec, pyr, hist, kdone, rstate, tile_zero_end, ragg, rinc;   // fused tile kernels
     size_t states, parts, hdr, scan_zero_end, ef;                              // scan kernels
-    size_t ceta, eta_bits, map_bits, lmr_b, lmr_t, plan, wctl, lists, streams, sizes, dsizes, offsets, mbuf, rstat, total;
+    size_t ceta, eta_bits, map_bits, lmr_b, lmr_t, plan, wctl, lists, mapbytes, streams, sizes, dsizes, offsets, mbuf, rstat, total;
 };
 
 static Layout layout(const Geo &g) {
@@ -95,6 +95,7 @@ static Layout layout(const Geo &g) {
     L.plan = o; o = align256(o + (lmr ? B * sizeof(LmrPlan) : 0));
     L.wctl = o; o = align256(o + (lmr ? sizeof(LmrWaveCtl) : 0));
     L.lists = o; o = align256(o + (lmr ? 8 * B * 4 : 0));
+    L.mapbytes = o; o = align256(o + (lmr ? 8 * B * 4 : 0));
     L.streams = o; o = align256(o + (lmr ? B * kLmrSlots * Tc * lmr_tile_stride_host(g.tile_log2, g.H, g.W) : 0));
     L.sizes = o; o = align256(o + (lmr ? B * kLmrSlots * Tc * 4 : 0));
     L.dsizes = o; o = align256(o + (lmr ? B * 2 * Tc * 4 : 0));
@@ -177,7 +178,7 @@ mmsb_status mmsb_content_owner_encode(const mmsb_shape *shape, const uint8_t *im
         // LMR: code eta and the candidate maps until both fit the MSB plane, then write it
         const LmrEncWS ew{at<LmrPlan>(ws, L.plan), at<LmrWaveCtl>(ws, L.wctl), at<int32_t>(ws, L.lists),
                           at<uint8_t>(ws, L.streams), at<int32_t>(ws, L.sizes), at<int32_t>(ws, L.dsizes),
-                          at<int32_t>(ws, L.offsets), at<uint8_t>(ws, L.mbuf)};
+                          at<int32_t>(ws, L.offsets), at<uint8_t>(ws, L.mbuf), at<int32_t>(ws, L.mapbytes)};
         run_kernel(K_LMR_PLAN, st, px, [&] { launch_lmr_plan(g, at<uint32_t>(ws, L.hist), ew, st); });
         for (int w = 0; w < 7; w++) {      // candidate waves; waves after the last undecided image exit at once
             run_kernel(K_CODER_ENC, st, px, [&] {

@@ -22,6 +22,7 @@ struct LmrPlan {
     int8_t state;                    // 0 undecided, 1 fits (b), 2 bad case
     int32_t b;
     int32_t dslot;                   // stream slot of the decided map (1 + its candidate index)
+    int32_t eta_bytes;               // coded eta bytes (after wave 0; -1: a tile over cap)
     long long K;                     // MSB-plane bits used: 7 + 32 T + 8 (bytes_eta + bytes_map)
 };
 
@@ -43,6 +44,7 @@ struct LmrEncWS {
     int32_t *dsizes;                 // [B][2][Tc] sizes of the decided eta + map streams
     int32_t *offsets;                // [B][2][Tc] their exclusive byte offsets
     uint8_t *cat;                    // [B][HW/8 + 128] the decided streams concatenated (MSB-plane bytes)
+    int32_t *mapbytes;               // [B][8] running coded bytes of each candidate's map (early abort)
 };
 __host__ __device__ inline int lmr_wave_k(int wave, int A, int Tc, int B, int R, int nc) {
     if (wave == 0) {                                            // eta + k candidates per image
