@@ -42,6 +42,7 @@ def parse():
     ap.add_argument("--batch", type=int, default=None, help="override the config's batch (testing only)")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--e2e-chunks", type=int, default=None, help="sub-batches of the pipelined e2e leg")
+    ap.add_argument("--e2e-lanes", type=int, default=3, help="streams of the pipelined e2e leg")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-security", action="store_true", help="skip the untimed statistics table")
@@ -338,8 +339,16 @@ def run_ours(args):
             self.MOUT = torch.zeros(sub, stride, dtype=torch.uint8, device=dev)
             self.SSE = torch.empty(sub, dtype=torch.int64, device=dev)
             self.done = torch.cuda.Event()
+            self.computed = torch.cuda.Event()
+            self.copied = None                    # last device->host copy of this lane's outputs
 
-    lanes = [Lane() for _ in range(min(3, nsub))]
+    lanes = [Lane() for _ in range(min(args.e2e_lanes, nsub))]
+    d2h_stream = torch.cuda.Stream(device=dev)   # device->host copies, off the lanes' streams
+
+    # one process: the lanes stream sub-batches back to back across steps (a lane reuses its
+    # buffers in its own stream order), so the copy engines do not drain at every step boundary;
+    # with several ranks each step ends with the records all-gather, so lanes join per step
+    streaming = world == 1
 
     def e2e_step():
         start = torch.cuda.Event()
@@ -347,13 +356,16 @@ def run_ours(args):
         for i in range(nsub):
             L = lanes[i % len(lanes)]
             a, z = i * sub, (i + 1) * sub
-            L.stream.wait_event(start)
+            if not streaming:
+                L.stream.wait_event(start)
             with torch.cuda.stream(L.stream):
                 L.I.copy_(hI[a:z], non_blocking=True)
                 L.K1.copy_(hK1[a:z], non_blocking=True)
                 L.K2.copy_(hK2[a:z], non_blocking=True)
                 L.MSG.copy_(hMSG[a:z], non_blocking=True)
                 L.NB.copy_(hNB[a:z], non_blocking=True)
+                if L.copied is not None:
+                    L.stream.wait_event(L.copied)    # the previous outputs of this lane are out
                 _, b_, c_, _ = G.encode(mid, L.I, L.K1, L.ws, out=L.enc)
                 G.embed(mid, L.enc, L.K2, L.MSG, L.NB, L.ws, out=L.marked)
                 G.extract(mid, L.marked, L.K2, stride, L.ws, out=L.MOUT)
@@ -361,23 +373,43 @@ def run_ours(args):
                 G.stats(L.I, L.rec, out=L.SSE)
                 if world > 1:
                     records[a:z] = P.make_records(b_, c_, L.SSE, st_)
+                L.computed.record(L.stream)
+            # the copy out on its own stream: the lane's next host->device copy need not wait for it
+            d2h_stream.wait_event(L.computed)
+            with torch.cuda.stream(d2h_stream):
                 hREC[a:z].copy_(L.rec, non_blocking=True)
                 hMOUT[a:z].copy_(L.MOUT, non_blocking=True)
                 hSSE[a:z].copy_(L.SSE, non_blocking=True)
-                L.done.record(L.stream)
-        for L in lanes:
-            stream.wait_event(L.done)
+                L.copied = torch.cuda.Event()
+                L.copied.record(d2h_stream)
+                L.done.record(d2h_stream)
+        if not streaming:
+            e2e_join()
         if world > 1:
             gathered[0] = P.gather_records(records, world)
 
+    def e2e_join():
+        for L in lanes:
+            L.done.record(L.stream)
+            stream.wait_event(L.done)
+        ev = torch.cuda.Event()
+        ev.record(d2h_stream)
+        stream.wait_event(ev)
+
     e2e_step()
+    e2e_join()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     f0.record(stream)
+    for L in lanes:                         # the lanes start after f0
+        L.stream.wait_event(f0)
+    t_issue = time.perf_counter()
     for _ in range(e2e_steps):
         e2e_step()
+    t_issue = (time.perf_counter() - t_issue) * 1e3 / e2e_steps    # host time to issue one step
+    e2e_join()
     f1.record(stream)
     torch.cuda.synchronize()
     te_ms = P.max_over_ranks(f0.elapsed_time(f1), dev, world)
@@ -421,7 +453,11 @@ def run_ours(args):
                 "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d * world),
                         "d2h_bytes_per_step": int(d2h * world), "steps": e2e_steps,
                         "path": f"pinned host -> cudaMemcpyAsync -> C ABI calls -> host; {nsub} sub-batches "
-                                f"of {sub} images pipelined over {len(lanes)} streams"},
+                                f"of {sub} images pipelined over {len(lanes)} streams"
+                                + (", streamed across steps (no drain at step boundaries)" if streaming else ""),
+                        "host_issue_ms_per_step": t_issue,
+                        "pcie_note": "both directions at once measured at 49.4 GB/s each on this box "
+                                     "(tools/pcie_probe.py): the e2e ceiling is bytes per step / 49.4 GB/s"},
                 "roofline": roof["dominant"],
                 "kernels": roof["kernels"],
                 "checks": {"payload_round_trip": ok_rt, "e2e_matches_device": ok_e2e,
