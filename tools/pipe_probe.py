@@ -1,3 +1,5 @@
+"""Copy-engine ceiling of the e2e pipeline shape (8 sub-batches over 3 streams, config-2 sizes):
+host->device and device->host copies with 0, 4 or 16 device-to-device copies as stand-in compute."""
 import torch, json
 B, HW, stride = 1000, 512*512, 46592
 hI = torch.empty(B, HW, dtype=torch.uint8).pin_memory()
