@@ -110,6 +110,20 @@ mmsb_status mmsb_receiver_recover(const mmsb_shape *shape, const uint8_t *marked
                                   void *stream);
 
 /*
+ * Capacity query (the SPEC's `capacity`): what an encrypted or marked image
+ * offers, derived the way the hider and the K2 receiver derive it -- no key needed.  b from the
+ * header (EMR: the LSBs of pixels 0..2, reading Q14; LMR: the MSB-plane header) and
+ * C = b' * (redundant pixels of the location map), b' = b (EMR) or b - 1 (LMR).
+ *   image        [B][H][W] device, an output of mmsb_content_owner_encode or mmsb_hider_embed.
+ *   b_out        [B] int32; 0 on FORMAT / BADCASE.
+ *   capacity_out [B] int64 bits (the frame, 32 + n, must fit); 0 on FORMAT / BADCASE.
+ *   img_status   [B]: OK, FORMAT or BADCASE.  Uses ws (LMR: the map decode).
+ */
+mmsb_status mmsb_capacity(const mmsb_shape *shape, const uint8_t *image, int32_t *b_out, int64_t *capacity_out,
+                          int32_t *img_status, void *ws, size_t ws_bytes, void *stream);
+
+/*
+ * Receiver holding both keys/*
  * Receiver holding both keys (EMR: P:842-843; LMR: P:1066-1067): extraction
  * with K2 and recovery with K1 in one call.  Outputs are those of mmsb_receiver_extract and
  * mmsb_receiver_recover on the same arguments; LMR decodes the coded maps (eta and the location

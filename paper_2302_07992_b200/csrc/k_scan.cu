@@ -546,6 +546,57 @@ void launch_scan(const Geo &g, bool embed, const uint8_t *in, uint8_t *out, cons
 }
 
 // ======================================================================================
+// capacity_kernel: the capacity an encrypted / marked image offers (the
+// SPEC's capacity query), as the hider and the K2 receiver derive it: b from the header (EMR:
+// 3 LSBs, Q14; LMR: the decoded MSB-plane header) and C = b' * (redundant pixels of the
+// location map).  One CTA per image.
+// ======================================================================================
+template <int METHOD>
+__global__ void __launch_bounds__(256) capacity_kernel(Geo g, const uint8_t *__restrict__ in,
+                                                       const uint32_t *__restrict__ map_bits,
+                                                       const int32_t *__restrict__ lmr_b, int32_t *__restrict__ b_out,
+                                                       int64_t *__restrict__ cap_out, int32_t *__restrict__ status) {
+    __shared__ unsigned long long red[8];
+    const int img = blockIdx.x, tid = threadIdx.x;
+    const uint8_t *src = in + (size_t)img * g.HW;
+    const int b = image_b<METHOD>(src, lmr_b, img);
+    if (b < 2) {                                              // EMR FORMAT; LMR status from the header kernel
+        if (tid == 0) {
+            b_out[img] = 0;
+            cap_out[img] = 0;
+            if constexpr (METHOD == 0) status[img] = 8;
+        }
+        return;
+    }
+    unsigned long long z = 0;
+    for (long long q = tid; q < g.HW / 16; q += 256) {
+        if constexpr (METHOD == 0) {
+            z += __popc(zero_mask16<0>(__ldg(reinterpret_cast<const uint4 *>(src) + q), 16 * q, nullptr, 0));
+        } else {
+            const long long pb = (long long)img * g.HW + 16 * q;
+            z += __popc(~(__ldg(map_bits + (pb >> 5)) >> (pb & 31)) & 0xFFFFu);
+        }
+    }
+#pragma unroll
+    for (int s2 = 16; s2 > 0; s2 >>= 1) z += __shfl_xor_sync(0xffffffffu, z, s2);
+    if ((tid & 31) == 0) red[tid >> 5] = z;
+    __syncthreads();
+    if (tid == 0) {
+        unsigned long long t = 0;
+        for (int w = 0; w < 8; w++) t += red[w];
+        b_out[img] = b;
+        cap_out[img] = (long long)(METHOD == 0 ? b : b - 1) * (long long)t;
+        status[img] = 0;
+    }
+}
+
+void launch_capacity(const Geo &g, const uint8_t *in, const uint32_t *map_bits, const int32_t *lmr_b,
+                     int32_t *b_out, int64_t *cap_out, int32_t *status, cudaStream_t st) {
+    if (g.method == 0) capacity_kernel<0><<<g.B, 256, 0, st>>>(g, in, map_bits, lmr_b, b_out, cap_out, status);
+    else capacity_kernel<1><<<g.B, 256, 0, st>>>(g, in, map_bits, lmr_b, b_out, cap_out, status);
+}
+
+// ======================================================================================
 // stats_kernel: per-image sum of squared differences, int64 via block reduction.
 // ======================================================================================
 __global__ void __launch_bounds__(256) stats_kernel(long long HW, const uint8_t *__restrict__ a,

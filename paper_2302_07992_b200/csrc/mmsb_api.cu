@@ -284,6 +284,21 @@ mmsb_status mmsb_receiver_both(const mmsb_shape *shape, const uint8_t *marked, c
     return check_launch();
 }
 
+mmsb_status mmsb_capacity(const mmsb_shape *shape, const uint8_t *image, int32_t *b_out, int64_t *capacity_out,
+                          int32_t *img_status, void *ws, size_t ws_bytes, void *stream) {
+    Geo g;
+    if (!geo_of(shape, &g) || !image || !b_out || !capacity_out || !img_status || !ws) return MMSB_E_INVAL;
+    const Layout L = layout(g);
+    if (ws_bytes < L.total) return MMSB_E_INVAL;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (cudaMemsetAsync(img_status, 0, (size_t)g.B * 4, st) != cudaSuccess) return MMSB_E_CUDA;
+    if (g.method == 1) lmr_decode_all(g, L, false, image, ws, img_status, nullptr, st);
+    launch_capacity(g, image, at<uint32_t>(ws, L.map_bits), at<int32_t>(ws, L.lmr_b), b_out, capacity_out,
+                    img_status, st);
+    g_launches += 1;
+    return check_launch();
+}
+
 mmsb_status mmsb_stats(const mmsb_shape *shape, const uint8_t *original, const uint8_t *recovered,
                        int64_t *sse_out, void *stream) {
     Geo g;

@@ -97,6 +97,8 @@ void launch_diff_stats(long long HW, int B, const uint8_t *a, const uint8_t *b, 
                        int64_t *absd, cudaStream_t st);
 void launch_ssim(int B, int H, int W, const uint8_t *a, const uint8_t *b, double *ssim, cudaStream_t st);
 void launch_status_merge(int B, const int32_t *second, int32_t *status, cudaStream_t st);
+void launch_capacity(const Geo &g, const uint8_t *in, const uint32_t *map_bits, const int32_t *lmr_b,
+                     int32_t *b_out, int64_t *cap_out, int32_t *status, cudaStream_t st);
 void launch_stats(long long HW, int B, const uint8_t *a, const uint8_t *b, int64_t *sse, cudaStream_t st);
 
 }  // namespace mmsb

@@ -47,6 +47,8 @@ def lib():
         L.mmsb_receiver_extract.argtypes = [sp, vp, vp, vp, C.c_int64, vp, vp, vp, C.c_size_t, vp]
         L.mmsb_receiver_recover.restype = C.c_int
         L.mmsb_receiver_recover.argtypes = [sp, vp, vp, vp, vp, vp, C.c_size_t, vp]
+        L.mmsb_capacity.restype = C.c_int
+        L.mmsb_capacity.argtypes = [sp, vp, vp, vp, vp, vp, C.c_size_t, vp]
         L.mmsb_receiver_both.restype = C.c_int
         L.mmsb_receiver_both.argtypes = [sp, vp, vp, vp, vp, C.c_int64, vp, vp, vp, vp, C.c_size_t, vp]
         L.mmsb_histogram.restype = C.c_int
@@ -186,6 +188,19 @@ def receive_both(method: int, marked: torch.Tensor, k1: torch.Tensor, k2: torch.
                                   _ptr(rec), _ptr(st), _ptr(ws.buf), ws.nbytes, _stream())
     _check(rc, "mmsb_receiver_both")
     return msg, nb, rec, st
+
+
+def capacity(method: int, image: torch.Tensor, ws: Workspace | None = None, tile_log2: int = 7):
+    """Capacity of an encrypted / marked image: returns (b, capacity_bits, status) -- mmsb_capacity."""
+    B, H, W = image.shape
+    ws = _ws(ws, method, B, H, W, tile_log2, image.device)
+    b = torch.empty(B, dtype=torch.int32, device=image.device)
+    cap = torch.empty(B, dtype=torch.int64, device=image.device)
+    st = torch.empty(B, dtype=torch.int32, device=image.device)
+    rc = lib().mmsb_capacity(C.byref(ws.shape), _ptr(image), _ptr(b), _ptr(cap), _ptr(st), _ptr(ws.buf), ws.nbytes,
+                             _stream())
+    _check(rc, "mmsb_capacity")
+    return b, cap, st
 
 
 def stats(original: torch.Tensor, recovered: torch.Tensor, out: torch.Tensor | None = None):
