@@ -49,6 +49,9 @@ def lib():
             u8p, i32p, i64p = C.POINTER(C.c_uint8), C.POINTER(C.c_int32), C.POINTER(C.c_int64)
             sig = {
                 "orc_chacha20_block": (None, [u8p, C.c_uint32, u8p, u8p]),
+                "orc_chacha_block": (None, [u8p, C.c_uint32, u8p, C.c_int, u8p]),
+                "orc_set_cipher_rounds": (None, [C.c_int]),
+                "orc_cipher_rounds": (C.c_int, []),
                 "orc_keystream": (None, [u8p, C.c_uint64, C.c_uint64, u8p]),
                 "orc_location_map": (None, [u8p, C.c_int, C.c_int, C.c_int, u8p]),
                 "orc_zero_counts": (None, [u8p, C.c_int, C.c_int, i64p]),
@@ -98,6 +101,22 @@ def chacha20_block(key: bytes, counter: int, nonce: bytes = bytes(12)) -> bytes:
     k, n, out = _u8(bytearray(key)), _u8(bytearray(nonce)), np.zeros(64, np.uint8)
     lib().orc_chacha20_block(_p(k), counter, _p(n), _p(out))
     return out.tobytes()
+
+
+def chacha_block(key: bytes, counter: int, rounds: int, nonce: bytes = bytes(12)) -> bytes:
+    """ChaCha block with an explicit round count (20 = RFC 8439; 12 / 8 = the reduced-round option)."""
+    k, n, out = _u8(bytearray(key)), _u8(bytearray(nonce)), np.zeros(64, np.uint8)
+    lib().orc_chacha_block(_p(k), counter, _p(n), rounds, _p(out))
+    return out.tobytes()
+
+
+def set_cipher_rounds(rounds: int) -> None:
+    """Rounds of the keystream every oracle call uses (20 unless 8 or 12): process-wide."""
+    lib().orc_set_cipher_rounds(int(rounds))
+
+
+def cipher_rounds() -> int:
+    return int(lib().orc_cipher_rounds())
 
 
 def keystream(key: bytes, offset: int, n: int) -> np.ndarray:

@@ -43,7 +43,9 @@ static void quarter_round(uint32_t *x, int a, int b, int c, int d)
     x[c] += x[d]; x[b] ^= x[c]; x[b] = rotl32(x[b], 7);
 }
 
-void orc_chacha20_block(const uint8_t key[32], uint32_t counter, const uint8_t nonce[12], uint8_t out[64])
+/* ChaCha block with an explicit round count (20 = RFC 8439; 12 and 8 = the reduced-round
+ * format option of SURVEY §8(f) NEXT 4: the same double rounds, fewer of them). */
+void orc_chacha_block(const uint8_t key[32], uint32_t counter, const uint8_t nonce[12], int rounds, uint8_t out[64])
 {
     uint32_t st[16], x[16];
     st[0] = 0x61707865u; st[1] = 0x3320646eu; st[2] = 0x79622d32u; st[3] = 0x6b206574u;
@@ -51,7 +53,7 @@ void orc_chacha20_block(const uint8_t key[32], uint32_t counter, const uint8_t n
     st[12] = counter;
     for (int i = 0; i < 3; i++) st[13 + i] = rd_le32(nonce + 4 * i);
     memcpy(x, st, sizeof x);
-    for (int r = 0; r < 10; r++) {               /* 20 rounds = 10 column+diagonal pairs */
+    for (int r = 0; r < rounds / 2; r++) {       /* column + diagonal round pairs (20 rounds = 10) */
         quarter_round(x, 0, 4, 8, 12); quarter_round(x, 1, 5, 9, 13);
         quarter_round(x, 2, 6, 10, 14); quarter_round(x, 3, 7, 11, 15);
         quarter_round(x, 0, 5, 10, 15); quarter_round(x, 1, 6, 11, 12);
@@ -64,13 +66,24 @@ void orc_chacha20_block(const uint8_t key[32], uint32_t counter, const uint8_t n
     }
 }
 
+/* rounds of the keystream cipher used by every call below: 20 (ChaCha20, reading Q12) unless a
+ * test selects the reduced-round option (8 or 12) -- process-wide, like the image format */
+static int g_cipher_rounds = 20;
+void orc_set_cipher_rounds(int rounds) { g_cipher_rounds = (rounds == 8 || rounds == 12) ? rounds : 20; }
+int orc_cipher_rounds(void) { return g_cipher_rounds; }
+
+void orc_chacha20_block(const uint8_t key[32], uint32_t counter, const uint8_t nonce[12], uint8_t out[64])
+{
+    orc_chacha_block(key, counter, nonce, 20, out);
+}
+
 void orc_keystream(const uint8_t key[32], uint64_t offset, uint64_t n, uint8_t *out)
 {
     static const uint8_t zero_nonce[12] = {0};
     uint8_t blk[64];
     for (uint64_t i = 0; i < n; i++) {
         uint64_t pos = offset + i;
-        if (i == 0 || pos % 64 == 0) orc_chacha20_block(key, (uint32_t)(pos / 64), zero_nonce, blk);
+        if (i == 0 || pos % 64 == 0) orc_chacha_block(key, (uint32_t)(pos / 64), zero_nonce, g_cipher_rounds, blk);
         out[i] = blk[pos % 64];
     }
 }

@@ -38,7 +38,12 @@
 
 /* ---- keystream ("a cryptographically secure stream cipher"; Q12) ---- */
 void orc_chacha20_block(const uint8_t key[32], uint32_t counter, const uint8_t nonce[12], uint8_t out[64]);
-/* bytes [offset, offset+n) of ChaCha20(key, nonce=0, counter=0) */
+/* the same block with `rounds` rounds (20, or the reduced-round option 12 / 8) */
+void orc_chacha_block(const uint8_t key[32], uint32_t counter, const uint8_t nonce[12], int rounds, uint8_t out[64]);
+/* rounds of the keystream every call uses: 20 (reading Q12) unless set to 8 or 12 */
+void orc_set_cipher_rounds(int rounds);
+int orc_cipher_rounds(void);
+/* bytes [offset, offset+n) of ChaCha(key, nonce=0, counter=0) with orc_cipher_rounds() rounds */
 void orc_keystream(const uint8_t key[32], uint64_t offset, uint64_t n, uint8_t *out);
 
 /* ---- location maps (eq. gliding1/gliding2; Q1-Q3) ---- */
