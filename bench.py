@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-security", action="store_true", help="skip the untimed statistics table")
     ap.add_argument("--lmr-emin", type=int, default=0, help="LMR rotation schedule {2^e..} (Tab. LMR_block_size)")
+    ap.add_argument("--cipher-rounds", type=int, default=0, choices=[0, 8, 12, 20],
+                    help="keystream rounds: 0/20 = ChaCha20 (default, reading Q12); 12 / 8 = reduced-round option")
     return ap.parse_args()
 
 
@@ -68,7 +70,9 @@ def config_json(args, cfg, method, B, world):
             "l2": "inputs larger than L2 (batch bytes >> 126 MB); no flush needed" if B * cfg["H"] * cfg["W"] > 126e6
             else "inputs smaller than L2",
             "keys": "ChaCha20 K = k128||k128 per image (reading Q13)",
-            "lmr_emin": (args.lmr_emin or 4) if method == "lmr" else None}
+            "lmr_emin": (args.lmr_emin or 4) if method == "lmr" else None,
+            "cipher": f"ChaCha{args.cipher_rounds or 20}" + ("" if args.cipher_rounds in (0, 20) else
+                                                              " (reduced-round format option, SURVEY 8(f) NEXT 4)")}
 
 
 # ------------------------------------------------------------------------------ clocks
@@ -125,7 +129,8 @@ class ClockSampler:
 def _oracle_one(a):
     import oracle as O
 
-    method, img, k1, k2, msg = a
+    method, img, k1, k2, msg, rounds = a
+    O.set_cipher_rounds(rounds or 20)
     st, E, b, C = O.encode(method, img, k1)
     n = max(C - 32, 0)
     _, Em = O.hide(method, E, k2, msg, n)
@@ -135,11 +140,11 @@ def _oracle_one(a):
     return img.size
 
 
-def oracle_throughput(method_id, imgs, k1, k2, msgs, seconds, cores):
+def oracle_throughput(method_id, imgs, k1, k2, msgs, seconds, cores, rounds=0):
     """The oracle as it stands, one image per task over a process pool of `cores` workers."""
     import multiprocessing as mp
 
-    tasks = [(method_id, imgs[j], k1[j].tobytes(), k2[j].tobytes(), msgs[j]) for j in range(len(imgs))]
+    tasks = [(method_id, imgs[j], k1[j].tobytes(), k2[j].tobytes(), msgs[j], rounds) for j in range(len(imgs))]
     ctx = mp.get_context("fork")
     with ctx.Pool(cores) as pool:
         pool.map(_oracle_one, tasks[:cores])                     # warm (builds/loads the oracle)
@@ -194,7 +199,7 @@ def run_reference(args):
     vals = []
     t_all = time.perf_counter()
     for s in range(args.warmup + args.steps):
-        v, n_img, dt = oracle_throughput(mid, imgs, k1, k2, msgs, per_step, cores)
+        v, n_img, dt = oracle_throughput(mid, imgs, k1, k2, msgs, per_step, cores, args.cipher_rounds)
         if s >= args.warmup:
             vals.append((v, n_img, dt))
     value = sum(n * H * W for _, n, _ in vals) / sum(dt for _, _, dt in vals) / 1e6
@@ -247,7 +252,7 @@ def run_ours(args):
     I = torch.from_numpy(imgs).to(dev)
     K1 = torch.from_numpy(k1).to(dev)
     K2 = torch.from_numpy(k2).to(dev)
-    ws = G.Workspace(mid, B, H, W, device=dev, lmr_emin=args.lmr_emin)
+    ws = G.Workspace(mid, B, H, W, device=dev, lmr_emin=args.lmr_emin, cipher_rounds=args.cipher_rounds)
     enc = torch.empty_like(I)
     marked = torch.empty_like(I)
     rec = torch.empty_like(I)
@@ -329,7 +334,7 @@ def run_ours(args):
     class Lane:
         def __init__(self):
             self.stream = torch.cuda.Stream(device=dev)
-            self.ws = G.Workspace(mid, sub, H, W, device=dev, lmr_emin=args.lmr_emin)
+            self.ws = G.Workspace(mid, sub, H, W, device=dev, lmr_emin=args.lmr_emin, cipher_rounds=args.cipher_rounds)
             self.I = torch.empty(sub, H, W, dtype=torch.uint8, device=dev)
             self.K1 = torch.empty(sub, 32, dtype=torch.uint8, device=dev)
             self.K2 = torch.empty(sub, 32, dtype=torch.uint8, device=dev)
@@ -470,7 +475,7 @@ def run_ours(args):
 
             cores = cpu_cores()
             v, n_img, dt = oracle_throughput(O.EMR if method == "emr" else O.LMR, imgs[:64], k1[:64], k2[:64],
-                                             msgs[:64], args.cpu_seconds, cores)
+                                             msgs[:64], args.cpu_seconds, cores, args.cipher_rounds)
             line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
                                     "sample": f"{n_img} images of this workload ({dt:.1f} s) through encode+embed+"
                                               f"extract+recover+SSE, one image per worker process; cpu: {cpu_model()}"}

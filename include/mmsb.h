@@ -56,6 +56,10 @@ typedef struct {
     int32_t lmr_emin;    /* LMR rotation blocks {2^e_min .. 2^e_max}: 0 = the paper's e_min = 4;
                             1..3 = the schedules of Tab. LMR_block_size.  Shared
                             protocol knowledge like the method (not stored in the image).  EMR: 1.  */
+    int32_t cipher_rounds; /* keystream cipher: 0 or 20 = ChaCha20 (RFC 8439, reading Q12); 12 or 8 =
+                            the reduced-round format option (P:656 asks only for
+                            "a cryptographically secure stream cipher").  Shared knowledge of both
+                            parties like the method; every K1 and K2 keystream uses it.            */
 } mmsb_shape;
 
 /* Bytes of device workspace the four calls need for this shape. 0 if the shape is invalid. */

@@ -133,7 +133,7 @@ __device__ __forceinline__ void key_role(const Geo &g, int img, int kidx, const 
     uint32_t key[8];
     load_key(keys, img, key);
     uint32_t blk[16];
-    chacha20_block(key, (uint32_t)(o >> 6), blk);
+    chacha20_block(key, (uint32_t)(o >> 6), blk, g.dr);
     uint32_t w[NW];
     if constexpr (NW == 16) {
 #pragma unroll

@@ -362,7 +362,7 @@ __global__ void __launch_bounds__(kScanThreads, 5) scan_kernel(Geo g, const uint
             }
         }))
         uint32_t ks[16];
-        if (tid < nblk) chacha20_block(key, (uint32_t)(blk0 + tid), ks);
+        if (tid < nblk) chacha20_block(key, (uint32_t)(blk0 + tid), ks, g.dr);
         __syncthreads();
         if (tid < nblk) {
 #pragma unroll
@@ -415,7 +415,7 @@ __global__ void __launch_bounds__(128) frame_encrypt_kernel(Geo g, const uint8_t
     uint32_t key[8];
     load_key(keys, img, key);
     uint32_t ks[16];
-    chacha20_block(key, (uint32_t)k, ks);
+    chacha20_block(key, (uint32_t)k, ks, g.dr);
     const uint32_t *mw = reinterpret_cast<const uint32_t *>(msg + (size_t)img * stride);
     const long long nmw = stride / 4;                            // message words in the row
     uint32_t o[16];

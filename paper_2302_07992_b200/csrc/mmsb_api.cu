@@ -122,7 +122,7 @@ static TileWS tile_ws(const Layout &L, void *ws) {
 
 static bool geo_of(const mmsb_shape *s, Geo *g) {
     if (!s) return false;
-    return make_geo(s->method, s->batch, s->height, s->width, s->tile_log2, s->lmr_emin, g);
+    return make_geo(s->method, s->batch, s->height, s->width, s->tile_log2, s->lmr_emin, g, s->cipher_rounds);
 }
 
 static mmsb_status check_launch() {

@@ -22,14 +22,24 @@ __device__ __forceinline__ uint32_t rotl32(uint32_t x, int n) { return __funnels
     a += b; d ^= a; d = rotl32(d, 16); c += d; b ^= c; b = rotl32(b, 12);       \
     a += b; d ^= a; d = rotl32(d, 8);  c += d; b ^= c; b = rotl32(b, 7);
 
-__device__ __forceinline__ void chacha20_block(const uint32_t k[8], uint32_t counter, uint32_t o[16]) {
+// dr = double rounds: 10 (ChaCha20: fully unrolled, branch-free) or 6 / 4 (the reduced-round
+// format option: a uniform loop)
+__device__ __forceinline__ void chacha20_block(const uint32_t k[8], uint32_t counter, uint32_t o[16], int dr = 10) {
     uint32_t x0 = 0x61707865u, x1 = 0x3320646eu, x2 = 0x79622d32u, x3 = 0x6b206574u;
     uint32_t x4 = k[0], x5 = k[1], x6 = k[2], x7 = k[3], x8 = k[4], x9 = k[5], x10 = k[6], x11 = k[7];
     uint32_t x12 = counter, x13 = 0, x14 = 0, x15 = 0;
+    if (dr == 10) {
 #pragma unroll
-    for (int i = 0; i < 10; i++) {
-        MMSB_QR(x0, x4, x8, x12) MMSB_QR(x1, x5, x9, x13) MMSB_QR(x2, x6, x10, x14) MMSB_QR(x3, x7, x11, x15)
-        MMSB_QR(x0, x5, x10, x15) MMSB_QR(x1, x6, x11, x12) MMSB_QR(x2, x7, x8, x13) MMSB_QR(x3, x4, x9, x14)
+        for (int i = 0; i < 10; i++) {
+            MMSB_QR(x0, x4, x8, x12) MMSB_QR(x1, x5, x9, x13) MMSB_QR(x2, x6, x10, x14) MMSB_QR(x3, x7, x11, x15)
+            MMSB_QR(x0, x5, x10, x15) MMSB_QR(x1, x6, x11, x12) MMSB_QR(x2, x7, x8, x13) MMSB_QR(x3, x4, x9, x14)
+        }
+    } else {
+#pragma unroll 2
+        for (int i = 0; i < dr; i++) {
+            MMSB_QR(x0, x4, x8, x12) MMSB_QR(x1, x5, x9, x13) MMSB_QR(x2, x6, x10, x14) MMSB_QR(x3, x7, x11, x15)
+            MMSB_QR(x0, x5, x10, x15) MMSB_QR(x1, x6, x11, x12) MMSB_QR(x2, x7, x8, x13) MMSB_QR(x3, x4, x9, x14)
+        }
     }
     o[0] = x0 + 0x61707865u; o[1] = x1 + 0x3320646eu; o[2] = x2 + 0x79622d32u; o[3] = x3 + 0x6b206574u;
     o[4] = x4 + k[0]; o[5] = x5 + k[1]; o[6] = x6 + k[2]; o[7] = x7 + k[3];

@@ -28,6 +28,7 @@ struct Geo {
     int tile_log2;       // LMR coder tile side 2^t
     int ntiles_coder;    // LMR coder tiles per plane
     uint32_t one;        // = 1, opaque to the compiler: multiplies that keep adds / shifts on the FMA pipe
+    int dr;              // keystream double rounds: 10 (ChaCha20), 6 (ChaCha12) or 4 (ChaCha8)
 };
 
 inline int ilog2(long long v) {
@@ -36,8 +37,10 @@ inline int ilog2(long long v) {
     return e;
 }
 
-inline bool make_geo(int method, int B, int H, int W, int tile_log2, int lmr_emin, Geo *g) {
+inline bool make_geo(int method, int B, int H, int W, int tile_log2, int lmr_emin, Geo *g, int cipher_rounds = 0) {
     if (B < 1 || H < 16 || W < 16 || H > 32768 || W > 32768) return false;
+    if (cipher_rounds != 0 && cipher_rounds != 20 && cipher_rounds != 12 && cipher_rounds != 8) return false;
+    g->dr = cipher_rounds ? cipher_rounds / 2 : 10;
     if ((H & (H - 1)) || (W & (W - 1))) return false;
     if (method != 0 && method != 1) return false;
     if (lmr_emin < 0 || lmr_emin > 4) return false;

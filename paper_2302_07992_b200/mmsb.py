@@ -21,7 +21,7 @@ _lib = None
 
 class _Shape(C.Structure):
     _fields_ = [("method", C.c_int32), ("batch", C.c_int32), ("height", C.c_int32), ("width", C.c_int32),
-                ("tile_log2", C.c_int32), ("lmr_emin", C.c_int32)]
+                ("tile_log2", C.c_int32), ("lmr_emin", C.c_int32), ("cipher_rounds", C.c_int32)]
 
 
 class MmsbError(RuntimeError):
@@ -73,8 +73,8 @@ def lib():
     return _lib
 
 
-def _shape(method: int, B: int, H: int, W: int, tile_log2: int = 7, lmr_emin: int = 0) -> _Shape:
-    return _Shape(method, B, H, W, tile_log2, lmr_emin)
+def _shape(method: int, B: int, H: int, W: int, tile_log2: int = 7, lmr_emin: int = 0, cipher_rounds: int = 0) -> _Shape:
+    return _Shape(method, B, H, W, tile_log2, lmr_emin, cipher_rounds)
 
 
 def _ptr(t: torch.Tensor | None):
@@ -103,8 +103,9 @@ def kernel_launches() -> int:
 class Workspace:
     """Caller-owned device scratch sized by mmsb_workspace_bytes (one per stream)."""
 
-    def __init__(self, method: int, B: int, H: int, W: int, tile_log2: int = 7, device=None, lmr_emin: int = 0):
-        self.shape = _shape(method, B, H, W, tile_log2, lmr_emin)
+    def __init__(self, method: int, B: int, H: int, W: int, tile_log2: int = 7, device=None, lmr_emin: int = 0,
+                 cipher_rounds: int = 0):
+        self.shape = _shape(method, B, H, W, tile_log2, lmr_emin, cipher_rounds)
         n = lib().mmsb_workspace_bytes(C.byref(self.shape))
         if n == 0:
             raise MmsbError(f"unsupported shape method={method} B={B} H={H} W={W} t={tile_log2}")

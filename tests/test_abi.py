@@ -35,7 +35,7 @@ def test_workspace_and_validation(lib):
     ok = _Shape(0, 1000, 512, 512, 7)
     assert lib.mmsb_workspace_bytes(C.byref(ok)) > 0
     for bad in [_Shape(0, 1, 500, 512, 7), _Shape(0, 1, 8, 8, 7), _Shape(2, 1, 64, 64, 7), _Shape(1, 1, 64, 64, 8),
-                _Shape(0, 0, 64, 64, 7)]:
+                _Shape(0, 0, 64, 64, 7), _Shape(0, 1, 64, 64, 7, 0, 9), _Shape(1, 1, 64, 64, 7, 0, 16)]:
         assert lib.mmsb_workspace_bytes(C.byref(bad)) == 0
     # null pointers are rejected synchronously, before any CUDA call
     lib.mmsb_content_owner_encode.restype = C.c_int
