@@ -11,9 +11,11 @@
 // 2^24 one byte at a time through a cache byte + 0xFF run, flush = 5 byte shifts; the
 // decoder reads bytes past the end of the tile's stream as 0.
 //
-// One GPU thread codes one tile (the coder is serial within a tile).  Each thread's model
-// (1024 x u16) lives in shared memory interleaved across the 32 lanes of the warp
-// (entry ctx of lane l at u16 index ctx*32 + l: at most 2-way bank conflicts).
+// One GPU thread codes one tile (the coder is serial within a tile); its model (1024 x u16)
+// lives in shared memory.  The fast kernels (tiles 32, 64 or 128 wide: every configured shape)
+// run 112-thread CTAs with a branch-free symbol step; the reference kernels
+// (coder_encode_kernel / coder_decode_kernel, one warp per CTA, model entry ctx of lane l at u16
+// index ctx*32 + l) serve narrower tiles.  Candidate maps are coded in waves (mmsb_kernels.h).
 #include <algorithm>
 
 #include "mmsb_device.cuh"
@@ -89,10 +91,9 @@ __device__ __forceinline__ bool wave_item(const Geo &g, int wave, int R, long lo
 }
 
 // ======================================================================================
-// coder_encode_kernel: one thread per (image, plane slot, coder tile).
-//   slot 0 = rotated eta (MSB of I_r, eq. MSB_map) -- wave 0 only;
-//   slot 1 = rotated location map L_b = [c_r < b] of candidate order[wave].
-// Images already decided (state != 0) are skipped.
+// coder_encode_kernel (tiles narrower than 32): one thread per work item of the wave
+// (wave_item): slot 0 = rotated eta (MSB of I_r, eq. MSB_map) -- wave 0 only; slot 1 + c =
+// rotated location map L_b = [c_r < b] of candidate c, b = order[c].
 // ======================================================================================
 __global__ void __launch_bounds__(kCoderThreads) coder_encode_kernel(Geo g, int wave, int round_tiles, const uint8_t *__restrict__ ceta,
                                                                      LmrEncWS ew) {
@@ -192,10 +193,11 @@ __global__ void lmr_plan_kernel(Geo g, const uint32_t *__restrict__ hist, LmrPla
 }
 
 // ======================================================================================
-// lmr_fit_kernel: one warp per image after wave `wave`: the first candidate for which
-// 7 + 16 (T_eta + T_L) + 8 (bytes_eta + bytes_L) <= M N decides b; otherwise the
-// image stays undecided, and after the last candidate it is a bad case.
-// Also produces the exclusive byte offsets of the streams (eta tiles, then map tiles).
+// lmr_fit_kernel: one warp per image after wave `wave`: among the candidates the wave coded, in
+// order, the first for which 7 + 16 (T_eta + T_L) + 8 (bytes_eta + bytes_L) <= M N decides b
+// (P:985); otherwise the image joins the next wave's list, and after the last candidate it is a
+// bad case.  Also produces the decided streams' sizes and exclusive byte offsets (eta
+// tiles, then map tiles).
 // ======================================================================================
 __global__ void lmr_fit_kernel(Geo g, int wave, int R, LmrEncWS e) {
     const int img = blockIdx.x, lane = threadIdx.x;
