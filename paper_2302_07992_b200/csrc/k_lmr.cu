@@ -272,16 +272,19 @@ __global__ void lmr_fit_kernel(Geo g, int wave, int R, LmrEncWS e) {
 // raster, eta first) into one byte string at their exclusive offsets: one CTA per stream,
 // coalesced copies.
 // ======================================================================================
-__global__ void __launch_bounds__(128) lmr_concat_kernel(Geo g, LmrEncWS ew) {
-    const int img = blockIdx.y, k = blockIdx.x;
+__global__ void __launch_bounds__(256) lmr_concat_kernel(Geo g, LmrEncWS ew) {
+    const int img = blockIdx.x;
     const LmrPlan pl = ew.plan[img];
     if (pl.state != 1) return;
     const int Tc = lmr_tile_count(g.H, g.W, g.tile_log2);
-    const int n = ew.dsizes[(size_t)img * 2 * Tc + k], o = ew.offsets[(size_t)img * 2 * Tc + k];
-    const int slot = k < Tc ? 0 : pl.dslot, tile = k < Tc ? k : k - Tc;
-    const uint8_t *src = ew.streams + (((size_t)img * kLmrSlots + slot) * Tc + tile) * lmr_tile_stride(g.tile_log2, g.H, g.W);
-    uint8_t *dst = ew.cat + (size_t)img * (g.HW / 8 + 128) + o;
-    for (int i = threadIdx.x; i < n; i += 128) dst[i] = src[i];
+    const int stride = lmr_tile_stride(g.tile_log2, g.H, g.W);
+    uint8_t *dst = ew.cat + (size_t)img * (g.HW / 8 + 128);
+    for (int k = 0; k < 2 * Tc; k++) {                          // streams in order, all threads per stream
+        const int n = ew.dsizes[(size_t)img * 2 * Tc + k], o = ew.offsets[(size_t)img * 2 * Tc + k];
+        const int slot = k < Tc ? 0 : pl.dslot, tile = k < Tc ? k : k - Tc;
+        const uint8_t *src = ew.streams + (((size_t)img * kLmrSlots + slot) * Tc + tile) * stride;
+        for (int i = threadIdx.x; i < n; i += 256) dst[o + i] = src[i];
+    }
 }
 
 // ======================================================================================
@@ -346,12 +349,14 @@ __global__ void __launch_bounds__(256) lmr_msb_write_kernel(Geo g, LmrEncWS ew,
         uint4 u = *reinterpret_cast<const uint4 *>(E + p);
         uint32_t wv[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
-        for (int i = 0; i < 16; i++) {
-            if (p + i < pl.K) {
-                const uint32_t bit = (bits16 >> (15 - i)) & 1u;
-                const int sh = 8 * (i & 3) + 7;
-                wv[i >> 2] = (wv[i >> 2] & ~(1u << sh)) | (bit << sh);
-            }
+        for (int i = 0; i < 4; i++) {
+            // the word's 4 plane bits (first pixel = nibble bit 3) to the byte MSBs: nib << (9k + 4)
+            // puts nibble bit 3-k at bit 8k+7, the four terms do not overlap
+            const uint32_t nib = (bits16 >> (12 - 4 * i)) & 0xFu;
+            const uint32_t msb = (nib * 0x80402010u) & 0x80808080u;
+            const long long nv = pl.K - (p + 4 * i);            // pixels of the word below K
+            const uint32_t bm = nv >= 4 ? 0xFFFFFFFFu : (nv <= 0 ? 0u : (1u << (8 * (int)nv)) - 1u);
+            wv[i] = (wv[i] & ~(bm & 0x80808080u)) | (msb & bm);
         }
         *reinterpret_cast<uint4 *>(E + p) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
     }
@@ -1050,10 +1055,9 @@ void launch_lmr_msb_write(const Geo &g, const LmrEncWS &e, const uint32_t *hist,
                           int64_t *cap_out, int32_t *status, cudaStream_t st) {
     const long long n16 = g.HW / 16;
     int bx = (int)((n16 + 255) / 256);
-    if (bx > 64) bx = 64;
+    if (bx > 16) bx = 16;
     dim3 grid(bx, g.B);
-    const int Tc = lmr_tile_count(g.H, g.W, g.tile_log2);
-    lmr_concat_kernel<<<dim3(2 * Tc, g.B), 128, 0, st>>>(g, e);
+    lmr_concat_kernel<<<g.B, 256, 0, st>>>(g, e);
     lmr_msb_write_kernel<<<grid, 256, 0, st>>>(g, e, hist, enc, b_out, cap_out, status);
 }
 
