@@ -81,11 +81,17 @@ __device__ __forceinline__ bool wave_item(const Geo &g, int wave, int R, long lo
     const int k = lmr_wave_k(wave, A, Tc, g.B, R, nc);
     const int per = (wave == 0 ? 1 : 0) + k;                     // slots per image in this wave
     if (gid >= (long long)A * per * Tc) return false;
-    const int i = (int)(gid / ((long long)per * Tc)), r = (int)(gid % ((long long)per * Tc));
-    const int j = r / Tc;
-    it.tile = r % Tc;
-    it.img = wave == 0 ? i : e.lists[(size_t)wave * g.B + i];
-    it.cand = wave == 0 ? j - 1 : nc + j;
+    if (wave == 0) {                                              // image-major: eta, candidates
+        const int i = (int)(gid / ((long long)per * Tc)), r = (int)(gid % ((long long)per * Tc));
+        it.tile = r % Tc;
+        it.img = i;
+        it.cand = r / Tc - 1;
+    } else {                                                      // candidate-major
+        const int j = (int)(gid / ((long long)A * Tc)), r = (int)(gid % ((long long)A * Tc));
+        it.tile = r % Tc;
+        it.img = e.lists[(size_t)wave * g.B + r / Tc];
+        it.cand = nc + j;
+    }
     it.slot = it.cand + 1;
     return true;
 }
@@ -1034,9 +1040,9 @@ void launch_coder_encode(const Geo &g, int wave, const uint8_t *ceta, const LmrE
     lmr_set_smem_attrs();
     const int Tc = lmr_tile_count(g.H, g.W, g.tile_log2);
     const int R = coder_round(g);
-    // most work items of this wave: wave 0 = B (1 + k0) Tc; later waves A k Tc <= max(R, B Tc)
+    // most work items of this wave: wave 0 = B (1 + k0) Tc; later waves A k Tc <= max(2R, B Tc)
     const long long total = wave == 0 ? (long long)g.B * (1 + lmr_wave_k(0, g.B, Tc, g.B, R, 0)) * Tc
-                                      : std::max<long long>(R, (long long)g.B * Tc);
+                                      : std::max<long long>(2ll * R, (long long)g.B * Tc);
     const unsigned grid = (unsigned)((total + kCoderThreads - 1) / kCoderThreads);
     const unsigned fgrid = (unsigned)((total + kFastThreads - 1) / kFastThreads);
     switch (lmr_tile_side(g.tile_log2, g.W)) {

@@ -27,8 +27,8 @@ struct LmrPlan {
 };
 
 // Candidate waves: wave w codes, for the count[w] images still undecided
-// (list[w]), candidates nc[w] .. nc[w]+k_w-1 of their order at once, k_w as many as fill one
-// round of resident tiles (wave 0: eta and candidate 0 for every image); the fit then takes the
+// (list[w]), candidates nc[w] .. nc[w]+k_w-1 of their order at once, k_w as many as fill two
+// rounds of resident tiles (wave 0: eta and candidate 0 for every image); the fit then takes the
 // first candidate in order that fits, exactly the serial walk's choice.
 constexpr int kLmrSlots = 8;         // stream slots per image: eta, candidates 0..6
 struct LmrWaveCtl {
@@ -51,8 +51,10 @@ __host__ __device__ inline int lmr_wave_k(int wave, int A, int Tc, int B, int R,
         const int k = R / (B * Tc) - 1;
         return k < 1 ? 1 : (k > 7 ? 7 : k);
     }
+    // later waves: up to two rounds of tiles; their items are candidate-major, so the CTAs of a
+    // failing candidate abort together and the next candidate's CTAs take their SMs
     if (A <= 0) return 1;
-    const int k = R / (A * Tc), left = 7 - nc;
+    const int k = 2 * R / (A * Tc), left = 7 - nc;
     return k < 1 ? 1 : (k > left ? left : k);
 }
 
