@@ -49,9 +49,27 @@ def main(tag):
         per_px[key[0]] = (rd + wr) / px
         launches[key[0]] = {"dram_read_bytes": rd, "dram_write_bytes": wr, "pixels": px,
                             "duration_us": float(d[idx["gpu__time_duration.sum"]])}
+    # LMR tile coder (units = coded symbols, as bench.py's profile counts them): wave 0 of an
+    # encode (eta + candidate 0 of 1000 config-3 images, 16 tiles of 16384 symbols each) and one
+    # decode (the map plane), from gpurun_out/prof_coder*.ncu-rep / prof_dec*.ncu-rep when present
+    for name, pattern, syms in (("coder_encode_kernel", "prof_coder", 1000 * 2 * 16 * 16384),
+                                ("lmr_pack+header+coder_decode_kernels", "prof_dec", 1000 * 16 * 16384)):
+        reps = sorted((f for f in os.listdir(OUT) if f.startswith(pattern) and f.endswith(".ncu-rep")),
+                      key=lambda f: os.path.getmtime(os.path.join(OUT, f)))
+        if not reps:
+            continue
+        rr = list(csv.reader(run(["ncu", "-i", os.path.join(OUT, reps[-1]), "--page", "raw", "--csv"]).splitlines()))
+        h2, u2, d2 = rr[0], rr[1], rr[2]
+        i2 = {h: i for i, h in enumerate(h2)}
+        rd = float(d2[i2["dram__bytes_read.sum"]]) * SCALE[u2[i2["dram__bytes_read.sum"]]]
+        wr = float(d2[i2["dram__bytes_write.sum"]]) * SCALE[u2[i2["dram__bytes_write.sum"]]]
+        per_px[name] = (rd + wr) / syms
+        launches[name] = {"dram_read_bytes": rd, "dram_write_bytes": wr, "symbols": syms, "report": reps[-1],
+                          "duration_us": float(d2[i2["gpu__time_duration.sum"]])}
     json.dump({"source": f"ncu --set full --clock-control none, tools/prof_run.py --batch 128 (config-2 images, "
                          f"EMR), {tag}; cold-cache serialized replay: writes still resident in L2 at kernel end "
-                         f"are not counted", "bytes_per_px": per_px, "launches": launches},
+                         f"are not counted; the LMR coder entries are bytes per coded symbol (config 3)",
+               "bytes_per_px": per_px, "launches": launches},
               open(os.path.join(PROF, "traffic.json"), "w"), indent=1)
     print(json.dumps(per_px, indent=1))
 
