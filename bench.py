@@ -43,6 +43,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--e2e-chunks", type=int, default=None, help="sub-batches of the pipelined e2e leg")
     ap.add_argument("--e2e-lanes", type=int, default=3, help="streams of the pipelined e2e leg")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the e2e leg (ncu launch-list runs only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-security", action="store_true", help="skip the untimed statistics table")
@@ -316,111 +317,113 @@ def run_ours(args):
     px_total = world * B * HW * args.steps
     value = px_total / (ms_max / 1e3) / 1e6
 
-    # ---- e2e: host (pinned) buffers through the ABI, copies inside the timed region.  The batch is
-    # cut into sub-batches pipelined over 3 streams, so that the host->device copy of one, the
-    # four calls on another and the device->host copy of a third overlap (PCIe bound).
-    e2e_steps = args.e2e_steps or max(3, min(10, args.steps // 10))
-    hI = torch.from_numpy(imgs).pin_memory()
-    hK1, hK2 = torch.from_numpy(k1).pin_memory(), torch.from_numpy(k2).pin_memory()
-    hMSG, hNB = torch.from_numpy(msgs).pin_memory(), torch.from_numpy(nbits_np).pin_memory()
-    hREC = torch.empty_like(hI).pin_memory()
-    hMOUT = torch.empty(B, stride, dtype=torch.uint8).pin_memory()
-    hSSE = torch.empty(B, dtype=torch.int64).pin_memory()
-    h2d = hI.numel() + hK1.numel() + hK2.numel() + hMSG.numel() + hNB.numel() * 8
-    d2h = hREC.numel() + hMOUT.numel() + hSSE.numel() * 8
-    nsub = next(k for k in (args.e2e_chunks, 8, 5, 4, 2, 1) if k and B % k == 0)
-    sub = B // nsub
+    e2e_value, ok_e2e, e2e_steps, h2d, d2h, t_issue, nsub, sub, streaming, nlanes = None, True, 0, 0, 0, 0.0, 0, 0, False, 0
+    if not args.no_e2e:
+        # ---- e2e: host (pinned) buffers through the ABI, copies inside the timed region.  The batch is
+        # cut into sub-batches pipelined over 3 streams, so that the host->device copy of one, the
+        # four calls on another and the device->host copy of a third overlap (PCIe bound).
+        e2e_steps = args.e2e_steps or max(3, min(10, args.steps // 10))
+        hI = torch.from_numpy(imgs).pin_memory()
+        hK1, hK2 = torch.from_numpy(k1).pin_memory(), torch.from_numpy(k2).pin_memory()
+        hMSG, hNB = torch.from_numpy(msgs).pin_memory(), torch.from_numpy(nbits_np).pin_memory()
+        hREC = torch.empty_like(hI).pin_memory()
+        hMOUT = torch.empty(B, stride, dtype=torch.uint8).pin_memory()
+        hSSE = torch.empty(B, dtype=torch.int64).pin_memory()
+        h2d = hI.numel() + hK1.numel() + hK2.numel() + hMSG.numel() + hNB.numel() * 8
+        d2h = hREC.numel() + hMOUT.numel() + hSSE.numel() * 8
+        nsub = next(k for k in (args.e2e_chunks, 8, 5, 4, 2, 1) if k and B % k == 0)
+        sub = B // nsub
 
-    class Lane:
-        def __init__(self):
-            self.stream = torch.cuda.Stream(device=dev)
-            self.ws = G.Workspace(mid, sub, H, W, device=dev, lmr_emin=args.lmr_emin, cipher_rounds=args.cipher_rounds)
-            self.I = torch.empty(sub, H, W, dtype=torch.uint8, device=dev)
-            self.K1 = torch.empty(sub, 32, dtype=torch.uint8, device=dev)
-            self.K2 = torch.empty(sub, 32, dtype=torch.uint8, device=dev)
-            self.MSG = torch.empty(sub, stride, dtype=torch.uint8, device=dev)
-            self.NB = torch.empty(sub, dtype=torch.int64, device=dev)
-            self.enc, self.marked, self.rec = (torch.empty_like(self.I) for _ in range(3))
-            self.MOUT = torch.zeros(sub, stride, dtype=torch.uint8, device=dev)
-            self.SSE = torch.empty(sub, dtype=torch.int64, device=dev)
-            self.done = torch.cuda.Event()
-            self.computed = torch.cuda.Event()
-            self.copied = None                    # last device->host copy of this lane's outputs
+        class Lane:
+            def __init__(self):
+                self.stream = torch.cuda.Stream(device=dev)
+                self.ws = G.Workspace(mid, sub, H, W, device=dev, lmr_emin=args.lmr_emin, cipher_rounds=args.cipher_rounds)
+                self.I = torch.empty(sub, H, W, dtype=torch.uint8, device=dev)
+                self.K1 = torch.empty(sub, 32, dtype=torch.uint8, device=dev)
+                self.K2 = torch.empty(sub, 32, dtype=torch.uint8, device=dev)
+                self.MSG = torch.empty(sub, stride, dtype=torch.uint8, device=dev)
+                self.NB = torch.empty(sub, dtype=torch.int64, device=dev)
+                self.enc, self.marked, self.rec = (torch.empty_like(self.I) for _ in range(3))
+                self.MOUT = torch.zeros(sub, stride, dtype=torch.uint8, device=dev)
+                self.SSE = torch.empty(sub, dtype=torch.int64, device=dev)
+                self.done = torch.cuda.Event()
+                self.computed = torch.cuda.Event()
+                self.copied = None                    # last device->host copy of this lane's outputs
 
-    lanes = [Lane() for _ in range(min(args.e2e_lanes, nsub))]
-    d2h_stream = torch.cuda.Stream(device=dev)   # device->host copies, off the lanes' streams
+        lanes = [Lane() for _ in range(min(args.e2e_lanes, nsub))]
+        d2h_stream = torch.cuda.Stream(device=dev)   # device->host copies, off the lanes' streams
 
-    # one process: the lanes stream sub-batches back to back across steps (a lane reuses its
-    # buffers in its own stream order), so the copy engines do not drain at every step boundary;
-    # with several ranks each step ends with the records all-gather, so lanes join per step
-    streaming = world == 1
+        # one process: the lanes stream sub-batches back to back across steps (a lane reuses its
+        # buffers in its own stream order), so the copy engines do not drain at every step boundary;
+        # with several ranks each step ends with the records all-gather, so lanes join per step
+        streaming = world == 1
 
-    def e2e_step():
-        start = torch.cuda.Event()
-        start.record(stream)
-        for i in range(nsub):
-            L = lanes[i % len(lanes)]
-            a, z = i * sub, (i + 1) * sub
+        def e2e_step():
+            start = torch.cuda.Event()
+            start.record(stream)
+            for i in range(nsub):
+                L = lanes[i % len(lanes)]
+                a, z = i * sub, (i + 1) * sub
+                if not streaming:
+                    L.stream.wait_event(start)
+                with torch.cuda.stream(L.stream):
+                    L.I.copy_(hI[a:z], non_blocking=True)
+                    L.K1.copy_(hK1[a:z], non_blocking=True)
+                    L.K2.copy_(hK2[a:z], non_blocking=True)
+                    L.MSG.copy_(hMSG[a:z], non_blocking=True)
+                    L.NB.copy_(hNB[a:z], non_blocking=True)
+                    if L.copied is not None:
+                        L.stream.wait_event(L.copied)    # the previous outputs of this lane are out
+                    _, b_, c_, _ = G.encode(mid, L.I, L.K1, L.ws, out=L.enc)
+                    G.embed(mid, L.enc, L.K2, L.MSG, L.NB, L.ws, out=L.marked)
+                    G.extract(mid, L.marked, L.K2, stride, L.ws, out=L.MOUT)
+                    _, st_ = G.recover(mid, L.marked, L.K1, L.ws, out=L.rec)
+                    G.stats(L.I, L.rec, out=L.SSE)
+                    if world > 1:
+                        records[a:z] = P.make_records(b_, c_, L.SSE, st_)
+                    L.computed.record(L.stream)
+                # the copy out on its own stream: the lane's next host->device copy need not wait for it
+                d2h_stream.wait_event(L.computed)
+                with torch.cuda.stream(d2h_stream):
+                    hREC[a:z].copy_(L.rec, non_blocking=True)
+                    hMOUT[a:z].copy_(L.MOUT, non_blocking=True)
+                    hSSE[a:z].copy_(L.SSE, non_blocking=True)
+                    L.copied = torch.cuda.Event()
+                    L.copied.record(d2h_stream)
+                    L.done.record(d2h_stream)
             if not streaming:
-                L.stream.wait_event(start)
-            with torch.cuda.stream(L.stream):
-                L.I.copy_(hI[a:z], non_blocking=True)
-                L.K1.copy_(hK1[a:z], non_blocking=True)
-                L.K2.copy_(hK2[a:z], non_blocking=True)
-                L.MSG.copy_(hMSG[a:z], non_blocking=True)
-                L.NB.copy_(hNB[a:z], non_blocking=True)
-                if L.copied is not None:
-                    L.stream.wait_event(L.copied)    # the previous outputs of this lane are out
-                _, b_, c_, _ = G.encode(mid, L.I, L.K1, L.ws, out=L.enc)
-                G.embed(mid, L.enc, L.K2, L.MSG, L.NB, L.ws, out=L.marked)
-                G.extract(mid, L.marked, L.K2, stride, L.ws, out=L.MOUT)
-                _, st_ = G.recover(mid, L.marked, L.K1, L.ws, out=L.rec)
-                G.stats(L.I, L.rec, out=L.SSE)
-                if world > 1:
-                    records[a:z] = P.make_records(b_, c_, L.SSE, st_)
-                L.computed.record(L.stream)
-            # the copy out on its own stream: the lane's next host->device copy need not wait for it
-            d2h_stream.wait_event(L.computed)
-            with torch.cuda.stream(d2h_stream):
-                hREC[a:z].copy_(L.rec, non_blocking=True)
-                hMOUT[a:z].copy_(L.MOUT, non_blocking=True)
-                hSSE[a:z].copy_(L.SSE, non_blocking=True)
-                L.copied = torch.cuda.Event()
-                L.copied.record(d2h_stream)
-                L.done.record(d2h_stream)
-        if not streaming:
-            e2e_join()
-        if world > 1:
-            gathered[0] = P.gather_records(records, world)
+                e2e_join()
+            if world > 1:
+                gathered[0] = P.gather_records(records, world)
 
-    def e2e_join():
-        for L in lanes:
-            L.done.record(L.stream)
-            stream.wait_event(L.done)
-        ev = torch.cuda.Event()
-        ev.record(d2h_stream)
-        stream.wait_event(ev)
+        def e2e_join():
+            for L in lanes:
+                L.done.record(L.stream)
+                stream.wait_event(L.done)
+            ev = torch.cuda.Event()
+            ev.record(d2h_stream)
+            stream.wait_event(ev)
 
-    e2e_step()
-    e2e_join()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    f0.record(stream)
-    for L in lanes:                         # the lanes start after f0
-        L.stream.wait_event(f0)
-    t_issue = time.perf_counter()
-    for _ in range(e2e_steps):
         e2e_step()
-    t_issue = (time.perf_counter() - t_issue) * 1e3 / e2e_steps    # host time to issue one step
-    e2e_join()
-    f1.record(stream)
-    torch.cuda.synchronize()
-    te_ms = P.max_over_ranks(f0.elapsed_time(f1), dev, world)
-    e2e_value = world * B * HW * e2e_steps / (te_ms / 1e3) / 1e6
-    ok_e2e = bool(np.array_equal(hREC.numpy(), rec.cpu().numpy())) and bool(
-        np.array_equal(hSSE.numpy(), SSE.cpu().numpy()))
+        e2e_join()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for L in lanes:                         # the lanes start after f0
+            L.stream.wait_event(f0)
+        t_issue = time.perf_counter()
+        for _ in range(e2e_steps):
+            e2e_step()
+        t_issue = (time.perf_counter() - t_issue) * 1e3 / e2e_steps    # host time to issue one step
+        e2e_join()
+        f1.record(stream)
+        torch.cuda.synchronize()
+        te_ms = P.max_over_ranks(f0.elapsed_time(f1), dev, world)
+        e2e_value = world * B * HW * e2e_steps / (te_ms / 1e3) / 1e6
+        ok_e2e = bool(np.array_equal(hREC.numpy(), rec.cpu().numpy())) and bool(
+            np.array_equal(hSSE.numpy(), SSE.cpu().numpy()))
 
     # the paper's security / quality table (Tab. analysis, Tab. EMR_results) on
     # this rank's batch, outside the timed region: entropy / chi^2 of I, I_e, I_e'; NPCR / UACI and
@@ -455,7 +458,8 @@ def run_ours(args):
                 "config": config_json(args, cfg, method, B, world),
                 "gpu_launches": int(launches),
                 "clocks": sampler.record(),
-                "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d * world),
+                "e2e": {"skipped": "--no-e2e (profiling runs only)"} if args.no_e2e else
+                       {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d * world),
                         "d2h_bytes_per_step": int(d2h * world), "steps": e2e_steps,
                         "path": f"pinned host -> cudaMemcpyAsync -> C ABI calls -> host; {nsub} sub-batches "
                                 f"of {sub} images pipelined over {len(lanes)} streams"
