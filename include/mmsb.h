@@ -84,11 +84,11 @@ mmsb_status mmsb_content_owner_encode(const mmsb_shape *shape, const uint8_t *im
  *   encrypted  [B][H][W] I_e
  *   k2         [B][32]   data-hiding keys K2
  *   msg_bytes  [B][stride_bytes] plain messages, msg_bits[B] (int64) bits each
- *   marked     [B][H][W] output I_e' (must NOT alias encrypted)
+ *   marked     [B][H][W] output I_e' (may alias encrypted: embedding in place)
  * The frame BE32(n) || message is XORed with the K2 keystream and written b (EMR, bit
  * positions 1..b) or b-1 (LMR, positions 2..b) bits per redundant pixel in raster order of
  * the rotated domain; all other bits are copied.  img_status: OK, CAPACITY (then marked ==
- * encrypted), FORMAT, BADCASE.
+ * encrypted: nothing is embedded), FORMAT, BADCASE.
  */
 mmsb_status mmsb_hider_embed(const mmsb_shape *shape, const uint8_t *encrypted, const uint8_t *k2,
                              const uint8_t *msg_bytes, const int64_t *msg_bits, int64_t stride_bytes,

@@ -172,6 +172,41 @@ __device__ __forceinline__ int image_b(const uint8_t *img0, const int32_t *lmr_b
     }
 }
 
+// embed's counting pass: zero pixels of every chunk and of the image, so that the chunk kernel
+// knows its prefix and the image's capacity before it writes (the hider may embed in place)
+template <int METHOD>
+__global__ void __launch_bounds__(kScanThreads) scan_count_kernel(Geo g, const uint8_t *__restrict__ in,
+                                                                  const uint32_t *__restrict__ map_bits, ScanWS ws) {
+    __shared__ uint32_t red[kScanThreads / 32];
+    const int tid = threadIdx.x;
+    const int img = blockIdx.x / g.nchunks, chunk = blockIdx.x % g.nchunks;
+    const int cpx = g.HW < kChunk ? (int)g.HW : kChunk;
+    const long long p0 = (long long)chunk * cpx;
+    const uint4 *src = reinterpret_cast<const uint4 *>(in + (size_t)img * g.HW + p0);
+    uint32_t c = 0;
+#pragma unroll
+    for (int r = 0; r < kScanRounds; r++) {
+        const int q = r * kScanThreads + tid;
+        if (16 * q >= cpx) continue;
+        if constexpr (METHOD == 0) {
+            c += __popc(zero_mask16<0>(__ldg(src + q), p0 + 16 * q, nullptr, 0));
+        } else {
+            const long long pb = (long long)img * g.HW + p0 + 16 * q;
+            c += __popc(~(__ldg(map_bits + (pb >> 5)) >> (pb & 31)) & 0xFFFFu);
+        }
+    }
+#pragma unroll
+    for (int s2 = 16; s2 > 0; s2 >>= 1) c += __shfl_xor_sync(0xffffffffu, c, s2);
+    if ((tid & 31) == 0) red[tid >> 5] = c;
+    __syncthreads();
+    if (tid == 0) {
+        uint32_t t = 0;
+        for (int w = 0; w < kScanThreads / 32; w++) t += red[w];
+        ws.counts[blockIdx.x] = t;
+        if (t) atomicAdd(ws.ztot + img, (unsigned long long)t);
+    }
+}
+
 template <int METHOD, bool EMBED>
 __global__ void __launch_bounds__(kScanThreads, 5) scan_kernel(Geo g, const uint8_t *__restrict__ in,
                                                             uint8_t *__restrict__ out, const uint8_t *__restrict__ keys,
@@ -187,6 +222,7 @@ __global__ void __launch_bounds__(kScanThreads, 5) scan_kernel(Geo g, const uint
     __shared__ uint32_t wtot[kScanRounds][kScanThreads / 32], woff[kScanRounds][kScanThreads / 32];
     __shared__ long long sh_prefix;
     __shared__ uint32_t sh_agg;
+    __shared__ uint32_t wpre[kScanThreads / 32];
     __shared__ uint32_t esel[16], csel[16];
 
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -219,8 +255,16 @@ __global__ void __launch_bounds__(kScanThreads, 5) scan_kernel(Geo g, const uint
     uint32_t key[8];
     load_key(keys, img, key);
     long long n = 0;
-    if constexpr (EMBED) n = msg_bits[img];
-    __syncthreads();                                         // barrier initialised
+    if constexpr (EMBED) {
+        n = msg_bits[img];
+        // this chunk's prefix: the zero counts of the image's earlier chunks (scan_count_kernel)
+        uint32_t part = 0;
+        for (int c = tid; c < chunk; c += kScanThreads) part += __ldg(ws.counts + (size_t)img * g.nchunks + c);
+#pragma unroll
+        for (int s2 = 16; s2 > 0; s2 >>= 1) part += __shfl_xor_sync(0xffffffffu, part, s2);
+        if (lane == 0) wpre[wid] = part;
+    }
+    __syncthreads();                                         // barrier initialised (and wpre written)
     mbar_wait(&bar, 0);
 
     if (b < 2) {                                             // FORMAT (EMR) / BADCASE, FORMAT (LMR)
@@ -268,11 +312,17 @@ __global__ void __launch_bounds__(kScanThreads, 5) scan_kernel(Geo g, const uint
         agg = __shfl_sync(0xffffffffu, incl, 31);
     }
 
-    // ---- single-pass decoupled look-back over the image's chunks (blockIdx order).  Warp 0
-    // publishes the aggregate, then inspects 32 predecessors per probe: each lane spins on its
-    // own predecessor until it has published; the nearest inclusive prefix ends the walk and
-    // the aggregates in front of it are summed.
-    if (wid == 0) {
+    // ---- extract: single-pass decoupled look-back over the image's chunks (blockIdx order).
+    // Warp 0 publishes the aggregate, then inspects 32 predecessors per probe: each lane spins
+    // on its own predecessor until it has published; the nearest inclusive prefix ends the walk
+    // and the aggregates in front of it are summed.  (Embed has its prefix from the counts.)
+    if constexpr (EMBED) {
+        if (wid == 0 && lane == 0) {
+            long long pre = 0;
+            for (int w = 0; w < kScanThreads / 32; w++) pre += wpre[w];
+            sh_prefix = pre;
+        }
+    } else if (wid == 0) {
         unsigned long long *st = ws.states + (size_t)img * g.nchunks;
         unsigned long long prefix = 0;
         if (chunk == 0) {
@@ -314,7 +364,10 @@ __global__ void __launch_bounds__(kScanThreads, 5) scan_kernel(Geo g, const uint
     const long long lo = prefix * bp, hi = (prefix + (long long)agg) * bp;
 
     if constexpr (EMBED) {
-        const bool n_ok = n >= 0 && n <= 8 * stride && n <= 0xFFFFFFFFll;
+        // the frame is written only when it fits the image's capacity (else the chunk is copied
+        // through unchanged: CAPACITY), so embedding in place needs no restore
+        const long long C = (long long)__ldcg(ws.ztot + img) * bp;
+        const bool n_ok = n >= 0 && n <= 8 * stride && n <= 0xFFFFFFFFll && 32 + n <= C;
         const long long F = n_ok ? 32 + n : 0;
         const long long hie = hi < F ? hi : F;
         const long long blk0 = lo >> 9;
@@ -462,19 +515,17 @@ __global__ void __launch_bounds__(256) scan_finish_kernel(Geo g, const uint8_t *
         return;
     }
     const int bp = METHOD == 0 ? b : b - 1;
-    const unsigned long long last = ld_acquire(ws.states + (size_t)img * g.nchunks + g.nchunks - 1);
-    const long long C = (long long)(last & kValMask) * bp;
     if constexpr (EMBED) {
+        // the chunk kernel embedded nothing unless the frame fits: CAPACITY leaves marked ==
+        // encrypted without a copy here
+        const long long C = (long long)__ldcg(ws.ztot + img) * bp;
         const long long n = msg_bits[img];
         const bool n_ok = n >= 0 && n <= 8 * stride && n <= 0xFFFFFFFFll;
         const bool fits = n_ok && 32 + n <= C;
         if (tid == 0) status[img] = fits ? 0 : (n_ok ? 3 : 2);
-        if (!fits) {                                          // CAPACITY: marked = encrypted
-            for (long long p = tid * 16; p < g.HW; p += 256 * 16)
-                *reinterpret_cast<uint4 *>(out + (size_t)img * g.HW + p) =
-                    __ldg(reinterpret_cast<const uint4 *>(src + p));
-        }
     } else {
+        const unsigned long long last = ld_acquire(ws.states + (size_t)img * g.nchunks + g.nchunks - 1);
+        const long long C = (long long)(last & kValMask) * bp;
         uint32_t *mo = reinterpret_cast<uint32_t *>(msg_out + (size_t)img * stride);
         const unsigned long long *pp = ws.parts + (size_t)img * g.nchunks * 2;
         const long long rw = C > 32 ? (C - 32 + 31) / 32 : 0;
@@ -523,6 +574,7 @@ static void launch_scan_t(const Geo &g, const uint8_t *in, uint8_t *out, const u
                           cudaStream_t st) {
     const unsigned grid = (unsigned)((long long)g.B * g.nchunks);
     if constexpr (EMBED) {
+        scan_count_kernel<METHOD><<<grid, kScanThreads, 0, st>>>(g, in, map_bits, ws);
         const long long fb = (32 + 8 * stride + 511) / 512;     // frame blocks (capped by ef_words in the kernel)
         const long long nb = fb < ws.ef_words / 16 ? fb : ws.ef_words / 16;
         frame_encrypt_kernel<<<dim3((unsigned)((nb + 127) / 128), g.B), 128, 0, st>>>(g, keys, msg, msg_bits, stride, ws);

@@ -18,7 +18,7 @@ static std::atomic<unsigned long long> g_launches{0};
 // ---- live per-kernel timing (CUDA events recorded on the launch stream around each kernel)
 enum KernelId { K_ENCODE = 0, K_RECOVER, K_EMBED, K_EXTRACT, K_STATS, K_LMR_PLAN, K_CODER_ENC, K_LMR_FIT,
                 K_LMR_MSB, K_LMR_DECODE, K_COUNT };
-static const char *kKernelNames[K_COUNT] = {"encode_kernel", "recover_kernel", "frame_encrypt+scan_kernel<embed>+finish",
+static const char *kKernelNames[K_COUNT] = {"encode_kernel", "recover_kernel", "scan_count+frame_encrypt+scan_kernel<embed>+finish",
                                             "scan_kernel<extract>+finish", "stats_kernel", "lmr_plan_kernel",
                                             "coder_encode_kernel", "lmr_fit_kernel", "lmr_concat+msb_write_kernels",
                                             "lmr_pack+header+coder_decode_kernels"};
@@ -63,7 +63,7 @@ static size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
 // worker CTA of the same launch shortly after, and then discarded from L2.
 struct Layout {
     size_t s, rec, pyr, hist, kdone, rstate, tile_zero_end, ragg, rinc;   // fused tile kernels
-    size_t states, parts, hdr, scan_zero_end, ef;                              // scan kernels
+    size_t states, parts, hdr, ztot, scan_zero_end, ef, counts;                // scan kernels
     size_t ceta, eta_bits, map_bits, lmr_b, lmr_t, plan, wctl, lists, mapbytes, streams, sizes, dsizes, offsets, mbuf, rstat, total;
 };
 
@@ -83,8 +83,10 @@ static Layout layout(const Geo &g) {
     L.states = o; o = align256(o + B * g.nchunks * 8);
     L.parts = o; o = align256(o + B * g.nchunks * 16);
     L.hdr = o; o = align256(o + B * 4);
+    L.ztot = o; o = align256(o + B * 8);
     L.scan_zero_end = o;
     L.ef = o; o = align256(o + B * (size_t)ef_words_of(g.HW) * 4);
+    L.counts = o; o = align256(o + B * g.nchunks * 4);
     const bool lmr = g.method == 1;
     L.ceta = o; o = align256(o + (lmr ? B * g.HW : 0));
     L.eta_bits = o; o = align256(o + (lmr ? B * g.HW / 8 : 0));
@@ -199,18 +201,19 @@ mmsb_status mmsb_hider_embed(const mmsb_shape *shape, const uint8_t *encrypted, 
     Geo g;
     if (!geo_of(shape, &g) || !encrypted || !k2 || !msg_bytes || !msg_bits || !marked || !img_status || !ws)
         return MMSB_E_INVAL;
-    if (stride_bytes <= 0 || stride_bytes % 16 || marked == encrypted) return MMSB_E_INVAL;
+    if (stride_bytes <= 0 || stride_bytes % 16) return MMSB_E_INVAL;      // (marked may alias encrypted)
     const Layout L = layout(g);
     if (ws_bytes < L.total) return MMSB_E_INVAL;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (cudaMemsetAsync(at<char>(ws, L.states), 0, L.scan_zero_end - L.states, st) != cudaSuccess) return MMSB_E_CUDA;
     if (g.method == 1) lmr_decode_all(g, L, false, encrypted, ws, img_status, nullptr, st);
     ScanWS sw{at<unsigned long long>(ws, L.states), at<unsigned long long>(ws, L.parts), at<uint32_t>(ws, L.hdr),
-              at<uint32_t>(ws, L.ef), ef_words_of(g.HW)};
+              at<uint32_t>(ws, L.ef), ef_words_of(g.HW), at<uint32_t>(ws, L.counts),
+              at<unsigned long long>(ws, L.ztot)};
     run_kernel(K_EMBED, st, (long long)g.B * g.HW, [&] {
         launch_scan(g, true, encrypted, marked, k2, msg_bytes, msg_bits, stride_bytes, nullptr, nullptr, img_status,
                     sw, at<uint32_t>(ws, L.map_bits), at<int32_t>(ws, L.lmr_b), st);
-    }, 3);
+    }, 4);
     return check_launch();
 }
 
@@ -228,7 +231,8 @@ mmsb_status mmsb_receiver_extract(const mmsb_shape *shape, const uint8_t *marked
     if (cudaMemsetAsync(at<char>(ws, L.states), 0, L.scan_zero_end - L.states, st) != cudaSuccess) return MMSB_E_CUDA;
     if (g.method == 1) lmr_decode_all(g, L, false, marked, ws, img_status, msg_bits_out, st);
     ScanWS sw{at<unsigned long long>(ws, L.states), at<unsigned long long>(ws, L.parts), at<uint32_t>(ws, L.hdr),
-              at<uint32_t>(ws, L.ef), ef_words_of(g.HW)};
+              at<uint32_t>(ws, L.ef), ef_words_of(g.HW), at<uint32_t>(ws, L.counts),
+              at<unsigned long long>(ws, L.ztot)};
     run_kernel(K_EXTRACT, st, (long long)g.B * g.HW, [&] {
         launch_scan(g, false, marked, nullptr, k2, nullptr, nullptr, stride_bytes, msg_out, msg_bits_out,
                     img_status, sw, at<uint32_t>(ws, L.map_bits), at<int32_t>(ws, L.lmr_b), st);
@@ -269,7 +273,8 @@ mmsb_status mmsb_receiver_both(const mmsb_shape *shape, const uint8_t *marked, c
     // LMR: the coded maps (eta and the location map) are decoded once for both parties' steps
     if (g.method == 1) lmr_decode_all(g, L, true, marked, ws, img_status, msg_bits_out, st);
     ScanWS sw{at<unsigned long long>(ws, L.states), at<unsigned long long>(ws, L.parts), at<uint32_t>(ws, L.hdr),
-              at<uint32_t>(ws, L.ef), ef_words_of(g.HW)};
+              at<uint32_t>(ws, L.ef), ef_words_of(g.HW), at<uint32_t>(ws, L.counts),
+              at<unsigned long long>(ws, L.ztot)};
     run_kernel(K_EXTRACT, st, (long long)g.B * g.HW, [&] {
         launch_scan(g, false, marked, nullptr, k2, nullptr, nullptr, stride_bytes, msg_out, msg_bits_out,
                     img_status, sw, at<uint32_t>(ws, L.map_bits), at<int32_t>(ws, L.lmr_b), st);

@@ -13,6 +13,8 @@ struct ScanWS {
     uint32_t *hdr;                   // [B] frame length word (extract)
     uint32_t *ef;                    // [B][ef_words] encrypted frame E_F = F XOR KS2 (embed)
     long long ef_words;              // words per image: ceil(7 HW / 512) + 1 ChaCha blocks of 16
+    uint32_t *counts;                // [B][nchunks] zero pixels per chunk (embed: scan_count_kernel)
+    unsigned long long *ztot;        // [B] zero pixels per image (embed)                -- zeroed per call
 };
 __host__ __device__ inline long long ef_words_of(long long HW) { return ((7 * HW + 511) / 512 + 1) * 16; }
 

@@ -138,3 +138,28 @@ def test_emr_parity_4096_config5_sample():
     msgs = S.payload(seed, stride)[None]
     out = _run_gpu(img, k1, k2, msgs, None, stride)
     _check_against_oracle(img, k1, k2, msgs, stride, out)
+
+
+@pytest.mark.parametrize("method", [G.EMR, G.LMR])
+def test_embed_in_place_equals_out_of_place(method):
+    """mmsb_hider_embed with marked aliasing encrypted: the same marked image and
+    statuses as out of place, including a CAPACITY image (left unchanged) and an empty message."""
+    H = W = 128
+    kinds = ["smooth", "textured", "smooth", "quantised"]
+    imgs = np.stack([S.random_image(950 + j, H, W, k) for j, k in enumerate(kinds)])
+    k1 = np.stack([np.frombuffer(S.key(950 + j, 1), np.uint8) for j in range(len(kinds))])
+    k2 = np.stack([np.frombuffer(S.key(950 + j, 2), np.uint8) for j in range(len(kinds))])
+    stride = S.msg_stride(H, W)
+    msgs = np.stack([S.payload(j, stride) for j in range(len(kinds))])
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    enc, b, cap, st = G.encode(method, dev(imgs), dev(k1))
+    nb = (cap - 32).clamp(min=0)
+    nb[1] = cap[1] - 31                                  # one bit over: CAPACITY
+    nb[3] = 0
+    ref, st_ref = G.embed(method, enc, dev(k2), dev(msgs), nb)
+    inplace = enc.clone()
+    out, st_in = G.embed(method, inplace, dev(k2), dev(msgs), nb, out=inplace)
+    torch.cuda.synchronize()
+    assert out.data_ptr() == inplace.data_ptr()
+    assert torch.equal(st_in, st_ref) and torch.equal(inplace, ref)
+    assert int(st_ref[1]) == O.E_CAPACITY and torch.equal(ref[1], enc[1])
