@@ -597,22 +597,31 @@ __device__ __forceinline__ uint32_t pick(const uint32_t (&r)[NW], int k) {      
     return v;
 }
 
-// context slices of half-word q (pixels 16q .. 16q+15 of the tile row; MSB-first words):
-// s1 = row y-1 from pixel 16q-2, s2 = row y-2 from pixel 16q-1 (pixels outside the tile = 0).
+// context slices of a half-word (pixels 16h .. 16h+15 of word K of the tile row; MSB-first
+// words): s1 = row y-1 from pixel 16h-2, s2 = row y-2 from pixel 16h-1 (pixels outside the tile
+// are 0), i.e. funnel shifts of words K-1, K (h = 0) or K, K+1 (h = 1).
+// the words K-1, K, K+1 of the two rows above, rolled along the row: the slices of the next
+// half-word need no search of the row arrays, only a word entering at each word boundary
 template <int NW>
-__device__ __forceinline__ void half_slices(const uint32_t (&p1)[NW], const uint32_t (&p2)[NW], int q, uint32_t &s1,
-                                            uint32_t &s2) {
-    const int K = q >> 1;
-    const uint32_t a1 = pick(p1, K - 1), c1 = pick(p1, K), n1 = pick(p1, K + 1);
-    const uint32_t a2 = pick(p2, K - 1), c2 = pick(p2, K), n2 = pick(p2, K + 1);
-    if (q & 1) {
-        s1 = __funnelshift_l(n1, c1, 14);
-        s2 = __funnelshift_l(n2, c2, 15);
-    } else {
+struct RowWin {
+    uint32_t a1, c1, n1, a2, c2, n2;
+    __device__ __forceinline__ void start(const uint32_t (&p1)[NW], const uint32_t (&p2)[NW], uint32_t &s1, uint32_t &s2) {
+        a1 = 0; c1 = p1[0]; n1 = NW > 1 ? p1[NW > 1 ? 1 : 0] : 0u;
+        a2 = 0; c2 = p2[0]; n2 = NW > 1 ? p2[NW > 1 ? 1 : 0] : 0u;
         s1 = __funnelshift_l(c1, a1, 30);
         s2 = __funnelshift_l(c2, a2, 31);
     }
-}
+    // slices of the half-word after half h of the current word (h = 1: half 0 of the next word)
+    __device__ __forceinline__ void next(int h, uint32_t &t1, uint32_t &t2) const {
+        t1 = __funnelshift_l(n1, c1, h ? 30 : 14);
+        t2 = __funnelshift_l(n2, c2, h ? 31 : 15);
+    }
+    __device__ __forceinline__ void advance(const uint32_t (&p1)[NW], const uint32_t (&p2)[NW], int K) {
+        a1 = c1; c1 = n1; n1 = pick(p1, K + 2);
+        a2 = c2; c2 = n2; n2 = pick(p2, K + 2);
+    }
+};
+
 // rows part (bits 7..0) of the context of symbol J of a half: 5 pixels x-2..x+2 of row y-1,
 // 3 pixels x-1..x+1 of row y-2 (J is a constant after unrolling)
 __device__ __forceinline__ uint32_t slice_ctx(uint32_t s1, uint32_t s2, int J) {
@@ -753,14 +762,15 @@ __global__ void __launch_bounds__(kFastThreads, 1) coder_encode_fast_kernel(Geo 
         }
         if (y + 1 < h) load_row(y + 1);
         uint32_t s1, s2;
-        half_slices(p1, p2, 0, s1, s2);
+        RowWin<NW> win;
+        win.start(p1, p2, s1, s2);
         uint32_t actx = mbase + slice_ctx(s1, s2, 0) * sbytes;         // hist bits 0 at the row start
         uint32_t p = lds_u16(actx);
         uint32_t prev8 = 0;                                            // previous bit << 8
 #pragma unroll 1
         for (int q = 0; q < 2 * NW; q++) {
             uint32_t t1, t2;
-            half_slices(p1, p2, q + 1, t1, t2);                        // next half (unused past the row)
+            win.next(q & 1, t1, t2);                                   // next half (unused past the row)
             uint32_t cb = pick(cw, q >> 1) << (16 * (q & 1));          // the half's bits from the MSB, rolled
             e.begin_half();
 #pragma unroll
@@ -788,6 +798,7 @@ __global__ void __launch_bounds__(kFastThreads, 1) coder_encode_fast_kernel(Geo 
             e.end_half(am);
             s1 = t1;
             s2 = t2;
+            if (q & 1) win.advance(p1, p2, q >> 1);
         }
 #pragma unroll
         for (int k = 0; k < NW; k++) { p2[k] = p1[k]; p1[k] = cw[k]; }
@@ -942,7 +953,8 @@ __global__ void __launch_bounds__(kFastThreads, 1) coder_decode_fast_kernel(Geo 
 #pragma unroll
         for (int q = 0; q < NW; q++) cw[q] = 0;
         uint32_t s1, s2;
-        half_slices(p1, p2, 0, s1, s2);
+        RowWin<NW> win;
+        win.start(p1, p2, s1, s2);
         uint32_t actx = mbase + slice_ctx(s1, s2, 0) * sbytes;
         uint32_t p = lds_u16(actx);
         uint32_t prev8 = 0, word = 0, acc = 0;
@@ -950,7 +962,7 @@ __global__ void __launch_bounds__(kFastThreads, 1) coder_decode_fast_kernel(Geo 
 #pragma unroll 1
         for (int q = 0; q < 2 * NW; q++) {
             uint32_t t1, t2;
-            half_slices(p1, p2, q + 1, t1, t2);
+            win.next(q & 1, t1, t2);
             uint32_t hw = 0, lw = 0;
 #pragma unroll
             for (int J = 0; J < 16; J++) {
@@ -980,6 +992,7 @@ __global__ void __launch_bounds__(kFastThreads, 1) coder_decode_fast_kernel(Geo 
             s2 = t2;
             if (q & 1) {
                 const int K = q >> 1;
+                win.advance(p1, p2, K);
                 word |= hw;
                 acc |= lw << 16;
 #pragma unroll
