@@ -284,7 +284,7 @@ __global__ void __launch_bounds__(256) lmr_concat_kernel(Geo g, LmrEncWS ew) {
     if (pl.state != 1) return;
     const int Tc = lmr_tile_count(g.H, g.W, g.tile_log2);
     const int stride = lmr_tile_stride(g.tile_log2, g.H, g.W);
-    uint8_t *dst = ew.cat + (size_t)img * (g.HW / 8 + 128);
+    uint8_t *dst = ew.cat + (size_t)img * (g.HW / 8);           // (a string never exceeds the plane: K <= HW)
     for (int k = 0; k < 2 * Tc; k++) {                          // streams in order, all threads per stream
         const int n = ew.dsizes[(size_t)img * 2 * Tc + k], o = ew.offsets[(size_t)img * 2 * Tc + k];
         const int slot = k < Tc ? 0 : pl.dslot, tile = k < Tc ? k : k - Tc;
@@ -323,7 +323,7 @@ __global__ void __launch_bounds__(256) lmr_msb_write_kernel(Geo g, LmrEncWS ew,
     }
     if (pl.state != 1) return;
     const int32_t *sz = ew.dsizes + (size_t)img * 2 * Tc;
-    const uint8_t *cat = ew.cat + (size_t)img * (g.HW / 8 + 128);
+    const uint8_t *cat = ew.cat + (size_t)img * (g.HW / 8);
     const long long hdr = 7 + 32ll * Tc;                        // header bits before the stream bytes
     const long long total = (pl.K - hdr) / 8;                   // stream bytes
     for (long long p = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * 16; p < pl.K;

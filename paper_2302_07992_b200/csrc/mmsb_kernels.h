@@ -45,7 +45,7 @@ struct LmrEncWS {
     int32_t *sizes;                  // [B][kLmrSlots][Tc] stream bytes (-1: over cap)
     int32_t *dsizes;                 // [B][2][Tc] sizes of the decided eta + map streams
     int32_t *offsets;                // [B][2][Tc] their exclusive byte offsets
-    uint8_t *cat;                    // [B][HW/8 + 128] the decided streams concatenated (MSB-plane bytes)
+    uint8_t *cat;                    // [B][HW/8] the decided streams concatenated (the mbuf region)
     int32_t *mapbytes;               // [B][8] running coded bytes of each candidate's map (early abort)
 };
 __host__ __device__ inline int lmr_wave_k(int wave, int A, int Tc, int B, int R, int nc) {
