@@ -37,11 +37,21 @@ def test_calls_stay_inside_the_workspace(method):
     msgs = np.stack([S.payload(j, stride) for j in range(B)])
     dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
     ws = _GuardedWs(method, B, H, W)
-    enc, b, cap, st = G.encode(method, dev(imgs), dev(k1), ws)
-    marked, _ = G.embed(method, enc, dev(k2), dev(msgs), (cap - 32).clamp(min=0), ws)
-    G.extract(method, marked, dev(k2), stride, ws)
-    G.recover(method, marked, dev(k1), ws)
-    G.receive_both(method, marked, dev(k1), dev(k2), stride, ws)
+    guarded = []
+
+    def out(*shape):                                   # an output tensor with guard bytes around it
+        n = int(np.prod(shape))
+        raw = torch.full((n + 2 * GUARD,), 0x5A, dtype=torch.uint8, device="cuda")
+        guarded.append((raw, n))
+        return raw[GUARD:GUARD + n].view(*shape)
+
+    enc, b, cap, st = G.encode(method, dev(imgs), dev(k1), ws, out=out(B, H, W))
+    marked, _ = G.embed(method, enc, dev(k2), dev(msgs), (cap - 32).clamp(min=0), ws, out=out(B, H, W))
+    G.extract(method, marked, dev(k2), stride, ws, out=out(B, stride))
+    G.recover(method, marked, dev(k1), ws, out=out(B, H, W))
+    G.receive_both(method, marked, dev(k1), dev(k2), stride, ws, msg_out=out(B, stride), rec_out=out(B, H, W))
     G.capacity(method, marked, ws)
     torch.cuda.synchronize()
     assert ws.intact()
+    for raw, n in guarded:
+        assert bool((raw[:GUARD] == 0x5A).all()) and bool((raw[GUARD + n:] == 0x5A).all())
