@@ -26,9 +26,9 @@ class _GuardedWs:
         return bool((self.raw[:GUARD] == 0xA5).all()) and bool((self.raw[GUARD + self.nbytes:] == 0xA5).all())
 
 
+@pytest.mark.parametrize("B,H,W", [(96, 128, 128), (8, 256, 1024), (2, 2048, 2048), (3, 64, 32)])
 @pytest.mark.parametrize("method", [G.EMR, G.LMR])
-def test_calls_stay_inside_the_workspace(method):
-    B, H, W = 96, 128, 128
+def test_calls_stay_inside_the_workspace(method, B, H, W):
     kinds = ["smooth", "textured", "noise", "smooth"]
     imgs = np.stack([S.random_image(1200 + j, H, W, kinds[j % 4]) for j in range(B)])
     k1 = np.stack([np.frombuffer(S.key(1200 + j, 1), np.uint8) for j in range(B)])
@@ -37,6 +37,7 @@ def test_calls_stay_inside_the_workspace(method):
     msgs = np.stack([S.payload(j, stride) for j in range(B)])
     dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
     ws = _GuardedWs(method, B, H, W)
+    assert ws.nbytes > 0
     guarded = []
 
     def out(*shape):                                   # an output tensor with guard bytes around it
