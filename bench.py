@@ -541,6 +541,13 @@ def kernel_model(name, der):
     }.get(name, dict(bytes=0.0, alu=0.0))
 
 
+def load_ncu_pipes():
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))["launches"]
+    except Exception:
+        return {}
+
+
 def load_traffic():
     """dram bytes per pixel per kernel from the committed ncu --set full capture (profiles/)."""
     try:
@@ -590,6 +597,10 @@ def roofline(prof, peaks, B, HW, cap, method):
     d["traffic_note"] = ("dram__bytes_read.sum + dram__bytes_write.sum per pixel from profiles/traffic.json "
                          "(ncu --set full), scaled to this launch's pixels")
     d["per_launch_ms"] = k["ms_per_launch"]
+    pipes = load_ncu_pipes().get(dom, {})
+    if "alu_pipe_pct" in pipes:                 # the same kernel's issue picture from the committed ncu capture
+        d["ncu_alu_pipe_pct"] = pipes["alu_pipe_pct"]
+        d["ncu_issue_active_pct"] = pipes.get("issue_active_pct")
     return {"dominant": d, "kernels": kern}
 
 

@@ -48,7 +48,9 @@ def main(tag):
         wr = float(d[idx["dram__bytes_write.sum"]]) * SCALE[units[idx["dram__bytes_write.sum"]]]
         per_px[key[0]] = (rd + wr) / px
         launches[key[0]] = {"dram_read_bytes": rd, "dram_write_bytes": wr, "pixels": px,
-                            "duration_us": float(d[idx["gpu__time_duration.sum"]])}
+                            "duration_us": float(d[idx["gpu__time_duration.sum"]]),
+                            "alu_pipe_pct": float(d[idx["sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"]]),
+                            "issue_active_pct": float(d[idx["smsp__issue_active.avg.pct_of_peak_sustained_active"]])}
     # LMR tile coder (units = coded symbols, as bench.py's profile counts them): wave 0 of an
     # encode (eta + candidate 0 of 1000 config-3 images, 16 tiles of 16384 symbols each) and one
     # decode (the map plane), from gpurun_out/prof_coder*.ncu-rep / prof_dec*.ncu-rep when present
@@ -65,7 +67,9 @@ def main(tag):
         wr = float(d2[i2["dram__bytes_write.sum"]]) * SCALE[u2[i2["dram__bytes_write.sum"]]]
         per_px[name] = (rd + wr) / syms
         launches[name] = {"dram_read_bytes": rd, "dram_write_bytes": wr, "symbols": syms, "report": reps[-1],
-                          "duration_us": float(d2[i2["gpu__time_duration.sum"]])}
+                          "duration_us": float(d2[i2["gpu__time_duration.sum"]]),
+                          "alu_pipe_pct": float(d2[i2["sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"]]),
+                          "issue_active_pct": float(d2[i2["smsp__issue_active.avg.pct_of_peak_sustained_active"]])}
     json.dump({"source": f"ncu --set full --clock-control none, tools/prof_run.py --batch 128 (config-2 images, "
                          f"EMR), {tag}; cold-cache serialized replay: writes still resident in L2 at kernel end "
                          f"are not counted; the LMR coder entries are bytes per coded symbol (config 3)",
