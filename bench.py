@@ -331,7 +331,7 @@ def run_ours(args):
         hSSE = torch.empty(B, dtype=torch.int64).pin_memory()
         h2d = hI.numel() + hK1.numel() + hK2.numel() + hMSG.numel() + hNB.numel() * 8
         d2h = hREC.numel() + hMOUT.numel() + hSSE.numel() * 8
-            # two sub-batches on two lanes measured best (EMR 25 / LMR 19 Gpx/s at configs 2 / 3, against
+        # two sub-batches on two lanes measured best (EMR 25 / LMR 19 Gpx/s at configs 2 / 3, against
         # 23 / 13 with eight over three): halves keep the LMR coder rounds full and the copies large
         nsub = next(k for k in (args.e2e_chunks, 2, 1) if k and B % k == 0)
         sub = B // nsub
