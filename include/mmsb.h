@@ -127,7 +127,6 @@ mmsb_status mmsb_capacity(const mmsb_shape *shape, const uint8_t *image, int32_t
                           int32_t *img_status, void *ws, size_t ws_bytes, void *stream);
 
 /*
- * Receiver holding both keys/*
  * Receiver holding both keys (EMR: P:842-843; LMR: P:1066-1067): extraction
  * with K2 and recovery with K1 in one call.  Outputs are those of mmsb_receiver_extract and
  * mmsb_receiver_recover on the same arguments; LMR decodes the coded maps (eta and the location
