@@ -72,3 +72,17 @@ def test_product_path_has_no_oracle_import():
             if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "mmsb_oracle" not in txt and "orc_" not in txt, f
+
+
+def test_header_is_clean_c():
+    """include/mmsb.h compiles as plain C with every warning an error (no torch / C++ types)."""
+    import shutil
+    import subprocess
+
+    gcc = shutil.which("gcc")
+    if gcc is None:
+        pytest.skip("no gcc")
+    hdr = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include", "mmsb.h")
+    r = subprocess.run([gcc, "-fsyntax-only", "-Wall", "-Wextra", "-Werror", "-x", "c", hdr], capture_output=True,
+                       text=True)
+    assert r.returncode == 0, r.stderr
