@@ -821,28 +821,34 @@ __global__ void __launch_bounds__(kFastThreads, 1) coder_encode_fast_kernel(Geo 
     ew.sizes[((size_t)img * kLmrSlots + slot) * Tc + tile] = (e.n <= cap && e.n <= 65535) ? e.n : -1;
 }
 
-// decoder input: the tile's stream as a 96-bit MSB-aligned bit buffer b0:b1:b2 (nb valid bits),
+// decoder input: the tile's stream as a 160-bit MSB-aligned bit buffer b0..b4 (nb valid bits),
 // refilled from stream words funnel-shifted out of the big-endian words of the MSB-plane bytes
-// (the stream starts at an arbitrary bit); stream bytes past nbytes read as 0.  A symbol takes at
-// most 16 bits, so the buffer is topped up to >= 64 bits once per 4 symbols (behind a warp vote)
-// and the per-symbol shift is branch-free.
+// (the stream starts at an arbitrary bit); stream bytes past nbytes read as 0.  A symbol takes
+// at most 16 bits, so the buffer is topped up to >= 128 bits once per 8 symbols: the common
+// top-up (nb in [96, 128]: one word into b3:b4) is branch-free, any other case (a group that
+// took more than 32 bits) runs behind a warp vote.
 struct FastIn {
     const uint32_t *w;                        // aligned word holding the next stream word's first bit
     uint32_t wa, wb, wc, wd;                  // w[0], w[1] (big-endian), w[2], w[3] (raw: loads in flight)
     int sh;                                   // stream bit 0 = bit sh of the first word
     int valid;                                // stream bits left to deliver (8 nbytes - delivered)
-    uint32_t b0, b1, b2;
+    uint32_t b0, b1, b2, b3, b4;
     int nb;
-    __device__ __forceinline__ uint32_t word() {                      // next 32 stream bits, masked
-        const uint32_t v = __funnelshift_l(wb, wa, sh);
-        const uint32_t keep = valid >= 32 ? 0xFFFFFFFFu : (valid <= 0 ? 0u : ~(0xFFFFFFFFu >> valid));
-        valid -= 32;
-        wa = wb;
-        wb = bswap32(wc);                     // (loaded two refills ago)
-        wc = wd;
-        ++w;
-        wd = __ldg(w + 3);
-        return v & keep;
+    __device__ __forceinline__ uint32_t keep() const {             // top min(valid, 32) bits
+        const int vc = valid < 0 ? 0 : (valid > 32 ? 32 : valid);
+        return ~__funnelshift_rc(0xFFFFFFFFu, 0u, vc);
+    }
+    // the next stream word when `take` (else 0); the word queue advances only then.  The load of
+    // the queue's new last word is unconditional (the same word again when the queue stands).
+    __device__ __forceinline__ uint32_t next_word(bool take) {
+        const uint32_t v = take ? __funnelshift_l(wb, wa, sh) & keep() : 0u;
+        valid -= take ? 32 : 0;
+        wa = take ? wb : wa;
+        wb = take ? bswap32(wc) : wb;
+        wc = take ? wd : wc;
+        w += take ? 1 : 0;
+        wd = take ? __ldg(w + 3) : wd;
+        return v;
     }
     __device__ __forceinline__ void init(const uint8_t *m, long long bit0, int nbytes) {
         w = reinterpret_cast<const uint32_t *>(m) + (bit0 >> 5);
@@ -852,42 +858,45 @@ struct FastIn {
         wb = bswap32(__ldg(w + 1));
         wc = __ldg(w + 2);
         wd = __ldg(w + 3);
-        b0 = word();
-        b1 = word();
-        b2 = word();
-        nb = 96;
+        b0 = next_word(true);
+        b1 = next_word(true);
+        b2 = next_word(true);
+        b3 = next_word(true);
+        b4 = next_word(true);
+        nb = 160;
     }
     __device__ __forceinline__ void consume(int s8) {                // s8 = 0, 8 or 16 bits
         b0 = __funnelshift_l(b1, b0, s8);
         b1 = __funnelshift_l(b2, b1, s8);
-        b2 <<= s8;
+        b2 = __funnelshift_l(b3, b2, s8);
+        b3 = __funnelshift_l(b4, b3, s8);
+        b4 <<= s8;
         nb -= s8;
     }
-    // one more stream word at bit offset nb (nb <= 64) when `need`, branch-free (predicated load)
-    __device__ __forceinline__ void add_word_if(bool need) {
-        const int vc = valid < 0 ? 0 : (valid > 32 ? 32 : valid);
-        const uint32_t keep = ~__funnelshift_rc(0xFFFFFFFFu, 0u, vc);  // top vc bits: bytes past the end read 0
-        const uint32_t v = need ? __funnelshift_l(wb, wa, sh) & keep : 0u;
-        if (need) {
-            valid -= 32;
-            wa = wb;
-            wb = bswap32(wc);                 // (loaded two words ago)
-            wc = wd;
-            ++w;
-            wd = __ldg(w + 3);
-        }
-        const int r = nb & 31;
+    // any position: one word at bit offset nb < 160 (rare path)
+    __device__ __forceinline__ void add_word_any(bool need) {
+        const uint32_t v = next_word(need);
+        const int k = nb >> 5, r = nb & 31;
         const uint32_t hi = v >> r, lo = __funnelshift_lc(0u, v, 32 - r);
-        b0 |= nb < 32 ? hi : 0u;
-        b1 |= nb < 32 ? lo : (nb < 64 ? hi : 0u);
-        b2 |= nb < 32 ? 0u : (nb < 64 ? lo : v);
+        b0 |= k == 0 ? hi : 0u;
+        b1 |= k == 0 ? lo : (k == 1 ? hi : 0u);
+        b2 |= k == 1 ? lo : (k == 2 ? hi : 0u);
+        b3 |= k == 2 ? lo : (k == 3 ? hi : 0u);
+        b4 |= k == 3 ? lo : (k == 4 ? hi : 0u);
         nb += need ? 32 : 0;
     }
-    // before each group of 4 symbols (<= 64 bits): nb in [0, 96] -> [64, 96]; the second word is
-    // rarely needed (a group that took more than 32 bits)
+    // before each group of 8 symbols (<= 128 bits): nb -> [128, 160]
     __device__ __forceinline__ void refill(unsigned am) {
-        add_word_if(nb <= 64);
-        if (__any_sync(am, nb < 64)) add_word_if(nb < 64);
+        const bool mid = nb >= 96 && nb <= 128;                       // the common case: into b3:b4
+        const uint32_t v = next_word(mid);
+        const int r = nb & 31;
+        b3 |= mid && nb < 128 ? v >> r : 0u;
+        b4 |= mid ? (nb < 128 ? __funnelshift_lc(0u, v, 32 - r) : v) : 0u;
+        nb += mid ? 32 : 0;
+        if (__any_sync(am, nb < 128)) {
+#pragma unroll 1
+            for (int i = 0; i < 4; i++) add_word_any(nb < 128);
+        }
     }
 };
 
@@ -939,8 +948,10 @@ __global__ void __launch_bounds__(kFastThreads, 1) coder_decode_fast_kernel(Geo 
     uint32_t range = 0xFFFFFFFFu, code = __funnelshift_l(in.b1, in.b0, 8);
     in.b0 = in.b1;
     in.b1 = in.b2;
-    in.b2 = 0;
-    in.nb = 64;
+    in.b2 = in.b3;
+    in.b3 = in.b4;
+    in.b4 = 0;
+    in.nb = 128;
     in.consume(8);
     in.refill(am);
     uint32_t *plane_out = plane == 0 ? eta_bits : map_bits;
@@ -966,7 +977,7 @@ __global__ void __launch_bounds__(kFastThreads, 1) coder_decode_fast_kernel(Geo 
             uint32_t hw = 0, lw = 0;
 #pragma unroll
             for (int J = 0; J < 16; J++) {
-                if ((J & 3) == 0) in.refill(am);                       // >= 64 bits for 4 symbols
+                if ((J & 7) == 0) in.refill(am);                       // >= 128 bits for 8 symbols
                 // both candidate contexts of the next symbol (its (0,-1) bit is the one decoded now)
                 const uint32_t nrows = J < 15 ? slice_ctx(s1, s2, J + 1) : slice_ctx(t1, t2, 0);
                 const uint32_t a0 = mbase + (prev8 | nrows) * sbytes, a1 = a0 + kHiOff;
