@@ -308,7 +308,8 @@ __device__ __forceinline__ void key_role(const Geo &g, int img, int kidx, const 
 constexpr int kMaxTilesX = 512;                  // W <= 32768 with 64-pixel tiles
 
 __device__ __forceinline__ uint32_t bits4_to_bytes(uint32_t m4) { return ((m4 & 0xFu) * 0x00204081u) & 0x01010101u; }
-__device__ __forceinline__ uint32_t bytes_to_bits4(uint32_t l) { return (l | (l >> 7) | (l >> 14) | (l >> 21)) & 0xFu; }
+// byte LSBs (bits 0, 8, 16, 24) -> bits 0..3: one multiply puts them at bits 21..24 (no other term lands there)
+__device__ __forceinline__ uint32_t bytes_to_bits4(uint32_t l) { return ((l * 0x00204081u) >> 21) & 0xFu; }
 
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");

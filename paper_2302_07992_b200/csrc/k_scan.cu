@@ -33,8 +33,10 @@ __device__ __forceinline__ uint32_t zero_mask16(const uint4 &u, long long p_img,
         uint32_t m = 0;
 #pragma unroll
         for (int i = 0; i < 4; i++) {
-            const uint32_t l = ~w[i] & 0x01010101u;              // LSB == 0 -> redundant
-            m |= ((l | (l >> 7) | (l >> 14) | (l >> 21)) & 0xFu) << (4 * i);
+            // LSB == 0 -> redundant; the byte LSBs (bits 0, 8, 16, 24) gathered by one multiply:
+            // l * (1 + 2^7 + 2^14 + 2^21) puts them at bits 21..24, no other term lands there
+            const uint32_t l = ~w[i] & 0x01010101u;
+            m |= (((l * 0x00204081u) >> 21) & 0xFu) << (4 * i);
         }
         if (p_img == 0) m &= ~7u;                                // r = 0..2 hold the header (Q14)
         return m;
