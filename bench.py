@@ -470,6 +470,7 @@ def run_ours(args):
                         "pcie_note": "both directions at once measured at 49.4 GB/s each on this box "
                                      "(tools/pcie_probe.py): the e2e ceiling is bytes per step / 49.4 GB/s"},
                 "roofline": roof["dominant"],
+                "step_hbm": step_hbm(roof["kernels"], value, float(cap.mean() / HW), load_peaks()),
                 "kernels": roof["kernels"],
                 "checks": {"payload_round_trip": ok_rt, "e2e_matches_device": ok_e2e,
                            "statuses_ok": bool((st0 == 0).all().item())},
@@ -556,6 +557,27 @@ def load_traffic():
         return json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))["bytes_per_px"]
     except Exception:
         return {}
+
+
+def step_hbm(kern, mpx_s, der, peaks):
+    """The metric's "% HBM roofline" for the whole step and for the three receiver-side calls
+    (embed + extract + recover): algorithmic bytes per pixel (encode 2, embed
+    2 + d/8, extract 1 + d/8, recover 2, statistics 2) x pixels/s over the measured HBM peak;
+    the three calls' pixel rate from their share of the measured kernel time."""
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    d8 = der / 8.0
+    step_b = 2.0 + (2.0 + d8) + (1.0 + d8) + 2.0 + 2.0
+    out = {"bytes_per_px": step_b, "achieved_GBps": step_b * mpx_s * 1e6 / 1e9, "peak": hbm}
+    out["frac"] = out["achieved_GBps"] / hbm
+    three = [k for k in kern if "embed" in k or "extract" in k or "decode" in k or k.startswith("recover")]
+    t_all = sum(kern[k]["ms_total"] for k in kern)
+    t3 = sum(kern[k]["ms_total"] for k in three)
+    if t3 > 0 and t_all > 0:
+        b3 = 5.0 + 2 * d8
+        mpx3 = mpx_s * t_all / t3
+        out["receiver_calls"] = {"calls": "embed+extract+recover", "bytes_per_px": b3, "mpx_s": mpx3,
+                                 "frac": b3 * mpx3 * 1e6 / 1e9 / hbm}
+    return out
 
 
 def roofline(prof, peaks, B, HW, cap, method):
