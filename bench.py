@@ -536,7 +536,7 @@ def kernel_model(name, der):
     return {
         "encode_kernel": dict(bytes=2.0, alu=CHACHA_ALU_PER_BYTE * 1.0),
         "recover_kernel": dict(bytes=2.0, alu=CHACHA_ALU_PER_BYTE * 1.0),
-        "scan_count+frame_encrypt+scan_kernel<embed>+finish": dict(bytes=2.0 + d8, alu=CHACHA_ALU_PER_BYTE * d8),
+        "embed_prep+scan_kernel<embed>+finish": dict(bytes=2.0 + d8, alu=CHACHA_ALU_PER_BYTE * d8),
         "scan_kernel<extract>+finish": dict(bytes=1.0 + d8, alu=CHACHA_ALU_PER_BYTE * d8),
         "stats_kernel": dict(bytes=2.0, alu=0.0),
         "coder_encode_kernel": dict(bytes=1.0, alu=CODER_ALU_PER_SYMBOL),   # per symbol: its byte of ceta

@@ -177,11 +177,11 @@ __device__ __forceinline__ int image_b(const uint8_t *img0, const int32_t *lmr_b
 // embed's counting pass: zero pixels of every chunk and of the image, so that the chunk kernel
 // knows its prefix and the image's capacity before it writes (the hider may embed in place)
 template <int METHOD>
-__global__ void __launch_bounds__(kScanThreads) scan_count_kernel(Geo g, const uint8_t *__restrict__ in,
-                                                                  const uint32_t *__restrict__ map_bits, ScanWS ws) {
+__device__ __forceinline__ void count_chunk(const Geo &g, const uint8_t *__restrict__ in,
+                                            const uint32_t *__restrict__ map_bits, const ScanWS &ws, int cidx) {
     __shared__ uint32_t red[kScanThreads / 32];
     const int tid = threadIdx.x;
-    const int img = blockIdx.x / g.nchunks, chunk = blockIdx.x % g.nchunks;
+    const int img = cidx / g.nchunks, chunk = cidx % g.nchunks;
     const int cpx = g.HW < kChunk ? (int)g.HW : kChunk;
     const long long p0 = (long long)chunk * cpx;
     const uint4 *src = reinterpret_cast<const uint4 *>(in + (size_t)img * g.HW + p0);
@@ -204,7 +204,7 @@ __global__ void __launch_bounds__(kScanThreads) scan_count_kernel(Geo g, const u
     if (tid == 0) {
         uint32_t t = 0;
         for (int w = 0; w < kScanThreads / 32; w++) t += red[w];
-        ws.counts[blockIdx.x] = t;
+        ws.counts[cidx] = t;
         if (t) atomicAdd(ws.ztot + img, (unsigned long long)t);
     }
 }
@@ -259,7 +259,7 @@ __global__ void __launch_bounds__(kScanThreads, 5) scan_kernel(Geo g, const uint
     long long n = 0;
     if constexpr (EMBED) {
         n = msg_bits[img];
-        // this chunk's prefix: the zero counts of the image's earlier chunks (scan_count_kernel)
+        // this chunk's prefix: the zero counts of the image's earlier chunks (embed_prep_kernel)
         uint32_t part = 0;
         for (int c = tid; c < chunk; c += kScanThreads) part += __ldg(ws.counts + (size_t)img * g.nchunks + c);
 #pragma unroll
@@ -374,7 +374,7 @@ __global__ void __launch_bounds__(kScanThreads, 5) scan_kernel(Geo g, const uint
         const long long hie = hi < F ? hi : F;
         const long long blk0 = lo >> 9;
         const int nblk = lo < hie ? (int)(((hie - 1) >> 9) - blk0 + 1) : 0;
-        // E_F words of the chunk's frame blocks (frame_encrypt_kernel), coalesced into smem
+        // E_F words of the chunk's frame blocks (embed_prep_kernel), coalesced into smem
         const uint32_t *ef = ws.ef + (size_t)img * ws.ef_words + blk0 * 16;
         for (int t = tid; t < nblk * 16; t += kScanThreads) kbuf[t] = __ldg(ef + t);
         __syncthreads();
@@ -452,16 +452,13 @@ __global__ void __launch_bounds__(kScanThreads, 5) scan_kernel(Geo g, const uint
 }
 
 // ======================================================================================
-// frame_encrypt_kernel: E_F = F XOR KS2 for every ChaCha20 block of the frame (reading Q17):
+// frame_block: E_F = F XOR KS2 for one ChaCha20 block of the frame (reading Q17):
 // F = BE32(n) || message, block k = frame words [16k, 16k+16).  Independent of the pixels,
 // so it runs at full occupancy before the chunk kernel, which copies the words it needs.
 // ======================================================================================
-__global__ void __launch_bounds__(128) frame_encrypt_kernel(Geo g, const uint8_t *__restrict__ keys,
-                                                            const uint8_t *__restrict__ msg,
-                                                            const int64_t *__restrict__ msg_bits, long long stride,
-                                                            ScanWS ws) {
-    const int img = blockIdx.y;
-    const long long k = (long long)blockIdx.x * 128 + threadIdx.x;
+__device__ __forceinline__ void frame_block(const Geo &g, const uint8_t *__restrict__ keys,
+                                            const uint8_t *__restrict__ msg, const int64_t *__restrict__ msg_bits,
+                                            long long stride, const ScanWS &ws, int img, long long k) {
     const long long n = msg_bits[img];
     const bool n_ok = n >= 0 && n <= 8 * stride && n <= 0xFFFFFFFFll;
     const long long F = n_ok ? 32 + n : 0;
@@ -486,6 +483,30 @@ __global__ void __launch_bounds__(128) frame_encrypt_kernel(Geo g, const uint8_t
     uint4 *dst = reinterpret_cast<uint4 *>(ws.ef + (size_t)img * ws.ef_words + k * 16);
 #pragma unroll
     for (int j = 0; j < 4; j++) dst[j] = make_uint4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
+}
+
+// embed_prep_kernel: embed's two pre-passes in one launch, their CTAs interleaved so that the
+// memory-bound counting (one CTA per chunk) overlaps the ALU-bound frame encryption (256
+// ChaCha blocks per CTA): even CTAs count while both kinds remain, odd ones encrypt.
+template <int METHOD>
+__global__ void __launch_bounds__(kScanThreads) embed_prep_kernel(Geo g, const uint8_t *__restrict__ in,
+                                                                  const uint32_t *__restrict__ map_bits,
+                                                                  const uint8_t *__restrict__ keys,
+                                                                  const uint8_t *__restrict__ msg,
+                                                                  const int64_t *__restrict__ msg_bits,
+                                                                  long long stride, ScanWS ws, int ncount, int fpi) {
+    const int nframe = g.B * fpi, both = ncount < nframe ? ncount : nframe;
+    const int i = blockIdx.x;
+    bool count;
+    int idx;
+    if (i < 2 * both) { count = (i & 1) == 0; idx = i >> 1; }
+    else { count = ncount > nframe; idx = both + (i - 2 * both); }
+    if (count) {
+        count_chunk<METHOD>(g, in, map_bits, ws, idx);
+    } else {
+        const int img = idx / fpi;
+        frame_block(g, keys, msg, msg_bits, stride, ws, img, (long long)(idx % fpi) * kScanThreads + threadIdx.x);
+    }
 }
 
 // ======================================================================================
@@ -576,10 +597,11 @@ static void launch_scan_t(const Geo &g, const uint8_t *in, uint8_t *out, const u
                           cudaStream_t st) {
     const unsigned grid = (unsigned)((long long)g.B * g.nchunks);
     if constexpr (EMBED) {
-        scan_count_kernel<METHOD><<<grid, kScanThreads, 0, st>>>(g, in, map_bits, ws);
         const long long fb = (32 + 8 * stride + 511) / 512;     // frame blocks (capped by ef_words in the kernel)
         const long long nb = fb < ws.ef_words / 16 ? fb : ws.ef_words / 16;
-        frame_encrypt_kernel<<<dim3((unsigned)((nb + 127) / 128), g.B), 128, 0, st>>>(g, keys, msg, msg_bits, stride, ws);
+        const int fpi = (int)((nb + kScanThreads - 1) / kScanThreads);       // frame CTAs per image
+        embed_prep_kernel<METHOD><<<grid + (unsigned)(g.B * fpi), kScanThreads, 0, st>>>(
+            g, in, map_bits, keys, msg, msg_bits, stride, ws, (int)grid, fpi);
     }
     scan_kernel<METHOD, EMBED><<<grid, kScanThreads, 0, st>>>(g, in, out, keys, msg, msg_bits, stride, msg_out, ws,
                                                               map_bits, lmr_b);

@@ -18,7 +18,7 @@ static std::atomic<unsigned long long> g_launches{0};
 // ---- live per-kernel timing (CUDA events recorded on the launch stream around each kernel)
 enum KernelId { K_ENCODE = 0, K_RECOVER, K_EMBED, K_EXTRACT, K_STATS, K_LMR_PLAN, K_CODER_ENC, K_LMR_FIT,
                 K_LMR_MSB, K_LMR_DECODE, K_COUNT };
-static const char *kKernelNames[K_COUNT] = {"encode_kernel", "recover_kernel", "scan_count+frame_encrypt+scan_kernel<embed>+finish",
+static const char *kKernelNames[K_COUNT] = {"encode_kernel", "recover_kernel", "embed_prep+scan_kernel<embed>+finish",
                                             "scan_kernel<extract>+finish", "stats_kernel", "lmr_plan_kernel",
                                             "coder_encode_kernel", "lmr_fit_kernel", "lmr_concat+msb_write_kernels",
                                             "lmr_pack+header+coder_decode_kernels"};
@@ -213,7 +213,7 @@ mmsb_status mmsb_hider_embed(const mmsb_shape *shape, const uint8_t *encrypted, 
     run_kernel(K_EMBED, st, (long long)g.B * g.HW, [&] {
         launch_scan(g, true, encrypted, marked, k2, msg_bytes, msg_bits, stride_bytes, nullptr, nullptr, img_status,
                     sw, at<uint32_t>(ws, L.map_bits), at<int32_t>(ws, L.lmr_b), st);
-    }, 4);
+    }, 3);
     return check_launch();
 }
 

@@ -14,7 +14,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT, PROF = os.path.join(ROOT, "gpurun_out"), os.path.join(ROOT, "profiles")
 NAME_MAP = {"encode_kernel": "encode_kernel", "recover_kernel": "recover_kernel",
-            "scan_kernel<0, 1>": "scan_count+frame_encrypt+scan_kernel<embed>+finish", "scan_kernel<0, 0>": "scan_kernel<extract>+finish",
+            "scan_kernel<0, 1>": "embed_prep+scan_kernel<embed>+finish", "scan_kernel<0, 0>": "scan_kernel<extract>+finish",
             "stats_kernel": "stats_kernel"}
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
