@@ -152,10 +152,11 @@ __device__ __forceinline__ void pair_rot_cw(uint32_t &top, uint32_t &bot, int aL
     // nibble tables indexed by angle: (byte0 src, byte1 src) for the left block
     const uint32_t TOPS = 0x51450410u;   // a0: 0,1  a1: 4,0  a2: 5,4  a3: 1,5
     const uint32_t BOTS = 0x40011554u;   // a0: 4,5  a1: 5,1  a2: 1,0  a3: 0,4
-    uint32_t tl = (TOPS >> (8 * aL)) & 0xFF, tr = ((TOPS >> (8 * aR)) & 0xFF) + 0x22;
-    uint32_t bl = (BOTS >> (8 * aL)) & 0xFF, br = ((BOTS >> (8 * aR)) & 0xFF) + 0x22;
-    uint32_t nt = __byte_perm(top, bot, tl | (tr << 8));
-    uint32_t nb = __byte_perm(top, bot, bl | (br << 8));
+    // the two selector bytes picked from the tables by one PRMT each: byte 0 = left table entry
+    // aL, byte 1 = the right block's entry aR (the same entry + 0x22: byte offsets 2, 3)
+    const uint32_t idx = (uint32_t)aL | ((uint32_t)(aR + 4) << 4);
+    uint32_t nt = __byte_perm(top, bot, __byte_perm(TOPS, TOPS + 0x22222222u, idx));
+    uint32_t nb = __byte_perm(top, bot, __byte_perm(BOTS, BOTS + 0x22222222u, idx));
     top = nt;
     bot = nb;
 }
