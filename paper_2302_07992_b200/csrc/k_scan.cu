@@ -50,34 +50,29 @@ __device__ __forceinline__ uint32_t zero_mask16(const uint4 &u, long long p_img,
 // Both directions work on one 32-bit word (4 pixels) at a time with byte permutes: the
 // fields of the set pixels of a word are consecutive in the frame stream, so a word needs
 // one 32-bit window of the stream and one PRMT whose selector depends only on the word's
-// 4-bit zero mask m4 (tables esel / csel in shared memory).
-//   esel[m4] nibble i = number of set bits of m4 below i   (stream field -> pixel byte)
-//   csel[m4] nibble k = index of the k-th set bit, 4 (zero byte) past popc(m4)
+// 4-bit zero mask m4 (tables esel / csel in shared memory).  Between the stream window and
+// the bytes, fields are held "left-aligned, MSB-first": stream field k in byte 3-k, at bits
+// [8-BP, 8) of the byte, so both conversions are two halving steps (a shift and a
+// select, or an add-multiply) instead of one shift and mask per field.
+//   esel[m4] nibble i = 3 - (number of set bits of m4 below i)   (stream field -> pixel byte)
+//   csel[m4] nibble 3-k = index of the k-th set bit, 4 (zero byte) past popc(m4)
 
-// 4 consecutive BP-bit fields, MSB-first at the top of x, -> byte i = field i at bit SHIFT
-template <int BP, int SHIFT>
+// 4 consecutive BP-bit fields, MSB-first at the top of x -> field k at bits [8-BP, 8) of
+// byte 3-k (the other bits of every byte are don't-care: callers mask them)
+template <int BP>
 __device__ __forceinline__ uint32_t fields_to_bytes(uint32_t x) {
-    uint32_t e = 0;
-#pragma unroll
-    for (int i = 0; i < 4; i++) {
-        constexpr uint32_t FM = ((1u << BP) - 1u) << SHIFT;
-        const int sh = 32 - (i + 1) * BP - (8 * i + SHIFT);     // right shift placing field i
-        const uint32_t t = sh >= 0 ? (x >> sh) : (x << -sh);
-        e |= t & (FM << (8 * i));
-    }
-    return e;
+    // fields 2, 3 to the top of the low half-word, then the second field of each half to the
+    // top of its low byte
+    const uint32_t x1 = __byte_perm(x, x >> (16 - 2 * BP), 0x3254);
+    const uint32_t sh = x1 >> (8 - BP);
+    return (x1 & 0xFF00FF00u) | (sh & 0x00FF00FFu);
 }
-// byte k (field value < 2^BP) -> BP-bit fields MSB-first at the top of the result
+// inverse: field k left-aligned in byte 3-k (other bits 0) -> 4 BP-bit fields MSB-first at
+// the top; a low byte / half-word is moved up onto its neighbour by t + lo * (2^s - 1)
 template <int BP>
 __device__ __forceinline__ uint32_t bytes_to_fields(uint32_t c) {
-    uint32_t p = 0;
-#pragma unroll
-    for (int k = 0; k < 4; k++) {
-        const int sh = 32 - (k + 1) * BP - 8 * k;                // left shift placing byte k
-        const uint32_t t = sh >= 0 ? (c << sh) : (c >> -sh);
-        p |= t & (((1u << BP) - 1u) << (32 - (k + 1) * BP));
-    }
-    return p;
+    const uint32_t x = c + (c & 0x00FF00FFu) * ((1u << (8 - BP)) - 1u);
+    return x + (x & 0xFFFFu) * ((1u << (16 - 2 * BP)) - 1u);
 }
 __device__ __forceinline__ uint32_t mask4_to_bytes(uint32_t m4) { return ((m4 & 0xFu) * 0x00204081u) & 0x01010101u; }
 
@@ -93,7 +88,8 @@ __device__ __forceinline__ void embed16(uint32_t w[4], uint32_t mm, const uint32
         const uint32_t m4 = (mm >> (4 * j)) & 0xFu;
         const int wi = o >> 5;
         const uint32_t x = __funnelshift_l(kbuf[wi + 1], kbuf[wi], o);   // stream bits [o, o+32)
-        const uint32_t e = fields_to_bytes<BP, SHIFT>(x);
+        uint32_t e = fields_to_bytes<BP>(x);
+        if constexpr (SHIFT != 8 - BP) e >>= (8 - BP - SHIFT);             // LMR: one bit lower
         const uint32_t v = __byte_perm(e, 0, esel[m4]);
         const uint32_t msk = mask4_to_bytes(m4) * FMB;
         w[j] = (w[j] & ~msk) | (v & msk);
@@ -125,7 +121,7 @@ __device__ __noinline__ uint4 embed16_tail(uint4 u, uint32_t mm, const uint32_t 
 template <int BP, int SHIFT>
 __device__ __forceinline__ void extract16(const uint32_t w[4], uint32_t mm, uint32_t *kbuf, int rel,
                                           const uint32_t *csel) {
-    constexpr uint32_t FB = ((1u << BP) - 1u) * 0x01010101u;
+    constexpr uint32_t FB = (((1u << BP) - 1u) << (8 - BP)) * 0x01010101u;
     int wi = rel >> 5;
     int nacc = rel & 31;                        // valid bits at the top of acc (leading pad = 0)
     unsigned long long acc = 0;
@@ -133,8 +129,8 @@ __device__ __forceinline__ void extract16(const uint32_t w[4], uint32_t mm, uint
 #pragma unroll
     for (int j = 0; j < 4; j++) {
         const uint32_t m4 = (mm >> (4 * j)) & 0xFu;
-        const uint32_t t = (w[j] >> SHIFT) & FB;                  // byte i = field of pixel i
-        const uint32_t c = __byte_perm(t, 0, csel[m4]);           // set pixels' fields, in order
+        const uint32_t t = (w[j] << (8 - BP - SHIFT)) & FB;       // byte i = field of pixel i, left-aligned
+        const uint32_t c = __byte_perm(t, 0, csel[m4]);           // set pixels' fields, bytes 3, 2, ..
         const uint32_t p = bytes_to_fields<BP>(c);
         acc |= ((unsigned long long)p << 32) >> nacc;
         nacc += BP * __popc(m4);
@@ -245,10 +241,10 @@ __global__ void __launch_bounds__(kScanThreads, 5) scan_kernel(Geo g, const uint
         uint32_t e = 0, c = 0;
         int k = 0;
         for (int i = 0; i < 4; i++) {
-            e |= (uint32_t)__popc(tid & ((1 << i) - 1)) << (4 * i);
-            if ((tid >> i) & 1) c |= (uint32_t)i << (4 * k++);
+            e |= (uint32_t)(3 - __popc(tid & ((1 << i) - 1))) << (4 * i);
+            if ((tid >> i) & 1) c |= (uint32_t)i << (4 * (3 - k++));
         }
-        for (; k < 4; k++) c |= 4u << (4 * k);
+        for (; k < 4; k++) c |= 4u << (4 * (3 - k));
         esel[tid] = e;
         csel[tid] = c;
     }

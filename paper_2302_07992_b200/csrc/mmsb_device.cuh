@@ -133,14 +133,16 @@ __device__ __forceinline__ Cell cell_transpose(Cell c) {
 // with T = transpose(in) and rev = byte reversal.
 __device__ __forceinline__ Cell cell_rot_cw(Cell c, int r) {
     const Cell t = cell_transpose(c);
-    const bool odd = r & 1, flip = r >= 2;
-    const uint32_t sel = (r == 1 || r == 2) ? 0x0123u : 0x3210u;
+    const bool odd = r & 1;
+    // out_i = PRMT(a_i, a_{3-i}, S): S = 0x3210 (a_i), 0x0123 (rev a_i), 0x4567 (rev a_{3-i}),
+    // 0x7654 (a_{3-i}) for r = 0..3, itself picked from a two-word table by one PRMT
+    const uint32_t S = __byte_perm(0x01233210u, 0x76544567u, (uint32_t)r * 0x22u + 0x10u);
     const uint32_t a0 = odd ? t.r0 : c.r0, a1 = odd ? t.r1 : c.r1, a2 = odd ? t.r2 : c.r2, a3 = odd ? t.r3 : c.r3;
     Cell o;
-    o.r0 = __byte_perm(flip ? a3 : a0, 0, sel);
-    o.r1 = __byte_perm(flip ? a2 : a1, 0, sel);
-    o.r2 = __byte_perm(flip ? a1 : a2, 0, sel);
-    o.r3 = __byte_perm(flip ? a0 : a3, 0, sel);
+    o.r0 = __byte_perm(a0, a3, S);
+    o.r1 = __byte_perm(a1, a2, S);
+    o.r2 = __byte_perm(a2, a1, S);
+    o.r3 = __byte_perm(a3, a0, S);
     return o;
 }
 
