@@ -23,7 +23,7 @@ namespace mmsb {
 
 constexpr unsigned long long kFlagAgg = 1ull << 62, kFlagInc = 2ull << 62, kValMask = (1ull << 62) - 1;
 constexpr int kMaxBlk = kChunk * 7 / 512 + 2;          // ChaCha blocks a chunk's bits can touch
-constexpr int kKbufWords = kMaxBlk * 16 + 2;
+constexpr int kKbufWords = kMaxBlk * 16 + 4;     // + 3 words of alignment offset (extract)
 
 // 16 zero-pixel flags of the pixels [p, p+16) of the chunk (bit i = pixel p+i is redundant)
 template <int METHOD>
@@ -206,7 +206,7 @@ __device__ __forceinline__ void count_chunk(const Geo &g, const uint8_t *__restr
 }
 
 template <int METHOD, bool EMBED>
-__global__ void __launch_bounds__(kScanThreads, 5) scan_kernel(Geo g, const uint8_t *__restrict__ in,
+__global__ void __launch_bounds__(kScanThreads, EMBED ? 5 : 6) scan_kernel(Geo g, const uint8_t *__restrict__ in,
                                                             uint8_t *__restrict__ out, const uint8_t *__restrict__ keys,
                                                             const uint8_t *__restrict__ msg,
                                                             const int64_t *__restrict__ msg_bits, long long stride,
@@ -397,11 +397,22 @@ __global__ void __launch_bounds__(kScanThreads, 5) scan_kernel(Geo g, const uint
             }
         }))
     } else {
-        // ---- extract: gather the chunk's bit string G[lo, hi) into smem, XOR KS2, write words
+        // ---- extract: gather the chunk's bit string G[lo, hi) into smem, XOR KS2, write words.
+        // kx = kbuf + 3 so that frame word W sits at kx[W - basew] and the message words
+        // W - 1 = 0 mod 4 start 16-byte aligned groups (basew is a multiple of 16).
+        uint32_t *kx = kbuf + 3;
         const long long blk0 = lo >> 9;
         const long long base = blk0 * 512, basew = blk0 * 16;
         const int nblk = lo < hi ? (int)(((hi - 1) >> 9) - blk0 + 1) : 0;
-        for (int t = tid; t < nblk * 16 + 1; t += kScanThreads) kbuf[t] = 0;
+        // every word a thread fills completely is stored plainly; only the first and last word
+        // of each 16-pixel group can be shared (ORed), so those are the words zeroed first
+#pragma unroll
+        for (int r = 0; r < kScanRounds; r++) {
+            if (!m[r]) continue;
+            const int rel = (int)((prefix + excl[r]) * bp - base);
+            kx[rel >> 5] = 0;
+            kx[(rel + bp * __popc(m[r]) - 1) >> 5] = 0;
+        }
         __syncthreads();
         MMSB_BP_SWITCH(bp, METHOD, ({
             _Pragma("unroll")
@@ -409,7 +420,7 @@ __global__ void __launch_bounds__(kScanThreads, 5) scan_kernel(Geo g, const uint
                 if (!m[r]) continue;
                 const uint4 u = spx[r * kScanThreads + tid];
                 const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-                extract16<BP, SH>(w, m[r], kbuf, (int)((prefix + excl[r]) * BP - base), csel);
+                extract16<BP, SH>(w, m[r], kx, (int)((prefix + excl[r]) * BP - base), csel);
             }
         }))
         uint32_t ks[16];
@@ -417,30 +428,49 @@ __global__ void __launch_bounds__(kScanThreads, 5) scan_kernel(Geo g, const uint
         __syncthreads();
         if (tid < nblk) {
 #pragma unroll
-            for (int j = 0; j < 16; j++) kbuf[tid * 16 + j] ^= bswap32(ks[j]);
+            for (int j = 0; j < 16; j++) kx[tid * 16 + j] ^= bswap32(ks[j]);
         }
         __syncthreads();
         uint32_t *mo = reinterpret_cast<uint32_t *>(msg_out + (size_t)img * stride);
         unsigned long long *parts = ws.parts + ((size_t)img * g.nchunks + chunk) * 2;
         if (lo < hi) {
             // frame words [w0, w1] (word indices < 7 HW / 32 fit 32 bits); the first and last
-            // may be shared with the neighbouring chunks, the ones in between are this chunk's
+            // may be shared with the neighbouring chunks (merged by scan_finish), the ones in
+            // between are this chunk's: the header word (W = 0) and message words W - 1 < wlim
             const int w0 = (int)(lo >> 5), w1 = (int)((hi - 1) >> 5), nw = w1 - w0 + 1;
             const bool hp = (lo & 31) != 0, tp = (hi & 31) != 0;
-            const int wlim = (int)(stride / 4);                  // message words in the row: W - 1 < wlim
-            const uint32_t *kb = kbuf + (w0 - (int)basew);
-            for (int i = tid; i < nw; i += kScanThreads) {
-                const int W = w0 + i;
-                const uint32_t v = kb[i];
-                if (!((i == 0 && hp) || (i == nw - 1 && tp))) {
-                    if (W == 0) ws.hdr[img] = v;
-                    else if (W <= wlim) mo[W - 1] = bswap32(v);
-                } else {                                     // shared word: merged by scan_finish
-                    const long long s0 = (long long)W * 32 > lo ? (long long)W * 32 : lo;
-                    const long long e0 = (long long)W * 32 + 32 < hi ? (long long)W * 32 + 32 : hi;
-                    const int len = (int)(e0 - s0), st0 = (int)(s0 - (long long)W * 32);
-                    const uint32_t msk = (len == 32 ? 0xFFFFFFFFu : ((1u << len) - 1u)) << (32 - st0 - len);
-                    parts[i == 0 ? 0 : 1] = ((unsigned long long)(W + 1) << 32) | (v & msk);
+            const int wlim = (int)(stride / 4);
+            const uint32_t *kb = kx - basew;                      // kb[W] = frame word W
+            if (tid < 2 && (tid == 0 ? hp : (tp && !(nw == 1 && hp)))) {
+                const int W = tid == 0 ? w0 : w1;
+                const uint32_t v = kb[W];
+                const long long s0 = (long long)W * 32 > lo ? (long long)W * 32 : lo;
+                const long long e0 = (long long)W * 32 + 32 < hi ? (long long)W * 32 + 32 : hi;
+                const int len = (int)(e0 - s0), st0 = (int)(s0 - (long long)W * 32);
+                const uint32_t msk = (len == 32 ? 0xFFFFFFFFu : ((1u << len) - 1u)) << (32 - st0 - len);
+                parts[W == w0 ? 0 : 1] = ((unsigned long long)(W + 1) << 32) | (v & msk);
+            }
+            const int o0 = w0 + (hp ? 1 : 0), o1 = w1 - (tp ? 1 : 0);   // own words [o0, o1]
+            if (o0 == 0 && o1 >= 0 && tid == 0) ws.hdr[img] = kb[0];
+            const int m0 = o0 > 1 ? o0 : 1, m1 = o1 < wlim ? o1 : wlim;   // own message words
+            if (m0 <= m1) {
+                // 16-byte groups W = a + 4 t (W - 1 = 0 mod 4) inside [m0, m1]; scalar words around
+                const bool vec = (stride & 15) == 0 && (reinterpret_cast<uintptr_t>(mo) & 15) == 0;
+                const int a = vec ? ((m0 + 2) & ~3) + 1 : m1 + 1;
+                const int ng = a + 3 <= m1 ? (m1 - a + 1) >> 2 : 0;
+                const int gend = ng ? a + 4 * ng : m0;              // first word after the groups
+                for (int t = tid; t < ng; t += kScanThreads) {
+                    const int W = a + 4 * t;
+                    const uint4 v = *reinterpret_cast<const uint4 *>(kb + W);
+                    *reinterpret_cast<uint4 *>(mo + W - 1) =
+                        make_uint4(bswap32(v.x), bswap32(v.y), bswap32(v.z), bswap32(v.w));
+                }
+                // scalar words: [m0, min(a, m1 + 1)) before the groups, [gend, m1] after them
+                const int hend = ng ? a : m1 + 1;
+                const int nh = hend - m0, nt = ng ? m1 - gend + 1 : 0;
+                for (int t = tid; t < nh + nt; t += kScanThreads) {
+                    const int W = t < nh ? m0 + t : gend + (t - nh);
+                    mo[W - 1] = bswap32(kb[W]);
                 }
             }
         }

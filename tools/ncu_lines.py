@@ -1,7 +1,7 @@
 """Executed instructions per CUDA source line (SASS correlated) for the first launch of one
 kernel in an ncu report, heaviest first.
 
-  python tools/ncu_lines.py report.ncu-rep kernel_regex [top]
+  python tools/ncu_lines.py report.ncu-rep kernel_regex [top] [launch_skip]
 """
 import csv
 import re
@@ -9,9 +9,9 @@ import subprocess
 import sys
 
 
-def main(rep, regex, top=40):
+def main(rep, regex, top=40, skip=0):
     out = subprocess.run(['ncu', '-i', rep, '--page', 'source', '--csv', '--print-source', 'sass,cuda', '-k',
-                          'regex:' + regex, '--launch-count', '1'], capture_output=True, text=True).stdout
+                          'regex:' + regex, '--launch-skip', str(skip), '--launch-count', '1'], capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
     res, hdr, path = [], None, None
     alu = set('LOP3 SHF ISETP PRMT IADD3 SEL LEA VIADD FLO POPC BREV VIMNMX IMNMX'.split())
@@ -47,4 +47,5 @@ def main(rep, regex, top=40):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2], int(sys.argv[3]) if len(sys.argv) > 3 else 40)
+    main(sys.argv[1], sys.argv[2], int(sys.argv[3]) if len(sys.argv) > 3 else 40,
+         int(sys.argv[4]) if len(sys.argv) > 4 else 0)
