@@ -587,6 +587,14 @@ __device__ __forceinline__ void sts_u16(uint32_t a, uint32_t v) {
     asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((unsigned short)v));
 }
 
+// a * b + c as an integer multiply-add (FMA pipe); asm so that a 0/1 factor is not turned back
+// into a select or mask on the ALU pipe
+__device__ __forceinline__ uint32_t imad(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t d;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+
 __device__ __forceinline__ uint32_t nib4(uint32_t t) { return ((t * 0x08040201u) >> 24) & 0xFu; }   // bytes' bit 0 -> MSB-first nibble
 
 template <int NW>
@@ -766,7 +774,8 @@ __global__ void __launch_bounds__(kFastThreads, 1) coder_encode_fast_kernel(Geo 
         win.start(p1, p2, s1, s2);
         uint32_t actx = mbase + slice_ctx(s1, s2, 0) * sbytes;         // hist bits 0 at the row start
         uint32_t p = lds_u16(actx);
-        uint32_t prev8 = 0;                                            // previous bit << 8
+        uint32_t bbase = mbase;                                        // mbase + (0,-2) bit * 256 sbytes
+        const uint32_t s256 = 256u * sbytes;
 #pragma unroll 1
         for (int q = 0; q < 2 * NW; q++) {
             uint32_t t1, t2;
@@ -775,17 +784,21 @@ __global__ void __launch_bounds__(kFastThreads, 1) coder_encode_fast_kernel(Geo 
             e.begin_half();
 #pragma unroll
             for (int J = 0; J < 16; J++) {
-                const bool bit = (int)cb < 0;
+                // The bit is kept as an integer bv in {0, 1} and the bit-dependent selects are
+                // written as multiply-adds: they issue on the FMA pipe, which the ALU-bound
+                // step otherwise leaves idle (same values as the select form).
+                const uint32_t bv = cb >> 31;
                 cb <<= 1;
                 const uint32_t nrows = J < 15 ? slice_ctx(s1, s2, J + 1) : slice_ctx(t1, t2, 0);
-                const uint32_t anctx = mbase + (prev8 | nrows) * sbytes + (bit ? kHiOff : 0u);
+                const uint32_t anctx = imad(bv, kHiOff, imad(nrows, sbytes, bbase));
                 const uint32_t np = lds_u16(anctx);
                 const uint32_t bound = (e.range >> 16) * p;
-                const uint32_t pu = bit ? p - (p >> 4) : p + ((65536u - p) >> 4);
-                const uint64_t a = (uint64_t)e.lo + (bit ? bound : 0u);       // low += bound (carry into hi)
-                e.lo = (uint32_t)a;
-                e.hi += (uint32_t)(a >> 32);
-                e.range = bit ? e.range - bound : bound;
+                const uint32_t tb = imad(bv, bound, 0u);                      // low += bound if 1
+                asm("add.cc.u32 %0, %0, %2;\n\taddc.u32 %1, %1, 0;" : "+r"(e.lo), "+r"(e.hi) : "r"(tb));
+                e.range = imad(bv, e.range, imad(tb, 0xFFFFFFFEu, bound));     // 1: range - bound, 0: bound
+                // p0 update: 1 -> p - (p >> 4) = p + floor((15 - p) / 16); 0 -> p + ((65536 - p) >> 4)
+                const int32_t dp = (int32_t)imad(bv, 15u - 65536u, 65536u - p);
+                const uint32_t pu = p + (uint32_t)(dp >> 4);
                 sts_u16(actx, pu);
                 const bool r24 = e.range < (1u << 24), r16 = e.range < (1u << 16);   // 1 / 2 digits out
                 const int s8 = (r24 ? 8 : 0) + (r16 ? 8 : 0);
@@ -793,7 +806,7 @@ __global__ void __launch_bounds__(kFastThreads, 1) coder_encode_fast_kernel(Geo 
                 e.range <<= s8;
                 p = anctx == actx ? pu : np;
                 actx = anctx;
-                prev8 = bit ? 256u : 0u;
+                bbase = imad(bv, s256, mbase);
             }
             e.end_half(am);
             s1 = t1;
@@ -968,7 +981,8 @@ __global__ void __launch_bounds__(kFastThreads, 1) coder_decode_fast_kernel(Geo 
         win.start(p1, p2, s1, s2);
         uint32_t actx = mbase + slice_ctx(s1, s2, 0) * sbytes;
         uint32_t p = lds_u16(actx);
-        uint32_t prev8 = 0, word = 0, acc = 0;
+        uint32_t bbase = mbase, word = 0, acc = 0;                     // bbase: mbase + (0,-2) bit * 256 sbytes
+        const uint32_t s256 = 256u * sbytes;
         uint32_t *orow = plane_out + (((size_t)img * g.HW + (size_t)(y0 + y) * g.W + x0) >> 5);
 #pragma unroll 1
         for (int q = 0; q < 2 * NW; q++) {
@@ -979,25 +993,30 @@ __global__ void __launch_bounds__(kFastThreads, 1) coder_decode_fast_kernel(Geo 
             for (int J = 0; J < 16; J++) {
                 if ((J & 7) == 0) in.refill(am);                       // >= 128 bits for 8 symbols
                 // both candidate contexts of the next symbol (its (0,-1) bit is the one decoded now)
+                // as in the encoder, the decoded bit is an integer bv in {0, 1} and the
+                // bit-dependent selects are multiply-adds on the FMA pipe
                 const uint32_t nrows = J < 15 ? slice_ctx(s1, s2, J + 1) : slice_ctx(t1, t2, 0);
-                const uint32_t a0 = mbase + (prev8 | nrows) * sbytes, a1 = a0 + kHiOff;
-                const uint32_t np0 = lds_u16(a0), np1 = lds_u16(a1);
-                const uint32_t pu0 = p + ((65536u - p) >> 4), pu1 = p - (p >> 4);
-                const uint32_t f0 = a0 == actx ? pu0 : np0, f1 = a1 == actx ? pu1 : np1;
+                const uint32_t a0 = imad(nrows, sbytes, bbase);
+                const uint32_t np0 = lds_u16(a0), np1 = lds_u16(a0 + kHiOff);
                 const uint32_t bound = (range >> 16) * p;
                 const bool bit = code >= bound;
-                range = bit ? range - bound : bound;
+                const uint32_t bv = bit ? 1u : 0u;
+                range = bit ? range - bound : bound;                            // the serial chain: selects
                 code = bit ? code - bound : code;
-                sts_u16(actx, bit ? pu1 : pu0);
+                const int32_t dp = (int32_t)imad(bv, 15u - 65536u, 65536u - p);
+                const uint32_t pu = p + (uint32_t)(dp >> 4);                  // the encoder's p0 update
+                sts_u16(actx, pu);
                 const int s8 = __clz(range) & 24;                     // 0, 8 or 16 bits to shift in
                 code = __funnelshift_l(in.b0, code, s8);
                 range <<= s8;
                 in.consume(s8);
-                hw |= bit ? 1u << (15 - J) : 0u;
-                lw |= bit ? 1u << J : 0u;
-                actx = bit ? a1 : a0;
-                p = bit ? f1 : f0;
-                prev8 = bit ? 256u : 0u;
+                hw = imad(bv, 1u << (15 - J), hw);
+                lw = imad(bv, 1u << J, lw);
+                const uint32_t anctx = imad(bv, kHiOff, a0);
+                const uint32_t np = bv ? np1 : np0;
+                p = anctx == actx ? pu : np;
+                actx = anctx;
+                bbase = imad(bv, s256, mbase);
             }
             s1 = t1;
             s2 = t2;
