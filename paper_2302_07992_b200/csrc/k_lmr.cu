@@ -795,7 +795,7 @@ __global__ void __launch_bounds__(kFastThreads, 1) coder_encode_fast_kernel(Geo 
                 const uint32_t bound = (e.range >> 16) * p;
                 const uint32_t tb = imad(bv, bound, 0u);                      // low += bound if 1
                 asm("add.cc.u32 %0, %0, %2;\n\taddc.u32 %1, %1, 0;" : "+r"(e.lo), "+r"(e.hi) : "r"(tb));
-                e.range = imad(bv, e.range, imad(tb, 0xFFFFFFFEu, bound));     // 1: range - bound, 0: bound
+                e.range = bv ? e.range - bound : bound;                         // (serial chain: select)
                 // p0 update: 1 -> p - (p >> 4) = p + floor((15 - p) / 16); 0 -> p + ((65536 - p) >> 4)
                 const int32_t dp = (int32_t)imad(bv, 15u - 65536u, 65536u - p);
                 const uint32_t pu = p + (uint32_t)(dp >> 4);
