@@ -988,7 +988,7 @@ __global__ void __launch_bounds__(kFastThreads, 1) coder_decode_fast_kernel(Geo 
         for (int q = 0; q < 2 * NW; q++) {
             uint32_t t1, t2;
             win.next(q & 1, t1, t2);
-            uint32_t hw = 0, lw = 0;
+            uint32_t hw = 0;
 #pragma unroll
             for (int J = 0; J < 16; J++) {
                 if ((J & 7) == 0) in.refill(am);                       // >= 128 bits for 8 symbols
@@ -1011,13 +1011,13 @@ __global__ void __launch_bounds__(kFastThreads, 1) coder_decode_fast_kernel(Geo 
                 range <<= s8;
                 in.consume(s8);
                 hw = imad(bv, 1u << (15 - J), hw);
-                lw = imad(bv, 1u << J, lw);
                 const uint32_t anctx = imad(bv, kHiOff, a0);
                 const uint32_t np = bv ? np1 : np0;
                 p = anctx == actx ? pu : np;
                 actx = anctx;
                 bbase = imad(bv, s256, mbase);
             }
+            const uint32_t lw = __brev(hw) >> 16;                      // the half's bits, pixel order
             s1 = t1;
             s2 = t2;
             if (q & 1) {
