@@ -776,6 +776,7 @@ __global__ void __launch_bounds__(kFastThreads, 1) coder_encode_fast_kernel(Geo 
         uint32_t p = lds_u16(actx);
         uint32_t bbase = mbase;                                        // mbase + (0,-2) bit * 256 sbytes
         const uint32_t s256 = 256u * sbytes;
+        const uint32_t two = g.one + g.one, neg1 = 0u - g.one;        // opaque 2 and -1: FMA-pipe multiplies
 #pragma unroll 1
         for (int q = 0; q < 2 * NW; q++) {
             uint32_t t1, t2;
@@ -788,7 +789,7 @@ __global__ void __launch_bounds__(kFastThreads, 1) coder_encode_fast_kernel(Geo 
                 // written as multiply-adds: they issue on the FMA pipe, which the ALU-bound
                 // step otherwise leaves idle (same values as the select form).
                 const uint32_t bv = cb >> 31;
-                cb <<= 1;
+                cb = imad(cb, two, 0u);
                 const uint32_t nrows = J < 15 ? slice_ctx(s1, s2, J + 1) : slice_ctx(t1, t2, 0);
                 const uint32_t anctx = imad(bv, kHiOff, imad(nrows, sbytes, bbase));
                 const uint32_t np = lds_u16(anctx);
@@ -797,7 +798,7 @@ __global__ void __launch_bounds__(kFastThreads, 1) coder_encode_fast_kernel(Geo 
                 asm("add.cc.u32 %0, %0, %2;\n\taddc.u32 %1, %1, 0;" : "+r"(e.lo), "+r"(e.hi) : "r"(tb));
                 e.range = bv ? e.range - bound : bound;                         // (serial chain: select)
                 // p0 update: 1 -> p - (p >> 4) = p + floor((15 - p) / 16); 0 -> p + ((65536 - p) >> 4)
-                const int32_t dp = (int32_t)imad(bv, 15u - 65536u, 65536u - p);
+                const int32_t dp = (int32_t)imad(bv, 15u - 65536u, imad(p, neg1, 65536u));
                 const uint32_t pu = p + (uint32_t)(dp >> 4);
                 sts_u16(actx, pu);
                 const bool r24 = e.range < (1u << 24), r16 = e.range < (1u << 16);   // 1 / 2 digits out
@@ -1003,7 +1004,7 @@ __global__ void __launch_bounds__(kFastThreads, 1) coder_decode_fast_kernel(Geo 
                 const uint32_t bv = bit ? 1u : 0u;
                 range = bit ? range - bound : bound;                            // the serial chain: selects
                 code = bit ? code - bound : code;
-                const int32_t dp = (int32_t)imad(bv, 15u - 65536u, 65536u - p);
+                const int32_t dp = (int32_t)imad(bv, 15u - 65536u, imad(p, 0xFFFFFFFFu, 65536u));
                 const uint32_t pu = p + (uint32_t)(dp >> 4);                  // the encoder's p0 update
                 sts_u16(actx, pu);
                 const int s8 = __clz(range) & 24;                     // 0, 8 or 16 bits to shift in
