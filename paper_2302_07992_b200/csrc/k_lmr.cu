@@ -907,10 +907,8 @@ struct FastIn {
         b3 |= mid && nb < 128 ? v >> r : 0u;
         b4 |= mid ? (nb < 128 ? __funnelshift_lc(0u, v, 32 - r) : v) : 0u;
         nb += mid ? 32 : 0;
-        if (__any_sync(am, nb < 128)) {
 #pragma unroll 1
-            for (int i = 0; i < 4; i++) add_word_any(nb < 128);
-        }
+        while (__any_sync(am, nb < 128)) add_word_any(nb < 128);   // rare: only as many words as the neediest lane
     }
 };
 
