@@ -182,13 +182,25 @@ __device__ __forceinline__ void count_chunk(const Geo &g, const uint8_t *__restr
     const long long p0 = (long long)chunk * cpx;
     const uint4 *src = reinterpret_cast<const uint4 *>(in + (size_t)img * g.HW + p0);
     uint32_t c = 0;
+    if constexpr (METHOD == 0) {
+        // zero pixels = LSB 0: byte-lane sums of ~w & 0x01..01 over the thread's 64 pixels (<= 16
+        // per lane), then one multiply adds the four lanes; the header pixels r = 0..2 (Q14) are
+        // taken out by the thread that holds them
+        uint32_t lanes = 0;
 #pragma unroll
-    for (int r = 0; r < kScanRounds; r++) {
-        const int q = r * kScanThreads + tid;
-        if (16 * q >= cpx) continue;
-        if constexpr (METHOD == 0) {
-            c += __popc(zero_mask16<0>(__ldg(src + q), p0 + 16 * q, nullptr, 0));
-        } else {
+        for (int r = 0; r < kScanRounds; r++) {
+            const int q = r * kScanThreads + tid;
+            if (16 * q >= cpx) continue;
+            const uint4 u = __ldg(src + q);
+            lanes += (~u.x & 0x01010101u) + (~u.y & 0x01010101u) + (~u.z & 0x01010101u) + (~u.w & 0x01010101u);
+            if (p0 + 16 * q == 0) lanes -= (~u.x & 0x00010101u);
+        }
+        c = (lanes * 0x01010101u) >> 24;
+    } else {
+#pragma unroll
+        for (int r = 0; r < kScanRounds; r++) {
+            const int q = r * kScanThreads + tid;
+            if (16 * q >= cpx) continue;
             const long long pb = (long long)img * g.HW + p0 + 16 * q;
             c += __popc(~(__ldg(map_bits + (pb >> 5)) >> (pb & 31)) & 0xFFFFu);
         }
