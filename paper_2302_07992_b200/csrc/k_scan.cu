@@ -27,7 +27,7 @@ constexpr int kKbufWords = kMaxBlk * 16 + 4;     // + 3 words of alignment offse
 
 // 16 zero-pixel flags of the pixels [p, p+16) of the chunk (bit i = pixel p+i is redundant)
 template <int METHOD>
-__device__ __forceinline__ uint32_t zero_mask16(const uint4 &u, long long p_img, const uint32_t *smap, int p_rel) {
+__device__ __forceinline__ uint32_t zero_mask16(const uint4 &u, bool first, const uint32_t *smap, int p_rel) {
     if constexpr (METHOD == 0) {
         const uint32_t w[4] = {u.x, u.y, u.z, u.w};
         uint32_t m = 0;
@@ -38,7 +38,7 @@ __device__ __forceinline__ uint32_t zero_mask16(const uint4 &u, long long p_img,
             const uint32_t l = ~w[i] & 0x01010101u;
             m |= (((l * 0x00204081u) >> 21) & 0xFu) << (4 * i);
         }
-        if (p_img == 0) m &= ~7u;                                // r = 0..2 hold the header (Q14)
+        if (first) m &= ~7u;                                     // image pixels 0..2 hold the header (Q14)
         return m;
     } else {
         return ~(smap[p_rel >> 5] >> (p_rel & 31)) & 0xFFFFu;
@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(kScanThreads, EMBED ? 5 : 6) scan_kernel(Geo g
 #pragma unroll
     for (int r = 0; r < kScanRounds; r++) {
         const int q = r * kScanThreads + tid;
-        m[r] = 16 * q < cpx ? zero_mask16<METHOD>(spx[q], p0 + 16 * q, smap, 16 * q) : 0u;
+        m[r] = 16 * q < cpx ? zero_mask16<METHOD>(spx[q], r == 0 && tid == 0 && chunk == 0, smap, 16 * q) : 0u;
     }
     // warp-inclusive scans of the 4 round counts, two per packed u32 (counts <= 512 per warp)
     uint32_t c01 = __popc(m[0]) | ((uint32_t)__popc(m[1]) << 16);
@@ -685,7 +685,7 @@ __global__ void __launch_bounds__(256) capacity_kernel(Geo g, const uint8_t *__r
     unsigned long long z = 0;
     for (long long q = tid; q < g.HW / 16; q += 256) {
         if constexpr (METHOD == 0) {
-            z += __popc(zero_mask16<0>(__ldg(reinterpret_cast<const uint4 *>(src) + q), 16 * q, nullptr, 0));
+            z += __popc(zero_mask16<0>(__ldg(reinterpret_cast<const uint4 *>(src) + q), q == 0, nullptr, 0));
         } else {
             const long long pb = (long long)img * g.HW + 16 * q;
             z += __popc(~(__ldg(map_bits + (pb >> 5)) >> (pb & 31)) & 0xFFFFu);
