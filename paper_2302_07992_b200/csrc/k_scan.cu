@@ -54,7 +54,8 @@ __device__ __forceinline__ uint32_t zero_mask16(const uint4 &u, bool first, cons
 // the bytes, fields are held "left-aligned, MSB-first": stream field k in byte 3-k, at bits
 // [8-BP, 8) of the byte, so both conversions are two halving steps (a shift and a
 // select, or an add-multiply) instead of one shift and mask per field.
-//   esel[m4] nibble i = 3 - (number of set bits of m4 below i)   (stream field -> pixel byte)
+//   esel[m4] nibble i = 3 - (number of set bits of m4 below i)   (stream field -> pixel byte) for a
+//                       set bit i, 4 + i (the pixel's own byte, second PRMT operand) otherwise
 //   csel[m4] nibble 3-k = index of the k-th set bit, 4 (zero byte) past popc(m4)
 
 // 4 consecutive BP-bit fields, MSB-first at the top of x -> field k at bits [8-BP, 8) of
@@ -74,7 +75,6 @@ __device__ __forceinline__ uint32_t bytes_to_fields(uint32_t c) {
     const uint32_t x = c + (c & 0x00FF00FFu) * ((1u << (8 - BP)) - 1u);
     return x + (x & 0xFFFFu) * ((1u << (16 - 2 * BP)) - 1u);
 }
-__device__ __forceinline__ uint32_t mask4_to_bytes(uint32_t m4) { return ((m4 & 0xFu) * 0x00204081u) & 0x01010101u; }
 
 // embed (fast path: every field of the group lies below the frame end): the set pixels of
 // the 16-pixel group receive consecutive BP-bit fields of the stream in kbuf from bit `rel`
@@ -90,9 +90,10 @@ __device__ __forceinline__ void embed16(uint32_t w[4], uint32_t mm, const uint32
         const uint32_t x = __funnelshift_l(kbuf[wi + 1], kbuf[wi], o);   // stream bits [o, o+32)
         uint32_t e = fields_to_bytes<BP>(x);
         if constexpr (SHIFT != 8 - BP) e >>= (8 - BP - SHIFT);             // LMR: one bit lower
-        const uint32_t v = __byte_perm(e, 0, esel[m4]);
-        const uint32_t msk = mask4_to_bytes(m4) * FMB;
-        w[j] = (w[j] & ~msk) | (v & msk);
+        // esel picks the field byte for a set pixel and the pixel's own byte otherwise, so one
+        // constant-mask merge writes exactly the set pixels' fields
+        const uint32_t v = __byte_perm(e, w[j], esel[m4]);
+        w[j] = (w[j] & ~(FMB * 0x01010101u)) | (v & (FMB * 0x01010101u));
         o += BP * __popc(m4);
     }
 }
@@ -253,7 +254,7 @@ __global__ void __launch_bounds__(kScanThreads, EMBED ? 5 : 6) scan_kernel(Geo g
         uint32_t e = 0, c = 0;
         int k = 0;
         for (int i = 0; i < 4; i++) {
-            e |= (uint32_t)(3 - __popc(tid & ((1 << i) - 1))) << (4 * i);
+            e |= (uint32_t)(((tid >> i) & 1) ? 3 - __popc(tid & ((1 << i) - 1)) : 4 + i) << (4 * i);
             if ((tid >> i) & 1) c |= (uint32_t)i << (4 * (3 - k++));
         }
         for (; k < 4; k++) c |= 4u << (4 * (3 - k));
