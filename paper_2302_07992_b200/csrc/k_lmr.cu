@@ -1082,9 +1082,9 @@ void launch_coder_encode(const Geo &g, int wave, const uint8_t *ceta, const LmrE
     lmr_set_smem_attrs();
     const int Tc = lmr_tile_count(g.H, g.W, g.tile_log2);
     const int R = coder_round(g);
-    // most work items of this wave: wave 0 = B (1 + k0) Tc; later waves A k Tc <= max(2R, B Tc)
+    // most work items of this wave: wave 0 = B (1 + k0) Tc; later waves A k Tc <= max(kLmrWaveRounds R, B Tc)
     const long long total = wave == 0 ? (long long)g.B * (1 + lmr_wave_k(0, g.B, Tc, g.B, R, 0)) * Tc
-                                      : std::max<long long>(2ll * R, (long long)g.B * Tc);
+                                      : std::max<long long>((long long)kLmrWaveRounds * R, (long long)g.B * Tc);
     const unsigned grid = (unsigned)((total + kCoderThreads - 1) / kCoderThreads);
     const unsigned fgrid = (unsigned)((total + kFastThreads - 1) / kFastThreads);
     switch (lmr_tile_side(g.tile_log2, g.W)) {
