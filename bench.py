@@ -41,7 +41,7 @@ def parse():
     ap.add_argument("--method", default=None, choices=["emr", "lmr"])
     ap.add_argument("--batch", type=int, default=None, help="override the config's batch (testing only)")
     ap.add_argument("--e2e-steps", type=int, default=None)
-    ap.add_argument("--e2e-chunks", type=int, default=None, help="sub-batches of the pipelined e2e leg")
+    ap.add_argument("--e2e-chunks", type=int, default=None, help="sub-batches per step of the pipelined e2e leg (default 1)")
     ap.add_argument("--e2e-lanes", type=int, default=2, help="streams of the pipelined e2e leg")
     ap.add_argument("--no-e2e", action="store_true", help="skip the e2e leg (ncu launch-list runs only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -319,10 +319,11 @@ def run_ours(args):
 
     e2e_value, ok_e2e, e2e_steps, h2d, d2h, t_issue, nsub, sub, streaming, nlanes = None, True, 0, 0, 0, 0.0, 0, 0, False, 0
     if not args.no_e2e:
-        # ---- e2e: host (pinned) buffers through the ABI, copies inside the timed region.  The batch is
-        # cut into sub-batches pipelined over 3 streams, so that the host->device copy of one, the
-        # four calls on another and the device->host copy of a third overlap (PCIe bound).
-        e2e_steps = args.e2e_steps or max(3, min(10, args.steps // 10))
+        # ---- e2e: host (pinned) buffers through the ABI, copies inside the timed region.  Lanes (each
+        # a stream with its own device buffers and workspace) take the (sub-)batches in turn, and the
+        # device->host copies run on a stream of their own, so that one step's host->device copy,
+        # another's calls and a third's device->host copy overlap (PCIe bound).
+        e2e_steps = args.e2e_steps or 10
         hI = torch.from_numpy(imgs).pin_memory()
         hK1, hK2 = torch.from_numpy(k1).pin_memory(), torch.from_numpy(k2).pin_memory()
         hMSG, hNB = torch.from_numpy(msgs).pin_memory(), torch.from_numpy(nbits_np).pin_memory()
@@ -331,9 +332,11 @@ def run_ours(args):
         hSSE = torch.empty(B, dtype=torch.int64).pin_memory()
         h2d = hI.numel() + hK1.numel() + hK2.numel() + hMSG.numel() + hNB.numel() * 8
         d2h = hREC.numel() + hMOUT.numel() + hSSE.numel() * 8
-        # two sub-batches on two lanes measured best (EMR 25 / LMR 19 Gpx/s at configs 2 / 3, against
-        # 23 / 13 with eight over three): halves keep the LMR coder rounds full and the copies large
-        nsub = next(k for k in (args.e2e_chunks, 2, 1) if k and B % k == 0)
+        # the whole batch per lane, two lanes taking turns across steps, measured best (EMR 25.3 / LMR
+        # 24.0 Gpx/s at configs 2 / 3, against 25.0 / 23.2 with two sub-batches and 23 / 13 with eight
+        # over three): one step's calls overlap the neighbouring steps' copies, the copies are large and
+        # the LMR coder rounds stay full
+        nsub = next(k for k in (args.e2e_chunks, 1) if k and B % k == 0)
         sub = B // nsub
 
         class Lane:
@@ -352,7 +355,7 @@ def run_ours(args):
                 self.computed = torch.cuda.Event()
                 self.copied = None                    # last device->host copy of this lane's outputs
 
-        lanes = [Lane() for _ in range(min(args.e2e_lanes, nsub))]
+        lanes = [Lane() for _ in range(args.e2e_lanes)]
         d2h_stream = torch.cuda.Stream(device=dev)   # device->host copies, off the lanes' streams
 
         # one process: the lanes stream sub-batches back to back across steps (a lane reuses its
@@ -360,11 +363,14 @@ def run_ours(args):
         # with several ranks each step ends with the records all-gather, so lanes join per step
         streaming = world == 1
 
+        turn = [0]                              # lanes take sub-batches in rotation, across steps too
+
         def e2e_step():
             start = torch.cuda.Event()
             start.record(stream)
             for i in range(nsub):
-                L = lanes[i % len(lanes)]
+                L = lanes[turn[0] % len(lanes)]
+                turn[0] += 1
                 a, z = i * sub, (i + 1) * sub
                 if not streaming:
                     L.stream.wait_event(start)
@@ -463,12 +469,14 @@ def run_ours(args):
                 "e2e": {"skipped": "--no-e2e (profiling runs only)"} if args.no_e2e else
                        {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d * world),
                         "d2h_bytes_per_step": int(d2h * world), "steps": e2e_steps,
-                        "path": f"pinned host -> cudaMemcpyAsync -> C ABI calls -> host; {nsub} sub-batches "
-                                f"of {sub} images pipelined over {len(lanes)} streams"
+                        "path": f"pinned host -> cudaMemcpyAsync -> C ABI calls -> host; {nsub} sub-batch(es) "
+                                f"of {sub} images per step, {len(lanes)} lanes (streams + buffers) taking them in turn, "
+                                f"device->host copies on their own stream"
                                 + (", streamed across steps (no drain at step boundaries)" if streaming else ""),
                         "host_issue_ms_per_step": t_issue,
                         "pcie_note": "both directions at once measured at 49.4 GB/s each on this box "
-                                     "(tools/pcie_probe.py): the e2e ceiling is bytes per step / 49.4 GB/s"},
+                                     "(tools/pcie_probe.py): the e2e ceiling is bytes per step / 49.4 GB/s; the "
+                                     "same copy pipeline without the calls moves 43-45 GB/s (tools/e2e_probe.py)"},
                 "roofline": roof["dominant"],
                 "step_hbm": step_hbm(roof["kernels"], value, float(cap.mean() / HW), load_peaks()),
                 "kernels": roof["kernels"],
