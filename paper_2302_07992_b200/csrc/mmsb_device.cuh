@@ -165,7 +165,9 @@ __device__ __forceinline__ void pair_rot_cw(uint32_t &top, uint32_t &bot, int aL
 
 // angle of block (by, bx) of level e in a tile's angle record (2-bit fields, one u64 per row)
 __device__ __forceinline__ int rec_angle(const uint64_t *rec, const Geo &g, int e, int by, int bx) {
-    return (int)((rec[g.lvl_off[e] + by] >> (2 * bx)) & 3);
+    // the 32-bit half holding field bx (little-endian u64): one 32-bit load and shift
+    const uint32_t *w = reinterpret_cast<const uint32_t *>(rec + g.lvl_off[e] + by);
+    return (int)((w[bx >> 4] >> ((2 * bx) & 31)) & 3);
 }
 
 // 2-bit-field addition mod 4 (SWAR): per field (a + b) mod 4
