@@ -47,31 +47,6 @@ __device__ __forceinline__ void chacha20_block(const uint32_t k[8], uint32_t cou
     o[12] = x12 + counter; o[13] = x13; o[14] = x14; o[15] = x15;
 }
 
-// One ChaCha20 block computed by 4 consecutive lanes (lane & 3 = c holds state column c:
-// words c, 4+c, 8+c, 12+c).  Column rounds are lane-local; for the diagonal rounds rows 1..3
-// are rotated across the 4 lanes with shuffles and rotated back.  All 32 lanes must call it.
-__device__ __forceinline__ void chacha20_block_x4(const uint32_t k[8], uint32_t counter, uint32_t o[4]) {
-    const int lane = threadIdx.x & 31, c = lane & 3, g0 = lane & ~3;
-    const uint32_t a0 = c == 0 ? 0x61707865u : c == 1 ? 0x3320646eu : c == 2 ? 0x79622d32u : 0x6b206574u;
-    const uint32_t b0 = c == 0 ? k[0] : c == 1 ? k[1] : c == 2 ? k[2] : k[3];
-    const uint32_t c0 = c == 0 ? k[4] : c == 1 ? k[5] : c == 2 ? k[6] : k[7];
-    const uint32_t d0 = c == 0 ? counter : 0u;
-    uint32_t a = a0, b = b0, cc = c0, d = d0;
-    const int l1 = g0 | ((c + 1) & 3), l2 = g0 | ((c + 2) & 3), l3 = g0 | ((c + 3) & 3);
-#pragma unroll
-    for (int i = 0; i < 10; i++) {
-        MMSB_QR(a, b, cc, d)
-        b = __shfl_sync(0xffffffffu, b, l1);
-        cc = __shfl_sync(0xffffffffu, cc, l2);
-        d = __shfl_sync(0xffffffffu, d, l3);
-        MMSB_QR(a, b, cc, d)
-        b = __shfl_sync(0xffffffffu, b, l3);
-        cc = __shfl_sync(0xffffffffu, cc, l2);
-        d = __shfl_sync(0xffffffffu, d, l1);
-    }
-    o[0] = a + a0; o[1] = b + b0; o[2] = cc + c0; o[3] = d + d0;
-}
-
 __device__ __forceinline__ void load_key(const uint8_t *keys, int img, uint32_t k[8]) {
     const uint4 *p = reinterpret_cast<const uint4 *>(keys + (size_t)img * 32);
     uint4 a = __ldg(p), b = __ldg(p + 1);
@@ -230,9 +205,6 @@ __device__ __forceinline__ void st_release_u32(unsigned *p, unsigned v) {
 __device__ __forceinline__ void red_release_add_u32(unsigned *p, unsigned v) {
     asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-__device__ __forceinline__ void st_relaxed_u32(unsigned *p, unsigned v) {
-    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
 
 // relaxed (but coherent at gpu scope) accesses for self-contained flag|value words: no L1
 // invalidation (CCTL.IVALL) per probe, unlike ld.acquire
@@ -243,9 +215,6 @@ __device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long lon
     unsigned long long v;
     asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
-}
-__device__ __forceinline__ void st_release(unsigned long long *p, unsigned long long v) {
-    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long *p) {
     unsigned long long v;
