@@ -537,6 +537,11 @@ CHACHA_ALU_PER_BYTE = 640 / 64
 # row windows shifted and masked, merged with the two history bits), bound = (range>>16)*p0 2,
 # interval update 2, model update 3, renormalisation test 1; its units are symbols, not pixels
 CODER_ALU_PER_SYMBOL = 12.0
+# the coder's issue floor: one warp per SM sub-partition (112 tiles per SM, smem-bound) issues at
+# most one instruction per cycle, and the unrolled symbol step is this many SASS instructions
+# (DESIGN.md §5.6), so no tile advances faster than one symbol per that many cycles
+CODER_SASS_PER_SYMBOL = {"coder_encode_kernel": 43.0, "lmr_pack+header+coder_decode_kernels": 41.0}
+CODER_TILES_PER_SM = 112
 
 
 def kernel_model(name, der):
@@ -604,6 +609,12 @@ def roofline(prof, peaks, B, HW, cap, method):
                       "algorithmic_GBps": gbs, "hbm_frac": gbs / hbm_peak,
                       "alu_Tops": tops, "alu_frac": tops / alu_peak,
                       "bytes_per_px": m["bytes"], "alu_ops_per_unit": m["alu"]}
+        if name in CODER_SASS_PER_SYMBOL:       # units are symbols: achieved vs the issue floor
+            sym_s = p["pixels"] / sec
+            floor = 148 * CODER_TILES_PER_SM * sm_mhz * 1e6 / CODER_SASS_PER_SYMBOL[name]
+            kern[name].update({"sym_per_s": sym_s, "issue_bound_sym_per_s": floor, "issue_bound_frac": sym_s / floor,
+                               "issue_bound_note": f"148 SMs x {CODER_TILES_PER_SM} tiles x f_SM / "
+                                                   f"{CODER_SASS_PER_SYMBOL[name]:.0f} SASS instructions per symbol"})
     total = sum(p["ms"] for p in prof.values()) or 1.0
     for k in kern:
         kern[k]["share"] = kern[k]["ms_total"] / total
@@ -624,6 +635,9 @@ def roofline(prof, peaks, B, HW, cap, method):
                            "a serial chain per tile, ~112 tiles in flight per SM"),
              "hbm": {"achieved_GBps": k["algorithmic_GBps"], "peak": hbm_peak, "frac": k["hbm_frac"]}}
     d["share_of_step"] = k["share"]
+    if "issue_bound_frac" in k:
+        d["coder_symbols"] = {"achieved_sym_per_s": k["sym_per_s"], "issue_bound_sym_per_s": k["issue_bound_sym_per_s"],
+                              "frac": k["issue_bound_frac"], "note": k["issue_bound_note"]}
     px_launch = prof[dom]["pixels"] / prof[dom]["launches"]
     d["traffic"] = traffic[dom] * px_launch if dom in traffic else None
     d["traffic_note"] = ("dram__bytes_read.sum + dram__bytes_write.sum per pixel from profiles/traffic.json "
