@@ -21,3 +21,26 @@ def test_bench_help_lists_the_driver_flags():
                          timeout=120).stdout
     for flag in ("--gpus", "--steps", "--warmup", "--impl", "--config", "--method"):
         assert flag in out
+
+
+def test_bench_roofline_fields():
+    """bench.roofline() on synthetic per-kernel timings: the dominant kernel, its bound and
+    fraction, and the coder's symbols/s against its issue floor."""
+    sys.path.insert(0, ROOT)
+    import bench
+    peaks = {"hbm_gbs": 6556.2, "sm_max_mhz": 1965}
+    HW = 512 * 512
+    prof = {"encode_kernel": {"ms": 10.0, "launches": 20, "pixels": 20 * 1000 * HW},
+            "coder_encode_kernel": {"ms": 30.0, "launches": 70, "pixels": 13_000_000_000},
+            "lmr_pack+header+coder_decode_kernels": {"ms": 32.0, "launches": 30, "pixels": 10_400_000_000}}
+    r = bench.roofline(prof, peaks, 1000, HW, [2.1 * HW] * 1000, "lmr")
+    d = r["dominant"]
+    assert d["kernel"] == "lmr_pack+header+coder_decode_kernels" and d["bound"] == "alu"
+    assert abs(d["frac"] - d["achieved"] / d["peak"]) < 1e-12
+    cs = d["coder_symbols"]
+    assert abs(cs["achieved_sym_per_s"] - 10_400_000_000 / 0.032) < 1.0
+    floor = 148 * 112 * 1965e6 / 41.0
+    assert abs(cs["issue_bound_sym_per_s"] - floor) < 1.0 and abs(cs["frac"] - cs["achieved_sym_per_s"] / floor) < 1e-12
+    k = r["kernels"]["encode_kernel"]
+    assert abs(k["algorithmic_GBps"] - 2.0 * 20 * 1000 * HW / 0.010 / 1e9) < 1e-6
+    assert abs(sum(v["share"] for v in r["kernels"].values()) - 1.0) < 1e-12
