@@ -229,7 +229,7 @@ __global__ void __launch_bounds__(kScanThreads, EMBED ? 5 : 6) scan_kernel(Geo g
     __shared__ __align__(128) uint4 spx[kChunk / 16];
     __shared__ __align__(16) uint32_t smap[METHOD == 1 ? kChunk / 32 : 4];
     __shared__ __align__(16) uint32_t kbuf[kKbufWords];
-    __shared__ __align__(8) uint64_t bar;
+    __shared__ __align__(8) uint64_t bar, bar_ef;
     __shared__ uint32_t wtot[kScanRounds][kScanThreads / 32], woff[kScanRounds][kScanThreads / 32];
     __shared__ long long sh_prefix;
     __shared__ uint32_t sh_agg;
@@ -244,6 +244,7 @@ __global__ void __launch_bounds__(kScanThreads, EMBED ? 5 : 6) scan_kernel(Geo g
 
     if (tid == 0) {
         mbar_init(&bar, 1);
+        if constexpr (EMBED) mbar_init(&bar_ef, 1);
         const unsigned bytes = (unsigned)cpx + (METHOD == 1 ? (unsigned)cpx / 8 : 0u);
         mbar_expect_tx(&bar, bytes);
         bulk_g2s(spx, src + p0, (unsigned)cpx, &bar);
@@ -276,6 +277,23 @@ __global__ void __launch_bounds__(kScanThreads, EMBED ? 5 : 6) scan_kernel(Geo g
         if (lane == 0) wpre[wid] = part;
     }
     __syncthreads();                                         // barrier initialised (and wpre written)
+    if constexpr (EMBED) {
+        // the chunk's frame range is known from the counts already (prefix = earlier chunks,
+        // aggregate = this chunk's count): its E_F blocks are fetched by one more bulk copy
+        // that lands while the chunk is scanned
+        if (tid == 0) {
+            long long pre = 0;
+            for (int w = 0; w < kScanThreads / 32; w++) pre += wpre[w];
+            const long long agg0 = __ldg(ws.counts + (size_t)img * g.nchunks + chunk);
+            const long long C = (long long)__ldcg(ws.ztot + img) * bp;
+            const bool n_ok = n >= 0 && n <= 8 * stride && n <= 0xFFFFFFFFll && 32 + n <= C;
+            const long long F = n_ok ? 32 + n : 0, lo = pre * bp, hi = (pre + agg0) * bp;
+            const long long hie = hi < F ? hi : F, blk0 = lo >> 9;
+            const int nblk = (b >= 2 && lo < hie) ? (int)(((hie - 1) >> 9) - blk0 + 1) : 0;
+            mbar_expect_tx(&bar_ef, (unsigned)nblk * 64u);
+            if (nblk) bulk_g2s(kbuf, ws.ef + (size_t)img * ws.ef_words + blk0 * 16, (unsigned)nblk * 64u, &bar_ef);
+        }
+    }
     mbar_wait(&bar, 0);
 
     if (b < 2) {                                             // FORMAT (EMR) / BADCASE, FORMAT (LMR)
@@ -383,10 +401,9 @@ __global__ void __launch_bounds__(kScanThreads, EMBED ? 5 : 6) scan_kernel(Geo g
         const long long hie = hi < F ? hi : F;
         const long long blk0 = lo >> 9;
         const int nblk = lo < hie ? (int)(((hie - 1) >> 9) - blk0 + 1) : 0;
-        // E_F words of the chunk's frame blocks (embed_prep_kernel), coalesced into smem
-        const uint32_t *ef = ws.ef + (size_t)img * ws.ef_words + blk0 * 16;
-        for (int t = tid; t < nblk * 16; t += kScanThreads) kbuf[t] = __ldg(ef + t);
-        __syncthreads();
+        // E_F words of the chunk's frame blocks (embed_prep_kernel): the bulk copy issued at the start
+        (void)nblk;
+        mbar_wait(&bar_ef, 0);
         const long long base = blk0 * 512;
         const long long fend = hie - base;
         uint8_t *dst = out + (size_t)img * g.HW + p0;
