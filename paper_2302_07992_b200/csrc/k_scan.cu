@@ -116,9 +116,9 @@ __device__ __noinline__ uint4 embed16_tail(uint4 u, uint32_t mm, const uint32_t 
     return make_uint4(w[0], w[1], w[2], w[3]);
 }
 
-// extract: the set pixels' BP-bit fields appended in raster order, ORed into kbuf from bit
-// `rel`; the first and last (partial) words are shared with the neighbouring threads
-// (shared-memory atomics), the words in between belong to this thread alone.
+// extract: the set pixels' BP-bit fields appended in raster order, XORed into kbuf (which holds
+// the keystream) from bit `rel`; the first and last (partial) words are shared with the
+// neighbouring threads (shared-memory atomics), the words in between belong to this thread alone.
 template <int BP, int SHIFT>
 __device__ __forceinline__ void extract16(const uint32_t w[4], uint32_t mm, uint32_t *kbuf, int rel,
                                           const uint32_t *csel) {
@@ -137,15 +137,15 @@ __device__ __forceinline__ void extract16(const uint32_t w[4], uint32_t mm, uint
         nacc += BP * __popc(m4);
         if (nacc >= 32) {
             const uint32_t word = (uint32_t)(acc >> 32);
-            if (first) atomicOr(&kbuf[wi], word);
-            else kbuf[wi] = word;
+            if (first) atomicXor(&kbuf[wi], word);
+            else kbuf[wi] ^= word;
             first = false;
             wi++;
             acc <<= 32;
             nacc -= 32;
         }
     }
-    if (nacc > 0 && (nacc > (rel & 31) || !first)) atomicOr(&kbuf[wi], (uint32_t)(acc >> 32));
+    if (nacc > 0 && (nacc > (rel & 31) || !first)) atomicXor(&kbuf[wi], (uint32_t)(acc >> 32));
 }
 
 #define MMSB_BP_SWITCH(bp, METHOD, BODY)                                                   \
@@ -434,14 +434,14 @@ __global__ void __launch_bounds__(kScanThreads, EMBED ? 5 : 6) scan_kernel(Geo g
         const long long blk0 = lo >> 9;
         const long long base = blk0 * 512, basew = blk0 * 16;
         const int nblk = lo < hi ? (int)(((hi - 1) >> 9) - blk0 + 1) : 0;
-        // every word a thread fills completely is stored plainly; only the first and last word
-        // of each 16-pixel group can be shared (ORed), so those are the words zeroed first
+        // the chunk's K2 keystream blocks go into kx first; every frame bit of [lo, hi) belongs to
+        // exactly one 16-pixel group, which XORs its fields onto them (shared boundary words by
+        // shared-memory atomics), so kx ends as G XOR KS2 with no zeroing or separate XOR pass
+        if (tid < nblk) {
+            uint32_t ks[16];
+            chacha20_block(key, (uint32_t)(blk0 + tid), ks, g.dr);
 #pragma unroll
-        for (int r = 0; r < kScanRounds; r++) {
-            if (!m[r]) continue;
-            const int rel = (int)((prefix + excl[r]) * bp - base);
-            kx[rel >> 5] = 0;
-            kx[(rel + bp * __popc(m[r]) - 1) >> 5] = 0;
+            for (int j = 0; j < 16; j++) kx[tid * 16 + j] = bswap32(ks[j]);
         }
         __syncthreads();
         MMSB_BP_SWITCH(bp, METHOD, ({
@@ -453,13 +453,6 @@ __global__ void __launch_bounds__(kScanThreads, EMBED ? 5 : 6) scan_kernel(Geo g
                 extract16<BP, SH>(w, m[r], kx, (int)((prefix + excl[r]) * BP - base), csel);
             }
         }))
-        uint32_t ks[16];
-        if (tid < nblk) chacha20_block(key, (uint32_t)(blk0 + tid), ks, g.dr);
-        __syncthreads();
-        if (tid < nblk) {
-#pragma unroll
-            for (int j = 0; j < 16; j++) kx[tid * 16 + j] ^= bswap32(ks[j]);
-        }
         __syncthreads();
         uint32_t *mo = reinterpret_cast<uint32_t *>(msg_out + (size_t)img * stride);
         unsigned long long *parts = ws.parts + ((size_t)img * g.nchunks + chunk) * 2;
