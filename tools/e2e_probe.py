@@ -14,13 +14,15 @@ ap.add_argument("--steps", type=int, default=20)
 ap.add_argument("--nsub", type=int, default=2)
 ap.add_argument("--compute_ms", type=float, default=0.0, help="a busy kernel of this length per sub-batch")
 ap.add_argument("--lanes", type=int, default=2)
+ap.add_argument("--msg_bytes", type=int, default=180480, help="payload row bytes per image (0: images only)")
 a = ap.parse_args()
-B, HW, MSGB = 1000, 512 * 512, 180480
+B, HW = 1000, 512 * 512
+MSGB = a.msg_bytes
 dev = torch.device("cuda")
 hI = torch.empty(B * HW, dtype=torch.uint8).pin_memory()
-hM = torch.empty(B * MSGB, dtype=torch.uint8).pin_memory()
+hM = torch.empty(max(B * MSGB, 1), dtype=torch.uint8).pin_memory()
 hR = torch.empty(B * HW, dtype=torch.uint8).pin_memory()
-hMO = torch.empty(B * MSGB, dtype=torch.uint8).pin_memory()
+hMO = torch.empty(max(B * MSGB, 1), dtype=torch.uint8).pin_memory()
 sub = B // a.nsub
 
 
@@ -28,9 +30,9 @@ class Lane:
     def __init__(self):
         self.s = torch.cuda.Stream()
         self.I = torch.empty(sub * HW, dtype=torch.uint8, device=dev)
-        self.M = torch.empty(sub * MSGB, dtype=torch.uint8, device=dev)
+        self.M = torch.empty(max(sub * MSGB, 1), dtype=torch.uint8, device=dev)
         self.R = torch.empty(sub * HW, dtype=torch.uint8, device=dev)
-        self.MO = torch.empty(sub * MSGB, dtype=torch.uint8, device=dev)
+        self.MO = torch.empty(max(sub * MSGB, 1), dtype=torch.uint8, device=dev)
         self.copied = None
         self.computed = torch.cuda.Event()
 
@@ -49,19 +51,22 @@ def step(compute):
         u, v = i * sub * MSGB, (i + 1) * sub * MSGB
         with torch.cuda.stream(L.s):
             L.I.copy_(hI[x:y], non_blocking=True)
-            L.M.copy_(hM[u:v], non_blocking=True)
+            if MSGB:
+                L.M.copy_(hM[u:v], non_blocking=True)
             if L.copied is not None:
                 L.s.wait_event(L.copied)
             if compute:
                 L.R.copy_(L.I)                     # device-side work standing in for the five calls
-                L.MO.copy_(L.M)
+                if MSGB:
+                    L.MO.copy_(L.M)
                 if a.compute_ms > 0:
                     torch.cuda._sleep(int(a.compute_ms * 1.9e6))
             L.computed.record(L.s)
         d2h.wait_event(L.computed)
         with torch.cuda.stream(d2h):
             hR[x:y].copy_(L.R, non_blocking=True)
-            hMO[u:v].copy_(L.MO, non_blocking=True)
+            if MSGB:
+                hMO[u:v].copy_(L.MO, non_blocking=True)
             L.copied = torch.cuda.Event()
             L.copied.record(d2h)
 
