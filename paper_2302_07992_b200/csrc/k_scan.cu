@@ -117,8 +117,8 @@ __device__ __noinline__ uint4 embed16_tail(uint4 u, uint32_t mm, const uint32_t 
 }
 
 // extract: the set pixels' BP-bit fields appended in raster order, XORed into kbuf (which holds
-// the keystream) from bit `rel`; the first and last (partial) words are shared with the
-// neighbouring threads (shared-memory atomics), the words in between belong to this thread alone.
+// the keystream) from bit `rel`; the first and last (partial) words can be shared with the
+// neighbouring threads, so every word goes in by a shared-memory atomic XOR.
 template <int BP, int SHIFT>
 __device__ __forceinline__ void extract16(const uint32_t w[4], uint32_t mm, uint32_t *kbuf, int rel,
                                           const uint32_t *csel) {
@@ -126,7 +126,6 @@ __device__ __forceinline__ void extract16(const uint32_t w[4], uint32_t mm, uint
     int wi = rel >> 5;
     int nacc = rel & 31;                        // valid bits at the top of acc (leading pad = 0)
     unsigned long long acc = 0;
-    bool first = true;
 #pragma unroll
     for (int j = 0; j < 4; j++) {
         const uint32_t m4 = (mm >> (4 * j)) & 0xFu;
@@ -135,17 +134,14 @@ __device__ __forceinline__ void extract16(const uint32_t w[4], uint32_t mm, uint
         const uint32_t p = bytes_to_fields<BP>(c);
         acc |= ((unsigned long long)p << 32) >> nacc;
         nacc += BP * __popc(m4);
-        if (nacc >= 32) {
-            const uint32_t word = (uint32_t)(acc >> 32);
-            if (first) atomicXor(&kbuf[wi], word);
-            else kbuf[wi] ^= word;
-            first = false;
+        if (nacc >= 32) {                       // XOR commutes: every word by one shared-memory atomic
+            atomicXor(&kbuf[wi], (uint32_t)(acc >> 32));
             wi++;
             acc <<= 32;
             nacc -= 32;
         }
     }
-    if (nacc > 0 && (nacc > (rel & 31) || !first)) atomicXor(&kbuf[wi], (uint32_t)(acc >> 32));
+    if (nacc > 0) atomicXor(&kbuf[wi], (uint32_t)(acc >> 32));
 }
 
 #define MMSB_BP_SWITCH(bp, METHOD, BODY)                                                   \
