@@ -323,7 +323,7 @@ def run_ours(args):
         # a stream with its own device buffers and workspace) take the (sub-)batches in turn, and the
         # device->host copies run on a stream of their own, so that one step's host->device copy,
         # another's calls and a third's device->host copy overlap (PCIe bound).
-        e2e_steps = args.e2e_steps or 10
+        e2e_steps = args.e2e_steps or 20
         hI = torch.from_numpy(imgs).pin_memory()
         hK1, hK2 = torch.from_numpy(k1).pin_memory(), torch.from_numpy(k2).pin_memory()
         hMSG, hNB = torch.from_numpy(msgs).pin_memory(), torch.from_numpy(nbits_np).pin_memory()
