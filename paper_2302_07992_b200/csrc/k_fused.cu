@@ -219,7 +219,7 @@ __device__ __forceinline__ void key_role(const Geo &g, int img, int kidx, const 
         if (tid < 7) {
             uint32_t v = 0;
             for (int w = 0; w < 8; w++) v += (hsum[w * 4 + (tid >> 1)] >> (16 * (tid & 1))) & 0xFFFFu;
-            if (v) atomicAdd(&ws.hist[img * 8 + 8 - tid], v);
+            if (v) atomicAdd(&ws.hist[img * kHistStride + 8 - tid], v);
         }
     }
     __syncthreads();
@@ -360,7 +360,7 @@ __device__ __forceinline__ void perm_role(const Geo &g, int img, int dty, int nK
             upper_walk_inverse(g, pyr, dty, j, sty, stx, q);
             S.smap[j] = (((sty << g.tlog) + stx) << 2) | q;
         }
-        if (tid == 0) S.sh[0] = METHOD == 0 ? emr_select_b(ws.hist + img * 8, g.HW) : 0;
+        if (tid == 0) S.sh[0] = METHOD == 0 ? emr_select_b(ws.hist + img * kHistStride, g.HW) : 0;
     }
     __syncthreads();
     const int b = S.sh[0];
@@ -469,7 +469,7 @@ __device__ __forceinline__ void perm_role(const Geo &g, int img, int dty, int nK
                     const uint32_t hb = (uint32_t)(b - 2);
                     const uint32_t hdr = ((hb >> 2) & 1u) | (((hb >> 1) & 1u) << 8) | ((hb & 1u) << 16);
                     e0 = (e0 & 0xFFFEFEFEu) | hdr;
-                    const long long zeros = g.HW - (long long)__ldcg(ws.hist + img * 8 + b);
+                    const long long zeros = g.HW - (long long)__ldcg(ws.hist + img * kHistStride + b);
                     b_out[img] = b;
                     cap_out[img] = (long long)b * (zeros - (3 - forced));
                     status[img] = 0;

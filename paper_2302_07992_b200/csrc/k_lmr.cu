@@ -180,7 +180,7 @@ __global__ void lmr_plan_kernel(Geo g, const uint32_t *__restrict__ hist, LmrPla
     for (int c = 0; c < 8; c++) mapbytes[(size_t)img * 8 + c] = 0;
     LmrPlan p{};
     long long val[9];
-    for (int b = 2; b <= 8; b++) val[b] = (long long)(b - 1) * (g.HW - (long long)hist[img * 8 + b]);
+    for (int b = 2; b <= 8; b++) val[b] = (long long)(b - 1) * (g.HW - (long long)hist[img * kHistStride + b]);
     int ord[7];
     for (int k = 0; k < 7; k++) ord[k] = k + 2;
     for (int k = 1; k < 7; k++) {
@@ -312,7 +312,7 @@ __global__ void __launch_bounds__(256) lmr_msb_write_kernel(Geo g, LmrEncWS ew,
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         if (pl.state == 1) {
             b_out[img] = pl.b;
-            cap_out[img] = (long long)(pl.b - 1) * (g.HW - (long long)hist[img * 8 + pl.b]);
+            cap_out[img] = (long long)(pl.b - 1) * (g.HW - (long long)hist[img * kHistStride + pl.b]);
             status[img] = 0;
         } else {
             b_out[img] = 0;

@@ -74,7 +74,7 @@ static Layout layout(const Geo &g) {
     L.s = o; o = align256(o + B * g.HW);
     L.rec = o; o = align256(o + B * nt * kRecSlots * 8);
     L.pyr = o; o = align256(o + B * (g.npyr > 0 ? g.npyr : 1) * 4);
-    L.hist = o; o = align256(o + B * 8 * 4);
+    L.hist = o; o = align256(o + B * kHistStride * 4);
     L.kdone = o; o = align256(o + B * 4);
     L.rstate = o; o = align256(o + B * nt * 16);
     L.tile_zero_end = o;

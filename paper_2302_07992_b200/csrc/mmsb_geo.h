@@ -10,6 +10,7 @@ constexpr int kChunk = kScanRounds * kScanThreads * 16;   // raster pixels per s
 constexpr int kRecSlots = 80;       // u64 slots of a tile's record: angles of levels 1..6 (slots 0..62),
                                     // the in-tile 8x8-group map (bytes of slots 64..71), padding to 5 lines
 constexpr int kRecGroupSlot = 64;
+constexpr int kHistStride = 16;  // u32 per image of the label histogram (counts for b = 2..8 at index b)
 
 struct Geo {
     int method;          // 0 EMR, 1 LMR

@@ -83,7 +83,7 @@ struct TileWS {
     uint8_t *s;          // [B][ntiles][T*T] K1 keystream, tile-major (transient, discarded from L2)
     uint64_t *rec;       // [B][ntiles][kRecSlots] in-tile angle records (transient)
     uint32_t *pyr;       // [B][npyr] upper-level block sums (mod 4 on read)        -- zeroed per call
-    uint32_t *hist;      // [B][8] non-redundant counts for b = 2..8 at index b      -- zeroed per call
+    uint32_t *hist;      // [B][kHistStride] non-redundant counts for b = 2..8 at index b -- zeroed per call
     uint32_t *kdone;     // [B] keystream CTAs finished                               -- zeroed per call
     unsigned long long *rstate;   // [B][ntiles][2] recover look-back: flag | row mask  -- zeroed per call
     uint8_t *ragg;       // [B][ntiles][T] per row: last non-redundant masked value in the tile

@@ -87,6 +87,30 @@ def _ptr(t: torch.Tensor | None):
     return C.c_void_p(t.data_ptr())
 
 
+def _arg(t: torch.Tensor, name: str, dtype: torch.dtype, shape: tuple, device=None) -> torch.Tensor:
+    """Checks one ABI argument before its raw pointer crosses the boundary: a wrong dtype, shape or
+    device would otherwise be an out-of-bounds device read or write (the C side sees sizes only)."""
+    if not isinstance(t, torch.Tensor):
+        raise MmsbError(f"mmsb: {name} must be a torch tensor")
+    if t.dtype != dtype:
+        raise MmsbError(f"mmsb: {name} must be {dtype}, got {t.dtype}")
+    if tuple(t.shape) != tuple(shape):
+        raise MmsbError(f"mmsb: {name} must have shape {tuple(shape)}, got {tuple(t.shape)}")
+    if not t.is_cuda:
+        raise MmsbError(f"mmsb: {name} must be a device tensor (the product path has no CPU fallback)")
+    if device is not None and t.device != device:
+        raise MmsbError(f"mmsb: {name} is on {t.device}, expected {device}")
+    if not t.is_contiguous():
+        raise MmsbError(f"mmsb: {name} must be contiguous")
+    return t
+
+
+def _images(t: torch.Tensor, name: str):
+    if not isinstance(t, torch.Tensor) or t.dim() != 3:
+        raise MmsbError(f"mmsb: {name} must be a [B, H, W] uint8 tensor")
+    return _arg(t, name, torch.uint8, tuple(t.shape)).shape
+
+
 def _stream():
     return C.c_void_p(torch.cuda.current_stream().cuda_stream)
 
@@ -123,7 +147,10 @@ def _ws(ws: Workspace | None, method, B, H, W, tile_log2, device):
 def encode(method: int, images: torch.Tensor, k1: torch.Tensor, ws: Workspace | None = None, tile_log2: int = 7,
            out: torch.Tensor | None = None):
     """Content owner: returns (encrypted, b, capacity_bits, status) -- mmsb_content_owner_encode."""
-    B, H, W = images.shape
+    B, H, W = _images(images, "images")
+    _arg(k1, "k1", torch.uint8, (B, 32), images.device)
+    if out is not None:
+        _arg(out, "out", torch.uint8, (B, H, W), images.device)
     ws = _ws(ws, method, B, H, W, tile_log2, images.device)
     enc = out if out is not None else torch.empty_like(images)
     b = torch.empty(B, dtype=torch.int32, device=images.device)
@@ -138,7 +165,17 @@ def encode(method: int, images: torch.Tensor, k1: torch.Tensor, ws: Workspace | 
 def embed(method: int, encrypted: torch.Tensor, k2: torch.Tensor, msg: torch.Tensor, msg_bits: torch.Tensor,
           ws: Workspace | None = None, tile_log2: int = 7, out: torch.Tensor | None = None):
     """Data hider: returns (marked, status) -- mmsb_hider_embed."""
-    B, H, W = encrypted.shape
+    B, H, W = _images(encrypted, "encrypted")
+    dev = encrypted.device
+    _arg(k2, "k2", torch.uint8, (B, 32), dev)
+    if msg.dim() != 2:
+        raise MmsbError("mmsb: msg must be a [B, stride_bytes] uint8 tensor")
+    _arg(msg, "msg", torch.uint8, (B, msg.shape[1]), dev)
+    if msg.shape[1] <= 0 or msg.shape[1] % 16:
+        raise MmsbError(f"mmsb: msg stride {msg.shape[1]} must be a positive multiple of 16 bytes")
+    _arg(msg_bits, "msg_bits", torch.int64, (B,), dev)
+    if out is not None:
+        _arg(out, "out", torch.uint8, (B, H, W), dev)
     ws = _ws(ws, method, B, H, W, tile_log2, encrypted.device)
     marked = out if out is not None else torch.empty_like(encrypted)
     st = torch.empty(B, dtype=torch.int32, device=encrypted.device)
@@ -151,7 +188,12 @@ def embed(method: int, encrypted: torch.Tensor, k2: torch.Tensor, msg: torch.Ten
 def extract(method: int, marked: torch.Tensor, k2: torch.Tensor, stride: int, ws: Workspace | None = None,
             tile_log2: int = 7, out: torch.Tensor | None = None):
     """Receiver with K2: returns (msg_bytes, msg_bits, status) -- mmsb_receiver_extract."""
-    B, H, W = marked.shape
+    B, H, W = _images(marked, "marked")
+    _arg(k2, "k2", torch.uint8, (B, 32), marked.device)
+    if stride <= 0 or stride % 16:
+        raise MmsbError(f"mmsb: stride {stride} must be a positive multiple of 16 bytes")
+    if out is not None:
+        _arg(out, "out", torch.uint8, (B, stride), marked.device)
     ws = _ws(ws, method, B, H, W, tile_log2, marked.device)
     msg = out if out is not None else torch.zeros(B, stride, dtype=torch.uint8, device=marked.device)
     nb = torch.empty(B, dtype=torch.int64, device=marked.device)
@@ -165,7 +207,10 @@ def extract(method: int, marked: torch.Tensor, k2: torch.Tensor, stride: int, ws
 def recover(method: int, marked: torch.Tensor, k1: torch.Tensor, ws: Workspace | None = None, tile_log2: int = 7,
             out: torch.Tensor | None = None):
     """Receiver with K1: returns (recovered, status) -- mmsb_receiver_recover."""
-    B, H, W = marked.shape
+    B, H, W = _images(marked, "marked")
+    _arg(k1, "k1", torch.uint8, (B, 32), marked.device)
+    if out is not None:
+        _arg(out, "out", torch.uint8, (B, H, W), marked.device)
     ws = _ws(ws, method, B, H, W, tile_log2, marked.device)
     rec = out if out is not None else torch.empty_like(marked)
     st = torch.empty(B, dtype=torch.int32, device=marked.device)
@@ -179,7 +224,15 @@ def receive_both(method: int, marked: torch.Tensor, k1: torch.Tensor, k2: torch.
                  ws: Workspace | None = None, tile_log2: int = 7, msg_out: torch.Tensor | None = None,
                  rec_out: torch.Tensor | None = None):
     """Receiver with both keys: returns (msg_bytes, msg_bits, recovered, status) -- mmsb_receiver_both."""
-    B, H, W = marked.shape
+    B, H, W = _images(marked, "marked")
+    _arg(k1, "k1", torch.uint8, (B, 32), marked.device)
+    _arg(k2, "k2", torch.uint8, (B, 32), marked.device)
+    if stride <= 0 or stride % 16:
+        raise MmsbError(f"mmsb: stride {stride} must be a positive multiple of 16 bytes")
+    if msg_out is not None:
+        _arg(msg_out, "msg_out", torch.uint8, (B, stride), marked.device)
+    if rec_out is not None:
+        _arg(rec_out, "rec_out", torch.uint8, (B, H, W), marked.device)
     ws = _ws(ws, method, B, H, W, tile_log2, marked.device)
     msg = msg_out if msg_out is not None else torch.zeros(B, stride, dtype=torch.uint8, device=marked.device)
     rec = rec_out if rec_out is not None else torch.empty_like(marked)
@@ -193,7 +246,7 @@ def receive_both(method: int, marked: torch.Tensor, k1: torch.Tensor, k2: torch.
 
 def capacity(method: int, image: torch.Tensor, ws: Workspace | None = None, tile_log2: int = 7):
     """Capacity of an encrypted / marked image: returns (b, capacity_bits, status) -- mmsb_capacity."""
-    B, H, W = image.shape
+    B, H, W = _images(image, "image")
     ws = _ws(ws, method, B, H, W, tile_log2, image.device)
     b = torch.empty(B, dtype=torch.int32, device=image.device)
     cap = torch.empty(B, dtype=torch.int64, device=image.device)
@@ -206,7 +259,10 @@ def capacity(method: int, image: torch.Tensor, ws: Workspace | None = None, tile
 
 def stats(original: torch.Tensor, recovered: torch.Tensor, out: torch.Tensor | None = None):
     """Per-image SSE (int64) -- mmsb_stats."""
-    B, H, W = original.shape
+    B, H, W = _images(original, "original")
+    _arg(recovered, "recovered", torch.uint8, (B, H, W), original.device)
+    if out is not None:
+        _arg(out, "out", torch.int64, (B,), original.device)
     sh = _shape(EMR, B, H, W)
     sse = out if out is not None else torch.empty(B, dtype=torch.int64, device=original.device)
     rc = lib().mmsb_stats(C.byref(sh), _ptr(original), _ptr(recovered), _ptr(sse), _stream())
@@ -229,7 +285,9 @@ def der_psnr(H: int, W: int, capacity_bits, sse):
 # ---------------------------------------------------------------- the paper's statistics (NEXT 2)
 def histogram(images: torch.Tensor, out: torch.Tensor | None = None):
     """[B, 256] int64 grey-level counts -- mmsb_histogram."""
-    B, H, W = images.shape
+    B, H, W = _images(images, "images")
+    if out is not None:
+        _arg(out, "out", torch.int64, (B, 256), images.device)
     h = out if out is not None else torch.empty(B, 256, dtype=torch.int64, device=images.device)
     _check(lib().mmsb_histogram(C.byref(_shape(EMR, B, H, W)), _ptr(images), _ptr(h), _stream()), "mmsb_histogram")
     return h
@@ -237,7 +295,8 @@ def histogram(images: torch.Tensor, out: torch.Tensor | None = None):
 
 def diff_stats(a: torch.Tensor, b: torch.Tensor):
     """(sse, ndiff, absdiff) int64 per image -- mmsb_diff_stats."""
-    B, H, W = a.shape
+    B, H, W = _images(a, "a")
+    _arg(b, "b", torch.uint8, (B, H, W), a.device)
     sse, nd, ad = (torch.empty(B, dtype=torch.int64, device=a.device) for _ in range(3))
     _check(lib().mmsb_diff_stats(C.byref(_shape(EMR, B, H, W)), _ptr(a), _ptr(b), _ptr(sse), _ptr(nd), _ptr(ad),
                                  _stream()), "mmsb_diff_stats")
@@ -246,7 +305,8 @@ def diff_stats(a: torch.Tensor, b: torch.Tensor):
 
 def ssim(a: torch.Tensor, b: torch.Tensor):
     """[B] float64 mean windowed SSIM -- mmsb_ssim."""
-    B, H, W = a.shape
+    B, H, W = _images(a, "a")
+    _arg(b, "b", torch.uint8, (B, H, W), a.device)
     out = torch.empty(B, dtype=torch.float64, device=a.device)
     _check(lib().mmsb_ssim(C.byref(_shape(EMR, B, H, W)), _ptr(a), _ptr(b), _ptr(out), _stream()), "mmsb_ssim")
     return out
