@@ -4,10 +4,17 @@
 One step = the whole hot path over one batch: content-owner encode (K1),
 hider embed (K2, full-capacity payload n = C - 32), receiver extract (K2), receiver recover
 (K1) and the per-image statistics (SSE -> DER/PSNR; all_gather of the per-image records
-over NCCL when N > 1).  Weak scaling: every rank processes its own batch of the workload.
+over NCCL when N > 1).  Weak scaling by default (every rank processes its own batch of the
+workload); --shard splits the config's batch across the ranks instead (strong scaling, the
+"10 000 images sharded across 1/2/4/8" of config 4).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--method emr|lmr]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--method emr|lmr] [--shard]
   python bench.py --impl reference ...     # the CPU oracle on the host cores
+
+--gpus N > 1 without a launcher re-executes itself under torch.distributed.run (one process per
+GPU, 127.0.0.1 rendezvous); under a launcher WORLD_SIZE must equal N.  With no --config and no
+--method the line is config 2 (EMR) and carries an "lmr" block: config 3 (LMR) measured in the
+same invocation with its own roofline, e2e, cpu_baseline and clocks.
 
 Prints ONE JSON line on rank 0 (contract in the task statement; fields explained in DESIGN.md §7).
 """
@@ -37,7 +44,11 @@ def parse():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=None, help="BASELINE.json config (default 2, plus 3 as the lmr block)")
+    ap.add_argument("--shard", action="store_true", help="strong scaling: split the config's batch over the ranks")
+    ap.add_argument("--no-lmr-block", action="store_true", help="default run without the config-3 LMR block")
+    ap.add_argument("--launcher-probe", action="store_true",
+                    help="test hook: exercise the launcher and the record gather (gloo on CPU) without the library")
     ap.add_argument("--method", default=None, choices=["emr", "lmr"])
     ap.add_argument("--batch", type=int, default=None, help="override the config's batch (testing only)")
     ap.add_argument("--e2e-steps", type=int, default=None)
@@ -53,22 +64,37 @@ def parse():
     return ap.parse_args()
 
 
-def workload(args):
+def workload(args, config=None, method=None):
     from paper_2302_07992_b200 import synth as S
 
-    cfg = S.CONFIGS[args.config]
-    method = args.method or ("lmr" if cfg["method"] == "lmr" else "emr")
+    config = config or args.config or 2
+    cfg = S.CONFIGS[config]
+    method = method or args.method or ("lmr" if cfg["method"] == "lmr" else "emr")
     B = args.batch or cfg["batch"]
-    return cfg, method, B
+    return config, cfg, method, B
 
 
-def config_json(args, cfg, method, B, world):
-    return {"workload": f"BASELINE.json configs[{args.config}]: {B} x {cfg['H']}x{cfg['W']} uint8 synthetic "
-                        f"1/f^alpha fields, {method.upper()}-RDHEI encode+embed+extract+recover+stats, "
+def rank_batch(B, rank, world, shard):
+    """(first image, images) of this rank: the whole batch per rank (weak scaling) or a contiguous
+    shard of it (strong scaling, parallel.shard)."""
+    if not shard:
+        return rank * B, B
+    from paper_2302_07992_b200 import parallel as P
+
+    return P.shard(B, rank, world)
+
+
+def config_json(args, config, cfg, method, B, world, shard=False):
+    per = -(-B // world) if shard else B
+    return {"workload": f"BASELINE.json configs[{config}]: {B * (1 if shard else world)} x {cfg['H']}x{cfg['W']} "
+                        f"uint8 synthetic 1/f^alpha fields, {method.upper()}-RDHEI encode+embed+extract+recover+stats, "
                         f"full-capacity payload",
-            "config_index": args.config, "method": method, "batch_per_gpu": B, "global_batch": B * world,
-            "height": cfg["H"], "width": cfg["W"], "parallelism": f"dp{world} (image shards, weak scaling)",
-            "l2": "inputs larger than L2 (batch bytes >> 126 MB); no flush needed" if B * cfg["H"] * cfg["W"] > 126e6
+            "config_index": config, "method": method, "batch_per_gpu": per,
+            "global_batch": B if shard else B * world,
+            "height": cfg["H"], "width": cfg["W"],
+            "parallelism": f"dp{world} (" + ("the batch sharded over the ranks, strong scaling)" if shard else
+                                              "image shards, weak scaling)"),
+            "l2": "inputs larger than L2 (batch bytes >> 126 MB); no flush needed" if per * cfg["H"] * cfg["W"] > 126e6
             else "inputs smaller than L2",
             "keys": "ChaCha20 K = k128||k128 per image (reading Q13)",
             "lmr_emin": (args.lmr_emin or 4) if method == "lmr" else None,
@@ -160,6 +186,40 @@ def oracle_throughput(method_id, imgs, k1, k2, msgs, seconds, cores, rounds=0):
     return done_px / dt / 1e6, n_img, dt
 
 
+def oracle_single_core(method_id, imgs, k1, k2, msgs, seconds, rounds=0):
+    """SURVEY §8(d) timing protocol (i): the oracle single-threaded in this process on a fixed
+    subset (whole images of the workload, in order, until `seconds` have passed), with the time of
+    each call -- encode (O7/O11), hide (O8/O12), extract (O9/O13), recover (O10/O14), SSE (O16)."""
+    import oracle as O
+
+    O.set_cipher_rounds(rounds or 20)
+    calls = {"encode": 0.0, "hide": 0.0, "extract": 0.0, "recover": 0.0, "sse": 0.0}
+    n = 0
+    t_all = time.perf_counter()
+    while n < len(imgs) and (n == 0 or time.perf_counter() - t_all < seconds):
+        img, a, b2, msg = imgs[n], k1[n].tobytes(), k2[n].tobytes(), msgs[n]
+        t0 = time.perf_counter()
+        st, E, b, C = O.encode(method_id, img, a)
+        t1 = time.perf_counter()
+        _, Em = O.hide(method_id, E, b2, msg, max(C - 32, 0))
+        t2 = time.perf_counter()
+        O.extract(method_id, Em, b2, len(msg))
+        t3 = time.perf_counter()
+        _, R = O.recover(method_id, Em, a)
+        t4 = time.perf_counter()
+        O.sse(img, R)
+        t5 = time.perf_counter()
+        for k, dt in zip(calls, (t1 - t0, t2 - t1, t3 - t2, t4 - t3, t5 - t4)):
+            calls[k] += dt
+        n += 1
+    tot = sum(calls.values())
+    return {"value": n * imgs[0].size / tot / 1e6, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "images": n, "seconds": tot,
+            "per_call_ms": {k: 1e3 * v / n for k, v in calls.items()},
+            "sample": f"the first {n} images of the workload, one after another in one thread "
+                      f"(SURVEY 8(d) protocol (i)); cpu: {cpu_model()}"}
+
+
 def cpu_cores():
     try:
         return len(os.sched_getaffinity(0))
@@ -177,6 +237,78 @@ def cpu_model():
     return "unknown"
 
 
+# ------------------------------------------------------------------------------ launcher
+def _free_port():
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def launcher_cmd(argv, n, port):
+    """The self-launch of --gpus N > 1: one process per GPU under torch.distributed.run."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+            "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *argv]
+
+
+def maybe_relaunch(args, argv):
+    """None when this process is (one rank of) the run; else the exit code of the relaunched run."""
+    world = os.environ.get("WORLD_SIZE")
+    if world is not None:
+        if int(world) != args.gpus:
+            raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+        return None
+    if args.gpus <= 1:
+        return None
+    import subprocess
+
+    return subprocess.call(launcher_cmd(argv, args.gpus, _free_port()))
+
+
+def init_dist(world, local, cpu=False):
+    import torch
+    import torch.distributed as dist
+
+    if world > 1 and not dist.is_initialized():
+        if cpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if int(os.environ.get("RANK", "0")) == 0:
+            print(f"bench.py: process group {dist.get_backend()} with {dist.get_world_size()} ranks",
+                  file=sys.stderr, flush=True)
+        assert dist.get_world_size() == world
+
+
+def run_launcher_probe(args):
+    """Test hook (CPU, gloo): the launcher, the shard split and the record all-gather of a real run,
+    with per-image records made on the host instead of by the library (no GPU needed)."""
+    import torch
+
+    from paper_2302_07992_b200 import parallel as P
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    init_dist(world, 0, cpu=True)
+    B = args.batch or 10
+    start, n = rank_batch(B, rank, world, args.shard)
+    counts = [rank_batch(B, r, world, args.shard)[1] for r in range(world)]
+    idx = torch.arange(start, start + n, dtype=torch.int64)
+    rec = P.make_records(2 + idx % 6, 1000 + 37 * idx, 3 * idx, torch.zeros_like(idx))
+    allrec = P.gather_records(rec, world, counts if args.shard else None)
+    rows = P.gather_rows(torch.stack([idx.double(), idx.double() ** 2], 1), world, counts if args.shard else None)
+    if rank == 0:
+        print(json.dumps({"probe": True, "n_gpus": world, "scaling": "strong" if args.shard else "weak",
+                          "shards": counts, "stats": P.aggregate(allrec, 512, 512),
+                          "row_means": rows.mean(0).tolist()}), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+    return 0
+
+
 # ------------------------------------------------------------------------------ reference arm
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
@@ -187,14 +319,14 @@ def run_reference(args):
     import oracle as O
 
     O.build()
-    cfg, method, B = workload(args)
+    config, cfg, method, B = workload(args)
     cores = cpu_cores()
     mid = O.EMR if method == "emr" else O.LMR
     H, W = cfg["H"], cfg["W"]
     nsamp = min(B, max(cores, 8))
-    imgs, k1, k2 = S.batch(args.config, n=nsamp)
+    imgs, k1, k2 = S.batch(config, n=nsamp)
     stride = S.msg_stride(H, W)
-    msgs = [S.payload(S.image_seed(args.config, j), stride) for j in range(nsamp)]
+    msgs = [S.payload(S.image_seed(config, j), stride) for j in range(nsamp)]
     # each step: one pass of `cores` images (one per worker); the run is bounded to a few minutes
     per_step = max(0.5, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
     vals = []
@@ -207,8 +339,8 @@ def run_reference(args):
     ms = 1e3 * sum(dt for _, _, dt in vals) / len(vals)
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-            "config": config_json(args, cfg, method, B, world),
+            "scaling": "strong" if args.shard else "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": config_json(args, config, cfg, method, B, world, args.shard),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
                              "sample": f"each step: >= {per_step:.1f} s of whole images of the workload "
                                        f"({nsamp} distinct) through encode+embed+extract+recover+SSE, one image "
@@ -226,27 +358,51 @@ def run_ours(args):
 
     from paper_2302_07992_b200 import build as BLD
     from paper_2302_07992_b200 import mmsb as G
-    from paper_2302_07992_b200 import parallel as P
-    from paper_2302_07992_b200 import synth as S
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    init_dist(world, local)
     if rank == 0 and not os.path.exists(BLD.LIB):
         BLD.build()
     if world > 1:
         dist.barrier()
     G.lib()
 
-    cfg, method, B = workload(args)
+    line = measure(args, rank, world, local)
+    if args.config is None and args.method is None and not args.no_lmr_block:
+        torch.cuda.empty_cache()
+        lmr = measure(args, rank, world, local, config=3, method="lmr")
+        if rank == 0:
+            line["lmr"] = {k: lmr[k] for k in ("metric", "value", "unit", "ms_per_step", "scaling", "dtype", "config",
+                                               "gpu_launches", "clocks", "e2e", "roofline", "step_hbm", "kernels",
+                                               "checks", "mean_der_bpp", "stats", "security", "cpu_baseline")
+                           if k in lmr}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def measure(args, rank, world, local, config=None, method=None):
+    """One workload (config, method) measured as the bench contract says; returns rank 0's line."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2302_07992_b200 import mmsb as G
+    from paper_2302_07992_b200 import parallel as P
+    from paper_2302_07992_b200 import synth as S
+
+    config, cfg, method, B_cfg = workload(args, config, method)
+    start, B = rank_batch(B_cfg, rank, world, args.shard)
+    counts = [rank_batch(B_cfg, r, world, args.shard)[1] for r in range(world)] if args.shard else None
     H, W = cfg["H"], cfg["W"]
     mid = G.EMR if method == "emr" else G.LMR
     HW = H * W
     t_gen = time.perf_counter()
-    imgs, k1, k2 = S.batch(args.config, n=B, start=rank * B)
+    imgs, k1, k2 = S.batch(config, n=B, start=start)
     gen_s = time.perf_counter() - t_gen
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
@@ -262,36 +418,32 @@ def run_ours(args):
     cap = cap0.cpu().numpy()
     nbits_np = np.maximum(cap - 32, 0).astype(np.int64)
     stride = int(max(16, ((int(nbits_np.max()) + 7) // 8 + 4 + 15) // 16 * 16))
-    msgs = np.stack([S.payload(S.image_seed(args.config, rank * B + j), stride) for j in range(B)])
+    msgs = np.stack([S.payload(S.image_seed(config, start + j), stride) for j in range(B)])
     MSG = torch.from_numpy(msgs).to(dev)
     NB = torch.from_numpy(nbits_np).to(dev)
     MOUT = torch.zeros(B, stride, dtype=torch.uint8, device=dev)
     SSE = torch.empty(B, dtype=torch.int64, device=dev)
     records = torch.empty(B, P.REC_COLS, dtype=torch.int64, device=dev)
     gathered = [records]
+    last = [None, None, None, None, None]
 
     def step(I_, K1_, K2_, MSG_, NB_):
-        _, b, c, _ = G.encode(mid, I_, K1_, ws, out=enc)
-        G.embed(mid, enc, K2_, MSG_, NB_, ws, out=marked)
+        _, b, c, st_e = G.encode(mid, I_, K1_, ws, out=enc)
+        _, st_h = G.embed(mid, enc, K2_, MSG_, NB_, ws, out=marked)
         _, nb_out, st_x = G.extract(mid, marked, K2_, stride, ws, out=MOUT)
         _, st_r = G.recover(mid, marked, K1_, ws, out=rec)
         G.stats(I_, rec, out=SSE)
-        last[:] = [b, c, st_r]
+        last[:] = [b, c, st_r, st_x, nb_out, st_e, st_h]
         if world > 1:   # the path's one exchange: per-image records to every rank (NCCL)
             records.copy_(P.make_records(b, c, SSE, st_r))
-            gathered[0] = P.gather_records(records, world)
+            gathered[0] = P.gather_records(records, world, counts)
         return b, c
 
-    last = [None, None, None]
-
     # warm-up
-    for _ in range(args.warmup):
+    for _ in range(max(1, args.warmup)):
         step(I, K1, K2, MSG, NB)
     torch.cuda.synchronize()
-    # correctness guard on the timed configuration: payload round trip + statuses
-    assert bool((MOUT[:, :1].shape[0] == B)), "shape"
-    nb_chk = G.extract(mid, marked, K2, stride, ws, out=MOUT)[1]
-    ok_rt = bool(torch.equal(nb_chk, NB))
+    checks = result_checks(mid, G, I, MSG, NB, MOUT, rec, last)
 
     # ---- timed region (device-resident inputs)
     launches0 = G.kernel_launches()
@@ -314,190 +466,244 @@ def run_ours(args):
     prof = read_profile(G)
     G.lib().mmsb_profile_enable(0)
     ms_max = P.max_over_ranks(ms, dev, world)
-    px_total = world * B * HW * args.steps
+    px_total = (B_cfg if args.shard else world * B) * HW * args.steps
     value = px_total / (ms_max / 1e3) / 1e6
 
-    e2e_value, ok_e2e, e2e_steps, h2d, d2h, t_issue, nsub, sub, streaming, nlanes = None, True, 0, 0, 0, 0.0, 0, 0, False, 0
+    e2e = {"skipped": "--no-e2e (profiling runs only)"}
     if not args.no_e2e:
-        # ---- e2e: host (pinned) buffers through the ABI, copies inside the timed region.  Lanes (each
-        # a stream with its own device buffers and workspace) take the (sub-)batches in turn, and the
-        # device->host copies run on a stream of their own, so that one step's host->device copy,
-        # another's calls and a third's device->host copy overlap (PCIe bound).
-        e2e_steps = args.e2e_steps or 20
-        hI = torch.from_numpy(imgs).pin_memory()
-        hK1, hK2 = torch.from_numpy(k1).pin_memory(), torch.from_numpy(k2).pin_memory()
-        hMSG, hNB = torch.from_numpy(msgs).pin_memory(), torch.from_numpy(nbits_np).pin_memory()
-        hREC = torch.empty_like(hI).pin_memory()
-        hMOUT = torch.empty(B, stride, dtype=torch.uint8).pin_memory()
-        hSSE = torch.empty(B, dtype=torch.int64).pin_memory()
-        h2d = hI.numel() + hK1.numel() + hK2.numel() + hMSG.numel() + hNB.numel() * 8
-        d2h = hREC.numel() + hMOUT.numel() + hSSE.numel() * 8
-        # the whole batch per lane, two lanes taking turns across steps, measured best (EMR 25.3 / LMR
-        # 24.0 Gpx/s at configs 2 / 3, against 25.0 / 23.2 with two sub-batches and 23 / 13 with eight
-        # over three): one step's calls overlap the neighbouring steps' copies, the copies are large and
-        # the LMR coder rounds stay full
-        nsub = next(k for k in (args.e2e_chunks, 1) if k and B % k == 0)
-        sub = B // nsub
+        e2e = measure_e2e(args, G, P, dev, stream, world, mid, B, H, W, stride, imgs, k1, k2, msgs, nbits_np, rec, SSE,
+                          records, gathered, counts, B_cfg)
 
-        class Lane:
-            def __init__(self):
-                self.stream = torch.cuda.Stream(device=dev)
-                self.ws = G.Workspace(mid, sub, H, W, device=dev, lmr_emin=args.lmr_emin, cipher_rounds=args.cipher_rounds)
-                self.I = torch.empty(sub, H, W, dtype=torch.uint8, device=dev)
-                self.K1 = torch.empty(sub, 32, dtype=torch.uint8, device=dev)
-                self.K2 = torch.empty(sub, 32, dtype=torch.uint8, device=dev)
-                self.MSG = torch.empty(sub, stride, dtype=torch.uint8, device=dev)
-                self.NB = torch.empty(sub, dtype=torch.int64, device=dev)
-                self.enc, self.marked, self.rec = (torch.empty_like(self.I) for _ in range(3))
-                self.MOUT = torch.zeros(sub, stride, dtype=torch.uint8, device=dev)
-                self.SSE = torch.empty(sub, dtype=torch.int64, device=dev)
-                self.done = torch.cuda.Event()
-                self.computed = torch.cuda.Event()
-                self.copied = None                    # last device->host copy of this lane's outputs
+    security = security_stats(G, P, I, enc, marked, rec, H, W, world, counts) if not args.no_security else None
 
-        lanes = [Lane() for _ in range(args.e2e_lanes)]
-        d2h_stream = torch.cuda.Stream(device=dev)   # device->host copies, off the lanes' streams
-
-        # one process: the lanes stream sub-batches back to back across steps (a lane reuses its
-        # buffers in its own stream order), so the copy engines do not drain at every step boundary;
-        # with several ranks each step ends with the records all-gather, so lanes join per step
-        streaming = world == 1
-
-        turn = [0]                              # lanes take sub-batches in rotation, across steps too
-
-        def e2e_step():
-            start = torch.cuda.Event()
-            start.record(stream)
-            for i in range(nsub):
-                L = lanes[turn[0] % len(lanes)]
-                turn[0] += 1
-                a, z = i * sub, (i + 1) * sub
-                if not streaming:
-                    L.stream.wait_event(start)
-                with torch.cuda.stream(L.stream):
-                    L.I.copy_(hI[a:z], non_blocking=True)
-                    L.K1.copy_(hK1[a:z], non_blocking=True)
-                    L.K2.copy_(hK2[a:z], non_blocking=True)
-                    L.MSG.copy_(hMSG[a:z], non_blocking=True)
-                    L.NB.copy_(hNB[a:z], non_blocking=True)
-                    if L.copied is not None:
-                        L.stream.wait_event(L.copied)    # the previous outputs of this lane are out
-                    _, b_, c_, _ = G.encode(mid, L.I, L.K1, L.ws, out=L.enc)
-                    G.embed(mid, L.enc, L.K2, L.MSG, L.NB, L.ws, out=L.marked)
-                    G.extract(mid, L.marked, L.K2, stride, L.ws, out=L.MOUT)
-                    _, st_ = G.recover(mid, L.marked, L.K1, L.ws, out=L.rec)
-                    G.stats(L.I, L.rec, out=L.SSE)
-                    if world > 1:
-                        records[a:z] = P.make_records(b_, c_, L.SSE, st_)
-                    L.computed.record(L.stream)
-                # the copy out on its own stream: the lane's next host->device copy need not wait for it
-                d2h_stream.wait_event(L.computed)
-                with torch.cuda.stream(d2h_stream):
-                    hREC[a:z].copy_(L.rec, non_blocking=True)
-                    hMOUT[a:z].copy_(L.MOUT, non_blocking=True)
-                    hSSE[a:z].copy_(L.SSE, non_blocking=True)
-                    L.copied = torch.cuda.Event()
-                    L.copied.record(d2h_stream)
-                    L.done.record(d2h_stream)
-            if not streaming:
-                e2e_join()
-            if world > 1:
-                gathered[0] = P.gather_records(records, world)
-
-        def e2e_join():
-            for L in lanes:
-                L.done.record(L.stream)
-                stream.wait_event(L.done)
-            ev = torch.cuda.Event()
-            ev.record(d2h_stream)
-            stream.wait_event(ev)
-
-        e2e_step()
-        e2e_join()
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        f0.record(stream)
-        for L in lanes:                         # the lanes start after f0
-            L.stream.wait_event(f0)
-        t_issue = time.perf_counter()
-        for _ in range(e2e_steps):
-            e2e_step()
-        t_issue = (time.perf_counter() - t_issue) * 1e3 / e2e_steps    # host time to issue one step
-        e2e_join()
-        f1.record(stream)
-        torch.cuda.synchronize()
-        te_ms = P.max_over_ranks(f0.elapsed_time(f1), dev, world)
-        e2e_value = world * B * HW * e2e_steps / (te_ms / 1e3) / 1e6
-        ok_e2e = bool(np.array_equal(hREC.numpy(), rec.cpu().numpy())) and bool(
-            np.array_equal(hSSE.numpy(), SSE.cpu().numpy()))
-
-    # the paper's security / quality table (Tab. analysis, Tab. EMR_results) on
-    # this rank's batch, outside the timed region: entropy / chi^2 of I, I_e, I_e'; NPCR / UACI and
-    # PSNR of I vs I_e and I vs I_e'; SSIM of I vs I' (all through the library's statistics calls)
-    security = None
-    if rank == 0 and not args.no_security:
-        def _mean(x):
-            return float(np.mean(x))
-
-        sec = {}
-        for name, X in (("I", I), ("I_e", enc), ("I_e_marked", marked)):
-            ent, chi = G.entropy_chi2(H, W, G.histogram(X).cpu().numpy())
-            sec[f"entropy_{name}"] = _mean(ent)
-            sec[f"chi2_{name}"] = _mean(chi)
-        for name, X in (("I_e", enc), ("I_e_marked", marked)):
-            sse_, nd, ad = (t.cpu().numpy() for t in G.diff_stats(I, X))
-            npcr, uaci = G.npcr_uaci(H, W, nd, ad)
-            _, psnr = G.der_psnr(H, W, np.zeros_like(sse_), sse_)
-            sec[f"npcr_I_vs_{name}"], sec[f"uaci_I_vs_{name}"] = _mean(npcr), _mean(uaci)
-            sec[f"psnr_I_vs_{name}"] = _mean(psnr)
-        ss = G.ssim(I, rec).cpu().numpy()
-        sec["ssim_I_vs_recovered_mean"], sec["ssim_I_vs_recovered_min"] = _mean(ss), float(ss.min())
-        sec["note"] = "means over this rank's batch; synthetic images (the paper's Lena / BOWS-2 are not available)"
-        security = sec
-
+    line = None
     if rank == 0:
         peaks = load_peaks()
         roof = roofline(prof, peaks, B, HW, cap, method)
+        recs = gathered[0] if world > 1 else P.make_records(last[0], last[1], SSE, last[2])
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-                "config": config_json(args, cfg, method, B, world),
+                "scaling": "strong" if args.shard else "weak", "vs_baseline": None, "dtype": "u8",
+                "data": "synthetic", "config": config_json(args, config, cfg, method, B_cfg, world, args.shard),
                 "gpu_launches": int(launches),
                 "clocks": sampler.record(),
-                "e2e": {"skipped": "--no-e2e (profiling runs only)"} if args.no_e2e else
-                       {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d * world),
-                        "d2h_bytes_per_step": int(d2h * world), "steps": e2e_steps,
-                        "path": f"pinned host -> cudaMemcpyAsync -> C ABI calls -> host; {nsub} sub-batch(es) "
-                                f"of {sub} images per step, {len(lanes)} lanes (streams + buffers) taking them in turn, "
-                                f"device->host copies on their own stream"
-                                + (", streamed across steps (no drain at step boundaries)" if streaming else ""),
-                        "host_issue_ms_per_step": t_issue,
-                        "pcie_note": "both directions at once measured at 49.4 GB/s each on this box "
-                                     "(tools/pcie_probe.py): the e2e ceiling is bytes per step / 49.4 GB/s; the "
-                                     "same copy pipeline without the calls moves 43-45 GB/s (tools/e2e_probe.py)"},
+                "e2e": e2e,
                 "roofline": roof["dominant"],
-                "step_hbm": step_hbm(roof["kernels"], value, float(cap.mean() / HW), load_peaks()),
+                "step_hbm": step_hbm(roof["kernels"], value / world, float(cap.mean() / HW), peaks),
                 "kernels": roof["kernels"],
-                "checks": {"payload_round_trip": ok_rt, "e2e_matches_device": ok_e2e,
-                           "statuses_ok": bool((st0 == 0).all().item())},
+                "checks": checks,
                 "mean_der_bpp": float(cap.mean() / HW), "gen_s": gen_s,
-                "stats": P.aggregate(gathered[0] if world > 1 else P.make_records(last[0], last[1], SSE, last[2]), H, W),
+                "stats": P.aggregate(recs, H, W),
                 "security": security}
         if world == 1 and not args.no_cpu_baseline:
             import oracle as O
 
             cores = cpu_cores()
-            v, n_img, dt = oracle_throughput(O.EMR if method == "emr" else O.LMR, imgs[:64], k1[:64], k2[:64],
-                                             msgs[:64], args.cpu_seconds, cores, args.cipher_rounds)
+            oid = O.EMR if method == "emr" else O.LMR
+            v, n_img, dt = oracle_throughput(oid, imgs[:64], k1[:64], k2[:64], msgs[:64], args.cpu_seconds, cores,
+                                             args.cipher_rounds)
             line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
                                     "sample": f"{n_img} images of this workload ({dt:.1f} s) through encode+embed+"
-                                              f"extract+recover+SSE, one image per worker process; cpu: {cpu_model()}"}
-        print(json.dumps(line), flush=True)
+                                              f"extract+recover+SSE, one image per worker process; cpu: {cpu_model()}",
+                                    "single_core": oracle_single_core(oid, imgs[:16], k1[:16], k2[:16], msgs[:16],
+                                                                      min(10.0, args.cpu_seconds), args.cipher_rounds)}
+    del ws, I, enc, marked, rec, MSG, MOUT
+    return line
+
+
+def result_checks(mid, G, I, MSG, NB, MOUT, rec, last):
+    """What the timed configuration produced: every status of the four calls, the
+    extracted bit counts and payload bits of every image against the embedded ones, and the
+    recovery property of the method (LMR: I' = I; EMR: bits 1..7 of I' = I)."""
+    import torch
+
+    b, c, st_r, st_x, nb_out, st_e, st_h = last
+    B, stride = MOUT.shape
+    col = torch.arange(stride, device=MOUT.device)[None, :]
+    nb = NB[:, None]
+    diff = MOUT ^ MSG
+    full_ok = int((diff * (col < nb // 8).to(torch.uint8)).sum()) == 0
+    lastb = diff.gather(1, (NB // 8).clamp(max=stride - 1)[:, None]).squeeze(1).to(torch.int64)
+    pmask = torch.bitwise_right_shift(torch.full_like(NB, 0xFF00), NB % 8) & 0xFF
+    part_ok = int((lastb & pmask)[NB % 8 != 0].sum()) == 0
+    out = {"statuses_ok": {k: bool((s == 0).all()) for k, s in
+                           (("encode", st_e), ("embed", st_h), ("extract", st_x), ("recover", st_r))},
+           "extracted_bits_equal_embedded": bool(torch.equal(nb_out, NB)),
+           "payload_round_trip": bool(full_ok and part_ok)}
+    if mid == G.LMR:
+        out["recovered_equals_original"] = bool(torch.equal(rec, I))
+    else:
+        out["recovered_bits_1_to_7_equal_original"] = bool(torch.equal(rec >> 1, I >> 1))
+    return out
+
+
+def measure_e2e(args, G, P, dev, stream, world, mid, B, H, W, stride, imgs, k1, k2, msgs, nbits_np, rec, SSE,
+                records, gathered, counts, B_cfg):
+    """e2e: host (pinned) buffers through the ABI, copies inside the timed region.  Lanes (each a
+    stream with its own device buffers and workspace) take the (sub-)batches in turn, and the
+    device->host copies run on a stream of their own, so that one step's host->device copy,
+    another's calls and a third's device->host copy overlap (PCIe bound)."""
+    import torch
+    import torch.distributed as dist
+
+    HW = H * W
+    e2e_steps = args.e2e_steps or 20
+    hI = torch.from_numpy(imgs).pin_memory()
+    hK1, hK2 = torch.from_numpy(k1).pin_memory(), torch.from_numpy(k2).pin_memory()
+    hMSG, hNB = torch.from_numpy(msgs).pin_memory(), torch.from_numpy(nbits_np).pin_memory()
+    hREC = torch.empty_like(hI).pin_memory()
+    hMOUT = torch.empty(B, stride, dtype=torch.uint8).pin_memory()
+    hSSE = torch.empty(B, dtype=torch.int64).pin_memory()
+    h2d = hI.numel() + hK1.numel() + hK2.numel() + hMSG.numel() + hNB.numel() * 8
+    d2h = hREC.numel() + hMOUT.numel() + hSSE.numel() * 8
+    # the whole batch per lane, two lanes taking turns across steps, measured best (EMR 25.3 / LMR
+    # 24.0 Gpx/s at configs 2 / 3, against 25.0 / 23.2 with two sub-batches and 23 / 13 with eight
+    # over three): one step's calls overlap the neighbouring steps' copies, the copies are large and
+    # the LMR coder rounds stay full
+    nsub = next(k for k in (args.e2e_chunks, 1) if k and B % k == 0)
+    sub = B // nsub
+
+    class Lane:
+        def __init__(self):
+            self.stream = torch.cuda.Stream(device=dev)
+            self.ws = G.Workspace(mid, sub, H, W, device=dev, lmr_emin=args.lmr_emin, cipher_rounds=args.cipher_rounds)
+            self.I = torch.empty(sub, H, W, dtype=torch.uint8, device=dev)
+            self.K1 = torch.empty(sub, 32, dtype=torch.uint8, device=dev)
+            self.K2 = torch.empty(sub, 32, dtype=torch.uint8, device=dev)
+            self.MSG = torch.empty(sub, stride, dtype=torch.uint8, device=dev)
+            self.NB = torch.empty(sub, dtype=torch.int64, device=dev)
+            self.enc, self.marked, self.rec = (torch.empty_like(self.I) for _ in range(3))
+            self.MOUT = torch.zeros(sub, stride, dtype=torch.uint8, device=dev)
+            self.SSE = torch.empty(sub, dtype=torch.int64, device=dev)
+            self.done = torch.cuda.Event()
+            self.computed = torch.cuda.Event()
+            self.copied = None                    # last device->host copy of this lane's outputs
+
+    lanes = [Lane() for _ in range(args.e2e_lanes)]
+    d2h_stream = torch.cuda.Stream(device=dev)   # device->host copies, off the lanes' streams
+    # one process: the lanes stream sub-batches back to back across steps (a lane reuses its
+    # buffers in its own stream order), so the copy engines do not drain at every step boundary;
+    # with several ranks each step ends with the records all-gather, so lanes join per step
+    streaming = world == 1
+    turn = [0]                              # lanes take sub-batches in rotation, across steps too
+
+    def e2e_join():
+        for L in lanes:
+            L.done.record(L.stream)
+            stream.wait_event(L.done)
+        ev = torch.cuda.Event()
+        ev.record(d2h_stream)
+        stream.wait_event(ev)
+
+    def e2e_step():
+        start = torch.cuda.Event()
+        start.record(stream)
+        for i in range(nsub):
+            L = lanes[turn[0] % len(lanes)]
+            turn[0] += 1
+            a, z = i * sub, (i + 1) * sub
+            if not streaming:
+                L.stream.wait_event(start)
+            with torch.cuda.stream(L.stream):
+                L.I.copy_(hI[a:z], non_blocking=True)
+                L.K1.copy_(hK1[a:z], non_blocking=True)
+                L.K2.copy_(hK2[a:z], non_blocking=True)
+                L.MSG.copy_(hMSG[a:z], non_blocking=True)
+                L.NB.copy_(hNB[a:z], non_blocking=True)
+                if L.copied is not None:
+                    L.stream.wait_event(L.copied)    # the previous outputs of this lane are out
+                _, b_, c_, _ = G.encode(mid, L.I, L.K1, L.ws, out=L.enc)
+                G.embed(mid, L.enc, L.K2, L.MSG, L.NB, L.ws, out=L.marked)
+                G.extract(mid, L.marked, L.K2, stride, L.ws, out=L.MOUT)
+                _, st_ = G.recover(mid, L.marked, L.K1, L.ws, out=L.rec)
+                G.stats(L.I, L.rec, out=L.SSE)
+                if world > 1:
+                    records[a:z] = P.make_records(b_, c_, L.SSE, st_)
+                L.computed.record(L.stream)
+            # the copy out on its own stream: the lane's next host->device copy need not wait for it
+            d2h_stream.wait_event(L.computed)
+            with torch.cuda.stream(d2h_stream):
+                hREC[a:z].copy_(L.rec, non_blocking=True)
+                hMOUT[a:z].copy_(L.MOUT, non_blocking=True)
+                hSSE[a:z].copy_(L.SSE, non_blocking=True)
+                L.copied = torch.cuda.Event()
+                L.copied.record(d2h_stream)
+                L.done.record(d2h_stream)
+        if not streaming:
+            e2e_join()
+        if world > 1:
+            gathered[0] = P.gather_records(records, world, counts)
+
+    e2e_step()
+    e2e_join()
+    torch.cuda.synchronize()
     if world > 1:
-        dist.destroy_process_group()
-    return 0
+        dist.barrier()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for L in lanes:                         # the lanes start after f0
+        L.stream.wait_event(f0)
+    t_issue = time.perf_counter()
+    for _ in range(e2e_steps):
+        e2e_step()
+    t_issue = (time.perf_counter() - t_issue) * 1e3 / e2e_steps    # host time to issue one step
+    e2e_join()
+    f1.record(stream)
+    torch.cuda.synchronize()
+    te_ms = P.max_over_ranks(f0.elapsed_time(f1), dev, world)
+    px = (B_cfg if args.shard else world * B) * HW * e2e_steps
+    e2e_value = px / (te_ms / 1e3) / 1e6
+    ok_e2e = bool(np.array_equal(hREC.numpy(), rec.cpu().numpy())) and bool(
+        np.array_equal(hSSE.numpy(), SSE.cpu().numpy()))
+    scale = 1 if args.shard else world
+    tot_h2d = int(h2d * scale) if not args.shard else int(h2d * B_cfg / B)
+    tot_d2h = int(d2h * scale) if not args.shard else int(d2h * B_cfg / B)
+    out = {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": tot_h2d, "d2h_bytes_per_step": tot_d2h,
+           "steps": e2e_steps, "matches_device": ok_e2e,
+           "path": f"pinned host -> cudaMemcpyAsync -> C ABI calls -> host; {nsub} sub-batch(es) "
+                   f"of {sub} images per step, {len(lanes)} lanes (streams + buffers) taking them in turn, "
+                   f"device->host copies on their own stream"
+                   + (", streamed across steps (no drain at step boundaries)" if streaming else ""),
+           "host_issue_ms_per_step": t_issue,
+           "pcie_note": "both directions at once measured at 49.4 GB/s each on this box "
+                        "(tools/pcie_probe.py): the e2e ceiling is bytes per step / 49.4 GB/s; the "
+                        "same copy pipeline without the calls moves 43-45 GB/s (tools/e2e_probe.py)"}
+    del lanes
+    return out
+
+
+def security_stats(G, P, I, enc, marked, rec, H, W, world, counts):
+    """The paper's security / quality table (Tab. analysis, Tab. EMR_results)
+    outside the timed region: per image entropy / chi^2 of I, I_e, I_e'; NPCR / UACI and PSNR of
+    I vs I_e and I vs I_e'; SSIM of I vs I' -- all through the library's statistics calls, then
+    the per-image rows of every rank gathered (NCCL all_gather) and averaged
+    over the whole job's images on rank 0."""
+    import torch
+
+    cols, names = [], []
+    for name, X in (("I", I), ("I_e", enc), ("I_e_marked", marked)):
+        ent, chi = G.entropy_chi2(H, W, G.histogram(X).cpu().numpy())
+        cols += [ent, chi]
+        names += [f"entropy_{name}", f"chi2_{name}"]
+    for name, X in (("I_e", enc), ("I_e_marked", marked)):
+        sse_, nd, ad = (t.cpu().numpy() for t in G.diff_stats(I, X))
+        npcr, uaci = G.npcr_uaci(H, W, nd, ad)
+        _, psnr = G.der_psnr(H, W, np.zeros_like(sse_), sse_)
+        cols += [npcr, uaci, psnr]
+        names += [f"npcr_I_vs_{name}", f"uaci_I_vs_{name}", f"psnr_I_vs_{name}"]
+    ss = G.ssim(I, rec).cpu().numpy()
+    cols.append(ss)
+    names.append("ssim_I_vs_recovered")
+    rows = torch.from_numpy(np.stack(cols, 1).astype(np.float64)).to(I.device)
+    allrows = P.gather_rows(rows, world, counts).cpu().numpy()
+    sec = {}
+    for j, n in enumerate(names):
+        sec[n if n != "ssim_I_vs_recovered" else "ssim_I_vs_recovered_mean"] = float(np.mean(allrows[:, j]))
+    sec["ssim_I_vs_recovered_min"] = float(allrows[:, -1].min())
+    sec["images"] = int(allrows.shape[0])
+    sec["note"] = ("means over every rank's images (per-image rows all-gathered); synthetic images "
+                   "(the paper's Lena / BOWS-2 are not available)")
+    return sec
 
 
 def read_profile(G):
@@ -573,15 +779,21 @@ def load_traffic():
 
 
 def step_hbm(kern, mpx_s, der, peaks):
-    """The metric's "% HBM roofline" for the whole step and for the three receiver-side calls
-    (embed + extract + recover): algorithmic bytes per pixel (encode 2, embed
-    2 + d/8, extract 1 + d/8, recover 2, statistics 2) x pixels/s over the measured HBM peak;
-    the three calls' pixel rate from their share of the measured kernel time."""
+    """The metric's "% HBM roofline" per GPU (mpx_s = this GPU's pixel rate).  SURVEY §8(d):
+    algorithmic bytes per pixel encode 2, embed 2 + d/8, extract 1 + d/8, recover 2 -> 7 + d/4
+    for the four calls; the timed step also runs the statistics call (SSE, 2 B/px: read I and
+    I'), so the step's own total is 9 + d/4 (both reported).  The three receiver-side calls
+    (embed + extract + recover, 5 + d/4) get their pixel rate from their share of the kernel time."""
     hbm = float(peaks.get("hbm_gbs", 6650.0))
     d8 = der / 8.0
-    step_b = 2.0 + (2.0 + d8) + (1.0 + d8) + 2.0 + 2.0
-    out = {"bytes_per_px": step_b, "achieved_GBps": step_b * mpx_s * 1e6 / 1e9, "peak": hbm}
+    four = 7.0 + 2 * d8
+    step_b = four + 2.0
+    out = {"bytes_per_px": step_b, "bytes_per_px_note": "4 calls 7 + d/4 (SURVEY 8(d)) + statistics 2",
+           "achieved_GBps": step_b * mpx_s * 1e6 / 1e9, "peak": hbm}
     out["frac"] = out["achieved_GBps"] / hbm
+    out["four_calls"] = {"bytes_per_px": four, "achieved_GBps": four * mpx_s * 1e6 / 1e9,
+                         "frac": four * mpx_s * 1e6 / 1e9 / hbm,
+                         "note": "the same step's pixel rate against the four calls' bytes only"}
     three = [k for k in kern if "embed" in k or "extract" in k or "decode" in k or k.startswith("recover")]
     t_all = sum(kern[k]["ms_total"] for k in kern)
     t3 = sum(kern[k]["ms_total"] for k in three)
@@ -652,6 +864,11 @@ def roofline(prof, peaks, B, HW, cap, method):
 
 def main():
     args = parse()
+    rc = maybe_relaunch(args, sys.argv[1:])
+    if rc is not None:
+        return rc
+    if args.launcher_probe:
+        return run_launcher_probe(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

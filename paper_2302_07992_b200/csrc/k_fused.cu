@@ -4,20 +4,27 @@
 //
 // Each launch mixes two CTA roles, scheduled by blockIdx in image groups:
 //   K (keystream) CTAs  -- a4: ChaCha20(K1) for TPC tiles (one 64-byte block per tile row,
-//       P:656, Q12), the tile's in-tile angle record (levels 1..tp, eq. roration),
-//       the tile total into the upper angle pyramid, and (encode) the per-image label
-//       histogram (eq. gliding1/2 P:604-625 reduce to the left neighbour).  The
-//       keystream goes to a tile-major scratch that only one consumer reads.
-//   W (worker) CTAs -- one per tile, after the image's K CTAs have signalled:
-//       encode (perm_role): a3 + a5, destination tile <- permuted source tile (+ left halo),
-//       location map into the LSB (EMR) or label plane for the coder (LMR), XOR s.
-//       recover (rec_role): a10, original tile <- de-permuted destination tile, decrypted,
-//       rows copied forward with the carry from the tile to the left found by a per-row
-//       decoupled look-back (the copy-forward of P:837 / P:1061 is a scan along each row).
+//       P:656, Q12), the tile's in-tile angles (levels 1..tp, eq. roration) turned into
+//       a worker record (group table + cell table), the tile total into the upper angle pyramid,
+//       and a copy of the call's input tile.  Encode also derives, per pixel, the thermometer code
+//       of p ^ left (EMR; its bit 8-b is the location map l = [c < b]) or the label c | eta
+//       (LMR), and the per-image label histogram (eq. gliding1/2 P:604-625 reduce to the left
+//       neighbour).  The scratch planes are tile blocks (TileBlock).
+//   W (worker) CTAs -- one per strip of tiles, after the image's K CTAs have signalled.  One thread
+//       per 4x4 cell; the tiles of the strip stream through a 3-stage shared-memory ring filled by
+//       bulk copies (one elected thread, mbarrier transaction counts; consumers release a stage
+//       per warp).
+//       encode (perm_role): a3 + a5, destination cell <- rotated source cell, location map into
+//       the LSB (EMR) or label plane for the coder (LMR), XOR s.
+//       recover (rec_role): a10, original cell <- de-rotated destination cell, decrypted; the
+//       copy-forward of P:837 / P:1061 is a scan along each row: per cell row a summary byte,
+//       a shuffle scan across the tile row, the carry passed from tile to tile.
 // Grid order: K(0) | K(1) W(0) | K(2) W(1) | ... | W(n-1): the keystream of group g+1 runs
 // while group g is permuted; a W CTA only ever waits for K CTAs dispatched before it.
-// The consumed keystream tile and angle record are dropped from L2 (discard.global.L2),
-// so the scratch never costs HBM bandwidth.
+// The consumed scratch lines are dropped from L2 (discard.global.L2), so the scratch never
+// costs HBM bandwidth.
+#include <cstdlib>
+
 #include "mmsb_device.cuh"
 #include "mmsb_kernels.h"
 
@@ -44,6 +51,23 @@ __device__ __forceinline__ Role role_of(const FusedSched &sc) {
     }
     return r;
 }
+
+// Scratch block of a tile: three T x T planes (keystream | input image | label), each row-major
+// with the rows of odd cell rows swapped in pairs (row r at position r ^ ((r >> 2) & 1)).  A
+// keystream CTA thread writes its tile row as 16-byte stores; a worker thread reads the four rows
+// of a 4x4 cell as 4-byte loads from two row pointers, and the 32 cells of a warp (two cell rows,
+// rows 4cy + i and 4cy + 4 + i fall in different bank halves) read its own cells without bank
+// conflicts.
+template <int T> struct TileBlock {
+    static constexpr int PLANE = T * T, BLOCK = 3 * T * T;
+    static __device__ __forceinline__ int row_pos(int r) { return r ^ ((r >> 2) & 1); }
+    static __device__ __forceinline__ uint4 load_cell(const uint8_t *P, int py, int px) {
+        const int p = py & 1;
+        const uint8_t *ae = P + (4 * py + p) * T + 4 * px, *ao = P + (4 * py + 1 - p) * T + 4 * px;
+        return make_uint4(*reinterpret_cast<const uint32_t *>(ae), *reinterpret_cast<const uint32_t *>(ao),
+                          *reinterpret_cast<const uint32_t *>(ae + 2 * T), *reinterpret_cast<const uint32_t *>(ao + 2 * T));
+    }
+};
 
 // destination tile -> source tile under the levels above the tile (walk e = emax .. tp+1)
 __device__ __forceinline__ void upper_walk_inverse(const Geo &g, const uint32_t *pyr_img, int dty, int dtx,
@@ -100,35 +124,89 @@ __device__ __forceinline__ void wait_keys(const TileWS &ws, int img, int nK) {
 }
 
 // Warp 0 of a worker CTA: wait for the image's keystream CTAs, then make the upper angle
-// pyramid walkable -- copied into shared memory in one parallel load when it is small
-// (<= kPyrSmem counters: images up to 2048^2), else walked in L2.  Returns the pointer.
-constexpr int kPyrSmem = 1536;
+// pyramid walkable -- copied into shared memory (spyr, sized at launch) in one parallel load.
 __device__ __forceinline__ const uint32_t *warp0_ready(const Geo &g, const TileWS &ws, int img, int nK,
                                                        uint32_t *spyr) {
     const int lane = threadIdx.x & 31;
     if (lane == 0) wait_keys(ws, img, nK);
     __syncwarp();
+    fence_proxy_async_global();                      // the scratch the bulk copies will read
     const uint32_t *pyr_img = ws.pyr + (size_t)img * g.npyr;
-    if (g.npyr > kPyrSmem) return pyr_img;
     for (int i = lane; i < g.npyr; i += 32) spyr[i] = __ldcg(pyr_img + i);
     __syncwarp();
     return spyr;
 }
 
 // ======================================================================================
-// K role: one thread per tile row, TPC = 256 / T tiles per CTA.
+// Label histogram helpers (encode K role).
 // ======================================================================================
-template <int TP, bool HIST, bool INV, bool LMR8 = true>
+// byte-wise thermometer code of x: every byte becomes 2^bitlen - 1 (bit k set iff byte >= 2^k).
+// The right shifts go through the opaque g.one as multiply-high so that they issue on the FMA
+// pipe (the ALU pipe is busy with ChaCha).
+__device__ __forceinline__ uint32_t smear_bytes(uint32_t x, uint32_t one) {
+    uint32_t y = x | (__umulhi(x, one << 31) & 0x7F7F7F7Fu);
+    y |= __umulhi(y, one << 30) & 0x3F3F3F3Fu;
+    y |= __umulhi(y, one << 28) & 0x0F0F0F0Fu;
+    return y;
+}
+// carry-save adder: (h, l) = (majority, parity) of three bit vectors
+__device__ __forceinline__ void csa(uint32_t &h, uint32_t &l, uint32_t a, uint32_t b, uint32_t c) {
+    const uint32_t u = a ^ b;
+    h = (a & b) | (u & c);
+    l = u ^ c;
+}
+// Harley-Seal vertical counter over 16 words (missing words are 0): every bit lane's count
+// = ones + 2 twos + 4 fours + 8 eights + 16 sixteens
+template <int N>
+__device__ __forceinline__ void hs16(const uint32_t (&y)[N], uint32_t p[5]) {
+    auto Y = [&](int i) -> uint32_t { return i < N ? y[i < N ? i : 0] : 0u; };
+    uint32_t ones = 0, twos = 0, fours = 0, eights = 0, twosA, twosB, foursA, foursB, eightsA, eightsB;
+    csa(twosA, ones, ones, Y(0), Y(1));
+    csa(twosB, ones, ones, Y(2), Y(3));
+    csa(foursA, twos, twos, twosA, twosB);
+    csa(twosA, ones, ones, Y(4), Y(5));
+    csa(twosB, ones, ones, Y(6), Y(7));
+    csa(foursB, twos, twos, twosA, twosB);
+    csa(eightsA, fours, fours, foursA, foursB);
+    csa(twosA, ones, ones, Y(8), Y(9));
+    csa(twosB, ones, ones, Y(10), Y(11));
+    csa(foursA, twos, twos, twosA, twosB);
+    csa(twosA, ones, ones, Y(12), Y(13));
+    csa(twosB, ones, ones, Y(14), Y(15));
+    csa(foursB, twos, twos, twosA, twosB);
+    csa(eightsB, fours, fours, foursA, foursB);
+    uint32_t sixteens;
+    csa(sixteens, eights, eights, eightsA, eightsB);
+    p[0] = ones; p[1] = twos; p[2] = fours; p[3] = eights; p[4] = sixteens;
+}
+
+// ======================================================================================
+// K role: one thread per tile row, TPC = 256 / T tiles per CTA.
+//   ENC: encode (copy I, label plane, histogram, inverse group table); else recover (copy I_e',
+//   forward group table).
+// ======================================================================================
+template <int TP>
+struct KSmem {
+    static constexpr int T = 1 << TP, TPC = 256 / T;
+    uint64_t rec[TPC][kRecSlots];                   // in-tile angles, levels 1..tp (slots lvl_off[e] + row)
+    __align__(16) uint8_t wrec[TPC][kWRecBytes];    // worker records being built
+    uint32_t hsum[8][4];
+};
+
+template <int TP, bool ENC, int METHOD>
 __device__ __forceinline__ void key_role(const Geo &g, int img, int kidx, const uint8_t *__restrict__ keys,
-                                         const uint8_t *__restrict__ images, const TileWS &ws, uint8_t *smem) {
-    constexpr int T = 1 << TP, NW = T / 4, TPC = 256 / T;
-    uint64_t(*rec)[kRecSlots] = reinterpret_cast<uint64_t(*)[kRecSlots]>(smem);
+                                         const uint8_t *__restrict__ src_img, const TileWS &ws, uint8_t *smem) {
+    constexpr int T = 1 << TP, NW = T / 4, TPC = 256 / T, NG = T / 8;
+    KSmem<TP> &S = *reinterpret_cast<KSmem<TP> *>(smem);
 
     const int tid = threadIdx.x, lt = tid / T, row = tid % T;
     const int tile = kidx * TPC + lt;
     const bool valid = tile < g.ntiles;
     const int ty = valid ? (tile >> g.tlog) : 0, tx = valid ? (tile & (g.tilesX - 1)) : 0;
     const long long o = (long long)(ty * T + row) * g.W + (long long)tx * T;
+    using TB = TileBlock<T>;
+    // this thread's row in the tile's scratch block
+    uint8_t *rowp = ws.s + ((size_t)img * g.ntiles + tile) * TB::BLOCK + TB::row_pos(row) * T;
 
     uint32_t key[8];
     load_key(keys, img, key);
@@ -143,12 +221,12 @@ __device__ __forceinline__ void key_role(const Geo &g, int img, int kidx, const 
 #pragma unroll
         for (int i = 0; i < NW; i++) w[i] = blk[boff + i];
     }
-    // keystream row -> tile-major scratch (a warp writes whole tiles rows: contiguous)
+    // keystream row -> cell-layout scratch (per word, 32 lanes write 128 contiguous bytes), kept
+    // in L2 until its worker has read it
+    const uint64_t keep = l2_evict_last_policy();
     if (valid) {
-        uint8_t *sd = ws.s + ((size_t)img * g.ntiles + tile) * (T * T) + row * T;
 #pragma unroll
-        for (int i = 0; i < NW; i += 4)
-            *reinterpret_cast<uint4 *>(sd + 4 * i) = make_uint4(w[i], w[i + 1], w[i + 2], w[i + 3]);
+        for (int c = 0; c < NW; c += 4) st_keep(rowp + 4 * c, make_uint4(w[c], w[c + 1], w[c + 2], w[c + 3]), keep);
     }
 
     // level 1: 2x2 block sums mod 4 -- horizontal pair sums per row, then the partner row
@@ -161,64 +239,84 @@ __device__ __forceinline__ void key_role(const Geo &g, int img, int kidx, const 
         h1 |= (uint64_t)q << (4 * i);
     }
     const uint64_t partner = __shfl_xor_sync(0xffffffffu, h1, 1);
-    if ((row & 1) == 0) rec[lt][g.lvl_off[1] + row / 2] = add2(h1, partner);
+    if ((row & 1) == 0) S.rec[lt][g.lvl_off[1] + row / 2] = add2(h1, partner);
 
-    if constexpr (HIST) {
-        // label histogram of this tile row: for b = 2..8, pixels with c < b (non-redundant),
-        // i.e. x = p ^ left >= 2^(8-b).  Bit-smear x into a thermometer code y, then count
-        // bit (8-b) of y with byte-lane counters (<= 16 * 8 per lane: no overflow).
-        const uint8_t *src = images + (size_t)img * g.HW + o;
-        uint32_t iw[NW];
+    // the tile row of the call's input image (one 16-byte load per 16 pixels) -> cell-layout scratch
+    uint32_t iw[NW];
+    {
+        const uint8_t *src = src_img + (size_t)img * g.HW + o;
 #pragma unroll
         for (int i = 0; i < NW; i += 4) {
-            const uint4 u = valid ? __ldg(reinterpret_cast<const uint4 *>(src) + i / 4) : make_uint4(0, 0, 0, 0);
+            const uint4 u = valid ? __ldcs(reinterpret_cast<const uint4 *>(src) + i / 4) : make_uint4(0, 0, 0, 0);
             iw[i] = u.x; iw[i + 1] = u.y; iw[i + 2] = u.z; iw[i + 3] = u.w;
         }
+        if (valid) {
+#pragma unroll
+            for (int c = 0; c < NW; c += 4)
+                st_keep(rowp + TB::PLANE + 4 * c, make_uint4(iw[c], iw[c + 1], iw[c + 2], iw[c + 3]), keep);
+        }
+    }
+
+    if constexpr (ENC) {
+        // per pixel x = p ^ left neighbour (column 0 forced non-redundant) and its
+        // thermometer code y (bit k set iff x >= 2^k, i.e. c = # leading equal bits < 8 - k).
+        // The label plane for the worker: EMR y itself (l = bit 8-b); LMR c | eta with c = 8 - bitlen.
+        const uint8_t *src = src_img + (size_t)img * g.HW + o;
         uint32_t prev = (valid && tx > 0) ? ((uint32_t)__ldg(src - 1) << 24) : 0u;
-        // The shifts (as multiply-high) and the counter adds (as multiply-add) go through the
-        // opaque g.one so that they issue on the FMA pipe: the ALU pipe is busy with ChaCha.
-        uint32_t acc[7] = {0, 0, 0, 0, 0, 0, 0};
-        const uint32_t one = g.one, h1 = one << 31, h2 = one << 30, h4 = one << 28;
+        uint32_t yv[NW], lv[NW];
 #pragma unroll
         for (int i = 0; i < NW; i++) {
             const uint32_t left = __byte_perm(prev, iw[i], 0x6543);   // [prev.b3, w.b0, w.b1, w.b2]
             uint32_t x = iw[i] ^ left;
-            if (i == 0 && tx == 0) x |= 0xFFu;                     // column 0 is non-redundant
+            if (i == 0 && tx == 0) x |= 0xFFu;
             prev = iw[i];
-            uint32_t y = x | (__umulhi(x, h1) & 0x7F7F7F7Fu);
-            y |= __umulhi(y, h2) & 0x3F3F3F3Fu;
-            y |= __umulhi(y, h4) & 0x0F0F0F0Fu;                    // byte = 2^bitlen(x) - 1
-            const uint32_t y4 = __umulhi(y, h4) & 0x0F0F0F0Fu;
-            if (LMR8) acc[0] = (y & 0x01010101u) * one + acc[0];   // b = 8: LMR only
-            acc[1] = (y & 0x02020202u) * one + acc[1];
-            acc[2] = (y & 0x04040404u) * one + acc[2];
-            acc[3] = (y & 0x08080808u) * one + acc[3];
-            acc[4] = (y4 & 0x01010101u) * one + acc[4];
-            acc[5] = (y4 & 0x02020202u) * one + acc[5];
-            acc[6] = (y4 & 0x04040404u) * one + acc[6];
+            const uint32_t y = smear_bytes(x, g.one);
+            yv[i] = valid ? y : 0u;
+            uint32_t lab;
+            if constexpr (METHOD == 0) {
+                lab = y;
+            } else {
+                uint32_t a = y - ((y >> 1) & 0x55555555u);          // byte popcount = bitlen(x)
+                a = (a & 0x33333333u) + ((a >> 2) & 0x33333333u);
+                a = (a + (a >> 4)) & 0x0F0F0F0Fu;
+                lab = (0x08080808u - a) | (iw[i] & 0x80808080u);
+            }
+            lv[i] = lab;
         }
-        // threshold bit k <-> b = 8 - k; per-thread counts <= 64, warp sums <= 2048: two
-        // counts per 32-bit word for the warp reduction
+        if (valid) {
+#pragma unroll
+            for (int c = 0; c < NW; c += 4)
+                st_keep(rowp + 2 * TB::PLANE + 4 * c, make_uint4(lv[c], lv[c + 1], lv[c + 2], lv[c + 3]), keep);
+        }
+        // label histogram: for b = 2..8 the non-redundant pixels (c < b) = bit 8-b of y.  The
+        // bit lanes of the row's words are counted by a carry-save (Harley-Seal) network, then
+        // threshold k = 8 - b is the sum over the 4 byte lanes of bit k of every plane.
+        uint32_t pl[5];
+        hs16<NW>(yv, pl);
         uint32_t cnt[7];
 #pragma unroll
-        for (int k = 0; k < 7; k++) cnt[k] = valid ? (((acc[k] >> (k & 3)) * 0x01010101u) >> 24) : 0u;
+        for (int k = 0; k < 7; k++) {
+            const uint32_t mk = 0x01010101u << k;
+            cnt[k] = __popc(pl[0] & mk) + 2 * __popc(pl[1] & mk) + 4 * __popc(pl[2] & mk) + 8 * __popc(pl[3] & mk) +
+                     16 * __popc(pl[4] & mk);
+        }
+        // threshold bit k <-> b = 8 - k; per-thread counts <= 64, warp sums <= 2048: two counts
+        // per 32-bit word for the warp reduction
         uint32_t pk[4] = {cnt[0] | (cnt[1] << 16), cnt[2] | (cnt[3] << 16), cnt[4] | (cnt[5] << 16), cnt[6]};
 #pragma unroll
         for (int j = 0; j < 4; j++) {
 #pragma unroll
             for (int s = 16; s > 0; s >>= 1) pk[j] += __shfl_xor_sync(0xffffffffu, pk[j], s);
         }
-        // per-CTA sum, then one atomic per count: a 4096^2 image has 1024 keystream CTAs, and
-        // per-warp atomics on the image's 7 counters serialised at L2
-        uint32_t *hsum = reinterpret_cast<uint32_t *>(&rec[TPC][0]);       // [8 warps][4]
+        // per-CTA sum, then one atomic per count (a 4096^2 image has 1024 keystream CTAs)
         if ((tid & 31) == 0) {
 #pragma unroll
-            for (int j = 0; j < 4; j++) hsum[(tid >> 5) * 4 + j] = pk[j];
+            for (int j = 0; j < 4; j++) S.hsum[tid >> 5][j] = pk[j];
         }
         __syncthreads();
-        if (tid < 7) {
+        if (tid < 7 && (METHOD == 1 || tid > 0)) {                  // b = 8 (k = 0): LMR only
             uint32_t v = 0;
-            for (int w = 0; w < 8; w++) v += (hsum[w * 4 + (tid >> 1)] >> (16 * (tid & 1))) & 0xFFFFu;
+            for (int w8 = 0; w8 < 8; w8++) v += (S.hsum[w8][tid >> 1] >> (16 * (tid & 1))) & 0xFFFFu;
             if (v) atomicAdd(&ws.hist[img * kHistStride + 8 - tid], v);
         }
     }
@@ -230,39 +328,51 @@ __device__ __forceinline__ void key_role(const Geo &g, int img, int kidx, const 
         const int R = T >> e;
         for (int t = tid; t < TPC * R; t += 256) {
             const int l2 = t / R, r = t % R;
-            const uint64_t v = add2(rec[l2][g.lvl_off[e - 1] + 2 * r], rec[l2][g.lvl_off[e - 1] + 2 * r + 1]);
+            const uint64_t v = add2(S.rec[l2][g.lvl_off[e - 1] + 2 * r], S.rec[l2][g.lvl_off[e - 1] + 2 * r + 1]);
             const uint64_t pe = v & 0x3333333333333333ull, po = (v >> 2) & 0x3333333333333333ull;
             uint64_t s = (pe + po) & 0x3333333333333333ull;
             s = (s | (s >> 2)) & 0x0F0F0F0F0F0F0F0Full;
             s = (s | (s >> 4)) & 0x00FF00FF00FF00FFull;
             s = (s | (s >> 8)) & 0x0000FFFF0000FFFFull;
             s = (s | (s >> 16)) & 0x00000000FFFFFFFFull;
-            rec[l2][g.lvl_off[e] + r] = s;
+            S.rec[l2][g.lvl_off[e] + r] = s;
         }
         __syncthreads();
     }
 
-    // in-tile 8x8-group map: levels 4..tp move 2x2-cell groups rigidly.  Forward (recover):
-    // entry[original group] = group after those levels << 2 | turns; inverse (encode):
-    // entry[group after those levels] = original group << 2 | turns (3-bit coordinates).
+    // Worker record.  Group table: levels 4..tp move 2x2-cell groups rigidly; the level-3 turn of
+    // the original group (a rotation of its 2x2 cells, applied first) is folded into the entry's
+    // turn count.  Forward (recover): entry[original group] = group after those levels << 2 | turns;
+    // inverse (encode): entry[group after those levels] = original group << 2 | turns (3-bit
+    // coordinates).  Then the level-1 rows (u64, 2-bit angle per 2x2 block) and the level-2 rows
+    // (u32, one angle per 4x4 cell) for the cells' own turns; levels below e_min are 0.
     {
-        constexpr int NG = T / 8, NGG = NG * NG;
+        constexpr int NGG = NG * NG;
         for (int t = tid; t < TPC * NGG; t += 256) {
             const int l2 = t / NGG, gi = t % NGG;
             int gy = gi / NG, gx = gi % NG, q = 0;
             for (int e = (g.emin > 4 ? g.emin : 4); e <= TP; e++) {
                 const int k = e - 3, m1 = (1 << k) - 1;
                 const int by = gy >> k, bx = gx >> k;
-                const int a = rec_angle(rec[l2], g, e, by, bx);
+                const int a = rec_angle(S.rec[l2], g, e, by, bx);
                 int oy = gy & m1, ox = gx & m1;
                 fwd_turn(a, m1, oy, ox);
                 gy = (by << k) | oy;
                 gx = (bx << k) | ox;
                 q += a;
             }
-            uint8_t *tab = reinterpret_cast<uint8_t *>(&rec[l2][kRecGroupSlot]);
-            if (INV) tab[gy * NG + gx] = (uint8_t)((((gi / NG) << 5) | ((gi % NG) << 2)) | (q & 3));
+            if (g.emin <= 3) q += rec_angle(S.rec[l2], g, 3, gi / NG, gi % NG);
+            uint8_t *tab = S.wrec[l2];
+            if constexpr (ENC) tab[gy * NG + gx] = (uint8_t)((((gi / NG) << 5) | ((gi % NG) << 2)) | (q & 3));
             else tab[gi] = (uint8_t)((gy << 5) | (gx << 2) | (q & 3));
+        }
+        for (int t = tid; t < TPC * (T / 2 + T / 4); t += 256) {
+            const int l2 = t / (T / 2 + T / 4), r = t % (T / 2 + T / 4);
+            if (r < T / 2)
+                reinterpret_cast<uint64_t *>(S.wrec[l2] + kWRecL1)[r] = g.emin <= 1 ? S.rec[l2][g.lvl_off[1] + r] : 0ull;
+            else
+                reinterpret_cast<uint32_t *>(S.wrec[l2] + kWRecL2)[r - T / 2] =
+                    g.emin <= 2 ? (uint32_t)S.rec[l2][g.lvl_off[2] + r - T / 2] : 0u;
         }
         __syncthreads();
     }
@@ -282,167 +392,185 @@ __device__ __forceinline__ void key_role(const Geo &g, int img, int kidx, const 
                     cur = blk;
                     acc = 0;
                 }
-                acc += (uint32_t)(rec[l2][g.lvl_off[TP]] & 3u);
+                acc += (uint32_t)(S.rec[l2][g.lvl_off[TP]] & 3u);
             }
             if (acc) atomicAdd(&ws.pyr[(size_t)img * g.npyr + g.pyr_off[e] + cur], acc);
         }
     }
-    // records out
-    for (int t = tid; t < TPC * kRecSlots; t += 256) {
-        const int l2 = t / kRecSlots, slot = t % kRecSlots;
+    // worker records out (16-byte stores)
+    for (int t = tid; t < TPC * (kWRecBytes / 16); t += 256) {
+        const int l2 = t / (kWRecBytes / 16), c = t % (kWRecBytes / 16);
         const int tl = kidx * TPC + l2;
-        if (tl < g.ntiles) ws.rec[((size_t)img * g.ntiles + tl) * kRecSlots + slot] = rec[l2][slot];
+        if (tl < g.ntiles)
+            reinterpret_cast<uint4 *>(ws.rec + ((size_t)img * g.ntiles + tl) * kRecSlots)[c] =
+                reinterpret_cast<const uint4 *>(S.wrec[l2])[c];
     }
-    // publish: the barrier orders the CTA's writes before thread 0's release arrival on the
-    // image's counter (release is cumulative)
+    // publish: the proxy fence and the barrier order the CTA's scratch writes before thread 0's
+    // release arrival on the image's counter (release is cumulative); workers read them by bulk copy
+    fence_proxy_async_global();
     __syncthreads();
     if (tid == 0) red_release_add_u32(ws.kdone + img, 1u);
 }
 
 // ======================================================================================
 // Worker roles.  One worker CTA per strip of tiles (one tile row of the image), walking the
-// strip left to right with a two-stage cp.async pipeline: the next tile's data is in flight
-// while the current one is transformed.  The tile map of the strip (upper-level walks) is
-// computed once, up front, by warp 0 from the angle pyramid.
+// strip left to right.  Stage ring of kStages tiles: thread 0 issues the bulk copies of tile
+// j + kStages once the 8 warps have released tile j (empty barrier, one arrival per warp).
 // ======================================================================================
 constexpr int kMaxTilesX = 512;                  // W <= 32768 with 64-pixel tiles
+constexpr int kStages = 3;
 
 __device__ __forceinline__ uint32_t bits4_to_bytes(uint32_t m4) { return ((m4 & 0xFu) * 0x00204081u) & 0x01010101u; }
 // byte LSBs (bits 0, 8, 16, 24) -> bits 0..3: one multiply puts them at bits 21..24 (no other term lands there)
 __device__ __forceinline__ uint32_t bytes_to_bits4(uint32_t l) { return ((l * 0x00204081u) >> 21) & 0xFu; }
 
-__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+// a cell's own turns from the worker record: level-2 angle (bits 0-1), level-1 angles of its
+// upper (bits 2-5) and lower (bits 6-9) 2x2 block pairs
+__device__ __forceinline__ uint32_t cell_turns(const uint8_t *wrec, int py, int px) {
+    const uint32_t *l1 = reinterpret_cast<const uint32_t *>(wrec + kWRecL1);
+    const uint32_t *l2 = reinterpret_cast<const uint32_t *>(wrec + kWRecL2);
+    const int sh = 4 * (px & 7), wi = 4 * py + (px >> 3);
+    return ((l2[py] >> (2 * px)) & 3u) | (((l1[wi] >> sh) & 0xFu) << 2) | (((l1[wi + 2] >> sh) & 0xFu) << 6);
 }
-__device__ __forceinline__ void cp_async4(void *smem, const void *gmem) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+
+template <int TP, bool ENC>
+struct WSmem {
+    static constexpr int T = 1 << TP;
+    struct Stage {
+        uint4 ks[ENC ? T * T / 16 : 1];      // encode: keystream of the destination tile
+        uint4 src[2 * T * T / 16];           // encode: source tile's image | label planes;
+                                             // recover: destination tile's keystream | image planes
+        uint4 rec[kWRecBytes / 16];          // worker record (encode: source tile; recover: original tile)
+    } st[kStages];
+    uint64_t full[kStages], empty[kStages];
+    int map[kMaxTilesX];                     // per tile of the strip: other tile << 2 | upper turns
+    uint32_t fsel[16];                       // copy-forward PRMT selectors by 4-bit map
+    int sh[4];
+};
+
+// copy-forward selector: nibble i = index of the last set bit of m at or below i, else 4
+__device__ __forceinline__ uint32_t fsel_of(int m) {
+    uint32_t v = 0;
+    int last = 4;
+    for (int i = 0; i < 4; i++) {
+        if ((m >> i) & 1) last = i;
+        v |= (uint32_t)last << (4 * i);
+    }
+    return v;
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N> __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// the consumed scratch leaves L2 unwritten (its bulk copies have completed): lines [0, n) of a
+// region, dropped by the 32 lanes of one warp
+__device__ __forceinline__ void discard_lines(const void *p, int n, int lane) {
+    for (int i = lane; i < n; i += 32) discard_l2(static_cast<const uint8_t *>(p) + 128 * i);
+}
 
 // ======================================================================================
-// W role, encode (a3, a5): destination strip dty, tiles left to right.
+// W role, encode (a3, a5): destination strip dty, tiles left to right, thread = destination cell.
 //   EMR: carrier v = (I & 0xFE) | l with l = [c < b] (location map), permuted as a
 //        whole byte; E = v_r XOR (s & 0xFE) (eq. image_encryption P:739 + LSB map P:744);
 //        header b-2 in the LSBs of r = 0..2 (Q14).
 //   LMR: E = I_r XOR s; second plane ceta = (I & 0x80) | c permuted alongside (for the coder).
-// The carrier / label of a source pixel needs its left neighbour: computed per cell row from
-// the staged source tile (and, at the tile's left edge, the staged halo word).
 // ======================================================================================
-template <int TP>
-struct PermSmem {
-    static constexpr int T = 1 << TP;
-    struct Stage {
-        uint32_t is[T * T / 4];              // source tile of I (row-major words)
-        uint32_t halo[T];                    // per row: the aligned word left of the row (byte 3)
-        uint32_t ss[T * T / 4];              // keystream of the destination tile (tile-major)
-        uint64_t rec[kRecSlots];             // angle record of the source tile
-    } st[2];
-    uint32_t pyr[kPyrSmem];                  // upper angle pyramid of the image (small images)
-    int smap[kMaxTilesX];                    // per destination tile of the strip: source << 2 | q
-    int sh[4];
-};
-
 template <int TP, int METHOD>
-__device__ __forceinline__ void perm_role(const Geo &g, int img, int dty, int nK, const uint8_t *__restrict__ images,
-                                          const TileWS &ws, uint8_t *__restrict__ enc, uint8_t *__restrict__ ceta_out,
+__device__ __forceinline__ void perm_role(const Geo &g, int img, int dty, int nK, const TileWS &ws,
+                                          uint8_t *__restrict__ enc, uint8_t *__restrict__ ceta_out,
                                           int32_t *__restrict__ b_out, int64_t *__restrict__ cap_out,
                                           int32_t *__restrict__ status, uint8_t *smem) {
-    constexpr int T = 1 << TP, NW = T / 4, NC = T / 4, NCELL = NC * NC, CPT = T * T / 16, NG = NC / 2;
-    PermSmem<TP> &S = *reinterpret_cast<PermSmem<TP> *>(smem);
-    const int tid = threadIdx.x;
-    const uint8_t *I = images + (size_t)img * g.HW;
+    constexpr int T = 1 << TP, NC = T / 4, NG = NC / 2;
+    using TB = TileBlock<T>;
+    using SM = WSmem<TP, true>;
+    SM &S = *reinterpret_cast<SM *>(smem);
+    uint32_t *spyr = reinterpret_cast<uint32_t *>(smem + sizeof(SM));
+    const int tid = threadIdx.x, lane = tid & 31;
 
+    if (tid == 0) {
+        for (int s = 0; s < kStages; s++) {
+            mbar_init(&S.full[s], 1);
+            mbar_init(&S.empty[s], 8);
+        }
+    }
     if (tid < 32) {
-        const uint32_t *pyr = warp0_ready(g, ws, img, nK, S.pyr);
+        const uint32_t *pyr = warp0_ready(g, ws, img, nK, spyr);
         for (int j = tid; j < g.tilesX; j += 32) {
             int sty, stx, q;
             upper_walk_inverse(g, pyr, dty, j, sty, stx, q);
-            S.smap[j] = (((sty << g.tlog) + stx) << 2) | q;
+            S.map[j] = (((sty << g.tlog) + stx) << 2) | q;
         }
         if (tid == 0) S.sh[0] = METHOD == 0 ? emr_select_b(ws.hist + img * kHistStride, g.HW) : 0;
     }
     __syncthreads();
     const int b = S.sh[0];
-    const uint32_t MB = METHOD == 0 ? ((0xFFu << (8 - b)) & 0xFFu) * 0x01010101u : 0u;
+    const int ntx = g.tilesX;
+    const uint8_t *blk0 = ws.s + (size_t)img * g.ntiles * TB::BLOCK;      // the image's scratch blocks
+    const uint64_t *rec0 = ws.rec + (size_t)img * g.ntiles * kRecSlots;
 
     auto issue = [&](int j) {
-        typename PermSmem<TP>::Stage &st = S.st[j & 1];
-        const int stile = S.smap[j] >> 2, sty = stile >> g.tlog, stx = stile & (g.tilesX - 1);
-        const size_t dslot = (size_t)img * g.ntiles + ((size_t)dty << g.tlog) + j;
-        for (int c = tid; c < CPT; c += 256) {
-            const int r = c / (T / 16), seg = c % (T / 16);
-            cp_async16(&st.is[r * NW + seg * 4], I + (size_t)(sty * T + r) * g.W + (size_t)stx * T + seg * 16);
-            cp_async16(&st.ss[4 * c], ws.s + dslot * (T * T) + 16 * c);
-        }
-        if (tid < T && stx > 0) cp_async4(&st.halo[tid], I + (size_t)(sty * T + tid) * g.W + (size_t)stx * T - 4);
-        if (tid < kRecSlots / 2)
-            cp_async16(&st.rec[2 * tid], ws.rec + ((size_t)img * g.ntiles + stile) * kRecSlots + 2 * tid);
-        cp_async_commit();
+        const int s = j % kStages;
+        if (j >= kStages) mbar_wait(&S.empty[s], ((j / kStages) - 1) & 1);
+        const int stile = S.map[j] >> 2, dtile = (dty << g.tlog) + j;
+        mbar_expect_tx(&S.full[s], 3 * T * T + kWRecBytes);
+        bulk_g2s(S.st[s].ks, blk0 + (size_t)dtile * TB::BLOCK, T * T, &S.full[s]);
+        bulk_g2s(S.st[s].src, blk0 + (size_t)stile * TB::BLOCK + TB::PLANE, 2 * T * T, &S.full[s]);
+        bulk_g2s(S.st[s].rec, rec0 + (size_t)stile * kRecSlots, kWRecBytes, &S.full[s]);
     };
+    if (tid == 0)
+        for (int j = 0; j < kStages && j < ntx; j++) issue(j);
 
-    issue(0);
-    for (int j = 0; j < g.tilesX; j++) {
-        if (j + 1 < g.tilesX) {
-            issue(j + 1);
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
-        }
-        __syncthreads();                                           // stage j landed for everyone
-        const typename PermSmem<TP>::Stage &st = S.st[j & 1];
-        const int mp = S.smap[j], stile = mp >> 2, q_up = mp & 3;
-        const int stx = stile & (g.tilesX - 1);
-        const int dtile = (dty << g.tlog) + j;
-        {   // the consumed scratch (destination keystream, source record) leaves L2 unwritten
-            const size_t dslot = (size_t)img * g.ntiles + dtile;
-            if (tid < (T * T) / 128) discard_l2(ws.s + dslot * (T * T) + 128 * tid);
-            else if (tid >= 64 && tid < 64 + kRecSlots * 8 / 128)
-                discard_l2(ws.rec + ((size_t)img * g.ntiles + stile) * kRecSlots + 16 * (tid - 64));
-        }
-        for (int c = tid; c < NCELL; c += 256) {
-            // destination cell -> source cell: group walk (levels >= 4, q_up), level 3 inside the
-            // group, then in-cell levels 1, 2
-            const int gi = c >> 2, sub = c & 3;
-            const int cy = 2 * (gi / NG) + (sub >> 1), cx = 2 * (gi % NG) + (sub & 1);
-            int dgy = gi / NG, dgx = gi % NG;
-            inv_turn(q_up, NG - 1, dgy, dgx);               // undo the tile's own turn, then the
-            const uint32_t ge = reinterpret_cast<const uint8_t *>(st.rec + kRecGroupSlot)[dgy * NG + dgx];
-            const int sgy = ge >> 5, sgx = (ge >> 2) & 7;    // in-tile levels >= 4 (group table)
-            int q = q_up + (int)(ge & 3);
-            if (g.emin <= 3) q += rec_angle(st.rec, g, 3, sgy, sgx);
-            int sy = sub >> 1, sx = sub & 1;
-            inv_turn(q & 3, 1, sy, sx);
-            const int py = 2 * sgy + sy, px = 2 * sgx + sx;
-            // source cell rows -> carrier (EMR) / image + label|eta (LMR)
-            uint32_t vr[4], cr[4] = {0, 0, 0, 0};
+    // this thread's destination cell and its candidate group / sub-cell positions for the 4
+    // possible upper turns of the tile (undo the tile's own turn first)
+    const bool act = tid < NC * NC;
+    const int cy = act ? tid / NC : 0, cx = act ? tid % NC : 0;
+    uint32_t gpos = 0, spos = 0;
 #pragma unroll
-            for (int i = 0; i < 4; i++) {
-                const int row = 4 * py + i;
-                const uint32_t w = st.is[row * NW + px];
-                const uint32_t pw = px > 0 ? st.is[row * NW + px - 1] : (stx > 0 ? st.halo[row] : 0u);
-                uint32_t x = w ^ __byte_perm(pw, w, 0x6543);      // p ^ left neighbour, per byte
-                if (px == 0 && stx == 0) x |= 0xFFu;               // column 0: always non-redundant
-                if constexpr (METHOD == 0) {
-                    const uint32_t t = x & MB;
-                    const uint32_t nz = (((t & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | t) & 0x80808080u;   // byte != 0
-                    vr[i] = (w & 0xFEFEFEFEu) | (nz >> 7);
-                } else {
-                    uint32_t cv = 0;                               // c = # leading equal bits per byte
-#pragma unroll
-                    for (int k = 0; k < 4; k++) {
-                        const uint32_t xb = (x >> (8 * k)) & 0xFFu;
-                        cv |= (xb ? (uint32_t)(__clz(xb) - 24) : 8u) << (8 * k);
-                    }
-                    cr[i] = cv | (w & 0x80808080u);
-                    vr[i] = w;
-                }
+    for (int q = 0; q < 4; q++) {
+        int gy = cy >> 1, gx = cx >> 1, sy = cy & 1, sx = cx & 1;
+        inv_turn(q, NG - 1, gy, gx);
+        inv_turn(q, 1, sy, sx);
+        gpos |= (uint32_t)(gy * NG + gx) << (8 * q);
+        spos |= (uint32_t)(sy * 2 + sx) << (2 * q);
+    }
+    const int lsh = 8 - b;                                   // EMR: map bit l = bit 8 - b of the thermometer code
+    // output rows of this thread's cell in tile 0 of the strip (the tile advances by T bytes)
+    const size_t W = (size_t)g.W;
+    uint8_t *eo = enc + (size_t)img * g.HW + (size_t)(dty * T + 4 * cy) * W + 4 * cx;
+    uint8_t *co = METHOD == 1 ? ceta_out + (size_t)img * g.HW + (size_t)(dty * T + 4 * cy) * W + 4 * cx : nullptr;
+
+    int s = 0;
+    unsigned ph = 0;
+    for (int j = 0; j < ntx; j++) {
+        mbar_wait_sleep(&S.full[s], ph);
+        const typename SM::Stage &st = S.st[s];
+        const int mp = S.map[j];
+        if (tid >= 224) {                                    // warp 7: drop the consumed scratch from L2
+            const int dtile = (dty << g.tlog) + j;
+            discard_lines(blk0 + (size_t)dtile * TB::BLOCK, T * T / 128, lane);
+            discard_lines(blk0 + (size_t)(mp >> 2) * TB::BLOCK + TB::PLANE, 2 * T * T / 128, lane);
+            discard_lines(rec0 + (size_t)(mp >> 2) * kRecSlots, kRecSlots * 8 / 128, lane);
+        }
+        if (act) {
+            const int q_up = mp & 3;
+            const uint8_t *wrec = reinterpret_cast<const uint8_t *>(st.rec);
+            const uint32_t ge = wrec[(gpos >> (8 * q_up)) & 0xFFu];
+            const int q = q_up + (int)ge;
+            const int s2 = (int)(spos >> (2 * (q & 3))) & 3;
+            const int py = 2 * (int)(ge >> 5) + (s2 >> 1), px = 2 * (int)((ge >> 2) & 7) + (s2 & 1);
+            const uint32_t ce = cell_turns(wrec, py, px);
+            const int r = (q + (int)ce) & 3;
+            const uint8_t *src = reinterpret_cast<const uint8_t *>(st.src);
+            const uint4 wv = TB::load_cell(src, py, px), yv = TB::load_cell(src + TB::PLANE, py, px);
+            Cell v, cl;
+            if constexpr (METHOD == 0) {
+                v.r0 = (wv.x & 0xFEFEFEFEu) | ((yv.x >> lsh) & 0x01010101u);
+                v.r1 = (wv.y & 0xFEFEFEFEu) | ((yv.y >> lsh) & 0x01010101u);
+                v.r2 = (wv.z & 0xFEFEFEFEu) | ((yv.z >> lsh) & 0x01010101u);
+                v.r3 = (wv.w & 0xFEFEFEFEu) | ((yv.w >> lsh) & 0x01010101u);
+            } else {
+                v = {wv.x, wv.y, wv.z, wv.w};
+                cl = {yv.x, yv.y, yv.z, yv.w};
             }
-            Cell v = {vr[0], vr[1], vr[2], vr[3]};
-            Cell cl = {cr[0], cr[1], cr[2], cr[3]};
             if (g.emin <= 1) {
-                const uint32_t a01 = (uint32_t)(st.rec[g.lvl_off[1] + 2 * py] >> (4 * px)) & 0xFu;
-                const uint32_t a23 = (uint32_t)(st.rec[g.lvl_off[1] + 2 * py + 1] >> (4 * px)) & 0xFu;
+                const uint32_t a01 = (ce >> 2) & 0xFu, a23 = (ce >> 6) & 0xFu;
                 pair_rot_cw(v.r0, v.r1, a01 & 3, a01 >> 2);
                 pair_rot_cw(v.r2, v.r3, a23 & 3, a23 >> 2);
                 if constexpr (METHOD == 1) {
@@ -450,18 +578,15 @@ __device__ __forceinline__ void perm_role(const Geo &g, int img, int dty, int nK
                     pair_rot_cw(cl.r2, cl.r3, a23 & 3, a23 >> 2);
                 }
             }
-            if (g.emin <= 2) q += rec_angle(st.rec, g, 2, py, px);
-            v = cell_rot_cw(v, q & 3);
-            if constexpr (METHOD == 1) cl = cell_rot_cw(cl, q & 3);
+            v = cell_rot_cw(v, r);
+            if constexpr (METHOD == 1) cl = cell_rot_cw(cl, r);
 
-            const uint32_t *sw = st.ss + (4 * cy) * NW + cx;
-            const uint32_t s0 = sw[0], s1 = sw[NW], s2 = sw[2 * NW], s3 = sw[3 * NW];
-            const size_t base = (size_t)(dty * T + 4 * cy) * g.W + (size_t)j * T + 4 * cx;
+            const uint4 sv = TB::load_cell(reinterpret_cast<const uint8_t *>(st.ks), cy, cx);
             uint32_t e0, e1, e2, e3;
             if constexpr (METHOD == 0) {
-                e0 = v.r0 ^ (s0 & 0xFEFEFEFEu); e1 = v.r1 ^ (s1 & 0xFEFEFEFEu);
-                e2 = v.r2 ^ (s2 & 0xFEFEFEFEu); e3 = v.r3 ^ (s3 & 0xFEFEFEFEu);
-                if (dtile == 0 && c == 0) {
+                e0 = v.r0 ^ (sv.x & 0xFEFEFEFEu); e1 = v.r1 ^ (sv.y & 0xFEFEFEFEu);
+                e2 = v.r2 ^ (sv.z & 0xFEFEFEFEu); e3 = v.r3 ^ (sv.w & 0xFEFEFEFEu);
+                if (dty == 0 && j == 0 && tid == 0) {
                     // header: LSB(E[r]) = bit (2 - r) of b - 2 for r = 0..2; the map there is
                     // forced to 1, so capacity counts zeros after forcing (Q14)
                     const uint32_t m = v.r0 & 0x00010101u;
@@ -475,73 +600,62 @@ __device__ __forceinline__ void perm_role(const Geo &g, int img, int dty, int nK
                     status[img] = 0;
                 }
             } else {
-                e0 = v.r0 ^ s0; e1 = v.r1 ^ s1; e2 = v.r2 ^ s2; e3 = v.r3 ^ s3;
-                uint8_t *co = ceta_out + (size_t)img * g.HW + base;
-                *reinterpret_cast<uint32_t *>(co) = cl.r0;
-                *reinterpret_cast<uint32_t *>(co + g.W) = cl.r1;
-                *reinterpret_cast<uint32_t *>(co + 2 * (size_t)g.W) = cl.r2;
-                *reinterpret_cast<uint32_t *>(co + 3 * (size_t)g.W) = cl.r3;
+                e0 = v.r0 ^ sv.x; e1 = v.r1 ^ sv.y; e2 = v.r2 ^ sv.z; e3 = v.r3 ^ sv.w;
+                __stcs(reinterpret_cast<unsigned *>(co), cl.r0);
+                __stcs(reinterpret_cast<unsigned *>(co + W), cl.r1);
+                __stcs(reinterpret_cast<unsigned *>(co + 2 * W), cl.r2);
+                __stcs(reinterpret_cast<unsigned *>(co + 3 * W), cl.r3);
+                co += T;
             }
-            uint8_t *eo = enc + (size_t)img * g.HW + base;
-            *reinterpret_cast<uint32_t *>(eo) = e0;
-            *reinterpret_cast<uint32_t *>(eo + g.W) = e1;
-            *reinterpret_cast<uint32_t *>(eo + 2 * (size_t)g.W) = e2;
-            *reinterpret_cast<uint32_t *>(eo + 3 * (size_t)g.W) = e3;
+            __stcs(reinterpret_cast<unsigned *>(eo), e0);
+            __stcs(reinterpret_cast<unsigned *>(eo + W), e1);
+            __stcs(reinterpret_cast<unsigned *>(eo + 2 * W), e2);
+            __stcs(reinterpret_cast<unsigned *>(eo + 3 * W), e3);
+            eo += T;
         }
-        __syncthreads();                                           // stage j free for tile j + 2
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&S.empty[s]);               // this warp is done with stage s
+        if (tid == 0 && j + kStages < ntx) issue(j + kStages);
+        if (++s == kStages) { s = 0; ph ^= 1u; }
     }
 }
 
 // ======================================================================================
-// W role, recover (a10): original strip ty, tiles left to right.
+// W role, recover (a10): original strip ty, tiles left to right, thread = original cell.
 //   X = I_e' XOR s (every bit, Q20); EMR: map bit = raw LSB of I_e' (r < 3 forced to 1);
 //   LMR: MSB := eta_r and the map come from the decoded planes.  Inverse cell transform into
-//   the original domain, then per row omega := masked bits of the last non-redundant pixel,
-//   replaced into the redundant ones; the row's omega carries from tile to
-//   tile inside the CTA.
+//   the original domain in registers, then per row omega := masked bits of the last
+//   non-redundant pixel, replaced into the redundant ones:
+//     * per cell row, xf = (X & mask) | flag for the non-redundant pixels (the flag bit lies
+//       outside the mask: EMR bit 0, b <= 7; LMR bit 7, restored from eta), and
+//       om = PRMT(xf, carry, fsel[m4]) gives every pixel the flagged value of the last
+//       non-redundant pixel at or before it (byte 3 = the cell row's summary);
+//     * the 4 summaries of a cell are one word; an inclusive shuffle scan over the cells of the
+//       tile row (combine = "right if flagged else left", per byte) gives each cell its carry,
+//       the tile's carry moves on to the next tile of the strip in a register.
 // ======================================================================================
-template <int TP>
-struct RecSmem {
-    static constexpr int T = 1 << TP, RS = T / 4 + 1;
-    struct Stage {
-        uint32_t es[T * T / 4];              // marked destination tile (row-major words)
-        uint32_t ss[T * T / 4];              // keystream of the destination tile (tile-major)
-        uint64_t rec[kRecSlots];             // angle record of the original tile
-        uint32_t mbits[T][2], ebits[T][2];   // LMR: decoded map / eta bits of the destination rows
-    } st[2];
-    uint32_t xo[T * RS], lo[T * RS];         // original domain of the current tile
-    uint32_t pyr[kPyrSmem];
-    int dmap[kMaxTilesX];                    // per original tile of the strip: destination << 2 | q
-    uint8_t carry[T];                        // per row: omega at the right edge of the previous tile
-    uint32_t fsel[16];                       // copy-forward PRMT selectors by 4-bit map
-    int sh[4];
-};
-
 template <int TP, int METHOD>
 __device__ __forceinline__ void rec_role(const Geo &g, int img, int ty, int nK, const uint8_t *__restrict__ marked,
                                          const TileWS &ws, const uint32_t *__restrict__ eta_bits,
                                          const uint32_t *__restrict__ map_bits, const int32_t *__restrict__ lmr_b,
                                          uint8_t *__restrict__ out, int32_t *__restrict__ status, uint8_t *smem) {
-    constexpr int T = 1 << TP, NW = T / 4, RS = T / 4 + 1, NC = T / 4, NCELL = NC * NC, CPT = T * T / 16;
-    constexpr int SEGS = T / 16, NG = NC / 2;
-    RecSmem<TP> &S = *reinterpret_cast<RecSmem<TP> *>(smem);
-    const int tid = threadIdx.x;
+    constexpr int T = 1 << TP, NC = T / 4, NG = NC / 2;
+    using TB = TileBlock<T>;
+    using SM = WSmem<TP, false>;
+    SM &S = *reinterpret_cast<SM *>(smem);
+    uint32_t *spyr = reinterpret_cast<uint32_t *>(smem + sizeof(SM));
+    const int tid = threadIdx.x, lane = tid & 31;
     const uint8_t *Em = marked + (size_t)img * g.HW;
     uint8_t *O = out + (size_t)img * g.HW;
 
-    if (tid >= 32 && tid < 48) {                        // fsel[m] nibble i: last set bit <= i, else 4
-        const int m = tid - 32;
-        uint32_t v = 0;
-        int last = 4;
-        for (int i = 0; i < 4; i++) {
-            if ((m >> i) & 1) last = i;
-            v |= (uint32_t)last << (4 * i);
-        }
-        S.fsel[m] = v;
-    }
+    if (tid >= 32 && tid < 48) S.fsel[tid - 32] = fsel_of(tid - 32);
     if (tid < 32) {
         int b = 0;
         if (tid == 0) {
+            for (int s = 0; s < kStages; s++) {
+                mbar_init(&S.full[s], 1);
+                mbar_init(&S.empty[s], 8);
+            }
             if constexpr (METHOD == 0) {
                 const int field = ((Em[0] & 1) << 2) | ((Em[1] & 1) << 1) | (Em[2] & 1);
                 b = field > 5 ? -1 : field + 2;
@@ -554,11 +668,11 @@ __device__ __forceinline__ void rec_role(const Geo &g, int img, int ty, int nK, 
         }
         b = __shfl_sync(0xffffffffu, b, 0);
         if (b > 0) {
-            const uint32_t *pyr = warp0_ready(g, ws, img, nK, S.pyr);
+            const uint32_t *pyr = warp0_ready(g, ws, img, nK, spyr);
             for (int j = tid; j < g.tilesX; j += 32) {
                 int dty, dtx, q;
                 upper_walk_forward(g, pyr, ty, j, dty, dtx, q);
-                S.dmap[j] = (((dty << g.tlog) + dtx) << 2) | q;
+                S.map[j] = (((dty << g.tlog) + dtx) << 2) | q;
             }
         }
     }
@@ -573,89 +687,92 @@ __device__ __forceinline__ void rec_role(const Geo &g, int img, int ty, int nK, 
     }
     const uint32_t mask = METHOD == 0 ? ((0xFFu << (8 - b)) & 0xFFu) : (0x7Fu & ~(0xFFu >> b));
     const uint32_t maskb = mask * 0x01010101u;
+    const int ntx = g.tilesX;
+    const uint8_t *blk0 = ws.s + (size_t)img * g.ntiles * TB::BLOCK;
+    const uint64_t *rec0 = ws.rec + ((size_t)img * g.ntiles + ((size_t)ty << g.tlog)) * kRecSlots;
 
     auto issue = [&](int j) {
-        typename RecSmem<TP>::Stage &st = S.st[j & 1];
-        const int dt = S.dmap[j] >> 2, dty = dt >> g.tlog, dtx = dt & (g.tilesX - 1);
-        const size_t dslot = (size_t)img * g.ntiles + dt;
-        for (int c = tid; c < CPT; c += 256) {
-            const int r = c / (T / 16), seg = c % (T / 16);
-            cp_async16(&st.es[r * NW + seg * 4], Em + (size_t)(dty * T + r) * g.W + (size_t)dtx * T + seg * 16);
-            cp_async16(&st.ss[4 * c], ws.s + dslot * (T * T) + 16 * c);
-        }
-        if (tid < kRecSlots / 2)
-            cp_async16(&st.rec[2 * tid],
-                       ws.rec + ((size_t)img * g.ntiles + ((size_t)ty << g.tlog) + j) * kRecSlots + 2 * tid);
-        if constexpr (METHOD == 1) {
-            if (tid < T) {
-                const size_t bit = (size_t)img * g.HW + (size_t)(dty * T + tid) * g.W + (size_t)dtx * T;
-                if constexpr (T >= 32) {
-                    for (int k = 0; k < T / 32; k++) {
-                        cp_async4(&st.mbits[tid][k], map_bits + (bit >> 5) + k);
-                        cp_async4(&st.ebits[tid][k], eta_bits + (bit >> 5) + k);
-                    }
-                } else {                                 // 16-pixel rows share words: plain loads
-                    st.mbits[tid][0] = __ldg(map_bits + (bit >> 5)) >> (bit & 31);
-                    st.ebits[tid][0] = __ldg(eta_bits + (bit >> 5)) >> (bit & 31);
-                }
-            }
-        }
-        cp_async_commit();
+        const int s = j % kStages;
+        if (j >= kStages) mbar_wait(&S.empty[s], ((j / kStages) - 1) & 1);
+        const int dt = S.map[j] >> 2;
+        mbar_expect_tx(&S.full[s], 2 * T * T + kWRecBytes);
+        bulk_g2s(S.st[s].src, blk0 + (size_t)dt * TB::BLOCK, 2 * T * T, &S.full[s]);
+        bulk_g2s(S.st[s].rec, rec0 + (size_t)j * kRecSlots, kWRecBytes, &S.full[s]);
     };
+    if (tid == 0)
+        for (int j = 0; j < kStages && j < ntx; j++) issue(j);
 
-    const bool rowthr = tid < T * SEGS;
-    const int r = tid / SEGS, seg = tid % SEGS;
-    issue(0);
-    for (int j = 0; j < g.tilesX; j++) {
-        if (j + 1 < g.tilesX) {
-            issue(j + 1);
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
-        }
-        __syncthreads();                                           // stage j landed for everyone
-        const typename RecSmem<TP>::Stage &st = S.st[j & 1];
-        const int mp = S.dmap[j], dt = mp >> 2, q_up = mp & 3;
-        // cells: original cell -> destination cell; X, L from the staged destination tile
-        for (int c = tid; c < NCELL; c += 256) {
-            const int gi = c >> 2, sub = c & 3;
-            const int ogy = gi / NG, ogx = gi % NG;
-            const int cy = 2 * ogy + (sub >> 1), cx = 2 * ogx + (sub & 1);
-            const uint32_t ge = reinterpret_cast<const uint8_t *>(st.rec + kRecGroupSlot)[gi];
-            int dgy = ge >> 5, dgx = (ge >> 2) & 7;          // in-tile levels >= 4 (group table),
-            fwd_turn(q_up, NG - 1, dgy, dgx);                // then the tile's own turn
-            int q = q_up + (int)(ge & 3);
-            if (g.emin <= 3) q += rec_angle(st.rec, g, 3, ogy, ogx);   // level 3 = the group itself
-            int sy = sub >> 1, sx = sub & 1;
-            fwd_turn(q & 3, 1, sy, sx);
-            const int py = 2 * dgy + sy, px = 2 * dgx + sx;
-            if (g.emin <= 2) q += rec_angle(st.rec, g, 2, cy, cx);
-            uint32_t xr[4], lr[4];
+    const bool act = tid < NC * NC;
+    const int cy = act ? tid / NC : 0, cx = act ? tid % NC : 0;
+    uint32_t spos = 0;                                   // sub-cell position after q turns (forward)
 #pragma unroll
-            for (int i = 0; i < 4; i++) {
-                const int row = 4 * py + i;
-                const uint32_t e = st.es[row * NW + px];
-                uint32_t x = e ^ st.ss[row * NW + px];
-                uint32_t l;
-                if constexpr (METHOD == 0) {
-                    l = e & 0x01010101u;
-                    if (i == 0 && dt == 0 && py == 0 && px == 0) l |= 0x00010101u;   // header pixels, map 1
-                } else {
-                    const int bp = 4 * px;
-                    l = bits4_to_bytes(st.mbits[row][bp >> 5] >> (bp & 31));
-                    x = (x & 0x7F7F7F7Fu) | (bits4_to_bytes(st.ebits[row][bp >> 5] >> (bp & 31)) << 7);  // MSB <- eta
+    for (int q = 0; q < 4; q++) {
+        int sy = cy & 1, sx = cx & 1;
+        fwd_turn(q, 1, sy, sx);
+        spos |= (uint32_t)(sy * 2 + sx) << (2 * q);
+    }
+    constexpr uint32_t HB = METHOD == 0 ? 0x01u : 0x80u;            // flag bit, outside the mask
+    constexpr uint32_t HBW = HB * 0x01010101u;
+    // combine(a, b) per byte: b if flagged else a
+    auto combine = [&](uint32_t a, uint32_t bb) -> uint32_t {
+        const uint32_t f = bb & HBW;
+        const uint32_t m = (METHOD == 0 ? f : (f >> 7)) * 0xFFu;
+        return (bb & m) | (a & ~m);
+    };
+    const int cw = NC < 32 ? NC : 32;                    // lanes holding one tile row's cells
+    const int hlast = (lane & ~(cw - 1)) + cw - 1;       // the last of them
+    uint32_t carry = 0;                                  // summaries leaving the previous tile (4 rows)
+    const size_t W = (size_t)g.W;
+    uint8_t *op = O + (size_t)(ty * T + 4 * cy) * W + 4 * cx;   // this cell's rows in tile 0 of the strip
+
+    int s = 0;
+    unsigned ph = 0;
+    for (int j = 0; j < ntx; j++) {
+        mbar_wait_sleep(&S.full[s], ph);
+        const int mp = S.map[j], dt = mp >> 2, q_up = mp & 3;
+        if (tid >= 224)                                      // warp 7: drop the consumed scratch from L2
+        {
+            discard_lines(blk0 + (size_t)dt * TB::BLOCK, 2 * T * T / 128, lane);
+            discard_lines(rec0 + (size_t)j * kRecSlots, kRecSlots * 8 / 128, lane);
+        }
+        const typename SM::Stage &st = S.st[s];
+        uint32_t xw[4] = {0, 0, 0, 0}, xf[4] = {0, 0, 0, 0}, sel[4] = {0x4444u, 0x4444u, 0x4444u, 0x4444u};
+        uint32_t summ = 0;
+        if (act) {
+            const uint8_t *wrec = reinterpret_cast<const uint8_t *>(st.rec);
+            const uint32_t ge = wrec[(cy >> 1) * NG + (cx >> 1)];
+            int dgy = (int)(ge >> 5), dgx = (int)((ge >> 2) & 7);
+            fwd_turn(q_up, NG - 1, dgy, dgx);                // then the tile's own turn
+            const int q = q_up + (int)ge;
+            const int s2 = (int)(spos >> (2 * (q & 3))) & 3;
+            const int py = 2 * dgy + (s2 >> 1), px = 2 * dgx + (s2 & 1);
+            const uint32_t ce = cell_turns(wrec, cy, cx);
+            const uint8_t *src = reinterpret_cast<const uint8_t *>(st.src);
+            const uint4 sv = TB::load_cell(src, py, px), ev = TB::load_cell(src + TB::PLANE, py, px);
+            Cell x = {ev.x ^ sv.x, ev.y ^ sv.y, ev.z ^ sv.z, ev.w ^ sv.w};
+            Cell l;
+            if constexpr (METHOD == 0) {
+                l = {ev.x & 0x01010101u, ev.y & 0x01010101u, ev.z & 0x01010101u, ev.w & 0x01010101u};
+                if (dt == 0 && py == 0 && px == 0) l.r0 |= 0x00010101u;   // header pixels, map 1
+            } else {
+                const int dty = dt >> g.tlog, dtx = dt & (g.tilesX - 1);
+                const size_t bit0 = (size_t)img * g.HW + (size_t)(dty * T + 4 * py) * g.W + (size_t)dtx * T + 4 * px;
+                uint32_t lr[4], er[4];
+#pragma unroll
+                for (int i = 0; i < 4; i++) {
+                    const size_t bit = bit0 + (size_t)i * g.W;
+                    lr[i] = bits4_to_bytes(__ldg(map_bits + (bit >> 5)) >> (bit & 31));
+                    er[i] = bits4_to_bytes(__ldg(eta_bits + (bit >> 5)) >> (bit & 31)) << 7;   // MSB <- eta
                 }
-                xr[i] = x;
-                lr[i] = l;
+                l = {lr[0], lr[1], lr[2], lr[3]};
+                x = {(x.r0 & 0x7F7F7F7Fu) | er[0], (x.r1 & 0x7F7F7F7Fu) | er[1], (x.r2 & 0x7F7F7F7Fu) | er[2],
+                     (x.r3 & 0x7F7F7F7Fu) | er[3]};
             }
-            Cell x = {xr[0], xr[1], xr[2], xr[3]};
-            Cell l = {lr[0], lr[1], lr[2], lr[3]};
-            const int rinv = (4 - (q & 3)) & 3;
+            const int rinv = (4 - ((q + (int)ce) & 3)) & 3;
             x = cell_rot_cw(x, rinv);
             l = cell_rot_cw(l, rinv);
             if (g.emin <= 1) {
-                const uint32_t a01 = (uint32_t)(st.rec[g.lvl_off[1] + 2 * cy] >> (4 * cx)) & 0xFu;
-                const uint32_t a23 = (uint32_t)(st.rec[g.lvl_off[1] + 2 * cy + 1] >> (4 * cx)) & 0xFu;
+                const uint32_t a01 = (ce >> 2) & 0xFu, a23 = (ce >> 6) & 0xFu;
                 const int aL0 = (4 - (a01 & 3)) & 3, aR0 = (4 - (a01 >> 2)) & 3;
                 const int aL1 = (4 - (a23 & 3)) & 3, aR1 = (4 - (a23 >> 2)) & 3;
                 pair_rot_cw(x.r0, x.r1, aL0, aR0);
@@ -663,81 +780,68 @@ __device__ __forceinline__ void rec_role(const Geo &g, int img, int ty, int nK, 
                 pair_rot_cw(l.r0, l.r1, aL0, aR0);
                 pair_rot_cw(l.r2, l.r3, aL1, aR1);
             }
-            S.xo[(4 * cy) * RS + cx] = x.r0; S.xo[(4 * cy + 1) * RS + cx] = x.r1;
-            S.xo[(4 * cy + 2) * RS + cx] = x.r2; S.xo[(4 * cy + 3) * RS + cx] = x.r3;
-            S.lo[(4 * cy) * RS + cx] = l.r0; S.lo[(4 * cy + 1) * RS + cx] = l.r1;
-            S.lo[(4 * cy + 2) * RS + cx] = l.r2; S.lo[(4 * cy + 3) * RS + cx] = l.r3;
-        }
-        __syncthreads();                                           // tile j in the original domain
-        {   // the consumed scratch (destination keystream, original record) leaves L2 unwritten
-            const size_t dslot = (size_t)img * g.ntiles + dt;
-            if (tid < (T * T) / 128) discard_l2(ws.s + dslot * (T * T) + 128 * tid);
-            else if (tid >= 64 && tid < 64 + kRecSlots * 8 / 128)
-                discard_l2(ws.rec + ((size_t)img * g.ntiles + ((size_t)ty << g.tlog) + j) * kRecSlots + 16 * (tid - 64));
-        }
-        // ---- rows: SEGS threads per row, 16 pixels each.  Copy-forward 4 pixels at a time:
-        // om = PRMT(x & mask, carry, fsel[m4]) gives every byte the masked value of the last
-        // non-redundant pixel at or before it (or the carry); out = (x & ~mask) | om is exact for
-        // both kinds of pixel (a non-redundant pixel takes its own bits).
-        uint32_t xw[4] = {0, 0, 0, 0}, sel[4] = {0, 0, 0, 0};
-        uint32_t m16 = 0;
-        if (rowthr) {
+            xw[0] = x.r0; xw[1] = x.r1; xw[2] = x.r2; xw[3] = x.r3;
+            const uint32_t lw[4] = {l.r0, l.r1, l.r2, l.r3};
+            const bool col0 = j == 0 && cx == 0;             // column 0: omega starts at its bits
+            uint32_t om0[4];
 #pragma unroll
             for (int i = 0; i < 4; i++) {
-                xw[i] = S.xo[r * RS + seg * 4 + i];
-                m16 |= bytes_to_bits4(S.lo[r * RS + seg * 4 + i]) << (4 * i);
+                const uint32_t lf = lw[i] | (col0 ? 1u : 0u);
+                sel[i] = S.fsel[bytes_to_bits4(lf)];
+                xf[i] = (xw[i] & maskb) | (METHOD == 0 ? lf : (lf << 7));
+                om0[i] = __byte_perm(xf[i], 0, sel[i]);
             }
-            if (j == 0 && seg == 0) m16 |= 1u;         // column 0: omega starts at its bits
+            // the cell's 4 row summaries (byte 3 of each om0) in one word
+            summ = __byte_perm(__byte_perm(om0[0], om0[1], 0x0073), __byte_perm(om0[2], om0[3], 0x7300), 0x7610);
         }
-        uint32_t c4 = 0;                                // segment summary with a zero carry-in
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&S.empty[s]);             // the stage's data is in registers
+        if (tid == 0 && j + kStages < ntx) issue(j + kStages);
+        // inclusive scan of the summaries over the cells of the tile row (cw lanes per row)
+        uint32_t v = summ;
 #pragma unroll
-        for (int i = 0; i < 4; i++) {
-            sel[i] = S.fsel[(m16 >> (4 * i)) & 0xFu];
-            c4 = __byte_perm(__byte_perm(xw[i] & maskb, c4, sel[i]), 0, 0x3333);
+        for (int d = 1; d < cw; d <<= 1) {
+            const uint32_t u = __shfl_up_sync(0xffffffffu, v, d, cw);
+            if (cx >= d) v = combine(u, v);
         }
-        const int has = m16 != 0, val = (int)(c4 & 0xFFu);
-        int ehas = 0, evl = 0;                          // last non-redundant before this segment
-#pragma unroll
-        for (int s2 = 0; s2 < SEGS - 1; s2++) {
-            const int oh = __shfl_sync(0xffffffffu, has, s2, SEGS);
-            const int ov = __shfl_sync(0xffffffffu, val, s2, SEGS);
-            if (s2 < seg && oh) { ehas = 1; evl = ov; }
-        }
-        if (rowthr) {
-            uint32_t cin = (ehas ? (uint32_t)evl : (uint32_t)S.carry[r]) * 0x01010101u;
+        const uint32_t left = __shfl_up_sync(0xffffffffu, v, 1, cw);
+        const uint32_t cin = cx == 0 ? carry : combine(carry, left);
+        carry = combine(carry, __shfl_sync(0xffffffffu, v, hlast));
+        if (act) {
+            uint32_t o4[4];
 #pragma unroll
             for (int i = 0; i < 4; i++) {
-                const uint32_t om = __byte_perm(xw[i] & maskb, cin, sel[i]);
-                xw[i] = (xw[i] & ~maskb) | om;
-                cin = __byte_perm(om, 0, 0x3333);
+                const uint32_t cb = __byte_perm(cin, 0, 0x1111u * (uint32_t)i);   // row i's carry in every byte
+                const uint32_t om = __byte_perm(xf[i], cb, sel[i]);
+                o4[i] = (xw[i] & ~maskb) | (om & maskb);
             }
-            *reinterpret_cast<uint4 *>(O + (size_t)(ty * T + r) * g.W + (size_t)j * T + seg * 16) =
-                make_uint4(xw[0], xw[1], xw[2], xw[3]);
-            if (seg == SEGS - 1) S.carry[r] = (uint8_t)cin;   // omega leaving the tile
+            __stcs(reinterpret_cast<unsigned *>(op), o4[0]);
+            __stcs(reinterpret_cast<unsigned *>(op + W), o4[1]);
+            __stcs(reinterpret_cast<unsigned *>(op + 2 * W), o4[2]);
+            __stcs(reinterpret_cast<unsigned *>(op + 3 * W), o4[3]);
+            op += T;
         }
-        __syncthreads();                                           // xo/lo, carry, stage j reusable
+        if (++s == kStages) { s = 0; ph ^= 1u; }
     }
 }
 
 // ======================================================================================
-// The fused kernels
+// The fused kernels (dynamic shared memory: max of the two roles' needs + the pyramid)
 // ======================================================================================
 template <int TP, int METHOD>
-__global__ void __launch_bounds__(256, 6) encode_kernel(Geo g, FusedSched sc, const uint8_t *__restrict__ images,
+__global__ void __launch_bounds__(256, 5) encode_kernel(Geo g, FusedSched sc, const uint8_t *__restrict__ images,
                                                      const uint8_t *__restrict__ keys, TileWS ws,
                                                      uint8_t *__restrict__ enc, uint8_t *__restrict__ ceta,
                                                      int32_t *__restrict__ b_out, int64_t *__restrict__ cap_out,
                                                      int32_t *__restrict__ status) {
-    constexpr int T = 1 << TP, TPC = 256 / T;
-    constexpr size_t KB = (TPC + 1) * kRecSlots * 8, PB = sizeof(PermSmem<TP>);
-    __shared__ __align__(128) uint8_t smem[KB > PB ? KB : PB];
+    extern __shared__ __align__(128) uint8_t smem[];
     const Role ro = role_of(sc);
     if (ro.img >= g.B) return;
 #ifdef MMSB_PROBE_ROLES   // performance probes only (tools/role_probe.py): 1 = keystream CTAs only, 2 = workers only
     if (!((MMSB_PROBE_ROLES >> (ro.key ? 0 : 1)) & 1)) return;
 #endif
-    if (ro.key) key_role<TP, true, true, METHOD == 1>(g, ro.img, ro.idx, keys, images, ws, smem);
-    else perm_role<TP, METHOD>(g, ro.img, ro.idx, 1 << sc.lgK, images, ws, enc, ceta, b_out, cap_out, status, smem);
+    if (ro.key) key_role<TP, true, METHOD>(g, ro.img, ro.idx, keys, images, ws, smem);
+    else perm_role<TP, METHOD>(g, ro.img, ro.idx, 1 << sc.lgK, ws, enc, ceta, b_out, cap_out, status, smem);
 }
 
 template <int TP, int METHOD>
@@ -747,15 +851,13 @@ __global__ void __launch_bounds__(256, 6) recover_kernel(Geo g, FusedSched sc, c
                                                       const uint32_t *__restrict__ map_bits,
                                                       const int32_t *__restrict__ lmr_b, uint8_t *__restrict__ out,
                                                       int32_t *__restrict__ status) {
-    constexpr int T = 1 << TP, TPC = 256 / T;
-    constexpr size_t KB = (TPC + 1) * kRecSlots * 8, RB = sizeof(RecSmem<TP>);
-    __shared__ __align__(128) uint8_t smem[KB > RB ? KB : RB];
+    extern __shared__ __align__(128) uint8_t smem[];
     const Role ro = role_of(sc);
     if (ro.img >= g.B) return;
 #ifdef MMSB_PROBE_ROLES
     if (!((MMSB_PROBE_ROLES >> (ro.key ? 0 : 1)) & 1)) return;
 #endif
-    if (ro.key) key_role<TP, false, false>(g, ro.img, ro.idx, keys, nullptr, ws, smem);
+    if (ro.key) key_role<TP, false, METHOD>(g, ro.img, ro.idx, keys, marked, ws, smem);
     else rec_role<TP, METHOD>(g, ro.img, ro.idx, 1 << sc.lgK, marked, ws, eta_bits, map_bits, lmr_b, out, status, smem);
 }
 
@@ -771,8 +873,12 @@ FusedSched fused_sched(const Geo &g) {
     sc.GI = gi;
     sc.ngroups = (g.B + gi - 1) / gi;
     // keystream rows run L rows ahead of their workers: enough to hide the keystream latency,
-    // few enough that the scratch (1 B/px) and the re-read images of L groups stay in L2
-    long long lag = (12ll << 20) / ((long long)gi * g.HW);
+    // few enough that the scratch (3 B/px) and the images of L groups stay in L2
+    static const long long budget = [] {
+        const char *e = getenv("MMSB_LAG_MPX");          // tuning probe only
+        return e ? (long long)(atof(e) * (1 << 20)) : (12ll << 20);
+    }();
+    long long lag = budget / ((long long)gi * g.HW);
     sc.L = (int)(lag < 1 ? 1 : lag > 6 ? 6 : lag);
     return sc;
 }
@@ -781,15 +887,25 @@ static dim3 fused_grid(const FusedSched &sc) {
     return dim3((unsigned)((sc.GI << sc.lgK) + (sc.GI << sc.lgW)), (unsigned)(sc.ngroups + sc.L));
 }
 
+template <int TP, bool ENC>
+static size_t fused_smem(const Geo &g) {
+    const size_t k = sizeof(KSmem<TP>), w = sizeof(WSmem<TP, ENC>) + (size_t)g.npyr * 4;
+    return k > w ? k : w;
+}
+
 template <int TP>
 static void launch_encode_tp(const Geo &g, const uint8_t *images, const uint8_t *keys, const TileWS &ws, uint8_t *enc,
                              uint8_t *ceta, int32_t *b_out, int64_t *cap_out, int32_t *status, cudaStream_t st) {
     const FusedSched sc = fused_sched(g);
     const dim3 grid = fused_grid(sc);
-    if (g.method == 0)
-        encode_kernel<TP, 0><<<grid, 256, 0, st>>>(g, sc, images, keys, ws, enc, ceta, b_out, cap_out, status);
-    else
-        encode_kernel<TP, 1><<<grid, 256, 0, st>>>(g, sc, images, keys, ws, enc, ceta, b_out, cap_out, status);
+    const size_t sm = fused_smem<TP, true>(g);
+    if (g.method == 0) {
+        cudaFuncSetAttribute(encode_kernel<TP, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        encode_kernel<TP, 0><<<grid, 256, sm, st>>>(g, sc, images, keys, ws, enc, ceta, b_out, cap_out, status);
+    } else {
+        cudaFuncSetAttribute(encode_kernel<TP, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        encode_kernel<TP, 1><<<grid, 256, sm, st>>>(g, sc, images, keys, ws, enc, ceta, b_out, cap_out, status);
+    }
 }
 
 void launch_encode(const Geo &g, const uint8_t *images, const uint8_t *keys, const TileWS &ws, uint8_t *enc,
@@ -807,10 +923,14 @@ static void launch_recover_tp(const Geo &g, const uint8_t *marked, const uint8_t
                               int32_t *status, cudaStream_t st) {
     const FusedSched sc = fused_sched(g);
     const dim3 grid = fused_grid(sc);
-    if (g.method == 0)
-        recover_kernel<TP, 0><<<grid, 256, 0, st>>>(g, sc, marked, keys, ws, eta, map, lmr_b, out, status);
-    else
-        recover_kernel<TP, 1><<<grid, 256, 0, st>>>(g, sc, marked, keys, ws, eta, map, lmr_b, out, status);
+    const size_t sm = fused_smem<TP, false>(g);
+    if (g.method == 0) {
+        cudaFuncSetAttribute(recover_kernel<TP, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        recover_kernel<TP, 0><<<grid, 256, sm, st>>>(g, sc, marked, keys, ws, eta, map, lmr_b, out, status);
+    } else {
+        cudaFuncSetAttribute(recover_kernel<TP, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        recover_kernel<TP, 1><<<grid, 256, sm, st>>>(g, sc, marked, keys, ws, eta, map, lmr_b, out, status);
+    }
 }
 
 void launch_recover(const Geo &g, const uint8_t *marked, const uint8_t *keys, const TileWS &ws, const uint32_t *eta,

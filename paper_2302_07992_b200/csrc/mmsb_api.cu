@@ -62,7 +62,7 @@ static size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
 // the whole batch but are transient: each tile is written by one keystream CTA, read by one
 // worker CTA of the same launch shortly after, and then discarded from L2.
 struct Layout {
-    size_t s, rec, pyr, hist, kdone, rstate, tile_zero_end, ragg, rinc;   // fused tile kernels
+    size_t s, rec, pyr, hist, kdone, tile_zero_end;                          // fused tile kernels
     size_t states, parts, hdr, ztot, scan_zero_end, ef, counts;                // scan kernels
     size_t ceta, eta_bits, map_bits, lmr_b, lmr_t, plan, wctl, lists, mapbytes, streams, sizes, dsizes, offsets, mbuf, rstat, total;
 };
@@ -71,15 +71,12 @@ static Layout layout(const Geo &g) {
     Layout L{};
     const size_t B = (size_t)g.B, nt = (size_t)g.ntiles;
     size_t o = 0;
-    L.s = o; o = align256(o + B * g.HW);
+    L.s = o; o = align256(o + 3 * B * g.HW);                // per tile: keystream | image | label planes
     L.rec = o; o = align256(o + B * nt * kRecSlots * 8);
     L.pyr = o; o = align256(o + B * (g.npyr > 0 ? g.npyr : 1) * 4);
     L.hist = o; o = align256(o + B * kHistStride * 4);
     L.kdone = o; o = align256(o + B * 4);
-    L.rstate = o; o = align256(o + B * nt * 16);
     L.tile_zero_end = o;
-    L.ragg = o; o = align256(o + B * nt * g.T);
-    L.rinc = o; o = align256(o + B * nt * g.T);
     L.states = o; o = align256(o + B * g.nchunks * 8);
     L.parts = o; o = align256(o + B * g.nchunks * 16);
     L.hdr = o; o = align256(o + B * 4);
@@ -116,9 +113,6 @@ static TileWS tile_ws(const Layout &L, void *ws) {
     t.pyr = reinterpret_cast<uint32_t *>(w + L.pyr);
     t.hist = reinterpret_cast<uint32_t *>(w + L.hist);
     t.kdone = reinterpret_cast<uint32_t *>(w + L.kdone);
-    t.rstate = reinterpret_cast<unsigned long long *>(w + L.rstate);
-    t.ragg = reinterpret_cast<uint8_t *>(w + L.ragg);
-    t.rinc = reinterpret_cast<uint8_t *>(w + L.rinc);
     return t;
 }
 

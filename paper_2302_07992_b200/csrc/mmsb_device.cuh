@@ -176,6 +176,25 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned phase) {
         "r"(phase)
         : "memory");
 }
+// the same with a long suspend-time hint: the waiting warp sleeps in the barrier until the phase
+// completes instead of re-polling (pipeline waits of worker warps that share the SM with ALU-bound
+// keystream warps)
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, unsigned phase) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+        " @!p bra W;\n}" ::"r"(smem_u32(bar)),
+        "r"(phase), "r"(1000000u)
+        : "memory");
+}
+
+// consumer release of a pipeline stage: one arrival (count = consumer warps) on its "empty" barrier
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// generic-proxy global writes (st.global) <-> async-proxy reads (cp.async.bulk) of the same data by
+// CTAs of one launch: a proxy fence on both sides of the release / acquire
+__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 
 // shared -> global bulk copy (generic-proxy smem writes must be fenced first)
 __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
@@ -191,6 +210,20 @@ __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.
 // consumer reads (keystream tiles, angle records) never costs HBM write bandwidth
 __device__ __forceinline__ void discard_l2(const void *p) {
     asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
+}
+
+// ------------------------------------------------------------------- L2 residency hints
+// scratch that a later CTA of the same launch reads once: keep it in L2 (evict_last) until the
+// reader discards it; streamed inputs / outputs: evict first (ld/st .cs)
+__device__ __forceinline__ uint64_t l2_evict_last_policy() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void st_keep(void *a, uint4 v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v4.b32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(a), "r"(v.x), "r"(v.y), "r"(v.z),
+                 "r"(v.w), "l"(pol)
+                 : "memory");
 }
 
 // ------------------------------------------------------------------- memory ordering

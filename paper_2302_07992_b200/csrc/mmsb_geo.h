@@ -7,9 +7,10 @@ namespace mmsb {
 constexpr int kScanThreads = 256;   // threads per scan CTA
 constexpr int kScanRounds = 4;      // 16-pixel groups per thread
 constexpr int kChunk = kScanRounds * kScanThreads * 16;   // raster pixels per scan chunk (16384)
-constexpr int kRecSlots = 80;       // u64 slots of a tile's record: angles of levels 1..6 (slots 0..62),
-                                    // the in-tile 8x8-group map (bytes of slots 64..71), padding to 5 lines
-constexpr int kRecGroupSlot = 64;
+constexpr int kRecSlots = 80;       // u64 slots of a tile's in-CTA angle record: levels 1..6 (slots 0..62)
+constexpr int kWRecBytes = 384;     // a tile's worker record: group table (64 B), level-1 rows (32 x u64),
+constexpr int kWRecL1 = 64;         //   level-2 rows (16 x u32); byte offsets of the two row tables
+constexpr int kWRecL2 = 320;
 constexpr int kHistStride = 16;  // u32 per image of the label histogram (counts for b = 2..8 at index b)
 
 struct Geo {

@@ -78,16 +78,18 @@ void launch_lmr_decode(const Geo &g, bool want_eta, const uint8_t *marked, uint8
 int lmr_tile_cap_host(int t, int H, int W);
 int lmr_tile_stride_host(int t, int H, int W);
 
-// per-call device state of the fused encode / recover kernels (k_fused.cu)
+// per-call device state of the fused encode / recover kernels (k_fused.cu).  Per tile a scratch
+// block of three T x T planes (row-major, rows swapped in pairs for odd cell rows: TileBlock):
+// written by the keystream CTAs, read once by one worker CTA of the same launch with bulk copies,
+// then discarded from L2.
 struct TileWS {
-    uint8_t *s;          // [B][ntiles][T*T] K1 keystream, tile-major (transient, discarded from L2)
-    uint64_t *rec;       // [B][ntiles][kRecSlots] in-tile angle records (transient)
+    uint8_t *s;          // [B][ntiles][3][T*T] per tile: K1 keystream (destination-domain tile), the
+                         // call's input image tile (encode: I; recover: I_e'), encode's label plane
+                         // (EMR: thermometer code of p ^ left; LMR: label c | eta)
+    uint64_t *rec;       // [B][ntiles][kRecSlots] worker record: group table + cell table
     uint32_t *pyr;       // [B][npyr] upper-level block sums (mod 4 on read)        -- zeroed per call
     uint32_t *hist;      // [B][kHistStride] non-redundant counts for b = 2..8 at index b -- zeroed per call
     uint32_t *kdone;     // [B] keystream CTAs finished                               -- zeroed per call
-    unsigned long long *rstate;   // [B][ntiles][2] recover look-back: flag | row mask  -- zeroed per call
-    uint8_t *ragg;       // [B][ntiles][T] per row: last non-redundant masked value in the tile
-    uint8_t *rinc;       // [B][ntiles][T] per row: carry out of the tile
 };
 // blockIdx -> role schedule: groups of GI images (a power of two), 2^lgK keystream and 2^lgW
 // worker CTAs per image, worker CTAs of group g dispatched L grid rows after its keystream CTAs

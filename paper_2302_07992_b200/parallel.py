@@ -77,3 +77,21 @@ def aggregate(records: torch.Tensor, height: int, width: int) -> dict:
            "capacity_bits_total": int(sum(int(r[i, REC_CAP]) for i in good)),
            "psnr_inf": n_inf, "psnr_mean_finite": sum(psnr_finite) / len(psnr_finite) if psnr_finite else None}
     return out
+
+
+def gather_rows(rows: torch.Tensor, world: int, counts=None) -> torch.Tensor:
+    """Per-image rows of any dtype / width (e.g. the float64 statistics of SURVEY §8(f) NEXT 2)
+    from every rank, concatenated in rank order = image order (padded exchange when the shards
+    differ in size)."""
+    if world == 1:
+        return rows
+    n = max(counts) if counts else rows.shape[0]
+    pad = rows
+    if rows.shape[0] < n:
+        pad = torch.zeros((n,) + tuple(rows.shape[1:]), dtype=rows.dtype, device=rows.device)
+        pad[: rows.shape[0]] = rows
+    parts = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(parts, pad.contiguous())
+    if counts:
+        parts = [p[:c] for p, c in zip(parts, counts)]
+    return torch.cat(parts, 0)
