@@ -418,7 +418,10 @@ __device__ __forceinline__ void key_role(const Geo &g, int img, int kidx, const 
 // j + kStages once the 8 warps have released tile j (empty barrier, one arrival per warp).
 // ======================================================================================
 constexpr int kMaxTilesX = 512;                  // W <= 32768 with 64-pixel tiles
-constexpr int kStages = 3;
+#ifndef MMSB_STAGES
+#define MMSB_STAGES 3
+#endif
+constexpr int kStages = MMSB_STAGES;
 
 __device__ __forceinline__ uint32_t bits4_to_bytes(uint32_t m4) { return ((m4 & 0xFu) * 0x00204081u) & 0x01010101u; }
 // byte LSBs (bits 0, 8, 16, 24) -> bits 0..3: one multiply puts them at bits 21..24 (no other term lands there)
@@ -789,7 +792,7 @@ __device__ __forceinline__ void rec_role(const Geo &g, int img, int ty, int nK, 
                 const uint32_t lf = lw[i] | (col0 ? 1u : 0u);
                 sel[i] = S.fsel[bytes_to_bits4(lf)];
                 xf[i] = (xw[i] & maskb) | (METHOD == 0 ? lf : (lf << 7));
-                om0[i] = __byte_perm(xf[i], 0, sel[i]);
+                om0[i] = prmt(xf[i], 0, sel[i]);
             }
             // the cell's 4 row summaries (byte 3 of each om0) in one word
             summ = __byte_perm(__byte_perm(om0[0], om0[1], 0x0073), __byte_perm(om0[2], om0[3], 0x7300), 0x7610);
@@ -812,7 +815,7 @@ __device__ __forceinline__ void rec_role(const Geo &g, int img, int ty, int nK, 
 #pragma unroll
             for (int i = 0; i < 4; i++) {
                 const uint32_t cb = __byte_perm(cin, 0, 0x1111u * (uint32_t)i);   // row i's carry in every byte
-                const uint32_t om = __byte_perm(xf[i], cb, sel[i]);
+                const uint32_t om = prmt(xf[i], cb, sel[i]);
                 o4[i] = (xw[i] & ~maskb) | (om & maskb);
             }
             __stcs(reinterpret_cast<unsigned *>(op), o4[0]);
@@ -879,7 +882,11 @@ FusedSched fused_sched(const Geo &g) {
         return e ? (long long)(atof(e) * (1 << 20)) : (12ll << 20);
     }();
     long long lag = budget / ((long long)gi * g.HW);
-    sc.L = (int)(lag < 1 ? 1 : lag > 6 ? 6 : lag);
+    static const int lcap = [] {
+        const char *e = getenv("MMSB_LAG_CAP");           // tuning probe only
+        return e ? atoi(e) : 6;
+    }();
+    sc.L = (int)(lag < 1 ? 1 : lag > lcap ? lcap : lag);
     return sc;
 }
 

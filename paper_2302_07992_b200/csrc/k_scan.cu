@@ -92,7 +92,7 @@ __device__ __forceinline__ void embed16(uint32_t w[4], uint32_t mm, const uint32
         if constexpr (SHIFT != 8 - BP) e >>= (8 - BP - SHIFT);             // LMR: one bit lower
         // esel picks the field byte for a set pixel and the pixel's own byte otherwise, so one
         // constant-mask merge writes exactly the set pixels' fields
-        const uint32_t v = __byte_perm(e, w[j], esel[m4]);
+        const uint32_t v = prmt(e, w[j], esel[m4]);
         w[j] = (w[j] & ~(FMB * 0x01010101u)) | (v & (FMB * 0x01010101u));
         o += BP * __popc(m4);
     }
@@ -130,7 +130,7 @@ __device__ __forceinline__ void extract16(const uint32_t w[4], uint32_t mm, uint
     for (int j = 0; j < 4; j++) {
         const uint32_t m4 = (mm >> (4 * j)) & 0xFu;
         const uint32_t t = (w[j] << (8 - BP - SHIFT)) & FB;       // byte i = field of pixel i, left-aligned
-        const uint32_t c = __byte_perm(t, 0, csel[m4]);           // set pixels' fields, bytes 3, 2, ..
+        const uint32_t c = prmt(t, 0, csel[m4]);           // set pixels' fields, bytes 3, 2, ..
         const uint32_t p = bytes_to_fields<BP>(c);
         acc |= ((unsigned long long)p << 32) >> nacc;
         nacc += BP * __popc(m4);

@@ -55,6 +55,14 @@ __device__ __forceinline__ void load_key(const uint8_t *keys, int img, uint32_t 
 
 __device__ __forceinline__ uint32_t bswap32(uint32_t v) { return __byte_perm(v, 0, 0x0123); }
 
+// PRMT with a runtime selector whose nibbles are already 0..7 (from a table or built that way):
+// __byte_perm would mask the selector with 0x7777 first (one more ALU op per use)
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t s) {
+    uint32_t r;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(s));
+    return r;
+}
+
 // --------------------------------------------------------------------------------------
 // Multi-scale block rotation (eq. roration; de-rotation P:819-835).
 //
@@ -111,13 +119,13 @@ __device__ __forceinline__ Cell cell_rot_cw(Cell c, int r) {
     const bool odd = r & 1;
     // out_i = PRMT(a_i, a_{3-i}, S): S = 0x3210 (a_i), 0x0123 (rev a_i), 0x4567 (rev a_{3-i}),
     // 0x7654 (a_{3-i}) for r = 0..3, itself picked from a two-word table by one PRMT
-    const uint32_t S = __byte_perm(0x01233210u, 0x76544567u, (uint32_t)r * 0x22u + 0x10u);
+    const uint32_t S = prmt(0x01233210u, 0x76544567u, (uint32_t)r * 0x22u + 0x10u);
     const uint32_t a0 = odd ? t.r0 : c.r0, a1 = odd ? t.r1 : c.r1, a2 = odd ? t.r2 : c.r2, a3 = odd ? t.r3 : c.r3;
     Cell o;
-    o.r0 = __byte_perm(a0, a3, S);
-    o.r1 = __byte_perm(a1, a2, S);
-    o.r2 = __byte_perm(a2, a1, S);
-    o.r3 = __byte_perm(a3, a0, S);
+    o.r0 = prmt(a0, a3, S);
+    o.r1 = prmt(a1, a2, S);
+    o.r2 = prmt(a2, a1, S);
+    o.r3 = prmt(a3, a0, S);
     return o;
 }
 
@@ -132,8 +140,8 @@ __device__ __forceinline__ void pair_rot_cw(uint32_t &top, uint32_t &bot, int aL
     // the two selector bytes picked from the tables by one PRMT each: byte 0 = left table entry
     // aL, byte 1 = the right block's entry aR (the same entry + 0x22: byte offsets 2, 3)
     const uint32_t idx = (uint32_t)aL | ((uint32_t)(aR + 4) << 4);
-    uint32_t nt = __byte_perm(top, bot, __byte_perm(TOPS, TOPS + 0x22222222u, idx));
-    uint32_t nb = __byte_perm(top, bot, __byte_perm(BOTS, BOTS + 0x22222222u, idx));
+    uint32_t nt = prmt(top, bot, prmt(TOPS, TOPS + 0x22222222u, idx));
+    uint32_t nb = prmt(top, bot, prmt(BOTS, BOTS + 0x22222222u, idx));
     top = nt;
     bot = nb;
 }
