@@ -20,7 +20,10 @@
  *  - Return value = synchronous validation (E_INVAL: null pointer, unsupported shape,
  *    workspace too small; E_CUDA: a launch failed).  Data-dependent outcomes are written,
  *    asynchronously, to the per-image device array img_status[batch] (OK, CAPACITY,
- *    INTEGRITY, BADCASE, FORMAT).
+ *    INTEGRITY, BADCASE, FORMAT).  img_status = E_CUDA marks an image whose cross-CTA wait
+ *    inside encode / recover (keystream CTAs -> worker CTAs) or extract (decoupled look-back)
+ *    timed out (~2 s): those waits rely on in-order CTA dispatch, and a launch that cannot
+ *    provide it (e.g. an SM partition holding back earlier CTAs) ends instead of hanging.
  *  - `ws` is caller-allocated device scratch of at least mmsb_workspace_bytes(shape) bytes,
  *    256-byte aligned; one workspace may serve every call made on the same stream.
  */

@@ -11,7 +11,7 @@
 //       (LMR), and the per-image label histogram (eq. gliding1/2 P:604-625 reduce to the left
 //       neighbour).  The scratch planes are tile blocks (TileBlock).
 //   W (worker) CTAs -- one per strip of tiles, after the image's K CTAs have signalled.  One thread
-//       per 4x4 cell; the tiles of the strip stream through a 3-stage shared-memory ring filled by
+//       per 4x4 cell; the tiles of the strip stream through a 2-stage shared-memory ring filled by
 //       bulk copies (one elected thread, mbarrier transaction counts; consumers release a stage
 //       per warp).
 //       encode (perm_role): a3 + a5, destination cell <- rotated source cell, location map into
@@ -116,25 +116,36 @@ __device__ __forceinline__ int emr_select_b(const uint32_t *hist_img, long long 
     return best;
 }
 
-__device__ __forceinline__ void wait_keys(const TileWS &ws, int img, int nK) {
+// Cross-CTA wait of a worker on its image's keystream CTAs.  It relies on in-order CTA dispatch
+// (the keystream CTAs sit L grid rows earlier); the wait is bounded (~2 s) so that a launch that
+// cannot make progress (e.g. an SM partition that holds back earlier CTAs) ends with status
+// E_CUDA for the image instead of hanging.
+constexpr unsigned kWaitSpins = 1u << 22;
+__device__ __forceinline__ bool wait_keys(const TileWS &ws, int img, int nK) {
 #if defined(MMSB_PROBE_ROLES)
-    if (!(MMSB_PROBE_ROLES & 1)) return;            // keystream CTAs disabled: nothing to wait for
+    if (!(MMSB_PROBE_ROLES & 1)) return true;       // keystream CTAs disabled: nothing to wait for
 #endif
-    while (ld_acquire_u32(ws.kdone + img) < (unsigned)nK) __nanosleep(512);
+    for (unsigned i = 0; i < kWaitSpins; i++) {
+        if (ld_acquire_u32(ws.kdone + img) >= (unsigned)nK) return true;
+        __nanosleep(512);
+    }
+    return false;
 }
 
 // Warp 0 of a worker CTA: wait for the image's keystream CTAs, then make the upper angle
 // pyramid walkable -- copied into shared memory (spyr, sized at launch) in one parallel load.
-__device__ __forceinline__ const uint32_t *warp0_ready(const Geo &g, const TileWS &ws, int img, int nK,
-                                                       uint32_t *spyr) {
+// Returns false (every lane) if the wait timed out.
+__device__ __forceinline__ bool warp0_ready(const Geo &g, const TileWS &ws, int img, int nK, uint32_t *spyr) {
     const int lane = threadIdx.x & 31;
-    if (lane == 0) wait_keys(ws, img, nK);
-    __syncwarp();
+    int ok = 1;
+    if (lane == 0) ok = wait_keys(ws, img, nK) ? 1 : 0;
+    ok = __shfl_sync(0xffffffffu, ok, 0);
+    if (!ok) return false;
     fence_proxy_async_global();                      // the scratch the bulk copies will read
     const uint32_t *pyr_img = ws.pyr + (size_t)img * g.npyr;
     for (int i = lane; i < g.npyr; i += 32) spyr[i] = __ldcg(pyr_img + i);
     __syncwarp();
-    return spyr;
+    return true;
 }
 
 // ======================================================================================
@@ -419,7 +430,7 @@ __device__ __forceinline__ void key_role(const Geo &g, int img, int kidx, const 
 // ======================================================================================
 constexpr int kMaxTilesX = 512;                  // W <= 32768 with 64-pixel tiles
 #ifndef MMSB_STAGES
-#define MMSB_STAGES 3
+#define MMSB_STAGES 2
 #endif
 constexpr int kStages = MMSB_STAGES;
 
@@ -494,15 +505,22 @@ __device__ __forceinline__ void perm_role(const Geo &g, int img, int dty, int nK
         }
     }
     if (tid < 32) {
-        const uint32_t *pyr = warp0_ready(g, ws, img, nK, spyr);
-        for (int j = tid; j < g.tilesX; j += 32) {
-            int sty, stx, q;
-            upper_walk_inverse(g, pyr, dty, j, sty, stx, q);
-            S.map[j] = (((sty << g.tlog) + stx) << 2) | q;
+        const bool ok = warp0_ready(g, ws, img, nK, spyr);
+        if (ok) {
+            for (int j = tid; j < g.tilesX; j += 32) {
+                int sty, stx, q;
+                upper_walk_inverse(g, spyr, dty, j, sty, stx, q);
+                S.map[j] = (((sty << g.tlog) + stx) << 2) | q;
+            }
         }
-        if (tid == 0) S.sh[0] = METHOD == 0 ? emr_select_b(ws.hist + img * kHistStride, g.HW) : 0;
+        if (tid == 0) {
+            S.sh[0] = METHOD == 0 && ok ? emr_select_b(ws.hist + img * kHistStride, g.HW) : 0;
+            S.sh[1] = ok;
+            if (!ok) status[img] = 6;                       // MMSB_E_CUDA: keystream CTAs never arrived
+        }
     }
     __syncthreads();
+    if (!S.sh[1]) return;
     const int b = S.sh[0];
     const int ntx = g.tilesX;
     const uint8_t *blk0 = ws.s + (size_t)img * g.ntiles * TB::BLOCK;      // the image's scratch blocks
@@ -671,11 +689,15 @@ __device__ __forceinline__ void rec_role(const Geo &g, int img, int ty, int nK, 
         }
         b = __shfl_sync(0xffffffffu, b, 0);
         if (b > 0) {
-            const uint32_t *pyr = warp0_ready(g, ws, img, nK, spyr);
-            for (int j = tid; j < g.tilesX; j += 32) {
-                int dty, dtx, q;
-                upper_walk_forward(g, pyr, ty, j, dty, dtx, q);
-                S.map[j] = (((dty << g.tlog) + dtx) << 2) | q;
+            if (warp0_ready(g, ws, img, nK, spyr)) {
+                for (int j = tid; j < g.tilesX; j += 32) {
+                    int dty, dtx, q;
+                    upper_walk_forward(g, spyr, ty, j, dty, dtx, q);
+                    S.map[j] = (((dty << g.tlog) + dtx) << 2) | q;
+                }
+            } else if (tid == 0) {
+                S.sh[0] = 0;
+                status[img] = 6;                            // MMSB_E_CUDA: keystream CTAs never arrived
             }
         }
     }
@@ -832,7 +854,7 @@ __device__ __forceinline__ void rec_role(const Geo &g, int img, int ty, int nK, 
 // The fused kernels (dynamic shared memory: max of the two roles' needs + the pyramid)
 // ======================================================================================
 template <int TP, int METHOD>
-__global__ void __launch_bounds__(256, 5) encode_kernel(Geo g, FusedSched sc, const uint8_t *__restrict__ images,
+__global__ void __launch_bounds__(256, 6) encode_kernel(Geo g, FusedSched sc, const uint8_t *__restrict__ images,
                                                      const uint8_t *__restrict__ keys, TileWS ws,
                                                      uint8_t *__restrict__ enc, uint8_t *__restrict__ ceta,
                                                      int32_t *__restrict__ b_out, int64_t *__restrict__ cap_out,

@@ -359,7 +359,13 @@ __global__ void __launch_bounds__(kScanThreads, EMBED ? 5 : 6) scan_kernel(Geo g
                 const int k = base - lane;
                 unsigned long long v = kFlagInc;                 // before chunk 0: inclusive 0
                 if (k >= 0) {
-                    do { v = ld_relaxed(st + k); } while ((v & ~kValMask) == 0);
+                    // bounded: a predecessor that never publishes (no in-order dispatch) ends the
+                    // walk with status E_CUDA for the image instead of a hang
+                    unsigned spins = 0;
+                    while (((v = ld_relaxed(st + k)) & ~kValMask) == 0) {
+                        if (++spins > (1u << 22)) { atomicOr(ws.err + img, 1u); v = kFlagInc; break; }
+                        if (spins > 64) __nanosleep(256);
+                    }
                 }
                 const unsigned inc = __ballot_sync(0xffffffffu, (v & ~kValMask) == kFlagInc);
                 const int last = inc ? __ffs(inc) - 1 : 31;
@@ -616,12 +622,13 @@ __global__ void __launch_bounds__(256) scan_finish_kernel(Geo g, const uint8_t *
         }
         __syncthreads();
         if (tid == 0) {
+            const bool lost = __ldcg(ws.err + img) != 0;     // a look-back wait timed out
             const long long n = C >= 32 ? (long long)__ldcg(ws.hdr + img) : -1;
-            const bool ok = fits && C >= 32 && n <= C - 32;
+            const bool ok = !lost && fits && C >= 32 && n <= C - 32;
             sh[0] = fits ? C : 0;
             sh[1] = ok ? n : -1;
             msg_bits_out[img] = ok ? n : -1;
-            status[img] = ok ? 0 : (fits ? 4 : 2);            // region beyond the caller's rows: E_INVAL
+            status[img] = lost ? 6 : ok ? 0 : (fits ? 4 : 2);  // region beyond the caller's rows: E_INVAL
         }
         __syncthreads();
         const long long Cf = sh[0], nn = sh[1];

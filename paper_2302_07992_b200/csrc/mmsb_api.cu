@@ -63,7 +63,7 @@ static size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
 // worker CTA of the same launch shortly after, and then discarded from L2.
 struct Layout {
     size_t s, rec, pyr, hist, kdone, tile_zero_end;                          // fused tile kernels
-    size_t states, parts, hdr, ztot, scan_zero_end, ef, counts;                // scan kernels
+    size_t states, parts, hdr, ztot, err, scan_zero_end, ef, counts;           // scan kernels
     size_t ceta, eta_bits, map_bits, lmr_b, lmr_t, plan, wctl, lists, mapbytes, streams, sizes, dsizes, offsets, mbuf, rstat, total;
 };
 
@@ -81,6 +81,7 @@ static Layout layout(const Geo &g) {
     L.parts = o; o = align256(o + B * g.nchunks * 16);
     L.hdr = o; o = align256(o + B * 4);
     L.ztot = o; o = align256(o + B * 8);
+    L.err = o; o = align256(o + B * 4);
     L.scan_zero_end = o;
     L.ef = o; o = align256(o + B * (size_t)ef_words_of(g.HW) * 4);
     L.counts = o; o = align256(o + B * g.nchunks * 4);
@@ -103,6 +104,14 @@ static Layout layout(const Geo &g) {
     L.rstat = o; o = align256(o + B * 4);
     L.total = o;
     return L;
+}
+
+static ScanWS scan_ws(const Geo &g, const Layout &L, void *ws) {
+    char *w = static_cast<char *>(ws);
+    return ScanWS{reinterpret_cast<unsigned long long *>(w + L.states), reinterpret_cast<unsigned long long *>(w + L.parts),
+                  reinterpret_cast<uint32_t *>(w + L.hdr), reinterpret_cast<uint32_t *>(w + L.ef), ef_words_of(g.HW),
+                  reinterpret_cast<uint32_t *>(w + L.counts), reinterpret_cast<unsigned long long *>(w + L.ztot),
+                  reinterpret_cast<uint32_t *>(w + L.err)};
 }
 
 static TileWS tile_ws(const Layout &L, void *ws) {
@@ -201,9 +210,7 @@ mmsb_status mmsb_hider_embed(const mmsb_shape *shape, const uint8_t *encrypted, 
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (cudaMemsetAsync(at<char>(ws, L.states), 0, L.scan_zero_end - L.states, st) != cudaSuccess) return MMSB_E_CUDA;
     if (g.method == 1) lmr_decode_all(g, L, false, encrypted, ws, img_status, nullptr, st);
-    ScanWS sw{at<unsigned long long>(ws, L.states), at<unsigned long long>(ws, L.parts), at<uint32_t>(ws, L.hdr),
-              at<uint32_t>(ws, L.ef), ef_words_of(g.HW), at<uint32_t>(ws, L.counts),
-              at<unsigned long long>(ws, L.ztot)};
+    const ScanWS sw = scan_ws(g, L, ws);
     run_kernel(K_EMBED, st, (long long)g.B * g.HW, [&] {
         launch_scan(g, true, encrypted, marked, k2, msg_bytes, msg_bits, stride_bytes, nullptr, nullptr, img_status,
                     sw, at<uint32_t>(ws, L.map_bits), at<int32_t>(ws, L.lmr_b), st);
@@ -224,9 +231,7 @@ mmsb_status mmsb_receiver_extract(const mmsb_shape *shape, const uint8_t *marked
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (cudaMemsetAsync(at<char>(ws, L.states), 0, L.scan_zero_end - L.states, st) != cudaSuccess) return MMSB_E_CUDA;
     if (g.method == 1) lmr_decode_all(g, L, false, marked, ws, img_status, msg_bits_out, st);
-    ScanWS sw{at<unsigned long long>(ws, L.states), at<unsigned long long>(ws, L.parts), at<uint32_t>(ws, L.hdr),
-              at<uint32_t>(ws, L.ef), ef_words_of(g.HW), at<uint32_t>(ws, L.counts),
-              at<unsigned long long>(ws, L.ztot)};
+    const ScanWS sw = scan_ws(g, L, ws);
     run_kernel(K_EXTRACT, st, (long long)g.B * g.HW, [&] {
         launch_scan(g, false, marked, nullptr, k2, nullptr, nullptr, stride_bytes, msg_out, msg_bits_out,
                     img_status, sw, at<uint32_t>(ws, L.map_bits), at<int32_t>(ws, L.lmr_b), st);
@@ -266,9 +271,7 @@ mmsb_status mmsb_receiver_both(const mmsb_shape *shape, const uint8_t *marked, c
     if (cudaMemsetAsync(rstat, 0, (size_t)g.B * 4, st) != cudaSuccess) return MMSB_E_CUDA;
     // LMR: the coded maps (eta and the location map) are decoded once for both parties' steps
     if (g.method == 1) lmr_decode_all(g, L, true, marked, ws, img_status, msg_bits_out, st);
-    ScanWS sw{at<unsigned long long>(ws, L.states), at<unsigned long long>(ws, L.parts), at<uint32_t>(ws, L.hdr),
-              at<uint32_t>(ws, L.ef), ef_words_of(g.HW), at<uint32_t>(ws, L.counts),
-              at<unsigned long long>(ws, L.ztot)};
+    const ScanWS sw = scan_ws(g, L, ws);
     run_kernel(K_EXTRACT, st, (long long)g.B * g.HW, [&] {
         launch_scan(g, false, marked, nullptr, k2, nullptr, nullptr, stride_bytes, msg_out, msg_bits_out,
                     img_status, sw, at<uint32_t>(ws, L.map_bits), at<int32_t>(ws, L.lmr_b), st);

@@ -15,6 +15,7 @@ struct ScanWS {
     long long ef_words;              // words per image: ceil(7 HW / 512) + 1 ChaCha blocks of 16
     uint32_t *counts;                // [B][nchunks] zero pixels per chunk (embed: scan_count_kernel)
     unsigned long long *ztot;        // [B] zero pixels per image (embed)                -- zeroed per call
+    uint32_t *err;                   // [B] a look-back wait timed out (status E_CUDA)  -- zeroed per call
 };
 __host__ __device__ inline long long ef_words_of(long long HW) { return ((7 * HW + 511) / 512 + 1) * 16; }
 

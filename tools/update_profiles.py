@@ -1,8 +1,10 @@
 """Copies the evidence of one tools/gpu_profile.sh run from gpurun_out/ into profiles/ (tracked):
-bench lines, the ncu launch list summary, the ncu --set full summary / instruction mix, and the
-per-kernel dram traffic per pixel that bench.py reports as roofline.traffic.
+the default bench line, the ncu launch list summary, the ncu --set full summary and instruction
+mix of one EMR step at the benched size (1000 x 512^2), and the per-kernel DRAM traffic that
+bench.py reports as roofline.traffic -- with the algorithmic bytes of SURVEY §8(d) beside it
+(the wasted-traffic ratio).
 
-  python tools/update_profiles.py r01
+  python tools/update_profiles.py r02
 """
 import csv
 import json
@@ -13,9 +15,16 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT, PROF = os.path.join(ROOT, "gpurun_out"), os.path.join(ROOT, "profiles")
-NAME_MAP = {"encode_kernel": "encode_kernel", "recover_kernel": "recover_kernel",
-            "scan_kernel<0, 1>": "embed_prep+scan_kernel<embed>+finish", "scan_kernel<0, 0>": "scan_kernel<extract>+finish",
-            "stats_kernel": "stats_kernel"}
+sys.path.insert(0, os.path.join(ROOT, "tools"))
+import ncu_mix  # noqa: E402
+
+PX = 1000 * 512 * 512                     # tools/prof_run.py --batch 1000 (config-2 images, EMR)
+# the bench's kernel classes (bench.kernel_model names) and the launches of one step they cover
+CLASSES = {"encode_kernel": ["encode_kernel"],
+           "embed_prep+scan_kernel<embed>+finish": ["embed_prep_kernel", "scan_kernel<0, 1>", "scan_finish_kernel<0, 1>"],
+           "scan_kernel<extract>+finish": ["scan_kernel<0, 0>", "scan_finish_kernel<0, 0>"],
+           "recover_kernel": ["recover_kernel"],
+           "stats_kernel": ["stats_kernel"]}
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
 
@@ -24,59 +33,87 @@ def run(cmd):
 
 
 def main(tag):
-    shutil.copy(os.path.join(OUT, "bench_full.log"), os.path.join(PROF, f"{tag}_bench_emr_config2.json"))
-    shutil.copy(os.path.join(OUT, "bench_lmr.log"), os.path.join(PROF, f"{tag}_bench_lmr_config3.json"))
+    sys.path.insert(0, ROOT)
+    import bench
+
+    line = json.loads([x for x in open(os.path.join(OUT, "bench_full.log")) if x.startswith("{")][-1])
+    with open(os.path.join(PROF, f"{tag}_bench_default.json"), "w") as f:
+        json.dump(line, f, indent=1)
+    der = line["mean_der_bpp"]
     with open(os.path.join(PROF, f"{tag}_launches_emr.txt"), "w") as f:
         f.write(run([sys.executable, "tools/ncu_summary.py", "gpurun_out/launches_emr.csv"]))
     rep = os.path.join(OUT, "prof_all.ncu-rep")
     with open(os.path.join(PROF, f"{tag}_ncu_full_summary.txt"), "w") as f:
+        f.write(f"# ncu --set full --clock-control none, one EMR step of tools/prof_run.py --batch 1000 "
+                f"(config-2 images, {PX} px, inputs 4x the L2)\n")
         f.write(run([sys.executable, "tools/ncu_brief.py", rep]))
-    with open(os.path.join(PROF, f"{tag}_ncu_instruction_mix.txt"), "w") as f:
-        for k in ("encode_kernel", "recover_kernel", "scan_kernel"):
-            f.write(f"=== {k} (first launch matching)\n")
-            f.write(run([sys.executable, "tools/ncu_mix.py", rep, k]))
     rows = list(csv.reader(run(["ncu", "-i", rep, "--page", "raw", "--csv"]).splitlines()))
     hdr, units, data = rows[0], rows[1], rows[2:]
     idx = {h: i for i, h in enumerate(hdr)}
-    px = 128 * 512 * 512                     # tools/prof_run.py --batch 128 (config-2 images)
-    per_px, launches = {}, {}
+
+    def val(d, k):
+        return float(d[idx[k]]) * SCALE.get(units[idx[k]], 1)
+
+    per = {}
     for d in data:
-        key = [v for k, v in NAME_MAP.items() if k in d[idx["Kernel Name"]]]
-        if not key:
-            continue
-        rd = float(d[idx["dram__bytes_read.sum"]]) * SCALE[units[idx["dram__bytes_read.sum"]]]
-        wr = float(d[idx["dram__bytes_write.sum"]]) * SCALE[units[idx["dram__bytes_write.sum"]]]
-        per_px[key[0]] = (rd + wr) / px
-        launches[key[0]] = {"dram_read_bytes": rd, "dram_write_bytes": wr, "pixels": px,
-                            "duration_us": float(d[idx["gpu__time_duration.sum"]]),
-                            "alu_pipe_pct": float(d[idx["sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"]]),
-                            "issue_active_pct": float(d[idx["smsp__issue_active.avg.pct_of_peak_sustained_active"]])}
-    # LMR tile coder (units = coded symbols, as bench.py's profile counts them): wave 0 of an
-    # encode (eta + candidate 0 of 1000 config-3 images, 16 tiles of 16384 symbols each) and one
-    # decode (the map plane), from gpurun_out/prof_coder*.ncu-rep / prof_dec*.ncu-rep when present
-    for name, pattern, syms in (("coder_encode_kernel", "prof_coder", 1000 * 2 * 16 * 16384),
-                                ("lmr_pack+header+coder_decode_kernels", "prof_dec", 1000 * 16 * 16384)):
-        reps = sorted((f for f in os.listdir(OUT) if f.startswith(pattern) and f.endswith(".ncu-rep")),
-                      key=lambda f: os.path.getmtime(os.path.join(OUT, f)))
-        if not reps:
-            continue
-        rr = list(csv.reader(run(["ncu", "-i", os.path.join(OUT, reps[-1]), "--page", "raw", "--csv"]).splitlines()))
-        h2, u2, d2 = rr[0], rr[1], rr[2]
-        i2 = {h: i for i, h in enumerate(h2)}
-        rd = float(d2[i2["dram__bytes_read.sum"]]) * SCALE[u2[i2["dram__bytes_read.sum"]]]
-        wr = float(d2[i2["dram__bytes_write.sum"]]) * SCALE[u2[i2["dram__bytes_write.sum"]]]
-        per_px[name] = (rd + wr) / syms
-        launches[name] = {"dram_read_bytes": rd, "dram_write_bytes": wr, "symbols": syms, "report": reps[-1],
-                          "duration_us": float(d2[i2["gpu__time_duration.sum"]]),
-                          "alu_pipe_pct": float(d2[i2["sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"]]),
-                          "issue_active_pct": float(d2[i2["smsp__issue_active.avg.pct_of_peak_sustained_active"]])}
-    json.dump({"source": f"ncu --set full --clock-control none, tools/prof_run.py --batch 128 (config-2 images, "
-                         f"EMR), {tag}; cold-cache serialized replay: writes still resident in L2 at kernel end "
-                         f"are not counted; the LMR coder entries are bytes per coded symbol (config 3)",
-               "bytes_per_px": per_px, "launches": launches},
+        name = d[idx["Kernel Name"]]
+        per.setdefault(name, []).append(d)
+    mixf = open(os.path.join(PROF, f"{tag}_ncu_instruction_mix.txt"), "w")
+    mixf.write("# executed-instruction mix per kernel (tools/ncu_mix.py: source page, one count per SASS address).\n"
+               "# smsp__inst_executed.sum is the raw-page counter of the same capture; the source page comes from\n"
+               "# another replay pass, so the two differ by the timing-dependent wait loops (SYNCS try_wait,\n"
+               "# NANOSLEEP of the cross-CTA waits and their branches).\n")
+    traffic, launches = {}, {}
+    for cls, parts in CLASSES.items():
+        rd = wr = dur = 0.0
+        for part in parts:
+            hits = [n for n in per if n.split("(")[0].split("::")[-1].replace("void ", "").strip().startswith(part)
+                    or (part in n and "<" in part)]
+            for n in hits:
+                d = per[n][0]
+                rd += val(d, "dram__bytes_read.sum")
+                wr += val(d, "dram__bytes_write.sum")
+                dur += float(d[idx["gpu__time_duration.sum"]])
+                mixf.write(f"=== {n[:100]}\n    smsp__inst_executed.sum {float(d[idx['smsp__inst_executed.sum']]):.0f}\n")
+                tot, alu, fma = 0, 0, 0
+                import io
+                import contextlib
+                buf = io.StringIO()
+                with contextlib.redirect_stdout(buf):
+                    kname = part.split("<")[0]
+                    skip = 1 if part == "scan_kernel<0, 0>" else 0
+                    ncu_mix.main(rep, kname, 0, 10 ** 9, skip)
+                mixf.write("    " + buf.getvalue().replace("\n", "\n    ").rstrip() + "\n")
+        alg = bench.kernel_model(cls, der)["bytes"]
+        traffic[cls] = (rd + wr) / PX
+        launches[cls] = {"dram_read_bytes": rd, "dram_write_bytes": wr, "pixels": PX, "duration_us": dur,
+                         "dram_bytes_per_px": (rd + wr) / PX, "algorithmic_bytes_per_px": alg,
+                         "wasted_ratio": (rd + wr) / PX / alg if alg else None}
+        d0 = per[[n for n in per if parts[0].split("<")[0] in n][0]][0]
+        for k, kk in (("alu_pipe_pct", "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"),
+                      ("issue_active_pct", "smsp__issue_active.avg.pct_of_peak_sustained_active")):
+            launches[cls][k] = float(d0[idx[kk]])
+    mixf.close()
+    old = {}
+    try:
+        old = json.load(open(os.path.join(PROF, "traffic.json")))
+    except Exception:
+        pass
+    for k in ("coder_encode_kernel", "lmr_pack+header+coder_decode_kernels"):   # LMR coder entries (config 3)
+        if k in old.get("bytes_per_px", {}):
+            traffic[k] = old["bytes_per_px"][k]
+            launches[k] = old["launches"][k]
+    json.dump({"source": f"ncu --set full --clock-control none, one EMR step of tools/prof_run.py --batch 1000 "
+                         f"(config-2 images, inputs 4x the L2), {tag}; per kernel class the DRAM bytes of its "
+                         f"launches per pixel beside SURVEY 8(d)'s algorithmic bytes (d = {der:.3f}); the LMR "
+                         f"coder entries are bytes per coded symbol (config 3, r01)",
+               "bytes_per_px": traffic, "launches": launches},
               open(os.path.join(PROF, "traffic.json"), "w"), indent=1)
-    print(json.dumps(per_px, indent=1))
+    for k, v in launches.items():
+        if "wasted_ratio" in v:
+            print(f"{k:40s} dram {v['dram_bytes_per_px']:.3f} B/px  algorithmic {v['algorithmic_bytes_per_px']:.3f}"
+                  f"  ratio {v['wasted_ratio'] if v['wasted_ratio'] is None else round(v['wasted_ratio'], 3)}")
 
 
 if __name__ == "__main__":
-    main(sys.argv[1] if len(sys.argv) > 1 else "r01")
+    main(sys.argv[1] if len(sys.argv) > 1 else "r02")
