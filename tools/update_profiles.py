@@ -81,7 +81,7 @@ def main(tag):
                 buf = io.StringIO()
                 with contextlib.redirect_stdout(buf):
                     kname = part.split("<")[0]
-                    skip = 1 if part == "scan_kernel<0, 0>" else 0
+                    skip = 1 if part in ("scan_kernel<0, 0>", "scan_finish_kernel<0, 0>") else 0
                     ncu_mix.main(rep, kname, 0, 10 ** 9, skip)
                 mixf.write("    " + buf.getvalue().replace("\n", "\n    ").rstrip() + "\n")
         alg = bench.kernel_model(cls, der)["bytes"]
