@@ -3,8 +3,8 @@
 
 One step = the whole hot path over one batch: content-owner encode (K1),
 hider embed (K2, full-capacity payload n = C - 32), receiver extract (K2), receiver recover
-(K1) and the per-image statistics (SSE -> DER/PSNR; all_gather of the per-image records
-over NCCL when N > 1).  Weak scaling by default (every rank processes its own batch of the
+(K1) with the per-image statistics' SSE fused into it (mmsb_receiver_recover_sse; SSE ->
+DER/PSNR; all_gather of the per-image records over NCCL when N > 1).  Weak scaling by default (every rank processes its own batch of the
 workload); --shard splits the config's batch across the ranks instead (strong scaling, the
 "10 000 images sharded across 1/2/4/8" of config 4).
 
@@ -431,8 +431,7 @@ def measure(args, rank, world, local, config=None, method=None):
         _, b, c, st_e = G.encode(mid, I_, K1_, ws, out=enc)
         _, st_h = G.embed(mid, enc, K2_, MSG_, NB_, ws, out=marked)
         _, nb_out, st_x = G.extract(mid, marked, K2_, stride, ws, out=MOUT)
-        _, st_r = G.recover(mid, marked, K1_, ws, out=rec)
-        G.stats(I_, rec, out=SSE)
+        _, st_r, _ = G.recover(mid, marked, K1_, ws, out=rec, original=I_, sse_out=SSE)   # + statistics (SSE)
         last[:] = [b, c, st_r, st_x, nb_out, st_e, st_h]
         if world > 1:   # the path's one exchange: per-image records to every rank (NCCL)
             records.copy_(P.make_records(b, c, SSE, st_r))
@@ -615,8 +614,7 @@ def measure_e2e(args, G, P, dev, stream, world, mid, B, H, W, stride, imgs, k1, 
                 _, b_, c_, _ = G.encode(mid, L.I, L.K1, L.ws, out=L.enc)
                 G.embed(mid, L.enc, L.K2, L.MSG, L.NB, L.ws, out=L.marked)
                 G.extract(mid, L.marked, L.K2, stride, L.ws, out=L.MOUT)
-                _, st_ = G.recover(mid, L.marked, L.K1, L.ws, out=L.rec)
-                G.stats(L.I, L.rec, out=L.SSE)
+                _, st_, _ = G.recover(mid, L.marked, L.K1, L.ws, out=L.rec, original=L.I, sse_out=L.SSE)
                 if world > 1:
                     records[a:z] = P.make_records(b_, c_, L.SSE, st_)
                 L.computed.record(L.stream)
@@ -755,6 +753,7 @@ def kernel_model(name, der):
     return {
         "encode_kernel": dict(bytes=2.0, alu=CHACHA_ALU_PER_BYTE * 1.0),
         "recover_kernel": dict(bytes=2.0, alu=CHACHA_ALU_PER_BYTE * 1.0),
+        "recover_kernel+sse": dict(bytes=3.0, alu=CHACHA_ALU_PER_BYTE * 1.0),     # + read of I for the SSE
         "embed_prep+scan_kernel<embed>+finish": dict(bytes=2.0 + d8, alu=CHACHA_ALU_PER_BYTE * d8),
         "scan_kernel<extract>+finish": dict(bytes=1.0 + d8, alu=CHACHA_ALU_PER_BYTE * d8),
         "stats_kernel": dict(bytes=2.0, alu=0.0),
@@ -781,14 +780,15 @@ def load_traffic():
 def step_hbm(kern, mpx_s, der, peaks):
     """The metric's "% HBM roofline" per GPU (mpx_s = this GPU's pixel rate).  SURVEY §8(d):
     algorithmic bytes per pixel encode 2, embed 2 + d/8, extract 1 + d/8, recover 2 -> 7 + d/4
-    for the four calls; the timed step also runs the statistics call (SSE, 2 B/px: read I and
-    I'), so the step's own total is 9 + d/4 (both reported).  The three receiver-side calls
-    (embed + extract + recover, 5 + d/4) get their pixel rate from their share of the kernel time."""
+    for the four calls; the timed step also computes the statistics' SSE, fused into the recovery
+    (+1 B/px: the read of I), so the step's own total is 8 + d/4 (both reported).  The three
+    receiver-side calls (embed + extract + recover, 5 + d/4) get their pixel rate from their
+    share of the kernel time."""
     hbm = float(peaks.get("hbm_gbs", 6650.0))
     d8 = der / 8.0
     four = 7.0 + 2 * d8
-    step_b = four + 2.0
-    out = {"bytes_per_px": step_b, "bytes_per_px_note": "4 calls 7 + d/4 (SURVEY 8(d)) + statistics 2",
+    step_b = four + 1.0
+    out = {"bytes_per_px": step_b, "bytes_per_px_note": "4 calls 7 + d/4 (SURVEY 8(d)) + the SSE's read of I 1",
            "achieved_GBps": step_b * mpx_s * 1e6 / 1e9, "peak": hbm}
     out["frac"] = out["achieved_GBps"] / hbm
     out["four_calls"] = {"bytes_per_px": four, "achieved_GBps": four * mpx_s * 1e6 / 1e9,

@@ -117,6 +117,18 @@ mmsb_status mmsb_receiver_recover(const mmsb_shape *shape, const uint8_t *marked
                                   void *stream);
 
 /*
+ * The same recovery fused with the statistics call's SSE (evaluation harnesses only: the
+ * receiver of the protocol does not hold the original).  sse_out[i] = sum over pixels of
+ * (original - recovered)^2 as int64 (PSNR P:746 via mmsb_der_psnr_host), computed from the
+ * recovered pixels while they are in registers: no second pass over I and I'.  original is
+ * [B][H][W] device memory; sse_out [B] int64 device memory (written, not accumulated);
+ * recovered and img_status exactly as mmsb_receiver_recover.
+ */
+mmsb_status mmsb_receiver_recover_sse(const mmsb_shape *shape, const uint8_t *marked, const uint8_t *k1,
+                                      const uint8_t *original, uint8_t *recovered, int64_t *sse_out,
+                                      int32_t *img_status, void *ws, size_t ws_bytes, void *stream);
+
+/*
  * Capacity query (the SPEC's `capacity`): what an encrypted or marked image
  * offers, derived the way the hider and the K2 receiver derive it -- no key needed.  b from the
  * header (EMR: the LSBs of pixels 0..2, reading Q14; LMR: the MSB-plane header) and

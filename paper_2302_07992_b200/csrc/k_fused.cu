@@ -655,11 +655,13 @@ __device__ __forceinline__ void perm_role(const Geo &g, int img, int dty, int nK
 //       tile row (combine = "right if flagged else left", per byte) gives each cell its carry,
 //       the tile's carry moves on to the next tile of the strip in a register.
 // ======================================================================================
-template <int TP, int METHOD>
+template <int TP, int METHOD, bool SSE>
 __device__ __forceinline__ void rec_role(const Geo &g, int img, int ty, int nK, const uint8_t *__restrict__ marked,
                                          const TileWS &ws, const uint32_t *__restrict__ eta_bits,
                                          const uint32_t *__restrict__ map_bits, const int32_t *__restrict__ lmr_b,
-                                         uint8_t *__restrict__ out, int32_t *__restrict__ status, uint8_t *smem) {
+                                         uint8_t *__restrict__ out, int32_t *__restrict__ status,
+                                         const uint8_t *__restrict__ orig, unsigned long long *__restrict__ sse,
+                                         uint8_t *smem) {
     constexpr int T = 1 << TP, NC = T / 4, NG = NC / 2;
     using TB = TileBlock<T>;
     using SM = WSmem<TP, false>;
@@ -704,9 +706,21 @@ __device__ __forceinline__ void rec_role(const Geo &g, int img, int ty, int nK, 
     __syncthreads();
     const int b = S.sh[0];
     if (b <= 0) {                                       // FORMAT / BADCASE: zero-filled output
+        uint32_t sq0 = 0;
         for (int c = tid; c < T * g.W / 16; c += 256) {
             const int r = c / (g.W / 16), col = c % (g.W / 16);
-            *reinterpret_cast<uint4 *>(O + (size_t)(ty * T + r) * g.W + col * 16) = make_uint4(0, 0, 0, 0);
+            const size_t off = (size_t)(ty * T + r) * g.W + col * 16;
+            *reinterpret_cast<uint4 *>(O + off) = make_uint4(0, 0, 0, 0);
+            if constexpr (SSE) {                         // (I - 0)^2
+                const uint4 v = __ldcs(reinterpret_cast<const uint4 *>(orig + (size_t)img * g.HW + off));
+                sq0 = __dp4a(v.x, v.x, __dp4a(v.y, v.y, __dp4a(v.z, v.z, __dp4a(v.w, v.w, sq0))));
+            }
+        }
+        if constexpr (SSE) {
+            unsigned long long v = sq0;
+#pragma unroll
+            for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+            if (lane == 0 && v) atomicAdd(sse + img, v);
         }
         return;
     }
@@ -749,6 +763,8 @@ __device__ __forceinline__ void rec_role(const Geo &g, int img, int ty, int nK, 
     uint32_t carry = 0;                                  // summaries leaving the previous tile (4 rows)
     const size_t W = (size_t)g.W;
     uint8_t *op = O + (size_t)(ty * T + 4 * cy) * W + 4 * cx;   // this cell's rows in tile 0 of the strip
+    const uint8_t *ip = SSE ? orig + (size_t)img * g.HW + (size_t)(ty * T + 4 * cy) * W + 4 * cx : nullptr;
+    uint32_t sq = 0;                                     // SSE of this thread's cells (<= 2^31 per strip)
 
     int s = 0;
     unsigned ph = 0;
@@ -845,8 +861,22 @@ __device__ __forceinline__ void rec_role(const Geo &g, int img, int ty, int nK, 
             __stcs(reinterpret_cast<unsigned *>(op + 2 * W), o4[2]);
             __stcs(reinterpret_cast<unsigned *>(op + 3 * W), o4[3]);
             op += T;
+            if constexpr (SSE) {                             // (I - I')^2 of the cell
+#pragma unroll
+                for (int i = 0; i < 4; i++) {
+                    const uint32_t d = __vabsdiffu4(__ldcs(reinterpret_cast<const unsigned *>(ip + i * W)), o4[i]);
+                    sq = __dp4a(d, d, sq);
+                }
+                ip += T;
+            }
         }
         if (++s == kStages) { s = 0; ph ^= 1u; }
+    }
+    if constexpr (SSE) {                                 // the strip's sum: one atomic per warp
+        unsigned long long v = sq;
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+        if (lane == 0 && v) atomicAdd(sse + img, v);
     }
 }
 
@@ -869,13 +899,14 @@ __global__ void __launch_bounds__(256, 6) encode_kernel(Geo g, FusedSched sc, co
     else perm_role<TP, METHOD>(g, ro.img, ro.idx, 1 << sc.lgK, ws, enc, ceta, b_out, cap_out, status, smem);
 }
 
-template <int TP, int METHOD>
+template <int TP, int METHOD, bool SSE>
 __global__ void __launch_bounds__(256, 6) recover_kernel(Geo g, FusedSched sc, const uint8_t *__restrict__ marked,
                                                       const uint8_t *__restrict__ keys, TileWS ws,
                                                       const uint32_t *__restrict__ eta_bits,
                                                       const uint32_t *__restrict__ map_bits,
                                                       const int32_t *__restrict__ lmr_b, uint8_t *__restrict__ out,
-                                                      int32_t *__restrict__ status) {
+                                                      int32_t *__restrict__ status, const uint8_t *__restrict__ orig,
+                                                      unsigned long long *__restrict__ sse) {
     extern __shared__ __align__(128) uint8_t smem[];
     const Role ro = role_of(sc);
     if (ro.img >= g.B) return;
@@ -883,7 +914,8 @@ __global__ void __launch_bounds__(256, 6) recover_kernel(Geo g, FusedSched sc, c
     if (!((MMSB_PROBE_ROLES >> (ro.key ? 0 : 1)) & 1)) return;
 #endif
     if (ro.key) key_role<TP, false, METHOD>(g, ro.img, ro.idx, keys, marked, ws, smem);
-    else rec_role<TP, METHOD>(g, ro.img, ro.idx, 1 << sc.lgK, marked, ws, eta_bits, map_bits, lmr_b, out, status, smem);
+    else rec_role<TP, METHOD, SSE>(g, ro.img, ro.idx, 1 << sc.lgK, marked, ws, eta_bits, map_bits, lmr_b, out, status,
+                                   orig, sse, smem);
 }
 
 // ---------------------------------------------------------------------------- launchers
@@ -946,28 +978,37 @@ void launch_encode(const Geo &g, const uint8_t *images, const uint8_t *keys, con
     }
 }
 
+template <int TP, int METHOD, bool SSE>
+static void launch_recover_k(const Geo &g, const FusedSched &sc, const uint8_t *marked, const uint8_t *keys,
+                             const TileWS &ws, const uint32_t *eta, const uint32_t *map, const int32_t *lmr_b,
+                             uint8_t *out, int32_t *status, const uint8_t *orig, unsigned long long *sse, cudaStream_t st) {
+    const size_t sm = fused_smem<TP, false>(g);
+    cudaFuncSetAttribute(recover_kernel<TP, METHOD, SSE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    recover_kernel<TP, METHOD, SSE><<<fused_grid(sc), 256, sm, st>>>(g, sc, marked, keys, ws, eta, map, lmr_b, out,
+                                                                      status, orig, sse);
+}
+
 template <int TP>
 static void launch_recover_tp(const Geo &g, const uint8_t *marked, const uint8_t *keys, const TileWS &ws,
                               const uint32_t *eta, const uint32_t *map, const int32_t *lmr_b, uint8_t *out,
-                              int32_t *status, cudaStream_t st) {
+                              int32_t *status, const uint8_t *orig, unsigned long long *sse, cudaStream_t st) {
     const FusedSched sc = fused_sched(g);
-    const dim3 grid = fused_grid(sc);
-    const size_t sm = fused_smem<TP, false>(g);
     if (g.method == 0) {
-        cudaFuncSetAttribute(recover_kernel<TP, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        recover_kernel<TP, 0><<<grid, 256, sm, st>>>(g, sc, marked, keys, ws, eta, map, lmr_b, out, status);
+        if (sse) launch_recover_k<TP, 0, true>(g, sc, marked, keys, ws, eta, map, lmr_b, out, status, orig, sse, st);
+        else launch_recover_k<TP, 0, false>(g, sc, marked, keys, ws, eta, map, lmr_b, out, status, orig, sse, st);
     } else {
-        cudaFuncSetAttribute(recover_kernel<TP, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        recover_kernel<TP, 1><<<grid, 256, sm, st>>>(g, sc, marked, keys, ws, eta, map, lmr_b, out, status);
+        if (sse) launch_recover_k<TP, 1, true>(g, sc, marked, keys, ws, eta, map, lmr_b, out, status, orig, sse, st);
+        else launch_recover_k<TP, 1, false>(g, sc, marked, keys, ws, eta, map, lmr_b, out, status, orig, sse, st);
     }
 }
 
 void launch_recover(const Geo &g, const uint8_t *marked, const uint8_t *keys, const TileWS &ws, const uint32_t *eta,
-                    const uint32_t *map, const int32_t *lmr_b, uint8_t *out, int32_t *status, cudaStream_t st) {
+                    const uint32_t *map, const int32_t *lmr_b, uint8_t *out, int32_t *status, cudaStream_t st,
+                    const uint8_t *original, unsigned long long *sse) {
     switch (g.tp) {
-        case 4: launch_recover_tp<4>(g, marked, keys, ws, eta, map, lmr_b, out, status, st); break;
-        case 5: launch_recover_tp<5>(g, marked, keys, ws, eta, map, lmr_b, out, status, st); break;
-        default: launch_recover_tp<6>(g, marked, keys, ws, eta, map, lmr_b, out, status, st); break;
+        case 4: launch_recover_tp<4>(g, marked, keys, ws, eta, map, lmr_b, out, status, original, sse, st); break;
+        case 5: launch_recover_tp<5>(g, marked, keys, ws, eta, map, lmr_b, out, status, original, sse, st); break;
+        default: launch_recover_tp<6>(g, marked, keys, ws, eta, map, lmr_b, out, status, original, sse, st); break;
     }
 }
 

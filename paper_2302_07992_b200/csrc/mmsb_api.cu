@@ -17,11 +17,11 @@ static std::atomic<unsigned long long> g_launches{0};
 
 // ---- live per-kernel timing (CUDA events recorded on the launch stream around each kernel)
 enum KernelId { K_ENCODE = 0, K_RECOVER, K_EMBED, K_EXTRACT, K_STATS, K_LMR_PLAN, K_CODER_ENC, K_LMR_FIT,
-                K_LMR_MSB, K_LMR_DECODE, K_COUNT };
+                K_LMR_MSB, K_LMR_DECODE, K_RECOVER_SSE, K_COUNT };
 static const char *kKernelNames[K_COUNT] = {"encode_kernel", "recover_kernel", "embed_prep+scan_kernel<embed>+finish",
                                             "scan_kernel<extract>+finish", "stats_kernel", "lmr_plan_kernel",
                                             "coder_encode_kernel", "lmr_fit_kernel", "lmr_concat+msb_write_kernels",
-                                            "lmr_pack+header+coder_decode_kernels"};
+                                            "lmr_pack+header+coder_decode_kernels", "recover_kernel+sse"};
 struct ProfRec { int id; cudaEvent_t a, b; long long units; };
 static std::mutex g_prof_mu;
 static bool g_prof_on = false;
@@ -252,6 +252,26 @@ mmsb_status mmsb_receiver_recover(const mmsb_shape *shape, const uint8_t *marked
     run_kernel(K_RECOVER, st, (long long)g.B * g.HW, [&] {
         launch_recover(g, marked, k1, tile_ws(L, ws), at<uint32_t>(ws, L.eta_bits), at<uint32_t>(ws, L.map_bits),
                        at<int32_t>(ws, L.lmr_b), recovered, img_status, st);
+    });
+    return check_launch();
+}
+
+mmsb_status mmsb_receiver_recover_sse(const mmsb_shape *shape, const uint8_t *marked, const uint8_t *k1,
+                                      const uint8_t *original, uint8_t *recovered, int64_t *sse_out,
+                                      int32_t *img_status, void *ws, size_t ws_bytes, void *stream) {
+    Geo g;
+    if (!geo_of(shape, &g) || !marked || !k1 || !original || !recovered || !sse_out || !img_status || !ws)
+        return MMSB_E_INVAL;
+    const Layout L = layout(g);
+    if (ws_bytes < L.total) return MMSB_E_INVAL;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (g.method == 1) lmr_decode_all(g, L, true, marked, ws, img_status, nullptr, st);
+    if (cudaMemsetAsync(at<char>(ws, L.pyr), 0, L.tile_zero_end - L.pyr, st) != cudaSuccess) return MMSB_E_CUDA;
+    if (cudaMemsetAsync(sse_out, 0, (size_t)g.B * 8, st) != cudaSuccess) return MMSB_E_CUDA;
+    run_kernel(K_RECOVER_SSE, st, (long long)g.B * g.HW, [&] {
+        launch_recover(g, marked, k1, tile_ws(L, ws), at<uint32_t>(ws, L.eta_bits), at<uint32_t>(ws, L.map_bits),
+                       at<int32_t>(ws, L.lmr_b), recovered, img_status, st, original,
+                       reinterpret_cast<unsigned long long *>(sse_out));
     });
     return check_launch();
 }

@@ -100,7 +100,8 @@ FusedSched fused_sched(const Geo &g);
 void launch_encode(const Geo &g, const uint8_t *images, const uint8_t *keys, const TileWS &ws, uint8_t *enc,
                    uint8_t *ceta, int32_t *b_out, int64_t *cap_out, int32_t *status, cudaStream_t st);
 void launch_recover(const Geo &g, const uint8_t *marked, const uint8_t *keys, const TileWS &ws, const uint32_t *eta,
-                    const uint32_t *map, const int32_t *lmr_b, uint8_t *out, int32_t *status, cudaStream_t st);
+                    const uint32_t *map, const int32_t *lmr_b, uint8_t *out, int32_t *status, cudaStream_t st,
+                    const uint8_t *original = nullptr, unsigned long long *sse = nullptr);
 void launch_scan(const Geo &g, bool embed, const uint8_t *in, uint8_t *out, const uint8_t *keys, const uint8_t *msg,
                  const int64_t *msg_bits, long long stride, uint8_t *msg_out, int64_t *msg_bits_out, int32_t *status,
                  const ScanWS &ws, const uint32_t *map_bits, const int32_t *lmr_b, cudaStream_t st);

@@ -47,6 +47,8 @@ def lib():
         L.mmsb_receiver_extract.argtypes = [sp, vp, vp, vp, C.c_int64, vp, vp, vp, C.c_size_t, vp]
         L.mmsb_receiver_recover.restype = C.c_int
         L.mmsb_receiver_recover.argtypes = [sp, vp, vp, vp, vp, vp, C.c_size_t, vp]
+        L.mmsb_receiver_recover_sse.restype = C.c_int
+        L.mmsb_receiver_recover_sse.argtypes = [sp, vp, vp, vp, vp, vp, vp, vp, C.c_size_t, vp]
         L.mmsb_capacity.restype = C.c_int
         L.mmsb_capacity.argtypes = [sp, vp, vp, vp, vp, vp, C.c_size_t, vp]
         L.mmsb_receiver_both.restype = C.c_int
@@ -205,8 +207,10 @@ def extract(method: int, marked: torch.Tensor, k2: torch.Tensor, stride: int, ws
 
 
 def recover(method: int, marked: torch.Tensor, k1: torch.Tensor, ws: Workspace | None = None, tile_log2: int = 7,
-            out: torch.Tensor | None = None):
-    """Receiver with K1: returns (recovered, status) -- mmsb_receiver_recover."""
+            out: torch.Tensor | None = None, original: torch.Tensor | None = None, sse_out: torch.Tensor | None = None):
+    """Receiver with K1: returns (recovered, status) -- mmsb_receiver_recover.  With `original`
+    (an evaluation harness's reference image) the SSE statistic is fused into the same pass and
+    (recovered, status, sse) is returned -- mmsb_receiver_recover_sse."""
     B, H, W = _images(marked, "marked")
     _arg(k1, "k1", torch.uint8, (B, 32), marked.device)
     if out is not None:
@@ -214,10 +218,18 @@ def recover(method: int, marked: torch.Tensor, k1: torch.Tensor, ws: Workspace |
     ws = _ws(ws, method, B, H, W, tile_log2, marked.device)
     rec = out if out is not None else torch.empty_like(marked)
     st = torch.empty(B, dtype=torch.int32, device=marked.device)
-    rc = lib().mmsb_receiver_recover(C.byref(ws.shape), _ptr(marked), _ptr(k1), _ptr(rec), _ptr(st), _ptr(ws.buf),
-                                     ws.nbytes, _stream())
-    _check(rc, "mmsb_receiver_recover")
-    return rec, st
+    if original is None:
+        rc = lib().mmsb_receiver_recover(C.byref(ws.shape), _ptr(marked), _ptr(k1), _ptr(rec), _ptr(st),
+                                         _ptr(ws.buf), ws.nbytes, _stream())
+        _check(rc, "mmsb_receiver_recover")
+        return rec, st
+    _arg(original, "original", torch.uint8, (B, H, W), marked.device)
+    sse = sse_out if sse_out is not None else torch.empty(B, dtype=torch.int64, device=marked.device)
+    _arg(sse, "sse_out", torch.int64, (B,), marked.device)
+    rc = lib().mmsb_receiver_recover_sse(C.byref(ws.shape), _ptr(marked), _ptr(k1), _ptr(original), _ptr(rec),
+                                         _ptr(sse), _ptr(st), _ptr(ws.buf), ws.nbytes, _stream())
+    _check(rc, "mmsb_receiver_recover_sse")
+    return rec, st, sse
 
 
 def receive_both(method: int, marked: torch.Tensor, k1: torch.Tensor, k2: torch.Tensor, stride: int,
