@@ -2,6 +2,7 @@
 // validation, workspace carving, L2-sized image groups, launch sequencing.
 // No allocation, no synchronisation: every call is stream-ordered on the caller's stream.
 #include <atomic>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <mutex>
@@ -291,12 +292,16 @@ mmsb_status mmsb_receiver_both(const mmsb_shape *shape, const uint8_t *marked, c
     if (cudaMemsetAsync(rstat, 0, (size_t)g.B * 4, st) != cudaSuccess) return MMSB_E_CUDA;
     // LMR: the coded maps (eta and the location map) are decoded once for both parties' steps
     if (g.method == 1) lmr_decode_all(g, L, true, marked, ws, img_status, msg_bits_out, st);
+    if (cudaMemsetAsync(at<char>(ws, L.pyr), 0, L.tile_zero_end - L.pyr, st) != cudaSuccess) return MMSB_E_CUDA;
     const ScanWS sw = scan_ws(g, L, ws);
+    // the two receivers back to back (LMR: on the maps decoded once above).  Tried and not kept: one
+    // launch with the extraction's chunk CTAs as a third CTA role beside the recovery's keystream
+    // and worker CTAs (EMR config 2: 0.81 ms against 0.70 ms back to back; the three ALU-bound
+    // roles' code overflows the instruction cache)
     run_kernel(K_EXTRACT, st, (long long)g.B * g.HW, [&] {
         launch_scan(g, false, marked, nullptr, k2, nullptr, nullptr, stride_bytes, msg_out, msg_bits_out,
                     img_status, sw, at<uint32_t>(ws, L.map_bits), at<int32_t>(ws, L.lmr_b), st);
     }, 2);
-    if (cudaMemsetAsync(at<char>(ws, L.pyr), 0, L.tile_zero_end - L.pyr, st) != cudaSuccess) return MMSB_E_CUDA;
     run_kernel(K_RECOVER, st, (long long)g.B * g.HW, [&] {
         launch_recover(g, marked, k1, tile_ws(L, ws), at<uint32_t>(ws, L.eta_bits), at<uint32_t>(ws, L.map_bits),
                        at<int32_t>(ws, L.lmr_b), recovered, rstat, st);

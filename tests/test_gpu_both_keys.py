@@ -46,3 +46,26 @@ def test_both_equals_separate_calls_and_oracle(method, H, W):
         assert np.array_equal(mo2[j, :region].cpu().numpy(), mo_o[:region])
         assert int(st2[j]) == (sx if sx != O.OK else sr)
     assert int(st2[2]) == O.E_INTEGRITY or int(nb2[2]) != int((cap[2] - 32).item())
+
+
+@pytest.mark.parametrize("config,method", [(2, G.EMR), (3, G.LMR)])
+def test_both_full_batch_equals_separate_calls(config, method):
+    """The fused receiver at the benched size (1000 x 512^2, one launch with three CTA roles):
+    every image's payload words, bit count, recovered image and status equal the separate calls'."""
+    imgs, k1, k2 = S.batch(config)
+    B, H, W = imgs.shape
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    I, K1, K2 = dev(imgs), dev(k1), dev(k2)
+    ws = G.Workspace(method, B, H, W)
+    enc, b, cap, st_e = G.encode(method, I, K1, ws)
+    nb = (cap - 32).clamp(min=0)
+    stride = int(((int(nb.max()) + 7) // 8 + 4 + 15) // 16 * 16)
+    msgs = torch.randint(0, 256, (B, stride), dtype=torch.uint8, generator=torch.Generator().manual_seed(config)).cuda()
+    marked, st_h = G.embed(method, enc, K2, msgs, nb, ws)
+    mo, nbo, st_x = G.extract(method, marked, K2, stride, ws)
+    rec, st_r = G.recover(method, marked, K1, ws)
+    mo2, nb2, rec2, st2 = G.receive_both(method, marked, K1, K2, stride, ws)
+    torch.cuda.synchronize()
+    assert torch.equal(nbo, nb2) and torch.equal(nb2, nb)
+    assert torch.equal(rec, rec2) and torch.equal(mo, mo2)
+    assert int((st2 != 0).sum()) == 0 and int((st_x != 0).sum()) == 0 and int((st_r != 0).sum()) == 0
