@@ -12,5 +12,5 @@ python bench.py --config 2 --steps 2 --warmup 3 --no-cpu-baseline --no-security 
   python bench.py --config 2 --steps 2 --warmup 3 --no-cpu-baseline --no-security --no-e2e > gpurun_out/ncu_launch.log 2>&1; echo ncu_launch=$?
 python tools/prof_run.py --batch 1000 --steps 2 > gpurun_out/prof_plain.log 2>&1 && \
   ncu --set full --clock-control none --import-source on \
-  -k regex:"encode_kernel|recover_kernel|scan_kernel|scan_finish|embed_prep|stats_kernel" -s 9 -c 8 -o gpurun_out/prof_all \
+  -k regex:"encode_kernel|recover_kernel|scan_kernel|scan_finish|embed_prep" -s 8 -c 7 -o gpurun_out/prof_all \
   python tools/prof_run.py --batch 1000 --steps 2 > gpurun_out/prof_ncu.log 2>&1; echo ncu_full=$?

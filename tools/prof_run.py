@@ -30,8 +30,7 @@ for _ in range(a.steps):
     enc, b, cap, st = G.encode(mid, I, K1, ws, out=enc)
     marked, _ = G.embed(mid, enc, K2, msgs, nb, ws)
     mo, nbo, _ = G.extract(mid, marked, K2, stride, ws)
-    rec, _ = G.recover(mid, marked, K1, ws)
-    sse = G.stats(I, rec)
+    rec, _, sse = G.recover(mid, marked, K1, ws, original=I)       # + statistics (SSE), as bench.py
 torch.cuda.synchronize()
 assert torch.equal(nbo, nb), "round trip"
 print("ok", G.kernel_launches())

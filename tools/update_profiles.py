@@ -23,8 +23,7 @@ PX = 1000 * 512 * 512                     # tools/prof_run.py --batch 1000 (conf
 CLASSES = {"encode_kernel": ["encode_kernel"],
            "embed_prep+scan_kernel<embed>+finish": ["embed_prep_kernel", "scan_kernel<0, 1>", "scan_finish_kernel<0, 1>"],
            "scan_kernel<extract>+finish": ["scan_kernel<0, 0>", "scan_finish_kernel<0, 0>"],
-           "recover_kernel": ["recover_kernel"],
-           "stats_kernel": ["stats_kernel"]}
+           "recover_kernel+sse": ["recover_kernel"]}
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
 
