@@ -177,7 +177,7 @@ __global__ void lmr_plan_kernel(Geo g, const uint32_t *__restrict__ hist, LmrPla
         for (int w = 0; w < 8; w++) { ctl->count[w] = w == 0 ? g.B : 0; ctl->nc[w] = 0; }
     }
     if (img >= g.B) return;
-    for (int c = 0; c < 8; c++) mapbytes[(size_t)img * 8 + c] = 0;
+    for (int c = 0; c < kMapStats; c++) mapbytes[(size_t)img * kMapStats + c] = c == 16 ? 127 : 0;
     LmrPlan p{};
     long long val[9];
     for (int b = 2; b <= 8; b++) val[b] = (long long)(b - 1) * (g.HW - (long long)hist[img * kHistStride + b]);
@@ -730,7 +730,7 @@ __global__ void __launch_bounds__(kFastThreads, 1) coder_encode_fast_kernel(Geo 
     int32_t *abort_cnt = nullptr;
     long long room = 0;
     if (wave > 0 && it.cand >= 0) {
-        abort_cnt = ew.mapbytes + (size_t)img * 8 + it.cand;
+        abort_cnt = ew.mapbytes + (size_t)img * kMapStats + it.cand;
         room = (g.HW - 7 - 32ll * Tc) / 8 - ew.plan[img].eta_bytes;
     }
     int published = 0, seen = 0;
@@ -817,13 +817,15 @@ __global__ void __launch_bounds__(kFastThreads, 1) coder_encode_fast_kernel(Geo 
 #pragma unroll
         for (int k = 0; k < NW; k++) { p2[k] = p1[k]; p1[k] = cw[k]; }
         if (abort_cnt) {
-            if (seen > room) { aborted = true; break; }
+            // stop once the map can no longer fit, or once an earlier candidate of the walk is
+            // known to fit (this one can then never be chosen)
+            if (seen > room || ld_relaxed_s32(abort_cnt + 16 - it.cand) < it.cand) { aborted = true; break; }
             const int cur = e.n + e.k;
             seen = atomicAdd(abort_cnt, cur - published) + (cur - published);
             published = cur;
         }
     }
-    if (aborted) {                                                     // over the room: does not fit
+    if (aborted) {                                                     // does not fit / cannot be chosen
         ew.sizes[((size_t)img * kLmrSlots + slot) * Tc + tile] = -1;
         return;
     }
@@ -832,7 +834,18 @@ __global__ void __launch_bounds__(kFastThreads, 1) coder_encode_fast_kernel(Geo 
     for (int i = 0; i < 5; i++) e.emit(true, false, 8);
     e.end_half(am);
     e.n += e.k;
-    ew.sizes[((size_t)img * kLmrSlots + slot) * Tc + tile] = (e.n <= cap && e.n <= 65535) ? e.n : -1;
+    const bool ok = e.n <= cap && e.n <= 65535;
+    ew.sizes[((size_t)img * kLmrSlots + slot) * Tc + tile] = ok ? e.n : -1;
+    if (abort_cnt) {
+        // the candidate's exact total once its last tile is in (a tile over its cap poisons it);
+        // the last tile decides whether it fits and publishes the first fitting candidate
+        atomicAdd(abort_cnt, (ok ? e.n : (1 << 28)) - published);
+        __threadfence();
+        if (atomicAdd(abort_cnt + 8, 1) == Tc - 1) {
+            const long long tot = atomicAdd(abort_cnt, 0);
+            if (tot <= room) atomicMin(abort_cnt + 16 - it.cand, it.cand);
+        }
+    }
 }
 
 // decoder input: the tile's stream as a 160-bit MSB-aligned bit buffer b0..b4 (nb valid bits),

@@ -96,7 +96,7 @@ static Layout layout(const Geo &g) {
     L.plan = o; o = align256(o + (lmr ? B * sizeof(LmrPlan) : 0));
     L.wctl = o; o = align256(o + (lmr ? sizeof(LmrWaveCtl) : 0));
     L.lists = o; o = align256(o + (lmr ? 8 * B * 4 : 0));
-    L.mapbytes = o; o = align256(o + (lmr ? 8 * B * 4 : 0));
+    L.mapbytes = o; o = align256(o + (lmr ? (size_t)kMapStats * B * 4 : 0));
     L.streams = o; o = align256(o + (lmr ? B * kLmrSlots * Tc * lmr_tile_stride_host(g.tile_log2, g.H, g.W) : 0));
     L.sizes = o; o = align256(o + (lmr ? B * kLmrSlots * Tc * 4 : 0));
     L.dsizes = o; o = align256(o + (lmr ? B * 2 * Tc * 4 : 0));

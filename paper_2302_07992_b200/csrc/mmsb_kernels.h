@@ -34,6 +34,7 @@ struct LmrPlan {
 // rounds of resident tiles (wave 0: eta and candidate 0 for every image); the fit then takes the
 // first candidate in order that fits, exactly the serial walk's choice.
 constexpr int kLmrSlots = 8;         // stream slots per image: eta, candidates 0..6
+constexpr int kMapStats = 32;        // ints per image of LmrEncWS::mapbytes
 struct LmrWaveCtl {
     int count[8];                    // images entering wave w (count[0] = B)
     int nc[8];                       // candidates tried before wave w
@@ -47,7 +48,8 @@ struct LmrEncWS {
     int32_t *dsizes;                 // [B][2][Tc] sizes of the decided eta + map streams
     int32_t *offsets;                // [B][2][Tc] their exclusive byte offsets
     uint8_t *cat;                    // [B][HW/8] the decided streams concatenated (the mbuf region)
-    int32_t *mapbytes;               // [B][8] running coded bytes of each candidate's map (early abort)
+    int32_t *mapbytes;               // [B][kMapStats]: [c] running coded bytes of candidate c's map (early
+                                     // abort), [8 + c] its finished tiles, [16] the first candidate known to fit
 };
 #ifndef MMSB_LMR_WAVE_ROUNDS
 #define MMSB_LMR_WAVE_ROUNDS 3
