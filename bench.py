@@ -362,8 +362,18 @@ def run_ours(args):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    ngpu = torch.cuda.device_count()
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
+    shared = local_world > ngpu
+    if shared:
+        # more ranks than GPUs: a functional check of the multi-rank path only (ranks share a GPU,
+        # the collectives go through host memory over gloo); the timing is not a multi-GPU number
+        if rank == 0:
+            print(f"bench.py: {local_world} ranks on {ngpu} GPU(s): ranks share GPUs, collectives over gloo; "
+                  "timings are not multi-GPU measurements", file=sys.stderr, flush=True)
+        local = local % ngpu
     torch.cuda.set_device(local)
-    init_dist(world, local)
+    init_dist(world, local, cpu=shared)
     if rank == 0 and not os.path.exists(BLD.LIB):
         BLD.build()
     if world > 1:
@@ -371,6 +381,8 @@ def run_ours(args):
     G.lib()
 
     line = measure(args, rank, world, local)
+    if shared and rank == 0:
+        line["shared_gpus"] = f"{local_world} ranks on {ngpu} GPU(s): functional run, not a multi-GPU timing"
     if args.config is None and args.method is None and not args.no_lmr_block:
         torch.cuda.empty_cache()
         lmr = measure(args, rank, world, local, config=3, method="lmr")

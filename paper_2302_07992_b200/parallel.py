@@ -26,6 +26,22 @@ def shard(total: int, rank: int, world: int) -> tuple[int, int]:
     return start, base + (1 if rank < extra else 0)
 
 
+def _host_staged() -> bool:
+    """gloo moves host tensors; it is the backend only when ranks share a GPU (bench.py) or in
+    the CPU tests, so device tensors are staged through host memory for it."""
+    return dist.get_backend() == "gloo"
+
+
+def _all_gather(parts, t: torch.Tensor) -> None:
+    if t.is_cuda and _host_staged():
+        host = [torch.empty_like(p, device="cpu") for p in parts]
+        dist.all_gather(host, t.cpu())
+        for p, h in zip(parts, host):
+            p.copy_(h)
+        return
+    dist.all_gather(parts, t)
+
+
 def make_records(b, cap, sse, status) -> torch.Tensor:
     """[B, 4] int64 records on the device of `sse` (no host round trip)."""
     rec = torch.empty(sse.shape[0], REC_COLS, dtype=torch.int64, device=sse.device)
@@ -47,7 +63,7 @@ def gather_records(rec: torch.Tensor, world: int, counts=None) -> torch.Tensor:
         pad = torch.full((n, REC_COLS), -1, dtype=rec.dtype, device=rec.device)
         pad[: rec.shape[0]] = rec
     parts = [torch.empty_like(pad) for _ in range(world)]
-    dist.all_gather(parts, pad.contiguous())
+    _all_gather(parts, pad.contiguous())
     if counts:
         parts = [p[:c] for p, c in zip(parts, counts)]
     return torch.cat(parts, 0)
@@ -57,7 +73,7 @@ def max_over_ranks(ms: float, device, world: int) -> float:
     """The slowest rank's device time (the step ends when every shard is done)."""
     if world == 1:
         return ms
-    t = torch.tensor([ms], dtype=torch.float64, device=device)
+    t = torch.tensor([ms], dtype=torch.float64, device="cpu" if _host_staged() else device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -91,7 +107,7 @@ def gather_rows(rows: torch.Tensor, world: int, counts=None) -> torch.Tensor:
         pad = torch.zeros((n,) + tuple(rows.shape[1:]), dtype=rows.dtype, device=rows.device)
         pad[: rows.shape[0]] = rows
     parts = [torch.empty_like(pad) for _ in range(world)]
-    dist.all_gather(parts, pad.contiguous())
+    _all_gather(parts, pad.contiguous())
     if counts:
         parts = [p[:c] for p, c in zip(parts, counts)]
     return torch.cat(parts, 0)

@@ -56,3 +56,21 @@ def test_shard_mode_one_rank():
     d = _run("--config", "4", "--shard", "--batch", "20", "--steps", "3", "--warmup", "3", "--no-cpu-baseline",
              "--no-security", "--e2e-steps", "2")
     assert d["scaling"] == "strong" and d["config"]["global_batch"] == 20 and d["stats"]["images"] == 20
+
+
+def test_two_ranks_sharded_match_one_rank():
+    """The multi-rank bench path on the hardware at hand: torchrun self-launch, shard split (ragged:
+    11 + 10 images), the record and statistics all-gathers and max-over-ranks timing. On a box with
+    fewer GPUs than ranks the ranks share a GPU over gloo (a functional run, flagged in the line);
+    the aggregates must equal the one-rank run's, image for image."""
+    import torch
+
+    common = ("--config", "4", "--shard", "--batch", "21", "--steps", "3", "--warmup", "3", "--no-cpu-baseline",
+              "--e2e-steps", "2")
+    one = _run(*common)
+    two = _run("--gpus", "2", *common)
+    assert two["n_gpus"] == 2 and two["scaling"] == "strong" and two["config"]["global_batch"] == 21
+    assert ("shared_gpus" in two) == (torch.cuda.device_count() < 2)
+    assert all(v is True or (isinstance(v, dict) and all(v.values())) for v in two["checks"].values())
+    assert two["stats"] == one["stats"]
+    assert two["security"] == one["security"]
