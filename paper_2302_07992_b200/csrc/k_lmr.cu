@@ -275,21 +275,34 @@ __global__ void lmr_fit_kernel(Geo g, int wave, int R, LmrEncWS e) {
 
 // ======================================================================================
 // lmr_concat_kernel: the decided eta and map streams of an image, concatenated in order (tile
-// raster, eta first) into one byte string at their exclusive offsets: one CTA per stream,
-// coalesced copies.
+// raster, eta first) into one byte string at their exclusive offsets: one warp per stream (a
+// 4096^2 image has 2 x 1024 of them), coalesced byte copies, 8 loads in flight per lane.
 // ======================================================================================
 __global__ void __launch_bounds__(256) lmr_concat_kernel(Geo g, LmrEncWS ew) {
-    const int img = blockIdx.x;
+    const int img = blockIdx.y;
     const LmrPlan pl = ew.plan[img];
     if (pl.state != 1) return;
     const int Tc = lmr_tile_count(g.H, g.W, g.tile_log2);
     const int stride = lmr_tile_stride(g.tile_log2, g.H, g.W);
+    const int lane = threadIdx.x & 31;
     uint8_t *dst = ew.cat + (size_t)img * (g.HW / 8);           // (a string never exceeds the plane: K <= HW)
-    for (int k = 0; k < 2 * Tc; k++) {                          // streams in order, all threads per stream
+    for (int k = blockIdx.x * 8 + (threadIdx.x >> 5); k < 2 * Tc; k += gridDim.x * 8) {
         const int n = ew.dsizes[(size_t)img * 2 * Tc + k], o = ew.offsets[(size_t)img * 2 * Tc + k];
         const int slot = k < Tc ? 0 : pl.dslot, tile = k < Tc ? k : k - Tc;
         const uint8_t *src = ew.streams + (((size_t)img * kLmrSlots + slot) * Tc + tile) * stride;
-        for (int i = threadIdx.x; i < n; i += 256) dst[o + i] = src[i];
+        for (int i0 = 0; i0 < n; i0 += 256) {                  // 8 coalesced byte loads in flight per lane
+            uint8_t v[8];
+#pragma unroll
+            for (int j = 0; j < 8; j++) {
+                const int i = i0 + 32 * j + lane;
+                v[j] = i < n ? src[i] : 0;
+            }
+#pragma unroll
+            for (int j = 0; j < 8; j++) {
+                const int i = i0 + 32 * j + lane;
+                if (i < n) dst[o + i] = v[j];
+            }
+        }
     }
 }
 
@@ -298,7 +311,7 @@ __global__ void __launch_bounds__(256) lmr_concat_kernel(Geo g, LmrEncWS ew) {
 //   [b-2: 3 bits][t: 4 bits][16-bit byte lengths of the eta tiles][... of the map tiles]
 //   [eta tile bytes][map tile bytes], MSB first, pixel r <- stream bit r for r < K; the
 //   remaining MSBs keep I_r XOR s.  Bad case: the b-field 7 (bits r = 0..2 set).
-// One thread per 16 pixels; the stream bits come from the concatenated string (3 bytes).
+// One thread per 32 pixels; the stream bits come from the concatenated string (5 bytes).
 // ======================================================================================
 __global__ void __launch_bounds__(256) lmr_msb_write_kernel(Geo g, LmrEncWS ew,
                                                             const uint32_t *__restrict__ hist,
@@ -326,19 +339,23 @@ __global__ void __launch_bounds__(256) lmr_msb_write_kernel(Geo g, LmrEncWS ew,
     const uint8_t *cat = ew.cat + (size_t)img * (g.HW / 8);
     const long long hdr = 7 + 32ll * Tc;                        // header bits before the stream bytes
     const long long total = (pl.K - hdr) / 8;                   // stream bytes
-    for (long long p = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * 16; p < pl.K;
-         p += (long long)gridDim.x * blockDim.x * 16) {
-        // the 16 plane bits of pixels [p, p+16), MSB first
-        uint32_t bits16 = 0;
+    for (long long p = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * 32; p < pl.K;
+         p += (long long)gridDim.x * blockDim.x * 32) {
+        // 32 pixels per thread (two 16-byte words in flight; HW is a power of two >= 256)
+        const uint4 u0 = *reinterpret_cast<const uint4 *>(E + p);
+        const uint4 u1 = *reinterpret_cast<const uint4 *>(E + p + 16);
+        // the 32 plane bits of pixels [p, p+32), MSB first
+        uint32_t bits32 = 0;
         if (p >= hdr) {
             const long long q = p - hdr, q0 = q >> 3;
             const int sh = (int)(q & 7);                        // bit offset inside byte q0
-            uint32_t b3 = 0;
+            unsigned long long b5 = 0;
 #pragma unroll
-            for (int i = 0; i < 3; i++) b3 = (b3 << 8) | (q0 + i < total ? (uint32_t)cat[q0 + i] : 0u);
-            bits16 = (b3 >> (8 - sh)) & 0xFFFFu;
+            for (int i = 0; i < 5; i++)
+                b5 = (b5 << 8) | (q0 + i < total ? (unsigned long long)cat[q0 + i] : 0ull);
+            bits32 = (uint32_t)(b5 >> (8 - sh));
         } else {
-            for (int i = 0; i < 16; i++) {
+            for (int i = 0; i < 32; i++) {
                 const long long r = p + i;
                 uint32_t bit = 0;
                 if (r < 3) bit = ((uint32_t)(pl.b - 2) >> (2 - r)) & 1u;
@@ -349,22 +366,22 @@ __global__ void __launch_bounds__(256) lmr_msb_write_kernel(Geo g, LmrEncWS ew,
                     const uint32_t by = q >> 3 < total ? (uint32_t)cat[q >> 3] : 0u;
                     bit = (by >> (7 - (q & 7))) & 1u;
                 }
-                bits16 |= bit << (15 - i);
+                bits32 |= bit << (31 - i);
             }
         }
-        uint4 u = *reinterpret_cast<const uint4 *>(E + p);
-        uint32_t wv[4] = {u.x, u.y, u.z, u.w};
+        uint32_t wv[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
 #pragma unroll
-        for (int i = 0; i < 4; i++) {
+        for (int i = 0; i < 8; i++) {
             // the word's 4 plane bits (first pixel = nibble bit 3) to the byte MSBs: nib << (9k + 4)
             // puts nibble bit 3-k at bit 8k+7, the four terms do not overlap
-            const uint32_t nib = (bits16 >> (12 - 4 * i)) & 0xFu;
+            const uint32_t nib = (bits32 >> (28 - 4 * i)) & 0xFu;
             const uint32_t msb = (nib * 0x80402010u) & 0x80808080u;
             const long long nv = pl.K - (p + 4 * i);            // pixels of the word below K
             const uint32_t bm = nv >= 4 ? 0xFFFFFFFFu : (nv <= 0 ? 0u : (1u << (8 * (int)nv)) - 1u);
             wv[i] = (wv[i] & ~(bm & 0x80808080u)) | (msb & bm);
         }
         *reinterpret_cast<uint4 *>(E + p) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+        *reinterpret_cast<uint4 *>(E + p + 16) = make_uint4(wv[4], wv[5], wv[6], wv[7]);
     }
 }
 
@@ -1114,11 +1131,13 @@ void launch_lmr_fit(const Geo &g, int wave, const LmrEncWS &e, cudaStream_t st) 
 
 void launch_lmr_msb_write(const Geo &g, const LmrEncWS &e, const uint32_t *hist, uint8_t *enc, int32_t *b_out,
                           int64_t *cap_out, int32_t *status, cudaStream_t st) {
-    const long long n16 = g.HW / 16;
-    int bx = (int)((n16 + 255) / 256);
+    const long long n32 = g.HW / 32;
+    int bx = (int)((n32 + 255) / 256);
     if (bx > 16) bx = 16;
     dim3 grid(bx, g.B);
-    lmr_concat_kernel<<<g.B, 256, 0, st>>>(g, e);
+    const int Tc = lmr_tile_count(g.H, g.W, g.tile_log2);
+    const int cx = (2 * Tc + 7) / 8 < 32 ? (2 * Tc + 7) / 8 : 32;
+    lmr_concat_kernel<<<dim3(cx, g.B), 256, 0, st>>>(g, e);
     lmr_msb_write_kernel<<<grid, 256, 0, st>>>(g, e, hist, enc, b_out, cap_out, status);
 }
 
