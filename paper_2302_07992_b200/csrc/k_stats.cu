@@ -72,7 +72,8 @@ __global__ void __launch_bounds__(256) diff_kernel(long long HW, const uint8_t *
 
 // ---- SSIM: one CTA per 32x32 block of window positions; the 42x42 source region of both
 // images in smem, a horizontal 11-tap pass of mu_a, mu_b, E[a^2], E[b^2], E[ab] into smem (fp64),
-// a vertical pass per position, the SSIM values summed per CTA and added into the image's sum.
+// a vertical pass per position, the SSIM values summed per CTA and added into the image's sum
+// (fixed point, so the mean is reproducible bit for bit).
 constexpr int kSsimTile = 32, kSsimSrc = kSsimTile + 10;
 
 struct SsimSmem {
@@ -139,13 +140,18 @@ __global__ void __launch_bounds__(256) ssim_kernel(int H, int W, const uint8_t *
     if (tid == 0) {
         double t = 0;
         for (int w = 0; w < 8; w++) t += S.red[w];
-        atomicAdd(sum + img, t);
+        // the image's sum accumulates in its output slot as 2^-32 fixed point (int64 adds are
+        // associative: the result does not depend on the order the CTAs finish in)
+        atomicAdd(reinterpret_cast<unsigned long long *>(sum + img), (unsigned long long)llrint(t * 4294967296.0));
     }
 }
 
 __global__ void ssim_finish_kernel(int B, double npos, double *__restrict__ ssim) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < B) ssim[i] = npos > 0 ? ssim[i] / npos : 0.0;
+    if (i < B) {
+        const long long fx = reinterpret_cast<const long long *>(ssim)[i];
+        ssim[i] = npos > 0 ? ((double)fx / 4294967296.0) / npos : 0.0;
+    }
 }
 
 // ---------------------------------------------------------------------------- launchers

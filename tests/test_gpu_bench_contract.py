@@ -2,7 +2,6 @@
 block, the result checks all true, clocks sampled, library launches counted, and the CPU-oracle
 baseline with its single-core per-call times; plus the default run's LMR block."""
 import json
-import math
 import os
 import subprocess
 import sys
@@ -74,10 +73,4 @@ def test_two_ranks_sharded_match_one_rank():
     assert ("shared_gpus" in two) == (torch.cuda.device_count() < 2)
     assert all(v is True or (isinstance(v, dict) and all(v.values())) for v in two["checks"].values())
     assert two["stats"] == one["stats"]
-    # the security table's float64 means: SSIM sums by float atomics (order-dependent last bits)
-    assert two["security"].keys() == one["security"].keys()
-    for k, v in one["security"].items():
-        if isinstance(v, float):
-            assert math.isclose(two["security"][k], v, rel_tol=1e-12), k
-        else:
-            assert two["security"][k] == v, k
+    assert two["security"] == one["security"]                # per-image statistics are deterministic

@@ -59,6 +59,16 @@ def test_ssim_parity(H, W):
     assert np.all(G.ssim(I, I).cpu().numpy() == pytest.approx(1.0, abs=1e-12))
 
 
+def test_ssim_is_reproducible():
+    """The per-image SSIM sum is accumulated in fixed point: repeated calls (and any CTA finishing
+    order) give the same bits."""
+    g = torch.Generator().manual_seed(11)
+    A = torch.randint(0, 256, (4, 512, 512), generator=g, dtype=torch.uint8).cuda()
+    B = (A.int() + torch.randint(-20, 21, A.shape, generator=g).cuda()).clamp(0, 255).to(torch.uint8)
+    runs = [G.ssim(A, B).cpu() for _ in range(5)]
+    assert all(torch.equal(r, runs[0]) for r in runs[1:])
+
+
 def test_closed_forms_on_gpu():
     dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
     const = dev(np.full((2, 512, 512), 17, np.uint8))
