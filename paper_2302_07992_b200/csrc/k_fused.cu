@@ -484,8 +484,8 @@ __device__ __forceinline__ void discard_lines(const void *p, int n, int lane) {
 //        header b-2 in the LSBs of r = 0..2 (Q14).
 //   LMR: E = I_r XOR s; second plane ceta = (I & 0x80) | c permuted alongside (for the coder).
 // ======================================================================================
-template <int TP, int METHOD>
-__device__ __forceinline__ void perm_role(const Geo &g, int img, int dty, int nK, const TileWS &ws,
+template <int TP, int METHOD, bool SPLIT>
+__device__ __forceinline__ void perm_role(const Geo &g, int img, int dty, int seg, int lgS, int nK, const TileWS &ws,
                                           uint8_t *__restrict__ enc, uint8_t *__restrict__ ceta_out,
                                           int32_t *__restrict__ b_out, int64_t *__restrict__ cap_out,
                                           int32_t *__restrict__ status, uint8_t *smem) {
@@ -495,6 +495,7 @@ __device__ __forceinline__ void perm_role(const Geo &g, int img, int dty, int nK
     SM &S = *reinterpret_cast<SM *>(smem);
     uint32_t *spyr = reinterpret_cast<uint32_t *>(smem + sizeof(SM));
     const int tid = threadIdx.x, lane = tid & 31;
+    if constexpr (!SPLIT) { seg = 0; lgS = 0; }
 
     if (tid == 0) {
         for (int s = 0; s < kStages; s++) {
@@ -505,9 +506,9 @@ __device__ __forceinline__ void perm_role(const Geo &g, int img, int dty, int nK
     if (tid < 32) {
         const bool ok = warp0_ready(g, ws, img, nK, spyr);
         if (ok) {
-            for (int j = tid; j < g.tilesX; j += 32) {
+            for (int j = tid; j < (g.tilesX >> lgS); j += 32) {
                 int sty, stx, q;
-                upper_walk_inverse(g, spyr, dty, j, sty, stx, q);
+                upper_walk_inverse(g, spyr, dty, (seg << (g.tlog - lgS)) + j, sty, stx, q);
                 S.map[j] = (((sty << g.tlog) + stx) << 2) | q;
             }
         }
@@ -520,14 +521,14 @@ __device__ __forceinline__ void perm_role(const Geo &g, int img, int dty, int nK
     __syncthreads();
     if (!S.sh[1]) return;
     const int b = S.sh[0];
-    const int ntx = g.tilesX;
+    const int ntx = g.tilesX >> lgS, j0 = seg * ntx;                // this worker's tiles [j0, j0 + ntx) of the strip
     const uint8_t *blk0 = ws.s + (size_t)img * g.ntiles * TB::BLOCK;      // the image's scratch blocks
     const uint64_t *rec0 = ws.rec + (size_t)img * g.ntiles * kRecSlots;
 
     auto issue = [&](int j) {
         const int s = j % kStages;
         if (j >= kStages) mbar_wait(&S.empty[s], ((j / kStages) - 1) & 1);
-        const int stile = S.map[j] >> 2, dtile = (dty << g.tlog) + j;
+        const int stile = S.map[j] >> 2, dtile = (dty << g.tlog) + j0 + j;
         mbar_expect_tx(&S.full[s], 3 * T * T + kWRecBytes);
         bulk_g2s(S.st[s].ks, blk0 + (size_t)dtile * TB::BLOCK, T * T, &S.full[s]);
         bulk_g2s(S.st[s].src, blk0 + (size_t)stile * TB::BLOCK + TB::PLANE, 2 * T * T, &S.full[s]);
@@ -550,10 +551,11 @@ __device__ __forceinline__ void perm_role(const Geo &g, int img, int dty, int nK
         spos |= (uint32_t)(sy * 2 + sx) << (2 * q);
     }
     const int lsh = 8 - b;                                   // EMR: map bit l = bit 8 - b of the thermometer code
-    // output rows of this thread's cell in tile 0 of the strip (the tile advances by T bytes)
+    // output rows of this thread's cell in the worker's first tile (the tile advances by T bytes)
     const size_t W = (size_t)g.W;
-    uint8_t *eo = enc + (size_t)img * g.HW + (size_t)(dty * T + 4 * cy) * W + 4 * cx;
-    uint8_t *co = METHOD == 1 ? ceta_out + (size_t)img * g.HW + (size_t)(dty * T + 4 * cy) * W + 4 * cx : nullptr;
+    uint8_t *eo = enc + (size_t)img * g.HW + (size_t)(dty * T + 4 * cy) * W + (size_t)j0 * T + 4 * cx;
+    uint8_t *co = METHOD == 1 ? ceta_out + (size_t)img * g.HW + (size_t)(dty * T + 4 * cy) * W + (size_t)j0 * T + 4 * cx
+                              : nullptr;
 
     int s = 0;
     unsigned ph = 0;
@@ -562,7 +564,7 @@ __device__ __forceinline__ void perm_role(const Geo &g, int img, int dty, int nK
         const typename SM::Stage &st = S.st[s];
         const int mp = S.map[j];
         if (tid >= 224) {                                    // warp 7: drop the consumed scratch from L2
-            const int dtile = (dty << g.tlog) + j;
+            const int dtile = (dty << g.tlog) + j0 + j;
             discard_lines(blk0 + (size_t)dtile * TB::BLOCK, T * T / 128, lane);
             discard_lines(blk0 + (size_t)(mp >> 2) * TB::BLOCK + TB::PLANE, 2 * T * T / 128, lane);
             discard_lines(rec0 + (size_t)(mp >> 2) * kRecSlots, kRecSlots * 8 / 128, lane);
@@ -605,7 +607,7 @@ __device__ __forceinline__ void perm_role(const Geo &g, int img, int dty, int nK
             if constexpr (METHOD == 0) {
                 e0 = v.r0 ^ (sv.x & 0xFEFEFEFEu); e1 = v.r1 ^ (sv.y & 0xFEFEFEFEu);
                 e2 = v.r2 ^ (sv.z & 0xFEFEFEFEu); e3 = v.r3 ^ (sv.w & 0xFEFEFEFEu);
-                if (dty == 0 && j == 0 && tid == 0) {
+                if (dty == 0 && j0 + j == 0 && tid == 0) {
                     // header: LSB(E[r]) = bit (2 - r) of b - 2 for r = 0..2; the map there is
                     // forced to 1, so capacity counts zeros after forcing (Q14)
                     const uint32_t m = v.r0 & 0x00010101u;
@@ -881,7 +883,7 @@ __device__ __forceinline__ void rec_role(const Geo &g, int img, int ty, int nK, 
 // ======================================================================================
 // The fused kernels (dynamic shared memory: max of the two roles' needs + the pyramid)
 // ======================================================================================
-template <int TP, int METHOD>
+template <int TP, int METHOD, bool SPLIT>
 __global__ void __launch_bounds__(256, 6) encode_kernel(Geo g, FusedSched sc, const uint8_t *__restrict__ images,
                                                      const uint8_t *__restrict__ keys, TileWS ws,
                                                      uint8_t *__restrict__ enc, uint8_t *__restrict__ ceta,
@@ -894,7 +896,11 @@ __global__ void __launch_bounds__(256, 6) encode_kernel(Geo g, FusedSched sc, co
     if (!((MMSB_PROBE_ROLES >> (ro.key ? 0 : 1)) & 1)) return;
 #endif
     if (ro.key) key_role<TP, true, METHOD>(g, ro.img, ro.idx, keys, images, ws, smem);
-    else perm_role<TP, METHOD>(g, ro.img, ro.idx, 1 << sc.lgK, ws, enc, ceta, b_out, cap_out, status, smem);
+    else if constexpr (SPLIT)
+        perm_role<TP, METHOD, true>(g, ro.img, ro.idx >> sc.lgS, ro.idx & ((1 << sc.lgS) - 1), sc.lgS, 1 << sc.lgK, ws,
+                                    enc, ceta, b_out, cap_out, status, smem);
+    else
+        perm_role<TP, METHOD, false>(g, ro.img, ro.idx, 0, 0, 1 << sc.lgK, ws, enc, ceta, b_out, cap_out, status, smem);
 }
 
 template <int TP, int METHOD, bool SSE>
@@ -917,12 +923,16 @@ __global__ void __launch_bounds__(256, 6) recover_kernel(Geo g, FusedSched sc, c
 }
 
 // ---------------------------------------------------------------------------- launchers
-FusedSched fused_sched(const Geo &g) {
+FusedSched fused_sched(const Geo &g, bool split_strips) {
     FusedSched sc;
     const int TPC = 256 / g.T;
     const int nK = g.ntiles >= TPC ? g.ntiles / TPC : 1;       // powers of two
     sc.lgK = ilog2(nK);
-    sc.lgW = ilog2(g.tilesY);                           // one worker CTA per strip of tiles
+    // one worker CTA per strip of tiles; encode cuts strips wider than 8 tiles into segments of
+    // 8 (a 4096^2 image: 512 workers of 8 tiles instead of 64 of 64, so the batch's last image
+    // does not leave a long tail of strip walks)
+    sc.lgS = split_strips && g.tilesX > 8 ? ilog2(g.tilesX / 8) : 0;
+    sc.lgW = ilog2(g.tilesY) + sc.lgS;
     int gi = 1;
     while ((long long)(gi * 2) * g.HW <= (2ll << 20) && gi < g.B) gi *= 2;   // ~2 Mpixel per group
     sc.GI = gi;
@@ -947,19 +957,27 @@ static size_t fused_smem(const Geo &g) {
     return k > w ? k : w;
 }
 
+template <int TP, bool SPLIT>
+static void launch_encode_k(const Geo &g, const FusedSched &sc, dim3 grid, size_t sm, const uint8_t *images,
+                            const uint8_t *keys, const TileWS &ws, uint8_t *enc, uint8_t *ceta, int32_t *b_out,
+                            int64_t *cap_out, int32_t *status, cudaStream_t st) {
+    if (g.method == 0) {
+        cudaFuncSetAttribute(encode_kernel<TP, 0, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        encode_kernel<TP, 0, SPLIT><<<grid, 256, sm, st>>>(g, sc, images, keys, ws, enc, ceta, b_out, cap_out, status);
+    } else {
+        cudaFuncSetAttribute(encode_kernel<TP, 1, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        encode_kernel<TP, 1, SPLIT><<<grid, 256, sm, st>>>(g, sc, images, keys, ws, enc, ceta, b_out, cap_out, status);
+    }
+}
+
 template <int TP>
 static void launch_encode_tp(const Geo &g, const uint8_t *images, const uint8_t *keys, const TileWS &ws, uint8_t *enc,
                              uint8_t *ceta, int32_t *b_out, int64_t *cap_out, int32_t *status, cudaStream_t st) {
-    const FusedSched sc = fused_sched(g);
+    const FusedSched sc = fused_sched(g, true);
     const dim3 grid = fused_grid(sc);
     const size_t sm = fused_smem<TP, true>(g);
-    if (g.method == 0) {
-        cudaFuncSetAttribute(encode_kernel<TP, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        encode_kernel<TP, 0><<<grid, 256, sm, st>>>(g, sc, images, keys, ws, enc, ceta, b_out, cap_out, status);
-    } else {
-        cudaFuncSetAttribute(encode_kernel<TP, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        encode_kernel<TP, 1><<<grid, 256, sm, st>>>(g, sc, images, keys, ws, enc, ceta, b_out, cap_out, status);
-    }
+    if (sc.lgS) launch_encode_k<TP, true>(g, sc, grid, sm, images, keys, ws, enc, ceta, b_out, cap_out, status, st);
+    else launch_encode_k<TP, false>(g, sc, grid, sm, images, keys, ws, enc, ceta, b_out, cap_out, status, st);
 }
 
 void launch_encode(const Geo &g, const uint8_t *images, const uint8_t *keys, const TileWS &ws, uint8_t *enc,

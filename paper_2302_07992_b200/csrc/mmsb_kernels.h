@@ -96,8 +96,10 @@ struct TileWS {
 };
 // blockIdx -> role schedule: groups of GI images (a power of two), 2^lgK keystream and 2^lgW
 // worker CTAs per image, worker CTAs of group g dispatched L grid rows after its keystream CTAs
-struct FusedSched { int GI, ngroups, lgK, lgW, L; };
-FusedSched fused_sched(const Geo &g);
+// worker CTAs per image = 2^lgW = strips x 2^lgS segments per strip (encode splits wide strips;
+// recovery keeps whole strips: its row copy-forward carries from tile to tile)
+struct FusedSched { int GI, ngroups, lgK, lgW, lgS, L; };
+FusedSched fused_sched(const Geo &g, bool split_strips = false);
 
 void launch_encode(const Geo &g, const uint8_t *images, const uint8_t *keys, const TileWS &ws, uint8_t *enc,
                    uint8_t *ceta, int32_t *b_out, int64_t *cap_out, int32_t *status, cudaStream_t st);
