@@ -226,8 +226,8 @@ static int lmr_emin(int M, int N, int req)           /* P:985 {2^4..}, Q10; Tab.
 
 /* ===================================================================================
  * Bi-level tile coder: stands in for JBIG-KIT (builder-defined, Q16).
- * Context: 10 causal tile-local pixels (out-of-tile = 0), MSB->LSB:
- *   (0,-1) (0,-2) (-1,-2) (-1,-1) (-1,0) (-1,+1) (-1,+2) (-2,-1) (-2,0) (-2,+1).
+ * Context: 9 causal tile-local pixels (out-of-tile = 0), MSB->LSB:
+ *   (0,-1) (-1,-2) (-1,-1) (-1,0) (-1,+1) (-1,+2) (-2,-1) (-2,0) (-2,+1)   (Q16).
  * Model: per context a 16-bit probability of a 0, p0, initially 32768; after a 0,
  *   p0 += (65536 - p0) >> 4; after a 1, p0 -= p0 >> 4.
  * Coder: carry-propagating binary range coder, 32-bit range, bound = (range >> 16) * p0;
@@ -235,12 +235,13 @@ static int lmr_emin(int M, int N, int req)           /* P:985 {2^4..}, Q10; Tab.
  *   by shifting out one byte (pending 0xFF run + cache byte); flush = 5 byte shifts.
  * =================================================================================== */
 #define ORC_RATE 4
+#define ORC_NCTX 512
 
 static int ctx_of(const uint8_t *bits, int h, int w, int y, int x)
 {
     (void)h;
 #define PX(dy, dx) ((y + (dy) >= 0 && x + (dx) >= 0 && x + (dx) < w) ? bits[(size_t)(y + (dy)) * w + (x + (dx))] : 0)
-    int c = (PX(0, -1) << 9) | (PX(0, -2) << 8) | (PX(-1, -2) << 7) | (PX(-1, -1) << 6) | (PX(-1, 0) << 5) |
+    int c = (PX(0, -1) << 8) | (PX(-1, -2) << 7) | (PX(-1, -1) << 6) | (PX(-1, 0) << 5) |
             (PX(-1, 1) << 4) | (PX(-1, 2) << 3) | (PX(-2, -1) << 2) | (PX(-2, 0) << 1) | PX(-2, 1);
 #undef PX
     return c;
@@ -278,8 +279,8 @@ static void rc_shift_low(rc_enc *e)
 
 int orc_tile_encode(const uint8_t *bits, int h, int w, uint8_t *out, int cap)
 {
-    uint16_t p0[1024];
-    for (int i = 0; i < 1024; i++) p0[i] = 32768;
+    uint16_t p0[ORC_NCTX];
+    for (int i = 0; i < ORC_NCTX; i++) p0[i] = 32768;
     rc_enc e = {0, 0xFFFFFFFFu, 0, 1, out, 0, cap, 0};
     for (int y = 0; y < h; y++)
         for (int x = 0; x < w; x++) {
@@ -304,8 +305,8 @@ int orc_tile_encode(const uint8_t *bits, int h, int w, uint8_t *out, int cap)
 
 void orc_tile_decode(const uint8_t *in, int nbytes, int h, int w, uint8_t *bits)
 {
-    uint16_t p0[1024];
-    for (int i = 0; i < 1024; i++) p0[i] = 32768;
+    uint16_t p0[ORC_NCTX];
+    for (int i = 0; i < ORC_NCTX; i++) p0[i] = 32768;
     int pos = 0;
 #define NEXT() ((uint32_t)(pos < nbytes ? in[pos++] : (pos++, 0)))
     uint32_t range = 0xFFFFFFFFu, code = 0;

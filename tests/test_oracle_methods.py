@@ -247,8 +247,9 @@ def test_coder_exhaustive_4x4():
         assert np.array_equal(O.tile_decode(O.tile_encode(p), 4, 4), p)
 
 
-def _ideal_bits(plane):
-    """Sum of -log2 P(bit) under the adaptive model with the coder's own integer p0."""
+def _ideal_bits(plane, with_left2=False):
+    """Sum of -log2 P(bit) under the adaptive model with the coder's own integer p0 (Q16's
+    template; with_left2 adds the (0,-2) pixel, SURVEY O15's 10-pixel template, for contrast)."""
     h, w = plane.shape
     p0 = np.full(1024, 32768, np.int64)
     pad = np.zeros((h + 2, w + 4), np.int64)
@@ -257,8 +258,9 @@ def _ideal_bits(plane):
     for y in range(h):
         for x in range(w):
             Y, X = y + 2, x + 2
-            nb = [pad[Y, X - 1], pad[Y, X - 2], pad[Y - 1, X - 2], pad[Y - 1, X - 1], pad[Y - 1, X],
-                  pad[Y - 1, X + 1], pad[Y - 1, X + 2], pad[Y - 2, X - 1], pad[Y - 2, X], pad[Y - 2, X + 1]]
+            nb = [pad[Y, X - 1]] + ([pad[Y, X - 2]] if with_left2 else []) + [
+                pad[Y - 1, X - 2], pad[Y - 1, X - 1], pad[Y - 1, X], pad[Y - 1, X + 1], pad[Y - 1, X + 2],
+                pad[Y - 2, X - 1], pad[Y - 2, X], pad[Y - 2, X + 1]]
             c = 0
             for v in nb:
                 c = (c << 1) | int(v)
@@ -279,6 +281,20 @@ def test_coder_round_trip_and_ideal_bound(density):
         assert np.array_equal(O.tile_decode(data, *shape), p)
         ideal = _ideal_bits(p)
         assert ideal - 8 <= 8 * len(data) <= ideal + 48, (shape, density, ideal, len(data))
+
+
+def test_coder_template_has_no_left2_pixel():
+    """Q16's 9-pixel template on a plane that tells the templates apart: rows repeating with period
+    2 (constant or alternating, the type random per row) are predictable from the (0,-2) pixel,
+    which the template leaves out.  The coded size matches the 9-pixel ideal within the coder's
+    overhead and is far from the 10-pixel (with (0,-2)) ideal."""
+    rng = np.random.default_rng(21)
+    h, w = 64, 128
+    rows = np.tile(rng.integers(0, 2, (h, 2)), (1, w // 2)).astype(np.uint8)     # b[y, x] = b[y, x - 2]
+    coded = 8 * len(O.tile_encode(rows))
+    i9, i10 = _ideal_bits(rows), _ideal_bits(rows, with_left2=True)
+    assert i10 < 0.5 * i9                                               # the plane separates the templates
+    assert i9 - 8 <= coded <= i9 + 48, (coded, i9, i10)
 
 
 def test_coder_many_random_planes():
