@@ -753,11 +753,13 @@ CHACHA_ALU_PER_BYTE = 640 / 64
 # row windows shifted and masked, merged with the two history bits), bound = (range>>16)*p0 2,
 # interval update 2, model update 3, renormalisation test 1; its units are symbols, not pixels
 CODER_ALU_PER_SYMBOL = 12.0
-# the coder's issue floor: one warp per SM sub-partition (112 tiles per SM, smem-bound) issues at
-# most one instruction per cycle, and the unrolled symbol step is this many SASS instructions
-# (DESIGN.md §5.6), so no tile advances faster than one symbol per that many cycles
-CODER_SASS_PER_SYMBOL = {"coder_encode_kernel": 43.0, "lmr_pack+header+coder_decode_kernels": 41.0}
-CODER_TILES_PER_SM = 112
+# the coder's issue floor: 224 tiles per SM (two CTAs of 112 threads, 1 KB model per tile,
+# smem-bound) in 7 warps over the 4 SM sub-partitions, each of which issues at most one warp
+# instruction per cycle (at most 4 x 32 = 128 symbol lanes per cycle per SM); the unrolled symbol
+# step is this many SASS instructions
+CODER_SASS_PER_SYMBOL = {"coder_encode_kernel": 44.0, "lmr_pack+header+coder_decode_kernels": 41.0}
+CODER_TILES_PER_SM = 224
+CODER_ISSUE_LANES_PER_SM = min(CODER_TILES_PER_SM, 4 * 32)
 
 
 def kernel_model(name, der):
@@ -835,9 +837,10 @@ def roofline(prof, peaks, B, HW, cap, method):
                       "bytes_per_px": m["bytes"], "alu_ops_per_unit": m["alu"]}
         if name in CODER_SASS_PER_SYMBOL:       # units are symbols: achieved vs the issue floor
             sym_s = p["pixels"] / sec
-            floor = 148 * CODER_TILES_PER_SM * sm_mhz * 1e6 / CODER_SASS_PER_SYMBOL[name]
+            floor = 148 * CODER_ISSUE_LANES_PER_SM * sm_mhz * 1e6 / CODER_SASS_PER_SYMBOL[name]
             kern[name].update({"sym_per_s": sym_s, "issue_bound_sym_per_s": floor, "issue_bound_frac": sym_s / floor,
-                               "issue_bound_note": f"148 SMs x {CODER_TILES_PER_SM} tiles x f_SM / "
+                               "issue_bound_note": f"148 SMs x {CODER_ISSUE_LANES_PER_SM} issue lanes "
+                                                   f"({CODER_TILES_PER_SM} tiles) x f_SM / "
                                                    f"{CODER_SASS_PER_SYMBOL[name]:.0f} SASS instructions per symbol"})
     total = sum(p["ms"] for p in prof.values()) or 1.0
     for k in kern:
@@ -856,7 +859,7 @@ def roofline(prof, peaks, B, HW, cap, method):
                             "DESIGN.md §5.4)",
              "ops_model": ("ChaCha20: 10 ALU ops per keystream byte" if "coder" not in dom else
                            f"tile coder: {CODER_ALU_PER_SYMBOL:.0f} integer ops per coded symbol (DESIGN.md §5.6); "
-                           "a serial chain per tile, ~112 tiles in flight per SM"),
+                           f"a serial chain per tile, {CODER_TILES_PER_SM} tiles in flight per SM"),
              "hbm": {"achieved_GBps": k["algorithmic_GBps"], "peak": hbm_peak, "frac": k["hbm_frac"]}}
     d["share_of_step"] = k["share"]
     if "issue_bound_frac" in k:

@@ -4,14 +4,14 @@
 // the hider, the K2 receiver and the K1 receiver.
 //
 // Coder (O15): tiles of side min(2^t, dim) coded independently in tile raster
-// order; 10-pixel causal tile-local context, MSB->LSB (0,-1) (0,-2) (-1,-2) (-1,-1) (-1,0)
-// (-1,+1) (-1,+2) (-2,-1) (-2,0) (-2,+1), out-of-tile pixels 0; per context a 16-bit
+// order; 9-pixel causal tile-local context (Q16), MSB->LSB (0,-1) (-1,-2) (-1,-1)
+// (-1,0) (-1,+1) (-1,+2) (-2,-1) (-2,0) (-2,+1), out-of-tile pixels 0; per context a 16-bit
 // probability of a 0, p0 = 32768 initially, p0 += (65536-p0)>>4 after a 0, p0 -= p0>>4 after
 // a 1; carry-propagating range coder, 32-bit range, bound = (range>>16)*p0, renormalise below
 // 2^24 one byte at a time through a cache byte + 0xFF run, flush = 5 byte shifts; the
 // decoder reads bytes past the end of the tile's stream as 0.
 //
-// One GPU thread codes one tile (the coder is serial within a tile); its model (1024 x u16)
+// One GPU thread codes one tile (the coder is serial within a tile); its model (512 x u16)
 // lives in shared memory.  The fast kernels (tiles 32, 64 or 128 wide: every configured shape)
 // run 112-thread CTAs with a branch-free symbol step; the reference kernels
 // (coder_encode_kernel / coder_decode_kernel, one warp per CTA, model entry ctx of lane l at u16
@@ -23,7 +23,8 @@
 
 namespace mmsb {
 
-constexpr int kCoderThreads = 32;                 // one warp per CTA (smem-bound: 64 KB of models)
+constexpr int kCoderThreads = 32;                 // one warp per CTA (smem-bound: 32 KB of models)
+constexpr int kNCtx = 512;                        // 9-pixel template
 constexpr int kRowWords = 6;                      // padded MSB-first row: 2 lead bits + <= 128 + pad
 
 __host__ __device__ inline int lmr_tile_side(int t, int dim) { return (1 << t) < dim ? (1 << t) : dim; }
@@ -103,7 +104,7 @@ __device__ __forceinline__ bool wave_item(const Geo &g, int wave, int R, long lo
 // ======================================================================================
 __global__ void __launch_bounds__(kCoderThreads) coder_encode_kernel(Geo g, int wave, int round_tiles, const uint8_t *__restrict__ ceta,
                                                                      LmrEncWS ew) {
-    extern __shared__ uint16_t p0s[];                                  // [1024][32]
+    extern __shared__ uint16_t p0s[];                                  // [kNCtx][32]
     __shared__ uint32_t rows[kCoderThreads][3][kRowWords];
     const int lane = threadIdx.x;
     const int Tc = lmr_tile_count(g.H, g.W, g.tile_log2);
@@ -122,7 +123,7 @@ __global__ void __launch_bounds__(kCoderThreads) coder_encode_kernel(Geo g, int 
     const int b = slot == 0 ? 0 : pl.order[it.cand < 0 ? 0 : it.cand];
     const int cap = lmr_tile_cap(g.tile_log2, g.H, g.W);
 
-    for (int c = 0; c < 1024; c++) p0s[c * 32 + lane] = 32768;
+    for (int c = 0; c < kNCtx; c++) p0s[c * 32 + lane] = 32768;
     uint32_t(*R)[kRowWords] = rows[lane];
     for (int r = 0; r < 3; r++)
         for (int k = 0; k < kRowWords; k++) R[r][k] = 0;
@@ -134,13 +135,12 @@ __global__ void __launch_bounds__(kCoderThreads) coder_encode_kernel(Geo g, int 
             uint32_t *cur = R[y % 3];
             const uint32_t *p1 = R[(y + 2) % 3], *p2 = R[(y + 1) % 3];     // rows y-1, y-2 (zero when absent)
             for (int k = 0; k < kRowWords; k++) cur[k] = 0;
-            uint32_t hist2 = 0;                                            // bits (0,-1), (0,-2)
+            uint32_t left = 0;                                             // bit (0,-1)
             const uint8_t *rowp = src + (size_t)(y0 + y) * g.W + x0;
             for (int x = 0; x < w; x++) {
                 const uint8_t v = rowp[x];
                 const uint32_t bit = slot == 0 ? (uint32_t)(v >> 7) : (uint32_t)((v & 0xF) < b);
-                const uint32_t ctx = ((hist2 & 1u) << 9) | ((hist2 >> 1) << 8) |
-                                     (row_window(p1, x, 5) << 3) | row_window(p2, x + 1, 3);
+                const uint32_t ctx = (left << 8) | (row_window(p1, x, 5) << 3) | row_window(p2, x + 1, 3);
                 uint16_t *pp = &p0s[ctx * 32 + lane];
                 const uint32_t p = *pp;
                 const uint32_t bound = (e.range >> 16) * p;
@@ -156,7 +156,7 @@ __global__ void __launch_bounds__(kCoderThreads) coder_encode_kernel(Geo g, int 
                     e.range <<= 8;
                     e.shift_low();
                 }
-                hist2 = ((hist2 << 1) | bit) & 3u;
+                left = bit;
                 if (bit) cur[(x + 2) >> 5] |= 0x80000000u >> ((x + 2) & 31);
             }
             // keep the two padding words beyond the row zero for the next rows' windows
@@ -491,7 +491,7 @@ __global__ void __launch_bounds__(kCoderThreads) coder_decode_kernel(Geo g, int 
     const int y0 = (tile / TN) * th, x0 = (tile % TN) * tw;
     const int h = g.H - y0 < th ? g.H - y0 : th, w = g.W - x0 < tw ? g.W - x0 : tw;
 
-    for (int c = 0; c < 1024; c++) p0s[c * 32 + lane] = 32768;
+    for (int c = 0; c < kNCtx; c++) p0s[c * 32 + lane] = 32768;
     uint32_t(*R)[kRowWords] = rows[lane];
     for (int r = 0; r < 3; r++)
         for (int k = 0; k < kRowWords; k++) R[r][k] = 0;
@@ -519,11 +519,10 @@ __global__ void __launch_bounds__(kCoderThreads) coder_decode_kernel(Geo g, int 
         uint32_t *cur = R[y % 3];
         const uint32_t *p1 = R[(y + 2) % 3], *p2 = R[(y + 1) % 3];
         for (int kk = 0; kk < kRowWords; kk++) cur[kk] = 0;
-        uint32_t hist2 = 0, acc = 0;
+        uint32_t left = 0, acc = 0;
         const long long rowbit = (long long)img * g.HW + (long long)(y0 + y) * g.W + x0;
         for (int x = 0; x < w; x++) {
-            const uint32_t ctx = ((hist2 & 1u) << 9) | ((hist2 >> 1) << 8) | (row_window(p1, x, 5) << 3) |
-                                 row_window(p2, x + 1, 3);
+            const uint32_t ctx = (left << 8) | (row_window(p1, x, 5) << 3) | row_window(p2, x + 1, 3);
             uint16_t *pp = &p0s[ctx * 32 + lane];
             const uint32_t p = *pp;
             const uint32_t bound = (range >> 16) * p;
@@ -542,7 +541,7 @@ __global__ void __launch_bounds__(kCoderThreads) coder_decode_kernel(Geo g, int 
                 range <<= 8;
                 code = (code << 8) | next();
             }
-            hist2 = ((hist2 << 1) | bit) & 3u;
+            left = bit;
             if (bit) cur[(x + 2) >> 5] |= 0x80000000u >> ((x + 2) & 31);
             acc |= bit << (x & 31);
             if ((x & 31) == 31 || x == w - 1) {
@@ -558,28 +557,30 @@ __global__ void __launch_bounds__(kCoderThreads) coder_decode_kernel(Geo g, int 
 // ======================================================================================
 // Fast coder kernels for tiles at least 32 pixels wide (every configured shape).  Same bit
 // stream as coder_encode_kernel / coder_decode_kernel, restructured for a
-// serial chain that has only a few warps per SM to hide its latency (the models, 2 KB per
-// tile, bound residency at ~112 tiles per SM):
+// serial chain that has only a few warps per SM to hide its latency (the models, 1 KB per
+// tile, bound residency at ~224 tiles per SM):
 //  * CTAs of kFastThreads = 112 threads (3.5 warps: all four SM sub-partitions busy) holding
-//    224 KB of models, one CTA per SM;
+//    112 KB of models, kFastCtas = 2 CTAs per SM;
 //  * the row is walked in half-words of 16 pixels with the 16 symbols fully unrolled: the
-//    10-pixel context of every symbol comes from two pre-aligned 32-bit slices of the rows
-//    above with immediate shifts;
+//    9-pixel context of every symbol comes from two pre-aligned 32-bit slices of the rows
+//    above with immediate shifts (only its (0,-1) bit depends on the symbol before);
 //  * the next symbol's probability is loaded while the current one is coded -- the decoder
-//    loads both candidates and forwards the freshly updated probability when the contexts
-//    coincide, so after the bit is known only one select remains;
+//    loads both candidates (their address does not depend on the bit being decoded) and
+//    forwards the freshly updated probability when the contexts coincide, so after the bit
+//    is known only one select remains;
 //  * renormalisation is branch-free: the number of bytes to shift is clz(range) >> 3 (0..2:
 //    range >= 3840 after any symbol), the decoder reads through a 64-bit MSB-aligned bit
 //    buffer refilled from funnel-shifted stream words (bytes past the end read as 0), the
 //    encoder's byte output is predicated (only a pending 0xFF run takes a branch).
 // ======================================================================================
 constexpr int kFastThreads = 112;
-constexpr int kHalfCtx = 512;                                  // contexts with (0,-1) = 0; the rest at +kHiOff
-constexpr uint32_t kHiOff = kFastThreads * kHalfCtx * 2;      // bytes: models of contexts 512..1023
+constexpr int kFastCtas = 2;                                   // resident CTAs per SM
+constexpr int kHalfCtx = kNCtx / 2;                            // contexts with (0,-1) = 0; the rest at +kHiOff
+constexpr uint32_t kHiOff = kFastThreads * kHalfCtx * 2;      // bytes: models of contexts 256..511
 static constexpr size_t fast_smem() { return 2 * (size_t)kHiOff; }
 
-// Model layout (224 KB): context ctx of thread tid at byte
-//   (ctx >> 9) * kHiOff + warp * 512 * 64 + (ctx & 511) * sbytes + lane * 2,
+// Model layout (112 KB): context ctx of thread tid at byte
+//   (ctx >> 8) * kHiOff + warp * 256 * 64 + (ctx & 255) * sbytes + lane * 2,
 // sbytes = 2 * (lanes of the warp): warp-interleaved (<= 2-way bank conflicts), and the two
 // contexts that differ only in the (0,-1) bit a fixed immediate offset apart.
 __device__ __forceinline__ void fast_model_init(uint16_t *p0s) {
@@ -713,7 +714,7 @@ struct FastEnc {
 };
 
 template <int NW>
-__global__ void __launch_bounds__(kFastThreads, 1) coder_encode_fast_kernel(Geo g, int wave, int R,
+__global__ void __launch_bounds__(kFastThreads, kFastCtas) coder_encode_fast_kernel(Geo g, int wave, int R,
                                                                          const uint8_t *__restrict__ ceta, LmrEncWS ew,
                                                                          unsigned long long *__restrict__ sym_count) {
     extern __shared__ __align__(16) uint16_t p0s[];
@@ -789,10 +790,8 @@ __global__ void __launch_bounds__(kFastThreads, 1) coder_encode_fast_kernel(Geo 
         uint32_t s1, s2;
         RowWin<NW> win;
         win.start(p1, p2, s1, s2);
-        uint32_t actx = mbase + slice_ctx(s1, s2, 0) * sbytes;         // hist bits 0 at the row start
+        uint32_t actx = mbase + slice_ctx(s1, s2, 0) * sbytes;         // (0,-1) = 0 at the row start
         uint32_t p = lds_u16(actx);
-        uint32_t bbase = mbase;                                        // mbase + (0,-2) bit * 256 sbytes
-        const uint32_t s256 = 256u * sbytes;
         const uint32_t two = g.one + g.one, neg1 = 0u - g.one;        // opaque 2 and -1: FMA-pipe multiplies
 #pragma unroll 1
         for (int q = 0; q < 2 * NW; q++) {
@@ -808,7 +807,7 @@ __global__ void __launch_bounds__(kFastThreads, 1) coder_encode_fast_kernel(Geo 
                 const uint32_t bv = cb >> 31;
                 cb = imad(cb, two, 0u);
                 const uint32_t nrows = J < 15 ? slice_ctx(s1, s2, J + 1) : slice_ctx(t1, t2, 0);
-                const uint32_t anctx = imad(bv, kHiOff, imad(nrows, sbytes, bbase));
+                const uint32_t anctx = imad(bv, kHiOff, imad(nrows, sbytes, mbase));
                 const uint32_t np = lds_u16(anctx);
                 const uint32_t bound = (e.range >> 16) * p;
                 const uint32_t tb = imad(bv, bound, 0u);                      // low += bound if 1
@@ -824,7 +823,6 @@ __global__ void __launch_bounds__(kFastThreads, 1) coder_encode_fast_kernel(Geo 
                 e.range <<= s8;
                 p = anctx == actx ? pu : np;
                 actx = anctx;
-                bbase = imad(bv, s256, mbase);
             }
             e.end_half(am);
             s1 = t1;
@@ -943,7 +941,7 @@ struct FastIn {
 };
 
 template <int NW>
-__global__ void __launch_bounds__(kFastThreads, 1) coder_decode_fast_kernel(Geo g, int want_eta, const uint8_t *__restrict__ mbuf,
+__global__ void __launch_bounds__(kFastThreads, kFastCtas) coder_decode_fast_kernel(Geo g, int want_eta, const uint8_t *__restrict__ mbuf,
                                                                          const int32_t *__restrict__ lmr_b,
                                                                          const int32_t *__restrict__ lmr_t,
                                                                          const int32_t *__restrict__ offsets,
@@ -1010,8 +1008,7 @@ __global__ void __launch_bounds__(kFastThreads, 1) coder_decode_fast_kernel(Geo 
         win.start(p1, p2, s1, s2);
         uint32_t actx = mbase + slice_ctx(s1, s2, 0) * sbytes;
         uint32_t p = lds_u16(actx);
-        uint32_t bbase = mbase, word = 0, acc = 0;                     // bbase: mbase + (0,-2) bit * 256 sbytes
-        const uint32_t s256 = 256u * sbytes;
+        uint32_t word = 0, acc = 0;
         uint32_t *orow = plane_out + (((size_t)img * g.HW + (size_t)(y0 + y) * g.W + x0) >> 5);
 #pragma unroll 1
         for (int q = 0; q < 2 * NW; q++) {
@@ -1025,7 +1022,7 @@ __global__ void __launch_bounds__(kFastThreads, 1) coder_decode_fast_kernel(Geo 
                 // as in the encoder, the decoded bit is an integer bv in {0, 1} and the
                 // bit-dependent selects are multiply-adds on the FMA pipe
                 const uint32_t nrows = J < 15 ? slice_ctx(s1, s2, J + 1) : slice_ctx(t1, t2, 0);
-                const uint32_t a0 = imad(nrows, sbytes, bbase);
+                const uint32_t a0 = imad(nrows, sbytes, mbase);
                 const uint32_t np0 = lds_u16(a0), np1 = lds_u16(a0 + kHiOff);
                 const uint32_t bound = (range >> 16) * p;
                 const bool bit = code >= bound;
@@ -1044,7 +1041,6 @@ __global__ void __launch_bounds__(kFastThreads, 1) coder_decode_fast_kernel(Geo 
                 const uint32_t np = bv ? np1 : np0;
                 p = anctx == actx ? pu : np;
                 actx = anctx;
-                bbase = imad(bv, s256, mbase);
             }
             const uint32_t lw = __brev(hw) >> 16;                      // the half's bits, pixel order
             s1 = t1;
@@ -1071,7 +1067,7 @@ __global__ void __launch_bounds__(kFastThreads, 1) coder_decode_fast_kernel(Geo 
 int lmr_tile_cap_host(int t, int H, int W) { return lmr_tile_cap(t, H, W); }
 int lmr_tile_stride_host(int t, int H, int W) { return lmr_tile_stride(t, H, W); }
 
-static size_t coder_smem() { return 1024 * 32 * sizeof(uint16_t); }
+static size_t coder_smem() { return kNCtx * 32 * sizeof(uint16_t); }
 
 void lmr_set_smem_attrs() {
     static bool done = false;
@@ -1101,10 +1097,10 @@ static int sm_count() {
     }
     return n;
 }
-// resident coder tiles per round: fast kernel one CTA of kFastThreads per SM, legacy 3 warps per SM
+// resident coder tiles per round: fast kernel kFastCtas CTAs of kFastThreads per SM, legacy 3 warps per SM
 static int coder_round(const Geo &g) {
     const int tw = lmr_tile_side(g.tile_log2, g.W);
-    return tw == 32 || tw == 64 || tw == 128 ? sm_count() * kFastThreads : sm_count() * 3 * kCoderThreads;
+    return tw == 32 || tw == 64 || tw == 128 ? sm_count() * kFastCtas * kFastThreads : sm_count() * 3 * kCoderThreads;
 }
 
 void launch_coder_encode(const Geo &g, int wave, const uint8_t *ceta, const LmrEncWS &e,
