@@ -59,6 +59,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-security", action="store_true", help="skip the untimed statistics table")
     ap.add_argument("--lmr-emin", type=int, default=0, help="LMR rotation schedule {2^e..} (Tab. LMR_block_size)")
+    ap.add_argument("--lmr-tile", type=int, default=7, help="LMR coder tile 2^t (reading Q16: t = 7)")
     ap.add_argument("--cipher-rounds", type=int, default=0, choices=[0, 8, 12, 20],
                     help="keystream rounds: 0/20 = ChaCha20 (default, reading Q12); 12 / 8 = reduced-round option")
     return ap.parse_args()
@@ -98,6 +99,7 @@ def config_json(args, config, cfg, method, B, world, shard=False):
             else "inputs smaller than L2",
             "keys": "ChaCha20 K = k128||k128 per image (reading Q13)",
             "lmr_emin": (args.lmr_emin or 4) if method == "lmr" else None,
+            "lmr_tile_log2": args.lmr_tile if method == "lmr" else None,
             "cipher": f"ChaCha{args.cipher_rounds or 20}" + ("" if args.cipher_rounds in (0, 20) else
                                                               " (reduced-round format option, SURVEY 8(f) NEXT 4)")}
 
@@ -421,7 +423,8 @@ def measure(args, rank, world, local, config=None, method=None):
     I = torch.from_numpy(imgs).to(dev)
     K1 = torch.from_numpy(k1).to(dev)
     K2 = torch.from_numpy(k2).to(dev)
-    ws = G.Workspace(mid, B, H, W, device=dev, lmr_emin=args.lmr_emin, cipher_rounds=args.cipher_rounds)
+    ws = G.Workspace(mid, B, H, W, tile_log2=args.lmr_tile, device=dev, lmr_emin=args.lmr_emin,
+                     cipher_rounds=args.cipher_rounds)
     enc = torch.empty_like(I)
     marked = torch.empty_like(I)
     rec = torch.empty_like(I)
@@ -577,7 +580,8 @@ def measure_e2e(args, G, P, dev, stream, world, mid, B, H, W, stride, imgs, k1, 
     class Lane:
         def __init__(self):
             self.stream = torch.cuda.Stream(device=dev)
-            self.ws = G.Workspace(mid, sub, H, W, device=dev, lmr_emin=args.lmr_emin, cipher_rounds=args.cipher_rounds)
+            self.ws = G.Workspace(mid, sub, H, W, tile_log2=args.lmr_tile, device=dev, lmr_emin=args.lmr_emin,
+                                  cipher_rounds=args.cipher_rounds)
             self.I = torch.empty(sub, H, W, dtype=torch.uint8, device=dev)
             self.K1 = torch.empty(sub, 32, dtype=torch.uint8, device=dev)
             self.K2 = torch.empty(sub, 32, dtype=torch.uint8, device=dev)

@@ -653,6 +653,13 @@ struct RowWin {
 __device__ __forceinline__ uint32_t slice_ctx(uint32_t s1, uint32_t s2, int J) {
     return ((s1 >> (24 - J)) & 0xF8u) | ((s2 >> (29 - J)) & 7u);
 }
+// number of bits to shift in after a symbol: clz(range) & 24 (0, 8 or 16) as one LOP3 on the
+// highest set bit's index (31 - f = ~f for f in [0, 31])
+__device__ __forceinline__ int renorm_shift(uint32_t range) {
+    uint32_t f;
+    asm("bfind.u32 %0, %1;" : "=r"(f) : "r"(range));
+    return (int)(~f & 24u);
+}
 
 __device__ __forceinline__ void st_u8_if(bool c, uint8_t *p, uint32_t v) {
     asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %0, 0;\n\t@q st.global.u8 [%1], %2;\n\t}" ::"r"((uint32_t)c), "l"(p),
@@ -1032,7 +1039,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtas) coder_decode_fast_ker
                 const int32_t dp = (int32_t)imad(bv, 15u - 65536u, imad(p, 0xFFFFFFFFu, 65536u));
                 const uint32_t pu = p + (uint32_t)(dp >> 4);                  // the encoder's p0 update
                 sts_u16(actx, pu);
-                const int s8 = __clz(range) & 24;                     // 0, 8 or 16 bits to shift in
+                const int s8 = renorm_shift(range);                   // 0, 8 or 16 bits to shift in
                 code = __funnelshift_l(in.b0, code, s8);
                 range <<= s8;
                 in.consume(s8);

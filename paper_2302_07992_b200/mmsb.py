@@ -140,13 +140,15 @@ class Workspace:
 
 
 def _ws(ws: Workspace | None, method, B, H, W, tile_log2, device):
+    if tile_log2 is None:                       # the workspace's coder tile size (default 2^7)
+        tile_log2 = ws.shape.tile_log2 if ws is not None else 7
     if ws is None or (ws.shape.method, ws.shape.batch, ws.shape.height, ws.shape.width, ws.shape.tile_log2) != (
             method, B, H, W, tile_log2):
         ws = Workspace(method, B, H, W, tile_log2, device)
     return ws
 
 
-def encode(method: int, images: torch.Tensor, k1: torch.Tensor, ws: Workspace | None = None, tile_log2: int = 7,
+def encode(method: int, images: torch.Tensor, k1: torch.Tensor, ws: Workspace | None = None, tile_log2: int | None = None,
            out: torch.Tensor | None = None):
     """Content owner: returns (encrypted, b, capacity_bits, status) -- mmsb_content_owner_encode."""
     B, H, W = _images(images, "images")
@@ -165,7 +167,7 @@ def encode(method: int, images: torch.Tensor, k1: torch.Tensor, ws: Workspace | 
 
 
 def embed(method: int, encrypted: torch.Tensor, k2: torch.Tensor, msg: torch.Tensor, msg_bits: torch.Tensor,
-          ws: Workspace | None = None, tile_log2: int = 7, out: torch.Tensor | None = None):
+          ws: Workspace | None = None, tile_log2: int | None = None, out: torch.Tensor | None = None):
     """Data hider: returns (marked, status) -- mmsb_hider_embed."""
     B, H, W = _images(encrypted, "encrypted")
     dev = encrypted.device
@@ -188,7 +190,7 @@ def embed(method: int, encrypted: torch.Tensor, k2: torch.Tensor, msg: torch.Ten
 
 
 def extract(method: int, marked: torch.Tensor, k2: torch.Tensor, stride: int, ws: Workspace | None = None,
-            tile_log2: int = 7, out: torch.Tensor | None = None):
+            tile_log2: int | None = None, out: torch.Tensor | None = None):
     """Receiver with K2: returns (msg_bytes, msg_bits, status) -- mmsb_receiver_extract."""
     B, H, W = _images(marked, "marked")
     _arg(k2, "k2", torch.uint8, (B, 32), marked.device)
@@ -206,7 +208,7 @@ def extract(method: int, marked: torch.Tensor, k2: torch.Tensor, stride: int, ws
     return msg, nb, st
 
 
-def recover(method: int, marked: torch.Tensor, k1: torch.Tensor, ws: Workspace | None = None, tile_log2: int = 7,
+def recover(method: int, marked: torch.Tensor, k1: torch.Tensor, ws: Workspace | None = None, tile_log2: int | None = None,
             out: torch.Tensor | None = None, original: torch.Tensor | None = None, sse_out: torch.Tensor | None = None):
     """Receiver with K1: returns (recovered, status) -- mmsb_receiver_recover.  With `original`
     (an evaluation harness's reference image) the SSE statistic is fused into the same pass and
@@ -233,7 +235,7 @@ def recover(method: int, marked: torch.Tensor, k1: torch.Tensor, ws: Workspace |
 
 
 def receive_both(method: int, marked: torch.Tensor, k1: torch.Tensor, k2: torch.Tensor, stride: int,
-                 ws: Workspace | None = None, tile_log2: int = 7, msg_out: torch.Tensor | None = None,
+                 ws: Workspace | None = None, tile_log2: int | None = None, msg_out: torch.Tensor | None = None,
                  rec_out: torch.Tensor | None = None):
     """Receiver with both keys: returns (msg_bytes, msg_bits, recovered, status) -- mmsb_receiver_both."""
     B, H, W = _images(marked, "marked")
@@ -256,7 +258,7 @@ def receive_both(method: int, marked: torch.Tensor, k1: torch.Tensor, k2: torch.
     return msg, nb, rec, st
 
 
-def capacity(method: int, image: torch.Tensor, ws: Workspace | None = None, tile_log2: int = 7):
+def capacity(method: int, image: torch.Tensor, ws: Workspace | None = None, tile_log2: int | None = None):
     """Capacity of an encrypted / marked image: returns (b, capacity_bits, status) -- mmsb_capacity."""
     B, H, W = _images(image, "image")
     ws = _ws(ws, method, B, H, W, tile_log2, image.device)
