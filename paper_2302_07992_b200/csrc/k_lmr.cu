@@ -693,7 +693,8 @@ struct FastEnc {
     __device__ __forceinline__ void emit(bool p1, bool p2, int s8) {
         cm |= (hi >> 8) << k;
         const uint32_t h8 = hi & 0xFFu;
-        uint8_t *op = obase + k;
+        uint8_t *op;                              // obase + k as a wide multiply-add (FMA pipe)
+        asm("mad.wide.u32 %0, %1, 1, %2;" : "=l"(op) : "r"((uint32_t)k), "l"(obase));
         st_u8_if(p1, op, h8);
         st_u8_if(p2, op + 1, lo >> 24);
         hi = __funnelshift_l(lo, h8, s8) & 0xFFu;
@@ -819,7 +820,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtas) coder_encode_fast_ker
                 const uint32_t bound = (e.range >> 16) * p;
                 const uint32_t tb = imad(bv, bound, 0u);                      // low += bound if 1
                 asm("add.cc.u32 %0, %0, %2;\n\taddc.u32 %1, %1, 0;" : "+r"(e.lo), "+r"(e.hi) : "r"(tb));
-                e.range = bv ? e.range - bound : bound;                         // (serial chain: select)
+                e.range = imad(bv, imad(bound, 0xFFFFFFFEu, e.range), bound);   // bound + bv (range - 2 bound)
                 // p0 update: 1 -> p - (p >> 4) = p + floor((15 - p) / 16); 0 -> p + ((65536 - p) >> 4)
                 const int32_t dp = (int32_t)imad(bv, 15u - 65536u, imad(p, neg1, 65536u));
                 const uint32_t pu = p + (uint32_t)(dp >> 4);
@@ -913,6 +914,15 @@ struct FastIn {
         b3 = next_word(true);
         b4 = next_word(true);
         nb = 160;
+    }
+    // n in [0, 32] bits (two symbols' worth)
+    __device__ __forceinline__ void consume2(int n) {
+        b0 = __funnelshift_lc(b1, b0, n);
+        b1 = __funnelshift_lc(b2, b1, n);
+        b2 = __funnelshift_lc(b3, b2, n);
+        b3 = __funnelshift_lc(b4, b3, n);
+        b4 = __funnelshift_lc(0u, b4, n);
+        nb -= n;
     }
     __device__ __forceinline__ void consume(int s8) {                // s8 = 0, 8 or 16 bits
         b0 = __funnelshift_l(b1, b0, s8);
@@ -1022,6 +1032,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtas) coder_decode_fast_ker
             uint32_t t1, t2;
             win.next(q & 1, t1, t2);
             uint32_t hw = 0;
+            int u = 0;                                                 // bits the even symbol took
 #pragma unroll
             for (int J = 0; J < 16; J++) {
                 if ((J & 7) == 0) in.refill(am);                       // >= 128 bits for 8 symbols
@@ -1035,17 +1046,24 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtas) coder_decode_fast_ker
                 const bool bit = code >= bound;
                 const uint32_t bv = bit ? 1u : 0u;
                 range = bit ? range - bound : bound;                            // the serial chain: selects
-                code = bit ? code - bound : code;
+                code = imad(bv, 0u - bound, code);
                 const int32_t dp = (int32_t)imad(bv, 15u - 65536u, imad(p, 0xFFFFFFFFu, 65536u));
                 const uint32_t pu = p + (uint32_t)(dp >> 4);                  // the encoder's p0 update
                 sts_u16(actx, pu);
                 const int s8 = renorm_shift(range);                   // 0, 8 or 16 bits to shift in
-                code = __funnelshift_l(in.b0, code, s8);
+                // the bit buffer is shifted once per symbol pair: the even symbol takes its bits
+                // from the buffer's top, the odd one from bit u (the even symbol's shift) on
+                if ((J & 1) == 0) {
+                    code = __funnelshift_l(in.b0, code, s8);
+                    u = s8;
+                } else {
+                    code = __funnelshift_l(__funnelshift_lc(in.b1, in.b0, u), code, s8);
+                    in.consume2(u + s8);
+                }
                 range <<= s8;
-                in.consume(s8);
                 hw = imad(bv, 1u << (15 - J), hw);
                 const uint32_t anctx = imad(bv, kHiOff, a0);
-                const uint32_t np = bv ? np1 : np0;
+                const uint32_t np = imad(bv, np1 - np0, np0);
                 p = anctx == actx ? pu : np;
                 actx = anctx;
             }
