@@ -27,3 +27,15 @@ def test_calls_check_before_the_library():
         G.recover(G.EMR, torch.zeros(16, 16, dtype=torch.uint8), torch.zeros(1, 32, dtype=torch.uint8))
     with pytest.raises(G.MmsbError):
         G.extract(G.EMR, imgs, torch.zeros(2, 32, dtype=torch.uint8), 24)         # stride % 16
+
+
+def test_calls_take_the_workspace_tile_size():
+    """tile_log2=None (the default of every call) means the workspace's coder tile size, so a
+    workspace made for t = 6 is used as it is instead of being re-allocated for t = 7."""
+
+    class FakeWs:
+        shape = G._shape(G.LMR, 2, 64, 64, tile_log2=6)
+
+    ws = FakeWs()
+    assert G._ws(ws, G.LMR, 2, 64, 64, None, "cpu") is ws
+    assert G._ws(ws, G.LMR, 2, 64, 64, 6, "cpu") is ws
