@@ -761,7 +761,7 @@ CODER_ALU_PER_SYMBOL = 12.0
 # smem-bound) in 7 warps over the 4 SM sub-partitions, each of which issues at most one warp
 # instruction per cycle (at most 4 x 32 = 128 symbol lanes per cycle per SM); the unrolled symbol
 # step is this many SASS instructions
-CODER_SASS_PER_SYMBOL = {"coder_encode_kernel": 44.0, "lmr_pack+header+coder_decode_kernels": 41.0}
+CODER_SASS_PER_SYMBOL = {"coder_encode_kernel": 44.0, "lmr_pack+header+coder_decode_kernels": 39.0}
 CODER_TILES_PER_SM = 224
 CODER_ISSUE_LANES_PER_SM = min(CODER_TILES_PER_SM, 4 * 32)
 

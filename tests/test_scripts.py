@@ -39,7 +39,7 @@ def test_bench_roofline_fields():
     assert abs(d["frac"] - d["achieved"] / d["peak"]) < 1e-12
     cs = d["coder_symbols"]
     assert abs(cs["achieved_sym_per_s"] - 10_400_000_000 / 0.032) < 1.0
-    floor = 148 * 128 * 1965e6 / 41.0     # 4 SMSPs x 32 issue lanes per SM (224 tiles resident)
+    floor = 148 * 128 * 1965e6 / 39.0     # 4 SMSPs x 32 issue lanes per SM (224 tiles resident)
     assert abs(cs["issue_bound_sym_per_s"] - floor) < 1.0 and abs(cs["frac"] - cs["achieved_sym_per_s"] / floor) < 1e-12
     k = r["kernels"]["encode_kernel"]
     assert abs(k["algorithmic_GBps"] - 2.0 * 20 * 1000 * HW / 0.010 / 1e9) < 1e-6
