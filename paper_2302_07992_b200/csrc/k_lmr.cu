@@ -569,9 +569,13 @@ __global__ void __launch_bounds__(kCoderThreads) coder_decode_kernel(Geo g, int 
 //    forwards the freshly updated probability when the contexts coincide, so after the bit
 //    is known only one select remains;
 //  * renormalisation is branch-free: the number of bytes to shift is clz(range) >> 3 (0..2:
-//    range >= 3840 after any symbol), the decoder reads through a 64-bit MSB-aligned bit
-//    buffer refilled from funnel-shifted stream words (bytes past the end read as 0), the
-//    encoder's byte output is predicated (only a pending 0xFF run takes a branch).
+//    range >= 3840 after any symbol), the decoder reads through a 160-bit MSB-aligned bit
+//    buffer refilled from funnel-shifted stream words (bytes past the end read as 0) and
+//    shifted once per symbol pair, the encoder's byte output is predicated (only a carry into
+//    already written digits takes a branch);
+//  * the step is ALU-pipe bound, so bit-dependent updates are multiply-adds with the bit as a
+//    0/1 factor on the FMA pipe wherever that does not lengthen the decoder's loop-carried
+//    chain.
 // ======================================================================================
 constexpr int kFastThreads = 112;
 constexpr int kFastCtas = 2;                                   // resident CTAs per SM
