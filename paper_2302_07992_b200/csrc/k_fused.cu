@@ -434,7 +434,8 @@ constexpr int kStages = MMSB_STAGES;
 
 __device__ __forceinline__ uint32_t bits4_to_bytes(uint32_t m4) { return ((m4 & 0xFu) * 0x00204081u) & 0x01010101u; }
 // byte LSBs (bits 0, 8, 16, 24) -> bits 0..3: one multiply puts them at bits 21..24 (no other term lands there)
-__device__ __forceinline__ uint32_t bytes_to_bits4(uint32_t l) { return ((l * 0x00204081u) >> 21) & 0xFu; }
+// (l * (2^7 + 2^14 + 2^21 + 2^28)) moves bit 8k to 28 + k with no other term at or above bit 28
+__device__ __forceinline__ uint32_t bytes_to_bits4(uint32_t l) { return (l * 0x10204080u) >> 28; }
 
 // a cell's own turns from the worker record: level-2 angle (bits 0-1), level-1 angles of its
 // upper (bits 2-5) and lower (bits 6-9) 2x2 block pairs

@@ -30,15 +30,15 @@ constexpr int kKbufWords = kMaxBlk * 16 + 4;     // + 3 words of alignment offse
 template <int METHOD>
 __device__ __forceinline__ uint32_t zero_mask16(const uint4 &u, bool first, const uint32_t *smap, int p_rel) {
     if constexpr (METHOD == 0) {
-        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-        uint32_t m = 0;
-#pragma unroll
-        for (int i = 0; i < 4; i++) {
-            // LSB == 0 -> redundant; the byte LSBs (bits 0, 8, 16, 24) gathered by one multiply:
-            // l * (1 + 2^7 + 2^14 + 2^21) puts them at bits 21..24, no other term lands there
-            const uint32_t l = ~w[i] & 0x01010101u;
-            m |= (((l * 0x00204081u) >> 21) & 0xFu) << (4 * i);
-        }
+        // LSB == 0 -> redundant.  Two words at a time: their byte LSBs interleaved as nibble bits
+        // (word a at bits 8k, word b at bits 8k + 4, one bit-select), inverted, and gathered into
+        // the top byte by one multiply: l * (2^3 + 2^10 + 2^17 + 2^24) moves bit 8k to 24 + k and
+        // bit 8k + 4 to 28 + k, and no two terms meet (no carries)
+        auto pair = [](uint32_t a, uint32_t b) -> uint32_t {
+            const uint32_t x = (a & 0x0F0F0F0Fu) | ((b << 4) & 0xF0F0F0F0u);
+            return ((~x & 0x11111111u) * 0x01020408u) >> 24;
+        };
+        uint32_t m = pair(u.x, u.y) | (pair(u.z, u.w) << 8);
         if (first) m &= ~7u;                                     // image pixels 0..2 hold the header (Q14)
         return m;
     } else {
