@@ -7,7 +7,7 @@
 //       P:656, Q12), the tile's in-tile angles (levels 1..tp, eq. roration) turned into
 //       a worker record (group table + cell table), the tile total into the upper angle pyramid,
 //       and a copy of the call's input tile.  Encode also derives, per pixel, the thermometer code
-//       of p ^ left (EMR; its bit 8-b is the location map l = [c < b]) or the label c | eta
+//       of p ^ left (EMR; its bit 8-b is the location map l = [c < b]) or eta | the thermometer code's bits 0..6
 //       (LMR), and the per-image label histogram (eq. gliding1/2 P:604-625 reduce to the left
 //       neighbour).  The scratch planes are tile blocks (TileBlock).
 //   W (worker) CTAs -- one per strip of tiles, after the image's K CTAs have signalled.  One thread
@@ -269,7 +269,8 @@ __device__ __forceinline__ void key_role(const Geo &g, int img, int kidx, const 
     if constexpr (ENC) {
         // per pixel x = p ^ left neighbour (column 0 forced non-redundant) and its
         // thermometer code y (bit k set iff x >= 2^k, i.e. c = # leading equal bits < 8 - k).
-        // The label plane for the worker: EMR y itself (l = bit 8-b); LMR c | eta with c = 8 - bitlen.
+        // The label plane for the worker: EMR y itself (l = bit 8-b); LMR eta in bit 7 and bits
+        // 0..6 of y (the coder's map bit [c < b] of candidate b = bit 8-b of y, b = 2..8).
         const uint8_t *src = src_img + (size_t)img * g.HW + o;
         uint32_t prev = (valid && tx > 0) ? ((uint32_t)__ldg(src - 1) << 24) : 0u;
         uint32_t yv[NW], lv[NW];
@@ -282,14 +283,8 @@ __device__ __forceinline__ void key_role(const Geo &g, int img, int kidx, const 
             const uint32_t y = smear_bytes(x, g.one);
             yv[i] = valid ? y : 0u;
             uint32_t lab;
-            if constexpr (METHOD == 0) {
-                lab = y;
-            } else {
-                uint32_t a = y - ((y >> 1) & 0x55555555u);          // byte popcount = bitlen(x)
-                a = (a & 0x33333333u) + ((a >> 2) & 0x33333333u);
-                a = (a + (a >> 4)) & 0x0F0F0F0Fu;
-                lab = (0x08080808u - a) | (iw[i] & 0x80808080u);
-            }
+            if constexpr (METHOD == 0) lab = y;
+            else lab = (y & 0x7F7F7F7Fu) | (iw[i] & 0x80808080u);
             lv[i] = lab;
         }
         if (valid) {
@@ -483,7 +478,8 @@ __device__ __forceinline__ void discard_lines(const void *p, int n, int lane) {
 //   EMR: carrier v = (I & 0xFE) | l with l = [c < b] (location map), permuted as a
 //        whole byte; E = v_r XOR (s & 0xFE) (eq. image_encryption P:739 + LSB map P:744);
 //        header b-2 in the LSBs of r = 0..2 (Q14).
-//   LMR: E = I_r XOR s; second plane ceta = (I & 0x80) | c permuted alongside (for the coder).
+//   LMR: E = I_r XOR s; second plane ceta = (I & 0x80) | (y & 0x7F) permuted alongside (for the
+//        coder: eta = bit 7, the map bit [c < b] = bit 8-b).
 // ======================================================================================
 template <int TP, int METHOD, bool SPLIT>
 __device__ __forceinline__ void perm_role(const Geo &g, int img, int dty, int seg, int lgS, int nK, const TileWS &ws,

@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(kCoderThreads) coder_encode_kernel(Geo g, int 
             const uint8_t *rowp = src + (size_t)(y0 + y) * g.W + x0;
             for (int x = 0; x < w; x++) {
                 const uint8_t v = rowp[x];
-                const uint32_t bit = slot == 0 ? (uint32_t)(v >> 7) : (uint32_t)((v & 0xF) < b);
+                const uint32_t bit = slot == 0 ? (uint32_t)(v >> 7) : (uint32_t)((v >> (8 - b)) & 1u);   // [c < b]
                 const uint32_t ctx = (left << 8) | (row_window(p1, x, 5) << 3) | row_window(p2, x + 1, 3);
                 uint16_t *pp = &p0s[ctx * 32 + lane];
                 const uint32_t p = *pp;
@@ -751,7 +751,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtas) coder_encode_fast_ker
         const unsigned v = __reduce_add_sync(am, (unsigned)(h * w));
         if ((tid & 31) == __ffs(am) - 1) atomicAdd(sym_count, (unsigned long long)v);
     }
-    const uint32_t bsub = slot == 0 ? 0u : (uint32_t)(0x80 - ew.plan[img].order[it.cand]) * 0x01010101u;
+    const int bsh = slot == 0 ? 7 : 8 - ew.plan[img].order[it.cand];      // eta: bit 7; map of b: bit 8-b
     const int cap = lmr_tile_cap(g.tile_log2, g.H, g.W);
 
     // early abort (waves >= 1, eta known): the candidate's map can no longer fit once its tiles'
@@ -771,7 +771,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtas) coder_encode_fast_ker
     uint32_t p1[NW], p2[NW];
 #pragma unroll
     for (int k = 0; k < NW; k++) { p1[k] = 0; p2[k] = 0; }
-    // the row's bits, MSB-first: eta = byte >> 7 (eq. MSB_map), map = [(byte & 15) < b];
+    // the row's bits, MSB-first: eta = bit 7 of the byte (eq. MSB_map), map = [c < b] = bit 8-b;
     // the next row's bytes are loaded while the current row is coded
     uint4 raw[2 * NW];
     auto load_row = [&](int y) {
@@ -791,8 +791,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastCtas) coder_encode_fast_ker
                 const uint32_t v[4] = {raw[2 * k + q].x, raw[2 * k + q].y, raw[2 * k + q].z, raw[2 * k + q].w};
 #pragma unroll
                 for (int i = 0; i < 4; i++) {
-                    const uint32_t t = slot == 0 ? (v[i] >> 7) & 0x01010101u
-                                                 : (~((v[i] & 0x0F0F0F0Fu) + bsub) >> 7) & 0x01010101u;
+                    const uint32_t t = (v[i] >> bsh) & 0x01010101u;
                     wv |= nib4(t) << (28 - 4 * (4 * q + i));
                 }
             }

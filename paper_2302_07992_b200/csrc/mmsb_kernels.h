@@ -88,7 +88,7 @@ int lmr_tile_stride_host(int t, int H, int W);
 struct TileWS {
     uint8_t *s;          // [B][ntiles][3][T*T] per tile: K1 keystream (destination-domain tile), the
                          // call's input image tile (encode: I; recover: I_e'), encode's label plane
-                         // (EMR: thermometer code of p ^ left; LMR: label c | eta)
+                         // (EMR: thermometer code of p ^ left; LMR: eta | its bits 0..6)
     uint64_t *rec;       // [B][ntiles][kRecSlots] worker record: group table + cell table
     uint32_t *pyr;       // [B][npyr] upper-level block sums (mod 4 on read)        -- zeroed per call
     uint32_t *hist;      // [B][kHistStride] non-redundant counts for b = 2..8 at index b -- zeroed per call
