@@ -67,7 +67,16 @@ template <int T> struct TileBlock {
     }
 };
 
+// one counter of an image's upper pyramid: from the worker's shared-memory copy, or (pyr_glob(g))
+// from the workspace in global memory (L2; written by the keystream CTAs' atomics)
+template <bool GLOB>
+__device__ __forceinline__ uint32_t pyr_at(const uint32_t *pyr_img, int i) {
+    if constexpr (GLOB) return __ldcg(pyr_img + i);
+    else return pyr_img[i];
+}
+
 // destination tile -> source tile under the levels above the tile (walk e = emax .. tp+1)
+template <bool GLOB>
 __device__ __forceinline__ void upper_walk_inverse(const Geo &g, const uint32_t *pyr_img, int dty, int dtx,
                                                    int &sty, int &stx, int &q) {
     int y = dty, x = dtx;
@@ -75,7 +84,7 @@ __device__ __forceinline__ void upper_walk_inverse(const Geo &g, const uint32_t 
     for (int e = g.emax; e > g.tp; e--) {
         const int k = e - g.tp, m1 = (1 << k) - 1;
         const int by = y >> k, bx = x >> k;
-        const int a = (int)(pyr_img[g.pyr_off[e] + by * (g.W >> e) + bx] & 3u);
+        const int a = (int)(pyr_at<GLOB>(pyr_img, g.pyr_off[e] + by * (g.W >> e) + bx) & 3u);
         int oy = y & m1, ox = x & m1;
         inv_turn(a, m1, oy, ox);
         y = (by << k) | oy;
@@ -86,6 +95,7 @@ __device__ __forceinline__ void upper_walk_inverse(const Geo &g, const uint32_t 
 }
 
 // original tile -> destination tile (walk e = tp+1 .. emax)
+template <bool GLOB>
 __device__ __forceinline__ void upper_walk_forward(const Geo &g, const uint32_t *pyr_img, int oty, int otx,
                                                    int &dty, int &dtx, int &q) {
     int y = oty, x = otx;
@@ -93,7 +103,7 @@ __device__ __forceinline__ void upper_walk_forward(const Geo &g, const uint32_t 
     for (int e = g.tp + 1; e <= g.emax; e++) {
         const int k = e - g.tp, m1 = (1 << k) - 1;
         const int by = y >> k, bx = x >> k;
-        const int a = (int)(pyr_img[g.pyr_off[e] + by * (g.W >> e) + bx] & 3u);
+        const int a = (int)(pyr_at<GLOB>(pyr_img, g.pyr_off[e] + by * (g.W >> e) + bx) & 3u);
         int oy = y & m1, ox = x & m1;
         fwd_turn(a, m1, oy, ox);
         y = (by << k) | oy;
@@ -133,6 +143,7 @@ __device__ __forceinline__ bool wait_keys(const TileWS &ws, int img, int nK) {
 // Warp 0 of a worker CTA: wait for the image's keystream CTAs, then make the upper angle
 // pyramid walkable -- copied into shared memory (spyr, sized at launch) in one parallel load.
 // Returns false (every lane) if the wait timed out.
+template <bool XL>
 __device__ __forceinline__ bool warp0_ready(const Geo &g, const TileWS &ws, int img, int nK, uint32_t *spyr) {
     const int lane = threadIdx.x & 31;
     int ok = 1;
@@ -140,8 +151,10 @@ __device__ __forceinline__ bool warp0_ready(const Geo &g, const TileWS &ws, int 
     ok = __shfl_sync(0xffffffffu, ok, 0);
     if (!ok) return false;
     fence_proxy_async_global();                      // the scratch the bulk copies will read
-    const uint32_t *pyr_img = ws.pyr + (size_t)img * g.npyr;
-    for (int i = lane; i < g.npyr; i += 32) spyr[i] = __ldcg(pyr_img + i);
+    if constexpr (!XL) {
+        const uint32_t *pyr_img = ws.pyr + (size_t)img * g.npyr;
+        for (int i = lane; i < g.npyr; i += 32) spyr[i] = __ldcg(pyr_img + i);
+    }
     __syncwarp();
     return true;
 }
@@ -421,7 +434,6 @@ __device__ __forceinline__ void key_role(const Geo &g, int img, int kidx, const 
 // strip left to right.  Stage ring of kStages tiles: thread 0 issues the bulk copies of tile
 // j + kStages once the 8 warps have released tile j (empty barrier, one arrival per warp).
 // ======================================================================================
-constexpr int kMaxTilesX = 512;                  // W <= 32768 with 64-pixel tiles
 #ifndef MMSB_STAGES
 #define MMSB_STAGES 2
 #endif
@@ -441,6 +453,7 @@ __device__ __forceinline__ uint32_t cell_turns(const uint8_t *wrec, int py, int 
     return ((l2[py] >> (2 * px)) & 3u) | (((l1[wi] >> sh) & 0xFu) << 2) | (((l1[wi + 2] >> sh) & 0xFu) << 6);
 }
 
+constexpr int kMapInline = 512;                  // strip tiles held in the struct (W <= 32768 at 64-pixel tiles)
 template <int TP, bool ENC>
 struct WSmem {
     static constexpr int T = 1 << TP;
@@ -451,7 +464,8 @@ struct WSmem {
         uint4 rec[kWRecBytes / 16];          // worker record (encode: source tile; recover: original tile)
     } st[kStages];
     uint64_t full[kStages], empty[kStages];
-    int map[kMaxTilesX];                     // per tile of the strip: other tile << 2 | upper turns
+    int map[kMapInline];                     // per tile of the strip: other tile << 2 | upper turns
+                                             // (longer strips: the dynamic tail, fused_smem)
     uint32_t fsel[16];                       // copy-forward PRMT selectors by 4-bit map
     int sh[4];
 };
@@ -481,7 +495,7 @@ __device__ __forceinline__ void discard_lines(const void *p, int n, int lane) {
 //   LMR: E = I_r XOR s; second plane ceta = (I & 0x80) | (y & 0x7F) permuted alongside (for the
 //        coder: eta = bit 7, the map bit [c < b] = bit 8-b).
 // ======================================================================================
-template <int TP, int METHOD, bool SPLIT>
+template <int TP, int METHOD, bool SPLIT, bool XL>
 __device__ __forceinline__ void perm_role(const Geo &g, int img, int dty, int seg, int lgS, int nK, const TileWS &ws,
                                           uint8_t *__restrict__ enc, uint8_t *__restrict__ ceta_out,
                                           int32_t *__restrict__ b_out, int64_t *__restrict__ cap_out,
@@ -491,6 +505,10 @@ __device__ __forceinline__ void perm_role(const Geo &g, int img, int dty, int se
     using SM = WSmem<TP, true>;
     SM &S = *reinterpret_cast<SM *>(smem);
     uint32_t *spyr = reinterpret_cast<uint32_t *>(smem + sizeof(SM));
+    // XL (images above 8192^2 or strips longer than kMapInline tiles, a separate instantiation):
+    // the upper pyramid is walked in global memory and the strip map lives in the dynamic tail
+    int *smap = XL ? reinterpret_cast<int *>(spyr) : S.map;
+    const uint32_t *gpyr = ws.pyr + (size_t)img * g.npyr;
     const int tid = threadIdx.x, lane = tid & 31;
     if constexpr (!SPLIT) { seg = 0; lgS = 0; }
 
@@ -501,12 +519,12 @@ __device__ __forceinline__ void perm_role(const Geo &g, int img, int dty, int se
         }
     }
     if (tid < 32) {
-        const bool ok = warp0_ready(g, ws, img, nK, spyr);
+        const bool ok = warp0_ready<XL>(g, ws, img, nK, spyr);
         if (ok) {
             for (int j = tid; j < (g.tilesX >> lgS); j += 32) {
                 int sty, stx, q;
-                upper_walk_inverse(g, spyr, dty, (seg << (g.tlog - lgS)) + j, sty, stx, q);
-                S.map[j] = (((sty << g.tlog) + stx) << 2) | q;
+                upper_walk_inverse<XL>(g, XL ? gpyr : spyr, dty, (seg << (g.tlog - lgS)) + j, sty, stx, q);
+                smap[j] = (((sty << g.tlog) + stx) << 2) | q;
             }
         }
         if (tid == 0) {
@@ -525,7 +543,7 @@ __device__ __forceinline__ void perm_role(const Geo &g, int img, int dty, int se
     auto issue = [&](int j) {
         const int s = j % kStages;
         if (j >= kStages) mbar_wait(&S.empty[s], ((j / kStages) - 1) & 1);
-        const int stile = S.map[j] >> 2, dtile = (dty << g.tlog) + j0 + j;
+        const int stile = smap[j] >> 2, dtile = (dty << g.tlog) + j0 + j;
         mbar_expect_tx(&S.full[s], 3 * T * T + kWRecBytes);
         bulk_g2s(S.st[s].ks, blk0 + (size_t)dtile * TB::BLOCK, T * T, &S.full[s]);
         bulk_g2s(S.st[s].src, blk0 + (size_t)stile * TB::BLOCK + TB::PLANE, 2 * T * T, &S.full[s]);
@@ -559,7 +577,7 @@ __device__ __forceinline__ void perm_role(const Geo &g, int img, int dty, int se
     for (int j = 0; j < ntx; j++) {
         mbar_wait_sleep(&S.full[s], ph);
         const typename SM::Stage &st = S.st[s];
-        const int mp = S.map[j];
+        const int mp = smap[j];
         if (tid >= 224) {                                    // warp 7: drop the consumed scratch from L2
             const int dtile = (dty << g.tlog) + j0 + j;
             discard_lines(blk0 + (size_t)dtile * TB::BLOCK, T * T / 128, lane);
@@ -652,7 +670,7 @@ __device__ __forceinline__ void perm_role(const Geo &g, int img, int dty, int se
 //       tile row (combine = "right if flagged else left", per byte) gives each cell its carry,
 //       the tile's carry moves on to the next tile of the strip in a register.
 // ======================================================================================
-template <int TP, int METHOD, bool SSE>
+template <int TP, int METHOD, bool SSE, bool XL>
 __device__ __forceinline__ void rec_role(const Geo &g, int img, int ty, int nK, const uint8_t *__restrict__ marked,
                                          const TileWS &ws, const uint32_t *__restrict__ eta_bits,
                                          const uint32_t *__restrict__ map_bits, const int32_t *__restrict__ lmr_b,
@@ -664,6 +682,10 @@ __device__ __forceinline__ void rec_role(const Geo &g, int img, int ty, int nK, 
     using SM = WSmem<TP, false>;
     SM &S = *reinterpret_cast<SM *>(smem);
     uint32_t *spyr = reinterpret_cast<uint32_t *>(smem + sizeof(SM));
+    // XL (images above 8192^2 or strips longer than kMapInline tiles, a separate instantiation):
+    // the upper pyramid is walked in global memory and the strip map lives in the dynamic tail
+    int *smap = XL ? reinterpret_cast<int *>(spyr) : S.map;
+    const uint32_t *gpyr = ws.pyr + (size_t)img * g.npyr;
     const int tid = threadIdx.x, lane = tid & 31;
     const uint8_t *Em = marked + (size_t)img * g.HW;
     uint8_t *O = out + (size_t)img * g.HW;
@@ -688,11 +710,11 @@ __device__ __forceinline__ void rec_role(const Geo &g, int img, int ty, int nK, 
         }
         b = __shfl_sync(0xffffffffu, b, 0);
         if (b > 0) {
-            if (warp0_ready(g, ws, img, nK, spyr)) {
+            if (warp0_ready<XL>(g, ws, img, nK, spyr)) {
                 for (int j = tid; j < g.tilesX; j += 32) {
                     int dty, dtx, q;
-                    upper_walk_forward(g, spyr, ty, j, dty, dtx, q);
-                    S.map[j] = (((dty << g.tlog) + dtx) << 2) | q;
+                    upper_walk_forward<XL>(g, XL ? gpyr : spyr, ty, j, dty, dtx, q);
+                    smap[j] = (((dty << g.tlog) + dtx) << 2) | q;
                 }
             } else if (tid == 0) {
                 S.sh[0] = 0;
@@ -730,7 +752,7 @@ __device__ __forceinline__ void rec_role(const Geo &g, int img, int ty, int nK, 
     auto issue = [&](int j) {
         const int s = j % kStages;
         if (j >= kStages) mbar_wait(&S.empty[s], ((j / kStages) - 1) & 1);
-        const int dt = S.map[j] >> 2;
+        const int dt = smap[j] >> 2;
         mbar_expect_tx(&S.full[s], 2 * T * T + kWRecBytes);
         bulk_g2s(S.st[s].src, blk0 + (size_t)dt * TB::BLOCK, 2 * T * T, &S.full[s]);
         bulk_g2s(S.st[s].rec, rec0 + (size_t)j * kRecSlots, kWRecBytes, &S.full[s]);
@@ -767,7 +789,7 @@ __device__ __forceinline__ void rec_role(const Geo &g, int img, int ty, int nK, 
     unsigned ph = 0;
     for (int j = 0; j < ntx; j++) {
         mbar_wait_sleep(&S.full[s], ph);
-        const int mp = S.map[j], dt = mp >> 2, q_up = mp & 3;
+        const int mp = smap[j], dt = mp >> 2, q_up = mp & 3;
         if (tid >= 224)                                      // warp 7: drop the consumed scratch from L2
         {
             discard_lines(blk0 + (size_t)dt * TB::BLOCK, 2 * T * T / 128, lane);
@@ -880,7 +902,7 @@ __device__ __forceinline__ void rec_role(const Geo &g, int img, int ty, int nK, 
 // ======================================================================================
 // The fused kernels (dynamic shared memory: max of the two roles' needs + the pyramid)
 // ======================================================================================
-template <int TP, int METHOD, bool SPLIT>
+template <int TP, int METHOD, bool SPLIT, bool XL>
 __global__ void __launch_bounds__(256, 6) encode_kernel(Geo g, FusedSched sc, const uint8_t *__restrict__ images,
                                                      const uint8_t *__restrict__ keys, TileWS ws,
                                                      uint8_t *__restrict__ enc, uint8_t *__restrict__ ceta,
@@ -894,13 +916,13 @@ __global__ void __launch_bounds__(256, 6) encode_kernel(Geo g, FusedSched sc, co
 #endif
     if (ro.key) key_role<TP, true, METHOD>(g, ro.img, ro.idx, keys, images, ws, smem);
     else if constexpr (SPLIT)
-        perm_role<TP, METHOD, true>(g, ro.img, ro.idx >> sc.lgS, ro.idx & ((1 << sc.lgS) - 1), sc.lgS, 1 << sc.lgK, ws,
+        perm_role<TP, METHOD, true, XL>(g, ro.img, ro.idx >> sc.lgS, ro.idx & ((1 << sc.lgS) - 1), sc.lgS, 1 << sc.lgK, ws,
                                     enc, ceta, b_out, cap_out, status, smem);
     else
-        perm_role<TP, METHOD, false>(g, ro.img, ro.idx, 0, 0, 1 << sc.lgK, ws, enc, ceta, b_out, cap_out, status, smem);
+        perm_role<TP, METHOD, false, XL>(g, ro.img, ro.idx, 0, 0, 1 << sc.lgK, ws, enc, ceta, b_out, cap_out, status, smem);
 }
 
-template <int TP, int METHOD, bool SSE>
+template <int TP, int METHOD, bool SSE, bool XL>
 __global__ void __launch_bounds__(256, 6) recover_kernel(Geo g, FusedSched sc, const uint8_t *__restrict__ marked,
                                                       const uint8_t *__restrict__ keys, TileWS ws,
                                                       const uint32_t *__restrict__ eta_bits,
@@ -915,7 +937,7 @@ __global__ void __launch_bounds__(256, 6) recover_kernel(Geo g, FusedSched sc, c
     if (!((MMSB_PROBE_ROLES >> (ro.key ? 0 : 1)) & 1)) return;
 #endif
     if (ro.key) key_role<TP, false, METHOD>(g, ro.img, ro.idx, keys, marked, ws, smem);
-    else rec_role<TP, METHOD, SSE>(g, ro.img, ro.idx, 1 << sc.lgK, marked, ws, eta_bits, map_bits, lmr_b, out, status,
+    else rec_role<TP, METHOD, SSE, XL>(g, ro.img, ro.idx, 1 << sc.lgK, marked, ws, eta_bits, map_bits, lmr_b, out, status,
                                    orig, sse, smem);
 }
 
@@ -948,23 +970,37 @@ static dim3 fused_grid(const FusedSched &sc) {
     return dim3((unsigned)((sc.GI << sc.lgK) + (sc.GI << sc.lgW)), (unsigned)(sc.ngroups + sc.L));
 }
 
+// the XL instantiation: images whose upper pyramid is too large for shared memory (pyr_glob) or
+// whose strips are longer than kMapInline tiles (H < 64 makes the tiles narrower than 64, e.g.
+// 16 x 32768: 2048 tiles per strip)
+static bool fused_xl(const Geo &g) { return pyr_glob(g) || g.tilesX > kMapInline; }
+
 template <int TP, bool ENC>
 static size_t fused_smem(const Geo &g) {
-    const size_t k = sizeof(KSmem<TP>), w = sizeof(WSmem<TP, ENC>) + (size_t)g.npyr * 4;
+    // worker: the stage ring and the upper angle pyramid; XL: the ring and the strip's tile map
+    const size_t k = sizeof(KSmem<TP>),
+                 w = sizeof(WSmem<TP, ENC>) + (fused_xl(g) ? (size_t)g.tilesX * 4 : (size_t)g.npyr * 4);
     return k > w ? k : w;
 }
 
+template <int TP, bool SPLIT, bool XL>
+static void launch_encode_x(const Geo &g, const FusedSched &sc, dim3 grid, size_t sm, const uint8_t *images,
+                            const uint8_t *keys, const TileWS &ws, uint8_t *enc, uint8_t *ceta, int32_t *b_out,
+                            int64_t *cap_out, int32_t *status, cudaStream_t st) {
+    if (g.method == 0) {
+        cudaFuncSetAttribute(encode_kernel<TP, 0, SPLIT, XL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        encode_kernel<TP, 0, SPLIT, XL><<<grid, 256, sm, st>>>(g, sc, images, keys, ws, enc, ceta, b_out, cap_out, status);
+    } else {
+        cudaFuncSetAttribute(encode_kernel<TP, 1, SPLIT, XL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        encode_kernel<TP, 1, SPLIT, XL><<<grid, 256, sm, st>>>(g, sc, images, keys, ws, enc, ceta, b_out, cap_out, status);
+    }
+}
 template <int TP, bool SPLIT>
 static void launch_encode_k(const Geo &g, const FusedSched &sc, dim3 grid, size_t sm, const uint8_t *images,
                             const uint8_t *keys, const TileWS &ws, uint8_t *enc, uint8_t *ceta, int32_t *b_out,
                             int64_t *cap_out, int32_t *status, cudaStream_t st) {
-    if (g.method == 0) {
-        cudaFuncSetAttribute(encode_kernel<TP, 0, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        encode_kernel<TP, 0, SPLIT><<<grid, 256, sm, st>>>(g, sc, images, keys, ws, enc, ceta, b_out, cap_out, status);
-    } else {
-        cudaFuncSetAttribute(encode_kernel<TP, 1, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        encode_kernel<TP, 1, SPLIT><<<grid, 256, sm, st>>>(g, sc, images, keys, ws, enc, ceta, b_out, cap_out, status);
-    }
+    if (fused_xl(g)) launch_encode_x<TP, SPLIT, true>(g, sc, grid, sm, images, keys, ws, enc, ceta, b_out, cap_out, status, st);
+    else launch_encode_x<TP, SPLIT, false>(g, sc, grid, sm, images, keys, ws, enc, ceta, b_out, cap_out, status, st);
 }
 
 template <int TP>
@@ -991,9 +1027,15 @@ static void launch_recover_k(const Geo &g, const FusedSched &sc, const uint8_t *
                              const TileWS &ws, const uint32_t *eta, const uint32_t *map, const int32_t *lmr_b,
                              uint8_t *out, int32_t *status, const uint8_t *orig, unsigned long long *sse, cudaStream_t st) {
     const size_t sm = fused_smem<TP, false>(g);
-    cudaFuncSetAttribute(recover_kernel<TP, METHOD, SSE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    recover_kernel<TP, METHOD, SSE><<<fused_grid(sc), 256, sm, st>>>(g, sc, marked, keys, ws, eta, map, lmr_b, out,
-                                                                      status, orig, sse);
+    if (fused_xl(g)) {
+        cudaFuncSetAttribute(recover_kernel<TP, METHOD, SSE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        recover_kernel<TP, METHOD, SSE, true><<<fused_grid(sc), 256, sm, st>>>(g, sc, marked, keys, ws, eta, map, lmr_b,
+                                                                                out, status, orig, sse);
+    } else {
+        cudaFuncSetAttribute(recover_kernel<TP, METHOD, SSE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        recover_kernel<TP, METHOD, SSE, false><<<fused_grid(sc), 256, sm, st>>>(g, sc, marked, keys, ws, eta, map, lmr_b,
+                                                                                 out, status, orig, sse);
+    }
 }
 
 template <int TP>

@@ -33,6 +33,10 @@ struct Geo {
     int dr;              // keystream double rounds: 10 (ChaCha20), 6 (ChaCha12) or 4 (ChaCha8)
 };
 
+// the workers walk the upper angle pyramid in global memory when it is too large for shared
+// memory (> 32 KB per image: images above 8192^2), else a copy in shared memory
+__host__ __device__ inline bool pyr_glob(const Geo &g) { return g.npyr > 8192; }
+
 inline int ilog2(long long v) {
     int e = 0;
     while ((2LL << e) <= v) e++;
