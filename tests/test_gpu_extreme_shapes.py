@@ -64,3 +64,28 @@ def test_maximum_square_image(method):
         assert torch.equal(rec, img)
     else:
         assert torch.equal(rec >> 1, img >> 1)
+
+
+@pytest.mark.parametrize("method", [G.EMR, G.LMR])
+def test_batch_beyond_2_to_32_pixels(method):
+    """20 480 images of 512^2 in one call: 5.4 G pixels, beyond 2^32, so a 32-bit pixel, bit or
+    byte offset anywhere on the path would wrap.  The batch repeats 64 distinct images (and
+    their keys and payloads) 320 times, and every repeat must reproduce the first copy's encrypted
+    image, b, capacity, marked image, payload and recovered image exactly; the first copies are
+    checked against the oracle elsewhere (config 2 / 3 samples), here 3 of them again."""
+    n0, reps = 64, 320
+    imgs, k1, k2 = S.batch(3, n=n0)
+    stride = S.msg_stride(512, 512)
+    msgs = np.stack([S.payload(S.image_seed(3, j), stride) for j in range(n0)])
+    rep = lambda a: _dev(a).repeat(reps, *([1] * (a.ndim - 1)))
+    I, K1, K2, M = rep(imgs), rep(k1), rep(k2), rep(msgs)
+    assert I.shape[0] * 512 * 512 > 2 ** 32
+    out = _run(method, I, K1, K2, M)
+    _batch_properties(method, I, M, out, expect_ok=False)
+    for k in ("enc", "b", "cap", "st_e", "marked", "st_h", "msg", "nb_out", "st_x", "rec", "st_r", "sse"):
+        v = out[k].reshape(reps, n0, *out[k].shape[1:])
+        assert bool((v == v[:1]).all()), k
+    del I, M
+    torch.cuda.empty_cache()
+    for j in (0, 1, n0 - 1):
+        _oracle_image(method, imgs[j], k1[j], k2[j], msgs[j], (reps - 1) * n0 + j, out)
