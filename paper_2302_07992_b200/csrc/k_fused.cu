@@ -314,6 +314,7 @@ __device__ __forceinline__ void key_role(const Geo &g, int img, int kidx, const 
 #pragma unroll
         for (int k = 0; k < 7; k++) {
             const uint32_t mk = 0x01010101u << k;
+            if (METHOD == 0 && k == 0) { cnt[k] = 0; continue; }        // b = 8: LMR only
             cnt[k] = __popc(pl[0] & mk) + 2 * __popc(pl[1] & mk) + 4 * __popc(pl[2] & mk) + 8 * __popc(pl[3] & mk) +
                      16 * __popc(pl[4] & mk);
         }
