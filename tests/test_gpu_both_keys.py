@@ -12,7 +12,9 @@ from paper_2302_07992_b200 import synth as S
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("method,H,W", [(G.EMR, 128, 128), (G.EMR, 64, 256), (G.LMR, 128, 128), (G.LMR, 256, 64)])
+@pytest.mark.parametrize("method,H,W", [(G.EMR, 128, 128), (G.EMR, 64, 256), (G.LMR, 128, 128), (G.LMR, 256, 64),
+                                        (G.EMR, 16, 32768), (G.LMR, 16, 32768), (G.EMR, 32768, 16),
+                                        (G.LMR, 32768, 16)])   # the envelope's edges (XL kernels)
 def test_both_equals_separate_calls_and_oracle(method, H, W):
     kinds = ["smooth", "textured", "smooth", "constant", "smooth"]
     B = len(kinds)

@@ -17,8 +17,8 @@ def _dev(a):
 
 
 @pytest.mark.parametrize("method", [G.EMR, G.LMR])
-def test_capacity_matches_encoder_and_oracle(method):
-    H = W = 128
+@pytest.mark.parametrize("H,W", [(128, 128), (16, 32768), (32768, 16)])
+def test_capacity_matches_encoder_and_oracle(method, H, W):
     kinds = ["smooth", "textured", "noise", "constant", "quantised", "smooth"]
     imgs = np.stack([S.random_image(500 + j, H, W, k) for j, k in enumerate(kinds)])
     k1 = np.stack([np.frombuffer(S.key(500 + j, 1), np.uint8) for j in range(len(kinds))])
