@@ -27,7 +27,7 @@ def _protocol_images(H, W, n=3):
     return I, enc, marked, rec
 
 
-@pytest.mark.parametrize("H,W", [(16, 16), (64, 64), (128, 256), (512, 512)])
+@pytest.mark.parametrize("H,W", [(16, 16), (64, 64), (128, 256), (512, 512), (16, 32768), (32768, 16)])
 def test_histogram_entropy_chi2_and_differences(H, W):
     I, enc, marked, rec = _protocol_images(H, W)
     for X in (I, enc, marked, rec):
@@ -48,7 +48,7 @@ def test_histogram_entropy_chi2_and_differences(H, W):
             assert npcr[j] == pytest.approx(n_o, rel=1e-12) and uaci[j] == pytest.approx(u_o, rel=1e-12)
 
 
-@pytest.mark.parametrize("H,W", [(16, 16), (64, 64), (128, 256), (256, 64)])
+@pytest.mark.parametrize("H,W", [(16, 16), (64, 64), (128, 256), (256, 64), (16, 4096), (4096, 16)])
 def test_ssim_parity(H, W):
     I, enc, marked, rec = _protocol_images(H, W)
     for A, B in ((I, rec), (I, enc), (I, I), (marked, rec)):
