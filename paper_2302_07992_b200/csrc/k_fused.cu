@@ -322,10 +322,7 @@ __device__ __forceinline__ void key_role(const Geo &g, int img, int kidx, const 
         // per 32-bit word for the warp reduction
         uint32_t pk[4] = {cnt[0] | (cnt[1] << 16), cnt[2] | (cnt[3] << 16), cnt[4] | (cnt[5] << 16), cnt[6]};
 #pragma unroll
-        for (int j = 0; j < 4; j++) {
-#pragma unroll
-            for (int s = 16; s > 0; s >>= 1) pk[j] += __shfl_xor_sync(0xffffffffu, pk[j], s);
-        }
+        for (int j = 0; j < 4; j++) pk[j] = __reduce_add_sync(0xffffffffu, pk[j]);   // REDUX: one instruction per word
         // per-CTA sum, then one atomic per count (a 4096^2 image has 1024 keystream CTAs)
         if ((tid & 31) == 0) {
 #pragma unroll

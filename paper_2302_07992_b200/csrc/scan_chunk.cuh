@@ -203,8 +203,7 @@ __device__ __forceinline__ void count_chunk(const Geo &g, const uint8_t *__restr
             c += __popc(~(__ldg(map_bits + (pb >> 5)) >> (pb & 31)) & 0xFFFFu);
         }
     }
-#pragma unroll
-    for (int s2 = 16; s2 > 0; s2 >>= 1) c += __shfl_xor_sync(0xffffffffu, c, s2);
+    c = __reduce_add_sync(0xffffffffu, c);
     if ((tid & 31) == 0) red[tid >> 5] = c;
     __syncthreads();
     if (tid == 0) {
@@ -271,8 +270,7 @@ __device__ __forceinline__ void scan_chunk(ScanSmem<METHOD, EMBED> &S, const Geo
         // this chunk's prefix: the zero counts of the image's earlier chunks (embed_prep_kernel)
         uint32_t part = 0;
         for (int c = tid; c < chunk; c += kScanThreads) part += __ldg(ws.counts + (size_t)img * g.nchunks + c);
-#pragma unroll
-        for (int s2 = 16; s2 > 0; s2 >>= 1) part += __shfl_xor_sync(0xffffffffu, part, s2);
+        part = __reduce_add_sync(0xffffffffu, part);
         if (lane == 0) S.wpre[wid] = part;
     }
     __syncthreads();                                         // barrier initialised (and S.wpre written)
