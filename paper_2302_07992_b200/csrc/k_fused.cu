@@ -552,7 +552,7 @@ __device__ __forceinline__ void perm_role(const Geo &g, int img, int dty, int se
 
     // this thread's destination cell and its candidate group / sub-cell positions for the 4
     // possible upper turns of the tile (undo the tile's own turn first)
-    const bool act = tid < NC * NC;
+    const bool act = NC * NC >= 256 || tid < NC * NC;    // 64-pixel tiles: every thread has a cell
     const int cy = act ? tid / NC : 0, cx = act ? tid % NC : 0;
     uint32_t gpos = 0, spos = 0;
 #pragma unroll
@@ -563,6 +563,9 @@ __device__ __forceinline__ void perm_role(const Geo &g, int img, int dty, int se
         gpos |= (uint32_t)(gy * NG + gx) << (8 * q);
         spos |= (uint32_t)(sy * 2 + sx) << (2 * q);
     }
+    // opaque from here on: under the 40-register cap ptxas otherwise recomputes both tables from
+    // tid in every tile iteration (ncu source page: 14 + ~30 instructions per tile and warp)
+    asm volatile("" : "+r"(gpos), "+r"(spos));
     const int lsh = 8 - b;                                   // EMR: map bit l = bit 8 - b of the thermometer code
     // output rows of this thread's cell in the worker's first tile (the tile advances by T bytes)
     const size_t W = (size_t)g.W;
@@ -758,7 +761,7 @@ __device__ __forceinline__ void rec_role(const Geo &g, int img, int ty, int nK, 
     if (tid == 0)
         for (int j = 0; j < kStages && j < ntx; j++) issue(j);
 
-    const bool act = tid < NC * NC;
+    const bool act = NC * NC >= 256 || tid < NC * NC;    // 64-pixel tiles: every thread has a cell
     const int cy = act ? tid / NC : 0, cx = act ? tid % NC : 0;
     uint32_t spos = 0;                                   // sub-cell position after q turns (forward)
 #pragma unroll
@@ -767,6 +770,7 @@ __device__ __forceinline__ void rec_role(const Geo &g, int img, int ty, int nK, 
         fwd_turn(q, 1, sy, sx);
         spos |= (uint32_t)(sy * 2 + sx) << (2 * q);
     }
+    asm volatile("" : "+r"(spos));                       // kept, not recomputed per tile (see perm_role)
     constexpr uint32_t HB = METHOD == 0 ? 0x01u : 0x80u;            // flag bit, outside the mask
     constexpr uint32_t HBW = HB * 0x01010101u;
     // combine(a, b) per byte: b if flagged else a
