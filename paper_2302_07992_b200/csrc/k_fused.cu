@@ -294,7 +294,7 @@ __device__ __forceinline__ void key_role(const Geo &g, int img, int kidx, const 
             if (i == 0 && tx == 0) x |= 0xFFu;
             prev = iw[i];
             const uint32_t y = smear_bytes(x, g.one);
-            yv[i] = valid ? y : 0u;
+            yv[i] = y;
             uint32_t lab;
             if constexpr (METHOD == 0) lab = y;
             else lab = (y & 0x7F7F7F7Fu) | (iw[i] & 0x80808080u);
@@ -321,6 +321,7 @@ __device__ __forceinline__ void key_role(const Geo &g, int img, int kidx, const 
         // threshold bit k <-> b = 8 - k; per-thread counts <= 64, warp sums <= 2048: two counts
         // per 32-bit word for the warp reduction
         uint32_t pk[4] = {cnt[0] | (cnt[1] << 16), cnt[2] | (cnt[3] << 16), cnt[4] | (cnt[5] << 16), cnt[6]};
+        if (!valid) pk[0] = pk[1] = pk[2] = pk[3] = 0;               // a row past the image's tiles counts nothing
 #pragma unroll
         for (int j = 0; j < 4; j++) pk[j] = __reduce_add_sync(0xffffffffu, pk[j]);   // REDUX: one instruction per word
         // per-CTA sum, then one atomic per count (a 4096^2 image has 1024 keystream CTAs)
