@@ -53,14 +53,25 @@ __device__ __forceinline__ void frame_block(const Geo &g, const uint8_t *__restr
     const uint32_t *mw = reinterpret_cast<const uint32_t *>(msg + (size_t)img * stride);
     const long long nmw = stride / 4;                            // message words in the row
     uint32_t o[16];
+    if (k > 0 && k * 16 + 15 < nmw && (reinterpret_cast<uintptr_t>(mw) & 15) == 0) {
+        // a block inside the message row: frame words 16k .. 16k+15 = message words 16k-1 .. 16k+14, one
+        // scalar and four 16-byte loads; bswap(m) ^ bswap(ks) = bswap(m ^ ks)
+        const uint4 *mv = reinterpret_cast<const uint4 *>(mw + k * 16);
+        const uint32_t m0 = __ldg(mw + k * 16 - 1);
+        const uint4 v0 = __ldg(mv), v1 = __ldg(mv + 1), v2 = __ldg(mv + 2), v3 = __ldg(mv + 3);
+        const uint32_t m[16] = {m0, v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w, v2.x, v2.y, v2.z, v2.w, v3.x, v3.y, v3.z};
 #pragma unroll
-    for (int j = 0; j < 16; j++) {
-        const long long wi = k * 16 + j;
-        uint32_t fw;
-        if (wi == 0) fw = (uint32_t)n;
-        else if (wi - 1 < nmw) fw = bswap32(__ldg(mw + (wi - 1)));
-        else fw = 0;
-        o[j] = fw ^ bswap32(ks[j]);
+        for (int j = 0; j < 16; j++) o[j] = bswap32(m[j] ^ ks[j]);
+    } else {
+#pragma unroll
+        for (int j = 0; j < 16; j++) {
+            const long long wi = k * 16 + j;
+            uint32_t fw;
+            if (wi == 0) fw = (uint32_t)n;
+            else if (wi - 1 < nmw) fw = bswap32(__ldg(mw + (wi - 1)));
+            else fw = 0;
+            o[j] = fw ^ bswap32(ks[j]);
+        }
     }
     uint4 *dst = reinterpret_cast<uint4 *>(ws.ef + (size_t)img * ws.ef_words + k * 16);
 #pragma unroll
