@@ -83,6 +83,11 @@ def main(tag):
                     skip = 1 if part in ("scan_kernel<0, 0>", "scan_finish_kernel<0, 0>") else 0
                     ncu_mix.main(rep, kname, 0, 10 ** 9, skip)
                 mixf.write("    " + buf.getvalue().replace("\n", "\n    ").rstrip() + "\n")
+                import re
+                mm = re.search(r"total (\d+) warp-inst; alu-pipe (\d+) .*fma-pipe (\d+)", buf.getvalue())
+                if mm:                                      # thread-instructions per pixel of the capture
+                    t_, a_, f_ = (int(x) * 32 / PX for x in mm.groups())
+                    mixf.write(f"    per pixel: {t_:.1f} thread-instructions, {a_:.1f} on the ALU pipe, {f_:.1f} on the FMA pipe\n")
         alg = bench.kernel_model(cls, der)["bytes"]
         traffic[cls] = (rd + wr) / PX
         launches[cls] = {"dram_read_bytes": rd, "dram_write_bytes": wr, "pixels": PX, "duration_us": dur,
