@@ -408,7 +408,11 @@ __device__ __forceinline__ void scan_chunk(ScanSmem<METHOD, EMBED> &S, const Geo
         (void)nblk;
         mbar_wait(&S.bar_ef, 0);
         const long long base = blk0 * 512;
-        const long long fend = hie - base;
+        // chunk-relative bit offsets fit 32 bits (lo - base < 512, a chunk holds < 2^17 frame bits):
+        // the per-group arithmetic below is 32-bit; a frame end before / far past the chunk clamps
+        const int rel0 = (int)(lo - base);
+        const long long fend64 = hie - base;
+        const int fend = fend64 < 0 ? 0 : fend64 > 0x3FFFFFFFll ? 0x3FFFFFFF : (int)fend64;
         uint8_t *dst = out + (size_t)img * g.HW + p0;
         MMSB_BP_SWITCH(bp, METHOD, ({
             _Pragma("unroll")
@@ -417,10 +421,10 @@ __device__ __forceinline__ void scan_chunk(ScanSmem<METHOD, EMBED> &S, const Geo
                 if (16 * q >= cpx) continue;
                 const uint4 u = S.spx[q];
                 uint32_t w[4] = {u.x, u.y, u.z, u.w};
-                const long long rel = (prefix + excl[r]) * BP - base;
+                const int rel = rel0 + (int)excl[r] * BP;
                 const int cnt = __popc(m[r]);
                 if (cnt && rel < fend) {
-                    if (rel + (long long)cnt * BP <= fend) embed16<BP, SH>(w, m[r], S.kbuf, (int)rel, S.esel);
+                    if (rel + cnt * BP <= fend) embed16<BP, SH>(w, m[r], S.kbuf, rel, S.esel);
                     else {
                         const uint4 t = embed16_tail<BP, SH>(make_uint4(w[0], w[1], w[2], w[3]), m[r], S.kbuf, rel, fend);
                         w[0] = t.x; w[1] = t.y; w[2] = t.z; w[3] = t.w;
